@@ -1,0 +1,449 @@
+#!/usr/bin/env python
+"""bench.py — GF(2) block decomposition on B200 (BASELINE.json metric).
+
+Default workload (BASELINE.json configs[3], the metric's headline): full
+decomposition P*A = L*U of a 65536 x 65536 dense F2 matrix, bits Bernoulli(0.5)
+from PackedMatrix::random_dense(seed 6) — synthetic input generated bit-exactly
+on the device.  One step = copy A -> W (the API never modifies its input,
+SPEC.md:379) + decompose_block(W).  Metric: Gbitop/s = n^3 / t.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun): column blocks round-robin over the ranks, one NCCL broadcast
+per panel (strong scaling: the job is one 65536^2 decomposition).
+
+The JSON line carries: value (device-resident, CUDA events, max over ranks),
+e2e (through the C-ABI host entry point: H2D of A from pinned memory, the
+decomposition, D2H of W/perm/r_j), roofline (the dominant kernel: the fused
+M4RM Schur update, measured live as the north-star unit
+C(65536x65536) ^= A(65536x64) * B(64x65536)), cpu_baseline (the reference
+CPU path on this host: bounded sample, extrapolated), clocks, gpu_launches.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
+METRIC = "GF(2) decomposition Gbitop/s (n^3/t) at 65536^2"
+UNIT = "Gbitop/s"
+
+
+def peaks() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference's own M4RM (oracle/_ref, compiled from the
+# reference headers) under the restated buildZ; bounded sample of panels.
+# ---------------------------------------------------------------------------
+def panel_work(n: int, mu: int, P: int) -> float:
+    """Remaining trailing area summed over the first P panels of a full-rank
+    n x 64mu decomposition (rows below the pivots x word-columns right of the
+    panel) — the Schur update work that dominates the CPU time."""
+    w = 0.0
+    for j in range(min(P, mu)):
+        w += max(n - 64 * (j + 1), 0) * (mu - j - 1) + (n - 64 * j)
+    return w
+
+
+def cpu_baseline(n: int, m: int, p: float, seed: int, panels: int, reps: int = 1) -> dict:
+    from oracle import pyoracle as po
+
+    threads = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
+    po.build(ref=False)
+    a = po.random_dense(n, m, p, seed)  # parallel jump-ahead twin of random_dense (pinned by tests)
+    mu = (m + 63) // 64
+    use_ref = po.ref_available()
+    best = float("inf")
+    for _ in range(reps):
+        if use_ref:
+            r = po.ref()
+            h = r.ref_matrix_new(a, n, m, a.shape[1])
+            perm = np.zeros(n, np.uint32)
+            rj = np.zeros(mu, np.uint32)
+            t0 = time.perf_counter()
+            r.ref_decompose_block(h, perm, rj, 8, panels)
+            dt = time.perf_counter() - t0
+            r.ref_matrix_free(h)
+        else:
+            w = a.copy()
+            perm = np.zeros(n, np.uint32)
+            rj = np.zeros(mu, np.uint32)
+            t0 = time.perf_counter()
+            po.lib().f2o_decompose_block(w, n, m, w.shape[1], perm, rj, 8, panels)
+            dt = time.perf_counter() - t0
+        best = min(best, dt)
+    frac = panel_work(n, mu, panels) / panel_work(n, mu, mu)
+    t_full = best / frac
+    return {
+        "value": round(n * n * min(n, m) / t_full / 1e9, 2),
+        "unit": UNIT,
+        "cores": threads,
+        "kind": "reference" if use_ref else "port",
+        "sample": (f"first {panels} of {mu} panels of the same {n}x{m} seed-{seed} decomposition "
+                   f"({'reference m4rm.hpp build_tables/mult_acc compiled from the reference headers + restated buildZ' if use_ref else 'oracle/f2oracle.c port'}), "
+                   f"OpenMP {threads} threads, {best:.2f} s measured = {frac:.3f} of the Schur work; "
+                   f"full-run time extrapolated {t_full:.1f} s"),
+        "t_sample_s": round(best, 3),
+        "t_full_est_s": round(t_full, 2),
+    }
+
+
+# ---------------------------------------------------------------------------
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def run_reference(args, cfg) -> None:
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    vals = []
+    base = None
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(cfg["n"], cfg["m"], cfg["p"], cfg["seed"], args.ref_panels)
+        if i >= args.warmup:
+            vals.append(cb["value"])
+            base = cb
+    v = float(np.median(vals))
+    t_step = cfg["n"] ** 2 * min(cfg["n"], cfg["m"]) / (v * 1e9)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 1),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (random_dense seed %d, p=%g)" % (cfg["seed"], cfg["p"]),
+        "config": cfg_json(cfg, args.gpus),
+        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cfg_json(cfg, gpus):
+    return {"workload": f"decompose_block {cfg['n']}x{cfg['m']} dense F2, Bernoulli({cfg['p']}), "
+                        f"seed {cfg['seed']} (BASELINE configs[3])",
+            "n": cfg["n"], "m": cfg["m"], "density": cfg["p"], "seed": cfg["seed"],
+            "word_bits": 64, "tables": "9 groups (7x8+8 bits), 16 word-cols/CTA",
+            "parallelism": f"column-round-robin x{gpus}" if gpus > 1 else "single GPU",
+            "l2": "inputs (512 MiB) larger than L2 (126 MB); no flush needed"}
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=65536, help="matrix size (default: BASELINE cfg4)")
+    ap.add_argument("--ref-panels", type=int, default=32, help="CPU sample size in panels")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--gemm", action="store_true", help="also time the cfg2 16384^2 GEMM")
+    args = ap.parse_args()
+    cfg = {"n": args.n, "m": args.n, "p": 0.5, "seed": 6}
+
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    import paper_1209_5198_b200 as f2
+    from paper_1209_5198_b200 import _lib
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _lib.load()
+    ctx = f2.Context(local)
+    # a real (non-legacy) stream shared by torch events and the library's kernels
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+    if world > 1:
+        obj = [f2.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx.init_comm(rank, world, obj[0])
+
+    n, m = cfg["n"], cfg["m"]
+    mu = (m + 63) // 64
+    A = f2.DeviceMatrix(n, m, ctx)
+    A.random_dense(cfg["p"], cfg["seed"])
+    if world > 1:
+        lw = int(lib.f2gpu_local_wcols(mu, rank, world))
+        Aloc = f2.DeviceMatrix(n, lw * 64, ctx)
+        _lib.check(lib.f2gpu_mat_select_wcols(ctx.handle, Aloc.handle, A.handle, rank, world, 0))
+        A.free()
+        A = Aloc
+    W = f2.DeviceMatrix(A.n, A.m, ctx)
+    perm = np.zeros(n, np.uint32)
+    rj = np.zeros(mu, np.uint32)
+    rk = C.c_size_t()
+
+    def step():
+        _lib.check(lib.f2gpu_mat_copy(ctx.handle, W.handle, A.handle))
+        if world > 1:
+            _lib.check(lib.f2gpu_decompose_block_dist(ctx.handle, W.handle, m, perm.ctypes.data,
+                                                      rj.ctypes.data, C.byref(rk)))
+        else:
+            _lib.check(lib.f2gpu_decompose_block(ctx.handle, W.handle, perm.ctypes.data,
+                                                 rj.ctypes.data, C.byref(rk)))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    clocks.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = ctx.launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ck = clocks.stop()
+    launches = ctx.launches() - l0
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = n * n * min(n, m) / (ms_step * 1e-3) / 1e9
+    rank_found = int(rk.value)
+
+    # ---- roofline: the dominant kernel, measured live (north-star unit) ----
+    roof = None
+    if rank == 0:
+        roof = measure_update_roofline(f2, lib, _lib, ctx, stream, torch, n)
+
+    # ---- e2e through the C-ABI host entry point (pinned host buffers) ----
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(f2, lib, _lib, ctx, torch, A, n, m, mu, world, rank, dist,
+                          steps=min(args.steps, 3))
+
+    gemm = None
+    if args.gemm and rank == 0:
+        gemm = measure_gemm(f2, lib, _lib, ctx, stream, torch)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(n, m, cfg["p"], cfg["seed"], args.ref_panels)
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+            "data": f"synthetic (random_dense seed {cfg['seed']}, p={cfg['p']}, generated on device)",
+            "config": cfg_json(cfg, world),
+            "rank": rank_found,
+            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": ck,
+            "gpu_launches": launches,
+        }
+        if gemm:
+            line["gemm"] = gemm
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def measure_update_roofline(f2, lib, _lib, ctx, stream, torch, n: int) -> dict:
+    """C(n x n) ^= A(n x 64) * B(64 x n) with the fused table-build + XOR kernel,
+    averaged over back-to-back launches (C = 512 MiB > L2, so every launch streams
+    C from HBM).  Algorithmic bytes = n*8 (A) + 64*n/8 (B) + 2*n*n/8 (C in+out)."""
+    mu = n // 64
+    Cm = f2.DeviceMatrix(n, n, ctx)
+    Cm.random_dense(0.5, 101)
+    Bm = f2.DeviceMatrix(64, n, ctx)
+    Bm.random_dense(0.5, 102)
+    a = torch.randint(-2**62, 2**62, (n,), dtype=torch.int64, device="cuda")
+
+    def launch():
+        _lib.check(lib.f2gpu_mult_acc(ctx.handle, Cm.handle, 0, 0, mu, C.c_void_p(a.data_ptr()), n, 64,
+                                      Bm.handle, 0, 0))
+
+    for _ in range(3):
+        launch()
+    torch.cuda.synchronize()
+    reps = 20
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        launch()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / reps * 1e-3
+    alg = n * 8 + 64 * n // 8 + 2 * n * n // 8
+    peak, src = peaks()
+    ach = alg / t / 1e9
+    traffic = None
+    tp = ROOT / "profiles" / "update_traffic.json"
+    if tp.exists():
+        try:
+            traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    Cm.free(); Bm.free()
+    return {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(ach / peak, 4), "traffic": traffic,
+            "kernel": "k_update (fused M4RM table build + XOR sweep)",
+            "unit_workload": f"C({n}x{n}) ^= A({n}x64)*B(64x{n})",
+            "algorithmic_bytes": alg, "us_per_launch": round(t * 1e6, 1),
+            "bitops_per_s": round(n * 64 * n / t, 1), "peak_source": src}
+
+
+def measure_e2e(f2, lib, _lib, ctx, torch, A, n, m, mu, world, rank, dist, steps: int) -> dict:
+    """Same metric through the public C-ABI host entry point with host buffers:
+    H2D of A (pinned) + decomposition + D2H of W, perm, r_j inside the region."""
+    host_stride = (n + 7) // 8 * 8
+    lw = A.m // 64 if world > 1 else mu
+    words = torch.empty((lw, host_stride), dtype=torch.int64, pin_memory=True)
+    wout = torch.empty((lw, host_stride), dtype=torch.int64, pin_memory=True)
+    hA = words.numpy().view(np.uint64)
+    hW = wout.numpy().view(np.uint64)
+    # the input as a host matrix in the reference layout
+    _lib.check(lib.f2gpu_mat_download(ctx.handle, A.handle, C.c_void_p(hA.ctypes.data), host_stride))
+    perm = np.zeros(n, np.uint32)
+    rj = np.zeros(mu, np.uint32)
+    rk = C.c_size_t()
+
+    def one():
+        if world > 1:
+            Wd = f2.DeviceMatrix(n, lw * 64, ctx)
+            Wd.upload_words(hA, host_stride)
+            _lib.check(lib.f2gpu_decompose_block_dist(ctx.handle, Wd.handle, m, perm.ctypes.data,
+                                                      rj.ctypes.data, C.byref(rk)))
+            _lib.check(lib.f2gpu_mat_download(ctx.handle, Wd.handle, C.c_void_p(hW.ctypes.data),
+                                              host_stride))
+            Wd.free()
+        else:
+            _lib.check(lib.f2gpu_decompose_block_host(
+                ctx.handle, C.c_void_p(hA.ctypes.data), n, m, host_stride,
+                C.c_void_p(hW.ctypes.data), perm.ctypes.data, rj.ctypes.data, C.byref(rk)))
+
+    one()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / steps
+    if dist:
+        t = torch.tensor([dt], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    hbytes = lw * host_stride * 8
+    return {"value": round(n * n * min(n, m) / dt / 1e9, 1), "unit": UNIT,
+            "h2d_bytes_per_step": hbytes * world,
+            "d2h_bytes_per_step": hbytes * world + 4 * n + 4 * mu,
+            "ms_per_step": round(dt * 1e3, 2), "api": "f2gpu_decompose_block_host" if world == 1
+            else "f2gpu_decompose_block_dist + host upload/download"}
+
+
+def measure_gemm(f2, lib, _lib, ctx, stream, torch) -> dict:
+    """BASELINE configs[1]: C = A*B, A, B 16384^2 (seeds 2, 3), M4RM and Strassen-Winograd."""
+    n = 16384
+    Am, Bm, Cm = (f2.DeviceMatrix(n, n, ctx) for _ in range(3))
+    Am.random_dense(0.5, 2)
+    Bm.random_dense(0.5, 3)
+    out = {}
+    for name, fn in (("m4rm", lambda: _lib.check(lib.f2gpu_m4rm_mult(ctx.handle, Am.handle, Bm.handle, Cm.handle, 0))),
+                     ("strassen", lambda: _lib.check(lib.f2gpu_strassen_mult(ctx.handle, Am.handle, Bm.handle, Cm.handle, 0)))):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(5):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 5 * 1e-3
+        out[name] = {"ms": round(t * 1e3, 3), "Gbitop_s": round(n ** 3 / t / 1e9, 1)}
+    return {"metric": "M4RM GEMM Gbitop/s (n^3/t), 16384^2 (BASELINE configs[1])", **out}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,157 @@
+/*
+ * f2gpu.h — C-ABI of the B200-native GF(2) block decomposition library
+ * (libf2gpu.so, built from paper_1209_5198_b200/csrc/).
+ *
+ * This is the drop-in boundary for the reference's free-function API on
+ * f2la::BitMatrix (= PackedMatrix<uint64_t>, /root/reference/proj/include/f2la/
+ * bit_matrix.hpp:348).  The reference has no FFI of its own: it is a header-only
+ * C++20 library.  Each entry point below names the reference interface it
+ * replaces (file:line); include/f2la_gpu.hpp is the C++ forwarding shim with
+ * the reference's own signatures, and INTEGRATION.md shows the bindings.
+ *
+ * Layout contract (bit_matrix.hpp:74-81): a matrix is n_rows x n_cols bits, as
+ * mu = ceil(n_cols/64) word-columns; word (i, q) is at base[q*col_stride + i];
+ * bit k of word (i,q) is entry (i, 64q+k) (LSB = leftmost column); padding bits
+ * are zero.  Host buffers carry their own col_stride (the reference uses
+ * ceil(n/8)*8, bit_matrix.hpp:330-333); device matrices use a 32-row stride.
+ *
+ * Errors: every function returns an int status.  The codes mirror the
+ * reference's exceptions: F2GPU_EINVAL <-> std::invalid_argument (shape
+ * mismatch, m4rm.hpp:181), F2GPU_ERANGE <-> std::out_of_range (m4rm.hpp:100,145).
+ * f2gpu_last_error() returns a thread-local message for the last failure.
+ *
+ * Threading: a context owns one CUDA device + stream; it is not shared between
+ * host threads (the reference contract is single-threaded per call).
+ * Distinct contexts may be used concurrently.
+ */
+#ifndef F2GPU_H
+#define F2GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define F2GPU_OK 0
+#define F2GPU_EINVAL 1 /* std::invalid_argument */
+#define F2GPU_ERANGE 2 /* std::out_of_range */
+#define F2GPU_ECUDA 3  /* CUDA runtime failure */
+#define F2GPU_ENCCL 4  /* NCCL failure / NCCL not loadable */
+#define F2GPU_ENOMEM 5 /* device allocation failed */
+
+typedef struct f2gpu_ctx f2gpu_ctx; /* device, stream, workspaces, NCCL comm */
+typedef struct f2gpu_mat f2gpu_mat; /* device-resident packed matrix (owning) */
+
+const char *f2gpu_last_error(void);
+const char *f2gpu_version(void);
+
+/* ---- context -------------------------------------------------------------- */
+int f2gpu_ctx_create(int device, f2gpu_ctx **out);
+int f2gpu_ctx_destroy(f2gpu_ctx *ctx);
+/* Run subsequent work on an external stream (e.g. torch's); NULL = own stream. */
+int f2gpu_ctx_set_stream(f2gpu_ctx *ctx, void *cuda_stream);
+int f2gpu_ctx_sync(f2gpu_ctx *ctx);
+/* Kernel launches issued through this context since creation (evidence for
+ * bench.py's gpu_launches). */
+uint64_t f2gpu_ctx_launches(const f2gpu_ctx *ctx);
+/* Tuning knobs: table-group layout is fixed (9 tables, 7x8+8 bits); the
+ * Strassen cutover (minimum dimension in bits below which the M4RM leaf runs;
+ * 0 = default) replaces tuning::strassen_threshold (tuning.hpp:30). */
+int f2gpu_ctx_set_strassen_cutover(f2gpu_ctx *ctx, size_t min_dim_bits);
+
+/* ---- device matrix store (replaces PackedMatrix<uint64_t> storage,
+ *      bit_matrix.hpp:82-346) ------------------------------------------------- */
+int f2gpu_mat_alloc(f2gpu_ctx *ctx, size_t n_rows, size_t n_cols, f2gpu_mat **out);
+int f2gpu_mat_free(f2gpu_mat *m);
+int f2gpu_mat_shape(const f2gpu_mat *m, size_t *n_rows, size_t *n_cols, size_t *col_stride);
+/* raw device pointer to word (0,0) (for interop, e.g. torch.from_blob) */
+int f2gpu_mat_device_ptr(const f2gpu_mat *m, uint64_t **dptr);
+int f2gpu_mat_zero(f2gpu_ctx *ctx, f2gpu_mat *m);
+/* host <-> device; host_stride in words (>= n_rows) */
+int f2gpu_mat_upload(f2gpu_ctx *ctx, f2gpu_mat *m, const uint64_t *host, size_t host_stride);
+int f2gpu_mat_download(f2gpu_ctx *ctx, const f2gpu_mat *m, uint64_t *host, size_t host_stride);
+/* Bit-exact device twin of PackedMatrix::random_dense (bit_matrix.hpp:125-142,
+ * Rng prng.hpp:18-47): entry (i,j) uses xorshift64* draw #(i*m+j). */
+int f2gpu_mat_random_dense(f2gpu_ctx *ctx, f2gpu_mat *m, double density, uint64_t seed);
+/* dst = src (same shape) */
+int f2gpu_mat_copy(f2gpu_ctx *ctx, f2gpu_mat *dst, const f2gpu_mat *src);
+/* dst word-column l = src word-column first + l*step (round-robin column
+ * sharding; scatter=0) or the reverse (scatter=1: src col l -> dst col first+l*step) */
+int f2gpu_mat_select_wcols(f2gpu_ctx *ctx, f2gpu_mat *dst, const f2gpu_mat *src, size_t first,
+                           size_t step, int scatter);
+/* entrywise dst ^= src (xor_with, bit_matrix.hpp:241-250) */
+int f2gpu_mat_xor(f2gpu_ctx *ctx, f2gpu_mat *dst, const f2gpu_mat *src);
+/* out = transpose(a) (transposed, bit_matrix.hpp:220-238); out must be m x n */
+int f2gpu_mat_transpose(f2gpu_ctx *ctx, const f2gpu_mat *a, f2gpu_mat *out);
+
+/* ---- M4RM products (m4rm.hpp:93-196) -------------------------------------- */
+/* C = A*B (m4rm_mult, m4rm.hpp:177-196). C must be a.rows x b.cols.
+ * `c` is the reference's table-size argument; the device kernel uses a fixed
+ * 9-table split (7x8+8 bits) sized for shared memory, so any c is accepted and
+ * results are identical (SPEC.md: "Result independent of the chosen splits"). */
+int f2gpu_m4rm_mult(f2gpu_ctx *ctx, const f2gpu_mat *a, const f2gpu_mat *b, f2gpu_mat *c,
+                    unsigned table_size);
+/* C ^= A*B */
+int f2gpu_m4rm_mult_acc(f2gpu_ctx *ctx, const f2gpu_mat *a, const f2gpu_mat *b, f2gpu_mat *c);
+/* C rows [c_row0, c_row0+n_rows) x word-cols [c_wcol0, c_wcol0+n_wcols)
+ *   ^= a_words * B[b_row0 .. b_row0+k_bits) x word-cols [b_wcol0, +n_wcols)
+ * with a_words a DEVICE array of n_rows words (bits >= k_bits must be zero).
+ * This is mult_acc over build_tables(B, row0, k, wcol0, n) (m4rm.hpp:93-113,
+ * 140-172) as one fused kernel (table build in shared memory + XOR sweep). */
+int f2gpu_mult_acc(f2gpu_ctx *ctx, f2gpu_mat *c, size_t c_row0, size_t c_wcol0,
+                   size_t n_wcols, const uint64_t *d_a_words, size_t n_rows, size_t k_bits,
+                   const f2gpu_mat *b, size_t b_row0, size_t b_wcol0);
+/* Strassen-Winograd over device sub-blocks, M4RM leaves
+ * below the cutover. threshold = 0 -> context cutover. C = A*B. */
+int f2gpu_strassen_mult(f2gpu_ctx *ctx, const f2gpu_mat *a, const f2gpu_mat *b, f2gpu_mat *c,
+                        size_t threshold);
+
+/* ---- decomposition ------------------- */
+/* decompose_block in place: on return `w` holds the overlay W (L below/left of
+ * the block staircase, U on the pivot rows), perm[n_rows]
+ * ((PA)_i = A_{perm[i]}, bit_matrix.hpp:350) and rj[mu] (block ranks) are
+ * written to HOST arrays (either may be NULL), *rank = sum rj. */
+int f2gpu_decompose_block(f2gpu_ctx *ctx, f2gpu_mat *w, uint32_t *perm, uint32_t *rj,
+                          size_t *rank);
+/* Same algorithm, column blocks distributed round-robin over `shards` logical
+ * shards that live on this device (testing the sharded driver on one GPU). */
+int f2gpu_decompose_block_sharded(f2gpu_ctx *ctx, f2gpu_mat *w, int shards, uint32_t *perm,
+                                  uint32_t *rj, size_t *rank);
+/* rank(A): transposes when n_rows < n_cols; a is not modified */
+int f2gpu_rank(f2gpu_ctx *ctx, const f2gpu_mat *a, size_t *rank);
+
+/* ---- host-buffer entry points (what the reference-side shim calls) ---------- */
+int f2gpu_m4rm_mult_host(f2gpu_ctx *ctx, const uint64_t *a, size_t n, size_t k, size_t sa,
+                         const uint64_t *b, size_t m, size_t sb, uint64_t *c, size_t sc,
+                         unsigned table_size);
+int f2gpu_strassen_mult_host(f2gpu_ctx *ctx, const uint64_t *a, size_t n, size_t k, size_t sa,
+                             const uint64_t *b, size_t m, size_t sb, uint64_t *c, size_t sc,
+                             size_t threshold);
+/* decompose a host matrix: w_out receives the overlay (same stride as input) */
+int f2gpu_decompose_block_host(f2gpu_ctx *ctx, const uint64_t *a, size_t n, size_t m,
+                               size_t stride, uint64_t *w_out, uint32_t *perm, uint32_t *rj,
+                               size_t *rank);
+int f2gpu_rank_host(f2gpu_ctx *ctx, const uint64_t *a, size_t n, size_t m, size_t stride,
+                    size_t *rank);
+
+/* ---- multi-GPU (one process per GPU, NCCL over NVLink) ---------------------- */
+/* 128-byte ncclUniqueId, produced on rank 0 and shared by the caller (e.g. via
+ * torch.distributed); NCCL is loaded at run time (dlopen libnccl.so.2). */
+int f2gpu_nccl_unique_id(void *out128);
+int f2gpu_ctx_init_comm(f2gpu_ctx *ctx, int rank, int world, const void *id128);
+/* Distributed decomposition: this rank holds word-columns q = rank, rank+world,
+ * ... of the global n x m matrix as a LOCAL matrix `w_local` (n rows, its local
+ * word-columns packed densely).  Per panel the owner factors and broadcasts
+ * {r_j, transpositions, Y}; every rank updates its own trailing columns.
+ * perm/rj are replicated on every rank. */
+int f2gpu_decompose_block_dist(f2gpu_ctx *ctx, f2gpu_mat *w_local, size_t n_cols_global,
+                               uint32_t *perm, uint32_t *rj, size_t *rank);
+/* number of local word-columns rank `rank` owns out of mu */
+size_t f2gpu_local_wcols(size_t mu, int rank, int world);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

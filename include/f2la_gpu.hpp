@@ -1,0 +1,132 @@
+// f2la_gpu.hpp — C++ forwarding shim: the reference's f2la free-function API,
+// executed by libf2gpu.so (hand-written sm_100a kernels) through the C-ABI in
+// f2gpu.h.  Header-only; include AFTER the reference's "f2la/bit_matrix.hpp".
+//
+//   reference (header-only CPU)                       this shim (B200)
+//   f2la::m4rm_mult(A, B, c)       m4rm.hpp:177-196   f2la::gpu::m4rm_mult(A, B, c)
+//   strassen_mult(A, B, thr, c)    SPEC.md:192-200    f2la::gpu::strassen_mult(A, B, thr, c)
+//   decompose_block(A)->LUFactors  SPEC.md:319-327    f2la::gpu::decompose_block(A)
+//   rank(A)                        SPEC.md:346-353    f2la::gpu::rank(A)
+//
+// Matrices are passed in the reference layout (PackedMatrix<uint64_t>:
+// col_block(q) + col_stride(), bit_matrix.hpp:74-81).  Errors are rethrown as
+// the reference's exception types (std::invalid_argument / std::out_of_range).
+#ifndef F2LA_GPU_HPP
+#define F2LA_GPU_HPP
+
+#include <cstddef>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "f2gpu.h"
+
+namespace f2la::gpu {
+
+inline void check(int rc, const char* what) {
+    if (rc == F2GPU_OK) return;
+    const std::string msg = std::string(what) + ": " + f2gpu_last_error();
+    if (rc == F2GPU_EINVAL) throw std::invalid_argument(msg);
+    if (rc == F2GPU_ERANGE) throw std::out_of_range(msg);
+    throw std::runtime_error(msg);
+}
+
+/// Per-thread default context on device 0 (the reference contract is one call
+/// per thread at a time).
+inline f2gpu_ctx* context() {
+    struct Holder {
+        f2gpu_ctx* c = nullptr;
+        Holder() { check(f2gpu_ctx_create(0, &c), "f2gpu_ctx_create"); }
+        ~Holder() { f2gpu_ctx_destroy(c); }
+    };
+    thread_local Holder h;
+    return h.c;
+}
+
+/// C = A*B over F2 (m4rm.hpp:177-196).  `c` is accepted for signature parity.
+template <class Matrix>
+Matrix m4rm_mult(const Matrix& a, const Matrix& b, std::size_t c = 0) {
+    if (a.cols() != b.rows()) throw std::invalid_argument("m4rm_mult: shape mismatch");
+    Matrix out(a.rows(), b.cols());
+    if (a.rows() == 0 || b.cols() == 0) return out;
+    check(f2gpu_m4rm_mult_host(context(), a.col_block(0), a.rows(), a.cols(), a.col_stride(),
+                               b.col_block(0), b.cols(), b.col_stride(), out.col_block(0),
+                               out.col_stride(), unsigned(c)),
+          "m4rm_mult");
+    return out;
+}
+
+/// Strassen-Winograd with M4RM leaves; threshold 0 = default.
+template <class Matrix>
+Matrix strassen_mult(const Matrix& a, const Matrix& b, std::size_t threshold = 0,
+                     std::size_t /*c*/ = 0) {
+    if (a.cols() != b.rows()) throw std::invalid_argument("strassen_mult: shape mismatch");
+    Matrix out(a.rows(), b.cols());
+    if (a.rows() == 0 || b.cols() == 0) return out;
+    check(f2gpu_strassen_mult_host(context(), a.col_block(0), a.rows(), a.cols(), a.col_stride(),
+                                   b.col_block(0), b.cols(), b.col_stride(), out.col_block(0),
+                                   out.col_stride(), threshold),
+          "strassen_mult");
+    return out;
+}
+
+/// LUFactors + the device overlay W it is derived from.
+template <class Matrix>
+struct LUFactors {
+    std::vector<std::uint32_t> P;      // (P A)_i = A_{P[i]}   (bit_matrix.hpp:350)
+    Matrix L;                          // n x rank, unit lower trapezoidal
+    Matrix U;                          // rank x m, block staircase
+    std::size_t rank = 0;
+    std::vector<std::size_t> block_ranks;
+    Matrix overlay;                    // W: L below/left of the staircase, U on pivot rows
+};
+
+/// decompose_block: P*A = L*U, column-swap free; A unmodified.
+template <class Matrix>
+LUFactors<Matrix> decompose_block(const Matrix& a) {
+    const std::size_t n = a.rows(), m = a.cols(), mu = a.word_cols();
+    LUFactors<Matrix> f;
+    f.overlay = Matrix(n, m);
+    f.P.resize(n);
+    std::vector<std::uint32_t> rj(mu);
+    std::size_t rank = 0;
+    if (n && m)
+        check(f2gpu_decompose_block_host(context(), a.col_block(0), n, m, a.col_stride(),
+                                         f.overlay.col_block(0), f.P.data(), rj.data(), &rank),
+              "decompose_block");
+    else
+        for (std::size_t i = 0; i < n; ++i) f.P[i] = std::uint32_t(i);
+    f.rank = rank;
+    f.block_ranks.assign(rj.begin(), rj.end());
+    f.L = Matrix(n, rank);
+    f.U = Matrix(rank, m);
+    std::size_t R = 0;
+    for (std::size_t j = 0; j < mu; ++j) {
+        const std::size_t r = rj[j];
+        if (!r) continue;
+        for (std::size_t i = R; i < n; ++i) {  // [I_r; Y^(j)] at bit offset R
+            const std::uint64_t bits = i < R + r ? (std::uint64_t(1) << (i - R))
+                                                 : f.overlay.word(i, j);
+            xor_bits_at(f.L, i, R, bits);  // reference helper, bit_matrix.hpp:402-413
+        }
+        for (std::size_t q = j; q < mu; ++q)
+            for (std::size_t t = 0; t < r; ++t) f.U.word(R + t, q) = f.overlay.word(R + t, q);
+        R += r;
+    }
+    return f;
+}
+
+/// rank(A) = sum r_j, transposing wide inputs.
+template <class Matrix>
+std::size_t rank(const Matrix& a) {
+    std::size_t r = 0;
+    if (a.rows() && a.cols())
+        check(f2gpu_rank_host(context(), a.col_block(0), a.rows(), a.cols(), a.col_stride(), &r),
+              "rank");
+    return r;
+}
+
+}  // namespace f2la::gpu
+
+#endif

@@ -1,0 +1,815 @@
+// api.cu — C-ABI (include/f2gpu.h) and the native host drivers:
+//   * device matrix store (PackedMatrix<uint64_t> analogue, bit_matrix.hpp:82-346)
+//   * decompose_block driver: per panel  buildZ -> swaps -> Y -> Schur,
+//     all enqueued without host synchronisation (R and r_j stay on the device)
+//   * sharded / distributed driver: word-columns round-robin over shards, the
+//     panel owner broadcasts {PanelState, panel column} (NCCL over NVLink)
+//   * Strassen-Winograd recursion over device sub-blocks
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <deque>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/f2gpu.h"
+#include "kernels.cuh"
+
+#define F2GPU_VERSION "0.1.0"
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                    \
+    do {                                                                                  \
+        cudaError_t _e = (expr);                                                          \
+        if (_e != cudaSuccess)                                                            \
+            return set_err(_e == cudaErrorMemoryAllocation ? F2GPU_ENOMEM : F2GPU_ECUDA, \
+                           std::string(#expr) + ": " + cudaGetErrorString(_e));           \
+    } while (0)
+
+#define F2_TRY(expr)                   \
+    do {                               \
+        int _rc = (expr);              \
+        if (_rc != F2GPU_OK) return _rc; \
+    } while (0)
+
+size_t ceil64(size_t x) { return (x + 63) / 64; }
+size_t dev_stride(size_t rows) { return std::max<size_t>(32, (rows + 31) / 32 * 32); }
+
+// ---- NCCL, loaded at run time --------------------------------------------
+struct Id128 { char b[128]; };  // ncclUniqueId (NCCL_UNIQUE_ID_BYTES = 128), passed by value
+typedef int (*CommInitRankFn)(void**, int, Id128, int);
+
+struct NcclApi {
+    void* h = nullptr;
+    int (*getUniqueId)(void*) = nullptr;
+    void* commInitRankSym = nullptr;
+    int (*broadcast)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*commDestroy)(void*) = nullptr;
+    const char* (*getErrorString)(int) = nullptr;
+    bool ok = false;
+    std::string why;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        const char* names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char* nm : names) {
+            api.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+            if (api.h) break;
+        }
+        if (!api.h) {
+            api.why = std::string("dlopen libnccl.so.2 failed: ") + dlerror();
+            return api;
+        }
+        api.getUniqueId = (int (*)(void*))dlsym(api.h, "ncclGetUniqueId");
+        api.commInitRankSym = dlsym(api.h, "ncclCommInitRank");
+        api.broadcast = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(
+            api.h, "ncclBroadcast");
+        api.commDestroy = (int (*)(void*))dlsym(api.h, "ncclCommDestroy");
+        api.getErrorString = (const char* (*)(int))dlsym(api.h, "ncclGetErrorString");
+        api.ok = api.getUniqueId && api.commInitRankSym && api.broadcast && api.commDestroy;
+        if (!api.ok) api.why = "libnccl.so.2 lacks required symbols";
+    }
+    return api;
+}
+
+constexpr int kNcclUint8 = 1;  // ncclDataType_t ncclUint8 (nccl.h)
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct f2gpu_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    uint64_t* d_jump = nullptr;
+    uint64_t launches = 0;
+    size_t strassen_cutover = 8192;
+    void* comm = nullptr;
+    int rank = 0, world = 1;
+};
+
+struct f2gpu_mat {
+    f2gpu_ctx* ctx = nullptr;
+    uint64_t* d = nullptr;
+    size_t rows = 0, cols = 0, stride = 0;
+};
+
+namespace {
+
+struct View {  // non-owning device sub-block: rows x cols bits, word (i,q) at p[q*stride+i]
+    uint64_t* p;
+    size_t rows, cols, stride;
+    size_t wcols() const { return ceil64(cols); }
+    View sub(size_t r0, size_t nr, size_t wc0, size_t nwc) const {
+        return View{p + wc0 * stride + r0, nr, nwc * 64, stride};
+    }
+};
+
+View view_of(const f2gpu_mat* m) { return View{m->d, m->rows, m->cols, m->stride}; }
+
+int count(f2gpu_ctx* c, int n = 1) {
+    c->launches += uint64_t(n);
+    return F2GPU_OK;
+}
+
+int check_launch(f2gpu_ctx* c, cudaError_t e, const char* what) {
+    if (e != cudaSuccess) return set_err(F2GPU_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return count(c);
+}
+
+int dev_alloc(f2gpu_ctx* c, void** p, size_t bytes) {
+    if (bytes == 0) bytes = 8;
+    cudaError_t e = cudaMallocAsync(p, bytes, c->stream);
+    if (e != cudaSuccess) return set_err(F2GPU_ENOMEM, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+    return F2GPU_OK;
+}
+void dev_free(f2gpu_ctx* c, void* p) {
+    if (p) cudaFreeAsync(p, c->stream);
+}
+
+struct DevBuf {  // RAII stream-ordered allocation
+    f2gpu_ctx* c;
+    void* p = nullptr;
+    explicit DevBuf(f2gpu_ctx* cc) : c(cc) {}
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { dev_free(c, p); }
+    int alloc(size_t bytes) { return dev_alloc(c, &p, bytes); }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+// C ^= A*B on views (stream-K M4RM kernel)
+int gemm_acc(f2gpu_ctx* c, View C, View A, View B) {
+    if (A.rows == 0 || A.cols == 0 || B.cols == 0) return F2GPU_OK;
+    f2::GemmArgs g{A.p, A.stride, A.rows, B.p, B.stride, A.cols, C.p, C.stride, int(C.wcols())};
+    return check_launch(c, f2::launch_gemm(g, c->num_sms, c->stream), "k_gemm");
+}
+
+int xor_views(f2gpu_ctx* c, View dst, bool acc, const View* a, const View* b = nullptr,
+              const View* cc = nullptr, const View* d = nullptr) {
+    return check_launch(
+        c,
+        f2::launch_xor(dst.p, dst.stride, a ? a->p : nullptr, a ? a->stride : 0, b ? b->p : nullptr,
+                       b ? b->stride : 0, cc ? cc->p : nullptr, cc ? cc->stride : 0,
+                       d ? d->p : nullptr, d ? d->stride : 0, dst.rows, dst.wcols(), acc,
+                       c->stream),
+        "k_xor");
+}
+
+int zero_view(f2gpu_ctx* c, View v) {
+    if (v.rows == 0 || v.wcols() == 0) return F2GPU_OK;
+    CUDA_TRY(cudaMemset2DAsync(v.p, v.stride * 8, 0, v.rows * 8, v.wcols(), c->stream));
+    return F2GPU_OK;
+}
+
+// Strassen-Winograd, C ^= A*B (7 products, Winograd's schedule over F2; SPEC.md:184-232,
+// PAPER.md:1474-1499).  Recurses while every dimension is >= cutover and halves
+// stay word-aligned (multiples of 64 rows/bits); otherwise the M4RM leaf runs.
+int strassen_acc(f2gpu_ctx* c, View C, View A, View B, size_t cutover) {
+    const size_t n = A.rows, k = A.cols, m = B.cols;
+    const bool split = n >= cutover && k >= cutover && m >= cutover && n % 128 == 0 &&
+                       k % 128 == 0 && m % 128 == 0 && cutover >= 128;
+    if (!split) return gemm_acc(c, C, A, B);
+    const size_t n2 = n / 2, k2 = k / 2, m2 = m / 2;
+    const size_t kw = k2 / 64, mw = m2 / 64;
+    View A11 = A.sub(0, n2, 0, kw), A12 = A.sub(0, n2, kw, kw);
+    View A21 = A.sub(n2, n2, 0, kw), A22 = A.sub(n2, n2, kw, kw);
+    View B11 = B.sub(0, k2, 0, mw), B12 = B.sub(0, k2, mw, mw);
+    View B21 = B.sub(k2, k2, 0, mw), B22 = B.sub(k2, k2, mw, mw);
+    View C11 = C.sub(0, n2, 0, mw), C12 = C.sub(0, n2, mw, mw);
+    View C21 = C.sub(n2, n2, 0, mw), C22 = C.sub(n2, n2, mw, mw);
+    DevBuf sb(c), tb(c), qb(c);
+    const size_t ss = dev_stride(n2), ts = dev_stride(k2), qs = dev_stride(n2);
+    F2_TRY(sb.alloc(ss * kw * 8));
+    F2_TRY(tb.alloc(ts * mw * 8));
+    F2_TRY(qb.alloc(qs * mw * 8));
+    View S{sb.as<uint64_t>(), n2, k2, ss}, T{tb.as<uint64_t>(), k2, m2, ts},
+        Q{qb.as<uint64_t>(), n2, m2, qs};
+    // Q = P1 = A11 B11 ; C11 ^= P1 ; C11 ^= P2 = A12 B21
+    F2_TRY(zero_view(c, Q));
+    F2_TRY(strassen_acc(c, Q, A11, B11, cutover));
+    F2_TRY(xor_views(c, C11, true, &Q));
+    F2_TRY(strassen_acc(c, C11, A12, B21, cutover));
+    // S2 = A21+A22+A11, T2 = B22+B12+B11 ; Q ^= P6 -> U2 = P1+P6 ; into C12, C21, C22
+    F2_TRY(xor_views(c, S, false, &A21, &A22, &A11));
+    F2_TRY(xor_views(c, T, false, &B22, &B12, &B11));
+    F2_TRY(strassen_acc(c, Q, S, T, cutover));
+    F2_TRY(xor_views(c, C12, true, &Q));
+    F2_TRY(xor_views(c, C21, true, &Q));
+    F2_TRY(xor_views(c, C22, true, &Q));
+    // P7 = S3 T3, S3 = A11+A21, T3 = B22+B12 -> C21, C22
+    F2_TRY(xor_views(c, S, false, &A11, &A21));
+    F2_TRY(xor_views(c, T, false, &B22, &B12));
+    F2_TRY(zero_view(c, Q));
+    F2_TRY(strassen_acc(c, Q, S, T, cutover));
+    F2_TRY(xor_views(c, C21, true, &Q));
+    F2_TRY(xor_views(c, C22, true, &Q));
+    // P5 = S1 T1, S1 = A21+A22, T1 = B12+B11 -> C12, C22
+    F2_TRY(xor_views(c, S, false, &A21, &A22));
+    F2_TRY(xor_views(c, T, false, &B12, &B11));
+    F2_TRY(zero_view(c, Q));
+    F2_TRY(strassen_acc(c, Q, S, T, cutover));
+    F2_TRY(xor_views(c, C12, true, &Q));
+    F2_TRY(xor_views(c, C22, true, &Q));
+    // P3 = S4 B22, S4 = A12+S2 = A11+A12+A21+A22 -> C12
+    F2_TRY(xor_views(c, S, false, &A11, &A12, &A21, &A22));
+    F2_TRY(strassen_acc(c, C12, S, B22, cutover));
+    // P4 = A22 T4, T4 = T2+B21 = B11+B12+B21+B22 -> C21
+    F2_TRY(xor_views(c, T, false, &B11, &B12, &B21, &B22));
+    F2_TRY(strassen_acc(c, C21, A22, T, cutover));
+    return F2GPU_OK;
+}
+
+// ---- decomposition drivers -------------------------------------------------
+
+// One logical shard: a local packed matrix of the word-columns it owns.
+struct Shard {
+    View w;                      // n rows x (local wcols * 64)
+    size_t lw = 0;               // local word-columns
+    f2::PanelState* st = nullptr;  // mu states (device)
+    uint32_t* perm = nullptr;    // device perm (replicated)
+    uint64_t* bcast = nullptr;   // [PanelState | n words] broadcast landing buffer
+};
+
+constexpr size_t kStateBytes = sizeof(f2::PanelState);
+constexpr size_t kBcastHdr = 2048;  // state padded
+
+// first local column whose global index is > j, for shard g of G
+size_t first_local_after(size_t j, int g, int G) {
+    if (j + 1 <= size_t(g)) return 0;
+    return (j - size_t(g)) / size_t(G) + 1;
+}
+
+// Enqueue one panel step of the single-shard (G=1) decomposition.
+int step_single(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t j) {
+    uint64_t* colj = s.w.p + j * s.w.stride;
+    F2_TRY(check_launch(c, f2::launch_panel(colj, n, s.st, int(j), c->stream), "k_panel"));
+    F2_TRY(check_launch(c, f2::launch_swaps(s.w.p, s.w.stride, int(mu), int(j), s.perm, s.st + j,
+                                            c->stream),
+                        "k_swaps"));
+    F2_TRY(check_launch(c, f2::launch_panel_y(colj, n, s.st + j, c->num_sms, c->stream),
+                        "k_panel_y"));
+    if (j + 1 < mu) {
+        f2::UpdateArgs u{};
+        u.C = s.w.p; u.sc = s.w.stride; u.c_wcol0 = j + 1; u.ncols = int(mu - j - 1);
+        u.row_lo = 0; u.row_hi = n; u.a = colj; u.k_bits = 0;
+        u.B = s.w.p; u.sb = s.w.stride; u.b_row0 = 0; u.b_wcol0 = j + 1;
+        u.st = s.st + j;
+        F2_TRY(check_launch(c, f2::launch_update(u, c->num_sms, c->stream), "k_update"));
+    }
+    return F2GPU_OK;
+}
+
+int read_results(f2gpu_ctx* c, const Shard& s, size_t n, size_t mu, uint32_t* perm,
+                 uint32_t* rj, size_t* rank) {
+    std::vector<f2::PanelState> hs(mu);
+    if (mu)
+        CUDA_TRY(cudaMemcpyAsync(hs.data(), s.st, mu * kStateBytes, cudaMemcpyDeviceToHost,
+                                 c->stream));
+    if (perm && n)
+        CUDA_TRY(cudaMemcpyAsync(perm, s.perm, n * 4, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    size_t tot = 0;
+    for (size_t j = 0; j < mu; ++j) {
+        if (rj) rj[j] = hs[j].r;
+        tot += hs[j].r;
+    }
+    if (rank) *rank = tot;
+    return F2GPU_OK;
+}
+
+int decompose_single(f2gpu_ctx* c, View w, uint32_t* perm, uint32_t* rj, size_t* rank) {
+    const size_t n = w.rows, mu = w.wcols();
+    if (n == 0 || mu == 0) {
+        if (rank) *rank = 0;
+        if (rj) std::fill(rj, rj + mu, 0u);
+        if (perm) for (size_t i = 0; i < n; ++i) perm[i] = uint32_t(i);
+        return F2GPU_OK;
+    }
+    DevBuf stb(c), pb(c);
+    F2_TRY(stb.alloc(mu * kStateBytes));
+    F2_TRY(pb.alloc(n * 4));
+    Shard s;
+    s.w = w; s.lw = mu; s.st = stb.as<f2::PanelState>(); s.perm = pb.as<uint32_t>();
+    F2_TRY(check_launch(c, f2::launch_iota(s.perm, n, c->stream), "k_iota"));
+    for (size_t j = 0; j < mu; ++j) F2_TRY(step_single(c, s, n, mu, j));
+    return read_results(c, s, n, mu, perm, rj, rank);
+}
+
+// Broadcast hook: copies the owner's {state j, panel column} into every
+// shard's landing buffer.  Virtual shards: device-to-device copies; NCCL: one
+// ncclBroadcast of the header + column from the owner rank.
+struct Exchange {
+    virtual ~Exchange() = default;
+    virtual int bcast(f2gpu_ctx* c, std::vector<Shard>& sh, int owner_local, int owner_global,
+                      size_t n) = 0;
+};
+
+struct LocalExchange : Exchange {
+    int bcast(f2gpu_ctx* c, std::vector<Shard>& sh, int owner, int, size_t n) override {
+        const size_t bytes = kBcastHdr + n * 8;
+        for (size_t g = 0; g < sh.size(); ++g) {
+            if (int(g) == owner) continue;
+            CUDA_TRY(cudaMemcpyAsync(sh[g].bcast, sh[owner].bcast, bytes,
+                                     cudaMemcpyDeviceToDevice, c->stream));
+        }
+        return F2GPU_OK;
+    }
+};
+
+struct NcclExchange : Exchange {
+    int bcast(f2gpu_ctx* c, std::vector<Shard>& sh, int, int owner_global, size_t n) override {
+        NcclApi& api = nccl();
+        const size_t bytes = kBcastHdr + n * 8;
+        int rc = api.broadcast(sh[0].bcast, sh[0].bcast, bytes, kNcclUint8, owner_global, c->comm,
+                               c->stream);
+        if (rc != 0)
+            return set_err(F2GPU_ENCCL, std::string("ncclBroadcast: ") +
+                                            (api.getErrorString ? api.getErrorString(rc) : "?"));
+        return F2GPU_OK;
+    }
+};
+
+// Sharded driver. `sh` holds the shards living in this process; global shard
+// index of sh[i] is shard_base + i; G = total shards.
+int decompose_sharded(f2gpu_ctx* c, std::vector<Shard>& sh, int shard_base, int G, size_t n,
+                      size_t mu, Exchange& ex) {
+    for (auto& s : sh) F2_TRY(check_launch(c, f2::launch_iota(s.perm, n, c->stream), "k_iota"));
+    for (size_t j = 0; j < mu; ++j) {
+        const int owner = int(j % size_t(G));
+        const size_t lj = j / size_t(G);
+        const int ol = owner - shard_base;  // local index of the owner (may be out of range)
+        const bool have_owner = ol >= 0 && ol < int(sh.size());
+        if (have_owner) {
+            Shard& o = sh[ol];
+            uint64_t* colj = o.w.p + lj * o.w.stride;
+            F2_TRY(check_launch(c, f2::launch_panel(colj, n, o.st, int(j), c->stream), "k_panel"));
+            F2_TRY(check_launch(c, f2::launch_swaps(o.w.p, o.w.stride, int(o.lw), int(lj), o.perm,
+                                                    o.st + j, c->stream),
+                                "k_swaps"));
+            F2_TRY(check_launch(c, f2::launch_panel_y(colj, n, o.st + j, c->num_sms, c->stream),
+                                "k_panel_y"));
+            CUDA_TRY(cudaMemcpyAsync(o.bcast, o.st + j, kStateBytes, cudaMemcpyDeviceToDevice,
+                                     c->stream));
+            CUDA_TRY(cudaMemcpyAsync(o.bcast + kBcastHdr / 8, colj, n * 8,
+                                     cudaMemcpyDeviceToDevice, c->stream));
+        }
+        F2_TRY(ex.bcast(c, sh, ol, owner, n));
+        for (size_t g = 0; g < sh.size(); ++g) {
+            Shard& s = sh[g];
+            const int gg = shard_base + int(g);
+            const f2::PanelState* stj = s.st + j;
+            if (gg != owner) {
+                CUDA_TRY(cudaMemcpyAsync(s.st + j, s.bcast, kStateBytes, cudaMemcpyDeviceToDevice,
+                                         c->stream));
+                F2_TRY(check_launch(c, f2::launch_swaps(s.w.p, s.w.stride, int(s.lw), -1, s.perm,
+                                                        stj, c->stream),
+                                    "k_swaps"));
+            }
+            const size_t l0 = first_local_after(j, gg, G);
+            if (l0 < s.lw) {
+                f2::UpdateArgs u{};
+                u.C = s.w.p; u.sc = s.w.stride; u.c_wcol0 = l0; u.ncols = int(s.lw - l0);
+                u.row_lo = 0; u.row_hi = n;
+                u.a = (gg == owner) ? s.w.p + lj * s.w.stride : s.bcast + kBcastHdr / 8;
+                u.B = s.w.p; u.sb = s.w.stride; u.b_wcol0 = l0;
+                u.st = stj;
+                F2_TRY(check_launch(c, f2::launch_update(u, c->num_sms, c->stream), "k_update"));
+            }
+        }
+    }
+    return F2GPU_OK;
+}
+
+int alloc_shard_aux(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, std::deque<DevBuf>& keep) {
+    keep.emplace_back(c);
+    F2_TRY(keep.back().alloc(mu * kStateBytes));
+    s.st = keep.back().as<f2::PanelState>();
+    keep.emplace_back(c);
+    F2_TRY(keep.back().alloc(n * 4));
+    s.perm = keep.back().as<uint32_t>();
+    keep.emplace_back(c);
+    F2_TRY(keep.back().alloc(kBcastHdr + n * 8));
+    s.bcast = keep.back().as<uint64_t>();
+    return F2GPU_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+const char* f2gpu_last_error(void) { return g_err.c_str(); }
+const char* f2gpu_version(void) { return F2GPU_VERSION " sm_100a"; }
+
+int f2gpu_ctx_create(int device, f2gpu_ctx** out) {
+    if (!out) return set_err(F2GPU_EINVAL, "ctx_create: null out");
+    *out = nullptr;
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return set_err(F2GPU_ERANGE, "ctx_create: device index");
+    CUDA_TRY(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return set_err(F2GPU_ECUDA, std::string("libf2gpu is built for sm_100a (B200); device is ") +
+                                        prop.name);
+    auto c = std::make_unique<f2gpu_ctx>();
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+    c->stream = c->own_stream;
+    CUDA_TRY(f2::init_kernel_attrs());
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    uint64_t jt[64 * 64];
+    f2::host_jump_tables(jt);
+    CUDA_TRY(cudaMalloc(&c->d_jump, sizeof(jt)));
+    CUDA_TRY(cudaMemcpy(c->d_jump, jt, sizeof(jt), cudaMemcpyHostToDevice));
+    *out = c.release();
+    return F2GPU_OK;
+}
+
+int f2gpu_ctx_destroy(f2gpu_ctx* c) {
+    if (!c) return F2GPU_OK;
+    cudaSetDevice(c->device);
+    if (c->comm && nccl().ok) nccl().commDestroy(c->comm);
+    if (c->own_stream) cudaStreamSynchronize(c->own_stream);
+    cudaFree(c->d_jump);
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    delete c;
+    return F2GPU_OK;
+}
+
+int f2gpu_ctx_set_stream(f2gpu_ctx* c, void* s) {
+    if (!c) return set_err(F2GPU_EINVAL, "null ctx");
+    c->stream = s ? static_cast<cudaStream_t>(s) : c->own_stream;
+    return F2GPU_OK;
+}
+
+int f2gpu_ctx_sync(f2gpu_ctx* c) {
+    if (!c) return set_err(F2GPU_EINVAL, "null ctx");
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return F2GPU_OK;
+}
+
+uint64_t f2gpu_ctx_launches(const f2gpu_ctx* c) { return c ? c->launches : 0; }
+
+int f2gpu_ctx_set_strassen_cutover(f2gpu_ctx* c, size_t v) {
+    if (!c) return set_err(F2GPU_EINVAL, "null ctx");
+    c->strassen_cutover = v ? v : 8192;
+    return F2GPU_OK;
+}
+
+// ---- matrices ----
+int f2gpu_mat_alloc(f2gpu_ctx* c, size_t n, size_t m, f2gpu_mat** out) {
+    if (!c || !out) return set_err(F2GPU_EINVAL, "mat_alloc: null argument");
+    *out = nullptr;
+    auto M = std::make_unique<f2gpu_mat>();
+    M->ctx = c; M->rows = n; M->cols = m; M->stride = dev_stride(n);
+    const size_t words = ceil64(m) * M->stride;
+    if (words) {
+        cudaError_t e = cudaMalloc(&M->d, words * 8);
+        if (e != cudaSuccess) return set_err(F2GPU_ENOMEM, std::string("mat_alloc: ") + cudaGetErrorString(e));
+        CUDA_TRY(cudaMemsetAsync(M->d, 0, words * 8, c->stream));
+    }
+    *out = M.release();
+    return F2GPU_OK;
+}
+
+int f2gpu_mat_free(f2gpu_mat* m) {
+    if (!m) return F2GPU_OK;
+    if (m->d) {
+        cudaStreamSynchronize(m->ctx->stream);
+        cudaFree(m->d);
+    }
+    delete m;
+    return F2GPU_OK;
+}
+
+int f2gpu_mat_shape(const f2gpu_mat* m, size_t* r, size_t* cc, size_t* s) {
+    if (!m) return set_err(F2GPU_EINVAL, "null mat");
+    if (r) *r = m->rows;
+    if (cc) *cc = m->cols;
+    if (s) *s = m->stride;
+    return F2GPU_OK;
+}
+
+int f2gpu_mat_device_ptr(const f2gpu_mat* m, uint64_t** p) {
+    if (!m || !p) return set_err(F2GPU_EINVAL, "null argument");
+    *p = m->d;
+    return F2GPU_OK;
+}
+
+int f2gpu_mat_zero(f2gpu_ctx* c, f2gpu_mat* m) {
+    if (!c || !m) return set_err(F2GPU_EINVAL, "null argument");
+    if (m->d) CUDA_TRY(cudaMemsetAsync(m->d, 0, ceil64(m->cols) * m->stride * 8, c->stream));
+    return F2GPU_OK;
+}
+
+int f2gpu_mat_upload(f2gpu_ctx* c, f2gpu_mat* m, const uint64_t* h, size_t hs) {
+    if (!c || !m || (!h && m->rows && m->cols)) return set_err(F2GPU_EINVAL, "mat_upload: null argument");
+    if (m->rows == 0 || m->cols == 0) return F2GPU_OK;
+    if (hs < m->rows) return set_err(F2GPU_EINVAL, "mat_upload: host stride < rows");
+    CUDA_TRY(cudaMemcpy2DAsync(m->d, m->stride * 8, h, hs * 8, m->rows * 8, ceil64(m->cols),
+                               cudaMemcpyHostToDevice, c->stream));
+    return F2GPU_OK;
+}
+
+int f2gpu_mat_download(f2gpu_ctx* c, const f2gpu_mat* m, uint64_t* h, size_t hs) {
+    if (!c || !m || (!h && m->rows && m->cols)) return set_err(F2GPU_EINVAL, "mat_download: null argument");
+    if (m->rows == 0 || m->cols == 0) return F2GPU_OK;
+    if (hs < m->rows) return set_err(F2GPU_EINVAL, "mat_download: host stride < rows");
+    CUDA_TRY(cudaMemcpy2DAsync(h, hs * 8, m->d, m->stride * 8, m->rows * 8, ceil64(m->cols),
+                               cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return F2GPU_OK;
+}
+
+int f2gpu_mat_random_dense(f2gpu_ctx* c, f2gpu_mat* m, double density, uint64_t seed) {
+    if (!c || !m) return set_err(F2GPU_EINVAL, "null argument");
+    return check_launch(c, f2::launch_random_dense(m->d, m->rows, m->cols, m->stride, density, seed,
+                                                   c->d_jump, c->stream),
+                        "k_random_dense");
+}
+
+int f2gpu_mat_copy(f2gpu_ctx* c, f2gpu_mat* dst, const f2gpu_mat* src) {
+    if (!c || !dst || !src) return set_err(F2GPU_EINVAL, "null argument");
+    if (dst->rows != src->rows || dst->cols != src->cols)
+        return set_err(F2GPU_EINVAL, "mat_copy: shape mismatch");
+    if (dst->d && src->d)
+        CUDA_TRY(cudaMemcpy2DAsync(dst->d, dst->stride * 8, src->d, src->stride * 8, src->rows * 8,
+                                   ceil64(src->cols), cudaMemcpyDeviceToDevice, c->stream));
+    return F2GPU_OK;
+}
+
+int f2gpu_mat_select_wcols(f2gpu_ctx* c, f2gpu_mat* dst, const f2gpu_mat* src, size_t first,
+                           size_t step, int scatter) {
+    if (!c || !dst || !src) return set_err(F2GPU_EINVAL, "null argument");
+    if (dst->rows != src->rows || step == 0) return set_err(F2GPU_EINVAL, "select_wcols: shape");
+    const f2gpu_mat* loc = scatter ? src : dst;   // the strided-over (local) side
+    const f2gpu_mat* glob = scatter ? dst : src;
+    const size_t nl = ceil64(loc->cols);
+    if (nl && first + (nl - 1) * step >= ceil64(glob->cols))
+        return set_err(F2GPU_ERANGE, "select_wcols: column outside matrix");
+    if (!nl || !src->rows) return F2GPU_OK;
+    // one strided 2D copy: rows*8 bytes per word-column, pitch step*stride on the global side
+    if (scatter)
+        CUDA_TRY(cudaMemcpy2DAsync(dst->d + first * dst->stride, step * dst->stride * 8, src->d,
+                                   src->stride * 8, src->rows * 8, nl, cudaMemcpyDeviceToDevice,
+                                   c->stream));
+    else
+        CUDA_TRY(cudaMemcpy2DAsync(dst->d, dst->stride * 8, src->d + first * src->stride,
+                                   step * src->stride * 8, src->rows * 8, nl,
+                                   cudaMemcpyDeviceToDevice, c->stream));
+    return F2GPU_OK;
+}
+
+int f2gpu_mat_xor(f2gpu_ctx* c, f2gpu_mat* dst, const f2gpu_mat* src) {
+    if (!c || !dst || !src) return set_err(F2GPU_EINVAL, "null argument");
+    if (dst->rows != src->rows || dst->cols != src->cols)
+        return set_err(F2GPU_EINVAL, "xor_with: shape mismatch");  // bit_matrix.hpp:243
+    View s = view_of(src);
+    return xor_views(c, view_of(dst), true, &s);
+}
+
+int f2gpu_mat_transpose(f2gpu_ctx* c, const f2gpu_mat* a, f2gpu_mat* out) {
+    if (!c || !a || !out) return set_err(F2GPU_EINVAL, "null argument");
+    if (out->rows != a->cols || out->cols != a->rows)
+        return set_err(F2GPU_EINVAL, "transpose: output shape");
+    return check_launch(c, f2::launch_transpose(a->d, a->rows, a->cols, a->stride, out->d,
+                                                out->stride, c->stream),
+                        "k_transpose");
+}
+
+// ---- products ----
+int f2gpu_m4rm_mult_acc(f2gpu_ctx* c, const f2gpu_mat* a, const f2gpu_mat* b, f2gpu_mat* cm) {
+    if (!c || !a || !b || !cm) return set_err(F2GPU_EINVAL, "null argument");
+    if (a->cols != b->rows) return set_err(F2GPU_EINVAL, "m4rm_mult: shape mismatch");  // m4rm.hpp:181
+    if (cm->rows != a->rows || cm->cols != b->cols)
+        return set_err(F2GPU_EINVAL, "m4rm_mult: output shape mismatch");
+    return gemm_acc(c, view_of(cm), view_of(a), view_of(b));
+}
+
+int f2gpu_m4rm_mult(f2gpu_ctx* c, const f2gpu_mat* a, const f2gpu_mat* b, f2gpu_mat* cm,
+                    unsigned) {
+    if (!c || !a || !b || !cm) return set_err(F2GPU_EINVAL, "null argument");
+    if (a->cols != b->rows) return set_err(F2GPU_EINVAL, "m4rm_mult: shape mismatch");
+    if (cm->rows != a->rows || cm->cols != b->cols)
+        return set_err(F2GPU_EINVAL, "m4rm_mult: output shape mismatch");
+    F2_TRY(f2gpu_mat_zero(c, cm));
+    return gemm_acc(c, view_of(cm), view_of(a), view_of(b));
+}
+
+int f2gpu_mult_acc(f2gpu_ctx* c, f2gpu_mat* cm, size_t c_row0, size_t c_wcol0, size_t n_wcols,
+                   const uint64_t* d_a, size_t n_rows, size_t k_bits, const f2gpu_mat* b,
+                   size_t b_row0, size_t b_wcol0) {
+    if (!c || !cm || !b || (!d_a && n_rows)) return set_err(F2GPU_EINVAL, "null argument");
+    if (k_bits > 64) return set_err(F2GPU_EINVAL, "build_tables: block taller than a word");  // m4rm.hpp:97-98
+    if (b_row0 + k_bits > b->rows || b_wcol0 + n_wcols > ceil64(b->cols))
+        return set_err(F2GPU_ERANGE, "build_tables: block outside B");  // m4rm.hpp:99-100
+    if (c_row0 + n_rows > cm->rows || c_wcol0 + n_wcols > ceil64(cm->cols))
+        return set_err(F2GPU_ERANGE, "mult_acc: destination outside C");  // m4rm.hpp:144-145
+    if (n_rows == 0 || n_wcols == 0 || k_bits == 0) return F2GPU_OK;
+    f2::UpdateArgs u{};
+    u.C = cm->d; u.sc = cm->stride; u.c_wcol0 = c_wcol0; u.ncols = int(n_wcols);
+    u.row_lo = c_row0; u.row_hi = c_row0 + n_rows;
+    u.a = d_a - c_row0;
+    u.k_bits = int(k_bits);
+    u.B = b->d; u.sb = b->stride; u.b_row0 = b_row0; u.b_wcol0 = b_wcol0;
+    u.st = nullptr;
+    return check_launch(c, f2::launch_update(u, c->num_sms, c->stream), "k_update");
+}
+
+int f2gpu_strassen_mult(f2gpu_ctx* c, const f2gpu_mat* a, const f2gpu_mat* b, f2gpu_mat* cm,
+                        size_t threshold) {
+    if (!c || !a || !b || !cm) return set_err(F2GPU_EINVAL, "null argument");
+    if (a->cols != b->rows) return set_err(F2GPU_EINVAL, "strassen_mult: shape mismatch");
+    if (cm->rows != a->rows || cm->cols != b->cols)
+        return set_err(F2GPU_EINVAL, "strassen_mult: output shape mismatch");
+    F2_TRY(f2gpu_mat_zero(c, cm));
+    return strassen_acc(c, view_of(cm), view_of(a), view_of(b),
+                        threshold ? threshold : c->strassen_cutover);
+}
+
+// ---- decomposition ----
+int f2gpu_decompose_block(f2gpu_ctx* c, f2gpu_mat* w, uint32_t* perm, uint32_t* rj, size_t* rank) {
+    if (!c || !w) return set_err(F2GPU_EINVAL, "null argument");
+    if (w->rows > 0xFFFFFFF0ull) return set_err(F2GPU_ERANGE, "decompose: too many rows for uint32 perm");
+    return decompose_single(c, view_of(w), perm, rj, rank);
+}
+
+int f2gpu_decompose_block_sharded(f2gpu_ctx* c, f2gpu_mat* w, int G, uint32_t* perm, uint32_t* rj,
+                                  size_t* rank) {
+    if (!c || !w) return set_err(F2GPU_EINVAL, "null argument");
+    if (G < 1) return set_err(F2GPU_EINVAL, "shards must be >= 1");
+    const size_t n = w->rows, mu = ceil64(w->cols);
+    if (n == 0 || mu == 0) return decompose_single(c, view_of(w), perm, rj, rank);
+    // scatter word-columns round-robin into G local matrices
+    std::deque<DevBuf> keep;
+    std::vector<Shard> sh(G);
+    for (int g = 0; g < G; ++g) {
+        sh[g].lw = f2gpu_local_wcols(mu, g, G);
+        keep.emplace_back(c);
+        F2_TRY(keep.back().alloc(std::max<size_t>(1, sh[g].lw) * w->stride * 8));
+        sh[g].w = View{keep.back().as<uint64_t>(), n, sh[g].lw * 64, w->stride};
+        for (size_t l = 0; l < sh[g].lw; ++l)
+            CUDA_TRY(cudaMemcpyAsync(sh[g].w.p + l * w->stride, w->d + (g + l * G) * w->stride,
+                                     w->stride * 8, cudaMemcpyDeviceToDevice, c->stream));
+        F2_TRY(alloc_shard_aux(c, sh[g], n, mu, keep));
+    }
+    LocalExchange ex;
+    F2_TRY(decompose_sharded(c, sh, 0, G, n, mu, ex));
+    for (int g = 0; g < G; ++g)
+        for (size_t l = 0; l < sh[g].lw; ++l)
+            CUDA_TRY(cudaMemcpyAsync(w->d + (g + l * G) * w->stride, sh[g].w.p + l * w->stride,
+                                     w->stride * 8, cudaMemcpyDeviceToDevice, c->stream));
+    return read_results(c, sh[0], n, mu, perm, rj, rank);
+}
+
+int f2gpu_rank(f2gpu_ctx* c, const f2gpu_mat* a, size_t* rank) {
+    if (!c || !a || !rank) return set_err(F2GPU_EINVAL, "null argument");
+    const bool tr = a->rows < a->cols;
+    f2gpu_mat* t = nullptr;
+    F2_TRY(f2gpu_mat_alloc(c, tr ? a->cols : a->rows, tr ? a->rows : a->cols, &t));
+    std::unique_ptr<f2gpu_mat, int (*)(f2gpu_mat*)> guard(t, f2gpu_mat_free);
+    if (tr) {
+        F2_TRY(f2gpu_mat_transpose(c, a, t));
+    } else if (a->rows && a->cols) {
+        CUDA_TRY(cudaMemcpyAsync(t->d, a->d, ceil64(a->cols) * a->stride * 8,
+                                 cudaMemcpyDeviceToDevice, c->stream));
+    }
+    return decompose_single(c, view_of(t), nullptr, nullptr, rank);
+}
+
+// ---- host-buffer entry points ----
+namespace {
+struct MatGuard {
+    f2gpu_mat* m = nullptr;
+    ~MatGuard() { f2gpu_mat_free(m); }
+};
+}  // namespace
+
+int f2gpu_m4rm_mult_host(f2gpu_ctx* c, const uint64_t* a, size_t n, size_t k, size_t sa,
+                         const uint64_t* b, size_t m, size_t sb, uint64_t* out, size_t sc,
+                         unsigned tc) {
+    if (!c) return set_err(F2GPU_EINVAL, "null ctx");
+    MatGuard A, B, C;
+    F2_TRY(f2gpu_mat_alloc(c, n, k, &A.m));
+    F2_TRY(f2gpu_mat_alloc(c, k, m, &B.m));
+    F2_TRY(f2gpu_mat_alloc(c, n, m, &C.m));
+    F2_TRY(f2gpu_mat_upload(c, A.m, a, sa));
+    F2_TRY(f2gpu_mat_upload(c, B.m, b, sb));
+    F2_TRY(f2gpu_m4rm_mult(c, A.m, B.m, C.m, tc));
+    return f2gpu_mat_download(c, C.m, out, sc);
+}
+
+int f2gpu_strassen_mult_host(f2gpu_ctx* c, const uint64_t* a, size_t n, size_t k, size_t sa,
+                             const uint64_t* b, size_t m, size_t sb, uint64_t* out, size_t sc,
+                             size_t threshold) {
+    if (!c) return set_err(F2GPU_EINVAL, "null ctx");
+    MatGuard A, B, C;
+    F2_TRY(f2gpu_mat_alloc(c, n, k, &A.m));
+    F2_TRY(f2gpu_mat_alloc(c, k, m, &B.m));
+    F2_TRY(f2gpu_mat_alloc(c, n, m, &C.m));
+    F2_TRY(f2gpu_mat_upload(c, A.m, a, sa));
+    F2_TRY(f2gpu_mat_upload(c, B.m, b, sb));
+    F2_TRY(f2gpu_strassen_mult(c, A.m, B.m, C.m, threshold));
+    return f2gpu_mat_download(c, C.m, out, sc);
+}
+
+int f2gpu_decompose_block_host(f2gpu_ctx* c, const uint64_t* a, size_t n, size_t m, size_t stride,
+                               uint64_t* w_out, uint32_t* perm, uint32_t* rj, size_t* rank) {
+    if (!c) return set_err(F2GPU_EINVAL, "null ctx");
+    MatGuard W;
+    F2_TRY(f2gpu_mat_alloc(c, n, m, &W.m));
+    F2_TRY(f2gpu_mat_upload(c, W.m, a, stride));
+    F2_TRY(f2gpu_decompose_block(c, W.m, perm, rj, rank));
+    if (w_out) F2_TRY(f2gpu_mat_download(c, W.m, w_out, stride));
+    return F2GPU_OK;
+}
+
+int f2gpu_rank_host(f2gpu_ctx* c, const uint64_t* a, size_t n, size_t m, size_t stride,
+                    size_t* rank) {
+    if (!c) return set_err(F2GPU_EINVAL, "null ctx");
+    MatGuard A;
+    F2_TRY(f2gpu_mat_alloc(c, n, m, &A.m));
+    F2_TRY(f2gpu_mat_upload(c, A.m, a, stride));
+    return f2gpu_rank(c, A.m, rank);
+}
+
+// ---- multi-GPU ----
+size_t f2gpu_local_wcols(size_t mu, int rank, int world) {
+    if (world <= 0 || rank < 0 || size_t(rank) >= mu) return 0;
+    return (mu - size_t(rank) + size_t(world) - 1) / size_t(world);
+}
+
+int f2gpu_nccl_unique_id(void* out) {
+    NcclApi& api = nccl();
+    if (!api.ok) return set_err(F2GPU_ENCCL, api.why);
+    int rc = api.getUniqueId(out);
+    if (rc) return set_err(F2GPU_ENCCL, "ncclGetUniqueId failed");
+    return F2GPU_OK;
+}
+
+int f2gpu_ctx_init_comm(f2gpu_ctx* c, int rank, int world, const void* id) {
+    if (!c || !id) return set_err(F2GPU_EINVAL, "null argument");
+    if (world < 1 || rank < 0 || rank >= world) return set_err(F2GPU_ERANGE, "rank/world");
+    c->rank = rank;
+    c->world = world;
+    // world == 1 needs no communicator; F2GPU_FORCE_NCCL=1 builds a 1-rank one so
+    // the NCCL exchange path can be exercised on a single GPU.
+    const char* force = getenv("F2GPU_FORCE_NCCL");
+    if (world == 1 && !(force && force[0] == '1')) return F2GPU_OK;
+    NcclApi& api = nccl();
+    if (!api.ok) return set_err(F2GPU_ENCCL, api.why);
+    CUDA_TRY(cudaSetDevice(c->device));
+    Id128 uid;
+    std::memcpy(uid.b, id, 128);
+    int rc = reinterpret_cast<CommInitRankFn>(api.commInitRankSym)(&c->comm, world, uid, rank);
+    if (rc) return set_err(F2GPU_ENCCL, "ncclCommInitRank failed");
+    return F2GPU_OK;
+}
+
+int f2gpu_decompose_block_dist(f2gpu_ctx* c, f2gpu_mat* w_local, size_t m_global, uint32_t* perm,
+                               uint32_t* rj, size_t* rank) {
+    if (!c || !w_local) return set_err(F2GPU_EINVAL, "null argument");
+    const size_t n = w_local->rows, mu = ceil64(m_global);
+    const size_t lw = f2gpu_local_wcols(mu, c->rank, c->world);
+    if (ceil64(w_local->cols) != lw)
+        return set_err(F2GPU_EINVAL, "decompose_dist: local matrix has the wrong number of word-columns");
+    if (c->world == 1 && !c->comm) return decompose_single(c, view_of(w_local), perm, rj, rank);
+    if (!c->comm) return set_err(F2GPU_ENCCL, "decompose_dist: communicator not initialised");
+    std::deque<DevBuf> keep;
+    std::vector<Shard> sh(1);
+    sh[0].w = View{w_local->d, n, lw * 64, w_local->stride};
+    sh[0].lw = lw;
+    F2_TRY(alloc_shard_aux(c, sh[0], n, mu, keep));
+    NcclExchange ex;
+    F2_TRY(decompose_sharded(c, sh, c->rank, c->world, n, mu, ex));
+    return read_results(c, sh[0], n, mu, perm, rj, rank);
+}
+
+}  // extern "C"

@@ -1,0 +1,79 @@
+// kernels.cuh — sm_100a kernels of the GF(2) block decomposition hot path.
+//
+// Layout (reference bit_matrix.hpp:74-81): word (i,q) at p[q*stride + i],
+// bit k = entry (i, 64q+k).  Device strides are multiples of 32 words so every
+// 16-row unit is 128-byte aligned (LDG/STG.256 friendly).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace f2 {
+
+// ---- M4RM table geometry (shared by the update and GEMM kernels) ----------
+// A 64-bit driving word is split into 9 groups: 8 x 7 bits + 1 x 8 bits
+// (make_splits analogue, m4rm.hpp:39-48, with mixed sizes — SPEC.md allows
+// any l_1..l_K summing to b).  Entries per column: 8*128 + 256 = 1280.
+// A CTA owns 16 word-columns: 1280 * 16 * 8 B = 160 KiB of shared memory, and
+// a half-warp reading 16 consecutive columns of one entry is one 128-byte
+// wavefront (bank-conflict free regardless of the data-dependent index).
+constexpr int kTabCols = 16;
+constexpr int kNumTab = 9;
+constexpr int kTabEntries = 1280;
+constexpr size_t kTabBytes = size_t(kTabEntries) * kTabCols * 8;  // 163840
+
+// Per-panel record, written by the panel kernel on the owner and broadcast to
+// every shard.  All row indices are relative to R.
+struct PanelState {
+    uint32_t R;       // rows eliminated before this panel (sum of earlier r_j)
+    uint32_t r;       // block rank r_j
+    uint32_t npairs;  // entries of the composite row permutation below
+    uint32_t flags;
+    uint64_t Z[64];   // compressed pseudo-inverse rows (bit t < r)
+    uint32_t dst[128];  // new[dst[e]] = old[src[e]]  (rows R + .)
+    uint32_t src[128];
+};
+static_assert(sizeof(PanelState) == 16 + 512 + 1024, "PanelState layout");
+
+struct UpdateArgs {
+    uint64_t* C; size_t sc; size_t c_wcol0; int ncols;   // destination word-columns
+    size_t row_lo, row_hi;                               // C rows to update
+    const uint64_t* a;                                   // a[i] = driving word of C row i
+    int k_bits;
+    const uint64_t* B; size_t sb; size_t b_row0; size_t b_wcol0;
+    const PanelState* st;  // non-null: R,r from state -> row_lo=R+r, k=r, b_row0=R
+};
+
+struct GemmArgs {
+    const uint64_t* A; size_t sa; size_t n;   // A: n rows, k bits
+    const uint64_t* B; size_t sb; size_t k;   // B: k rows
+    uint64_t* C; size_t sc; int mcols;        // C: n rows, mcols word-columns (XOR-accumulated)
+};
+
+// launchers (return cudaError_t of the launch)
+cudaError_t launch_random_dense(uint64_t* w, size_t n, size_t m, size_t stride, double density,
+                                uint64_t seed, const uint64_t* d_jump, cudaStream_t s);
+cudaError_t launch_update(const UpdateArgs& a, int num_sms, cudaStream_t s);
+cudaError_t launch_gemm(const GemmArgs& g, int num_sms, cudaStream_t s);
+cudaError_t launch_panel(uint64_t* col, size_t n, PanelState* st_all, int j, cudaStream_t s);
+cudaError_t launch_panel_y(uint64_t* col, size_t n, const PanelState* st, int num_sms,
+                           cudaStream_t s);
+cudaError_t launch_swaps(uint64_t* w, size_t stride, int ncols, int skip_col, uint32_t* perm,
+                         const PanelState* st, cudaStream_t s);
+// dst = (acc ? dst : 0) ^ a ^ b ^ c ^ d over a rows x wcols block (any input may be null)
+cudaError_t launch_xor(uint64_t* dst, size_t sd, const uint64_t* a, size_t sa,
+                       const uint64_t* b, size_t sb, const uint64_t* c, size_t scc,
+                       const uint64_t* d, size_t sdd, size_t rows, size_t wcols, bool acc,
+                       cudaStream_t s);
+cudaError_t launch_transpose(const uint64_t* a, size_t n, size_t m, size_t sa, uint64_t* out,
+                             size_t so, cudaStream_t s);
+cudaError_t launch_iota(uint32_t* p, size_t n, cudaStream_t s);
+cudaError_t launch_mask_cols(uint64_t* w, size_t stride, size_t n, size_t m, cudaStream_t s);
+
+// per-device one-time setup (dynamic shared memory opt-in)
+cudaError_t init_kernel_attrs();
+
+// host helper: the 64 jump matrices T^(2^s) of the xorshift64* state map
+void host_jump_tables(uint64_t out[64 * 64]);
+
+}  // namespace f2

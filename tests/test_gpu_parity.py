@@ -1,0 +1,246 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, bit-exact.
+
+All integer/bitwise work, so the bar is bit-exact equality (no tolerance).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def bm(f2, arr, n, m):
+    return f2.BitMatrix(n, m, arr)
+
+
+def same(a, b, n):
+    return np.array_equal(a[:, :n], b[:, :n])
+
+
+# ---------------------------------------------------------------------------
+# K0 random_dense
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("n,m", [(1, 1), (4, 5), (100, 130), (65, 64), (333, 777), (1000, 4096),
+                                 (4097, 1000), (31, 4160)])
+@pytest.mark.parametrize("p", [0.5, 0.05, 0.3])
+def test_random_dense(f2, ctx, po, n, m, p):
+    seed = n * 7 + m
+    want = po.random_dense(n, m, p, seed)
+    got = f2.BitMatrix.random_dense(n, m, p, seed, ctx=ctx)
+    assert same(got.words, want, n)
+    assert got.padding_is_zero()
+
+
+@pytest.mark.parametrize("p", [0.0, 1.0, -1.0, 2.0])
+def test_random_dense_degenerate(f2, ctx, po, p):
+    want = po.random_dense(70, 130, p, 3)
+    got = f2.BitMatrix.random_dense(70, 130, p, 3, ctx=ctx)
+    assert same(got.words, want, 70)
+
+
+def test_random_dense_seed_zero(f2, ctx, po):
+    assert same(f2.BitMatrix.random_dense(50, 200, 0.5, 0, ctx=ctx).words,
+                po.random_dense(50, 200, 0.5, 0), 50)
+
+
+# ---------------------------------------------------------------------------
+# K1+K2 M4RM products
+# ---------------------------------------------------------------------------
+SHAPES = [(1, 1, 1), (5, 64, 7), (64, 64, 64), (100, 129, 200), (300, 129, 200), (1025, 63, 17),
+          (2047, 130, 1030), (1000, 1000, 1000), (4096, 4096, 4096), (33, 5000, 1024),
+          (3000, 64, 1500), (1024, 1, 2048)]
+
+
+@pytest.mark.parametrize("n,k,m", SHAPES)
+def test_m4rm_mult(f2, ctx, po, n, k, m):
+    a = po.random_dense(n, k, 0.5, n + 1)
+    b = po.random_dense(k, m, 0.5, m + 2)
+    want = po.m4rm_mult(a, n, k, b, m)
+    got = f2.m4rm_mult(bm(f2, a, n, k), bm(f2, b, k, m), ctx=ctx)
+    assert same(got.words, want, n)
+
+
+def test_m4rm_mult_random_shapes(f2, ctx, po):
+    rng = np.random.default_rng(7)
+    for t in range(60):
+        n, k, m = (int(x) for x in rng.integers(1, 1100, 3))
+        a = po.random_dense(n, k, [0.5, 0.1, 0.01][t % 3], 100 + t)
+        b = po.random_dense(k, m, 0.5, 200 + t)
+        want = po.mul_naive(a, n, k, b, m) if n * k * m < 2e8 else po.m4rm_mult(a, n, k, b, m)
+        got = f2.m4rm_mult(bm(f2, a, n, k), bm(f2, b, k, m), ctx=ctx)
+        assert same(got.words, want, n), (n, k, m)
+
+
+def test_m4rm_mult_shape_mismatch(f2, ctx):
+    with pytest.raises(ValueError):
+        f2.m4rm_mult(f2.BitMatrix(4, 5), f2.BitMatrix(6, 7), ctx=ctx)
+
+
+def test_m4rm_mult_cfg2(f2, ctx, po):
+    """BASELINE config 2: 16384^2 x 16384^2, seeds A=2, B=3."""
+    n = 16384
+    a = po.random_dense(n, n, 0.5, 2)
+    b = po.random_dense(n, n, 0.5, 3)
+    want = po.m4rm_mult(a, n, n, b, n)
+    got = f2.m4rm_mult(bm(f2, a, n, n), bm(f2, b, n, n), ctx=ctx)
+    assert same(got.words, want, n)
+
+
+@pytest.mark.parametrize("n,k,m,cut", [(256, 256, 256, 128), (1024, 512, 768, 256),
+                                       (512, 1024, 2048, 256), (2048, 2048, 2048, 512),
+                                       (1000, 1000, 1000, 128)])
+def test_strassen(f2, ctx, po, n, k, m, cut):
+    a = po.random_dense(n, k, 0.5, 11)
+    b = po.random_dense(k, m, 0.5, 12)
+    want = po.m4rm_mult(a, n, k, b, m)
+    got = f2.strassen_mult(bm(f2, a, n, k), bm(f2, b, k, m), threshold=cut, ctx=ctx)
+    assert same(got.words, want, n)
+
+
+def test_strassen_cfg2(f2, ctx, po):
+    n = 16384
+    a = po.random_dense(n, n, 0.5, 2)
+    b = po.random_dense(n, n, 0.5, 3)
+    want = po.m4rm_mult(a, n, n, b, n)
+    got = f2.strassen_mult(bm(f2, a, n, n), bm(f2, b, n, n), threshold=4096, ctx=ctx)
+    assert same(got.words, want, n)
+
+
+@pytest.mark.parametrize("k", [1, 7, 13, 56, 57, 64])
+def test_mult_acc(f2, ctx, po, k):
+    """C[r0.., w0..w0+nw) ^= a * B[b0..b0+k, bw0..] (m4rm.hpp:93-172 semantics)."""
+    n, m = 3000, 64 * 40
+    c = po.random_dense(n, m, 0.5, 5)
+    b = po.random_dense(200, m, 0.5, 6)
+    r0, nr, w0, nw, b0, bw0 = 37, 2500, 3, 21, 11, 5
+    rng = np.random.default_rng(k)
+    aw = rng.integers(0, 2**63, nr, dtype=np.uint64) & np.uint64((1 << k) - 1 if k < 64 else 2**64 - 1)
+    want = c.copy()
+    for q in range(nw):
+        brow = b[bw0 + q, b0:b0 + k]
+        for i in range(nr):
+            x = int(aw[i])
+            acc = 0
+            while x:
+                t = (x & -x).bit_length() - 1
+                acc ^= int(brow[t])
+                x &= x - 1
+            want[w0 + q, r0 + i] ^= np.uint64(acc)
+    dc = f2.DeviceMatrix.from_host(bm(f2, c, n, m), ctx)
+    tables = f2.build_tables(bm(f2, b, 200, m), b0, k, bw0, nw, ctx=ctx)
+    f2.mult_acc(dc, r0, w0, aw, tables)
+    assert same(dc.download().words, want, n)
+
+
+def test_mult_acc_errors(f2, ctx):
+    with pytest.raises(ValueError):
+        f2.build_tables(f2.BitMatrix(100, 64), 0, 65, 0, 1, ctx=ctx)
+    with pytest.raises(IndexError):
+        f2.build_tables(f2.BitMatrix(100, 64), 50, 64, 0, 1, ctx=ctx)
+
+
+# ---------------------------------------------------------------------------
+# decomposition
+# ---------------------------------------------------------------------------
+def check_decomp(f2, ctx, po, a, n, m, shards=1):
+    w, perm, rj, rank = po.decompose_block(a, n, m)
+    got = f2.decompose_block(bm(f2, a, n, m), ctx=ctx, shards=shards)
+    assert got.rank == rank
+    assert np.array_equal(got.block_ranks, rj)
+    assert np.array_equal(got.P.perm, perm)
+    assert same(got.overlay.words, w, n)
+    return got
+
+
+DECOMP_SHAPES = [(1, 1), (4, 5), (64, 64), (100, 100), (200, 130), (130, 200), (513, 257),
+                 (1000, 640), (640, 1000), (2048, 2048), (100, 3000), (3000, 100)]
+
+
+@pytest.mark.parametrize("n,m", DECOMP_SHAPES)
+@pytest.mark.parametrize("p", [0.5, 0.1, 0.01])
+def test_decompose(f2, ctx, po, n, m, p):
+    a = po.random_dense(n, m, p, n * 31 + m)
+    check_decomp(f2, ctx, po, a, n, m)
+
+
+def test_decompose_paper_example(f2, ctx, po):
+    """PAPER.md section 3 example: rank 4."""
+    A = f2.BitMatrix.from_rows(["10111", "10001", "11010", "00111"])
+    got = check_decomp(f2, ctx, po, A.words, 4, 5)
+    assert got.rank == 4
+
+
+def test_decompose_adversarial(f2, ctx, po):
+    n, m = 700, 500
+    cases = [np.zeros((8, 704), np.uint64)]
+    ident = f2.BitMatrix.identity(500)
+    cases_nm = [(cases[0], n, m), (ident.words, 500, 500)]
+    # rank-1 outer product u v^T
+    rng = np.random.default_rng(1)
+    u = rng.integers(0, 2, n).astype(np.uint8)
+    v = rng.integers(0, 2, m).astype(np.uint8)
+    cases_nm.append((po.from_dense(np.outer(u, v).astype(np.uint8)), n, m))
+    # duplicate rows
+    d = rng.integers(0, 2, (n, m)).astype(np.uint8)
+    d[1::2] = d[0::2]
+    cases_nm.append((po.from_dense(d), n, m))
+    for a, nn, mm in cases_nm:
+        got = check_decomp(f2, ctx, po, a, nn, mm)
+        assert got.rank == po.rank_ge(a, nn, mm)
+
+
+def test_decompose_rank_deficient_xy(f2, ctx, po):
+    """cfg3 in miniature: A = X*Y with X 2048x1500, Y 1500x8192 (rank <= 1500)."""
+    x = po.random_dense(2048, 1500, 0.5, 4)
+    y = po.random_dense(1500, 8192, 0.5, 5)
+    a = po.m4rm_mult(x, 2048, 1500, y, 8192)
+    got = check_decomp(f2, ctx, po, a, 2048, 8192)
+    assert got.rank == 1500
+
+
+@pytest.mark.parametrize("shards", [2, 3, 4, 8])
+def test_decompose_sharded(f2, ctx, po, shards):
+    for (n, m, p) in [(1000, 1000, 0.5), (700, 1300, 0.1), (1500, 640, 0.5)]:
+        a = po.random_dense(n, m, p, 17 + shards)
+        check_decomp(f2, ctx, po, a, n, m, shards=shards)
+
+
+def test_decompose_recomposes(f2, ctx, po):
+    n, m = 1000, 900
+    a = po.random_dense(n, m, 0.5, 9)
+    got = f2.decompose_block(bm(f2, a, n, m), ctx=ctx)
+    L, U = got.L, got.U
+    lu = po.mul_naive(L.words, n, got.rank, U.words, m)
+    pa = a[:, got.P.perm]
+    assert np.array_equal(lu[:, :n], pa[:, :n])
+
+
+def test_decompose_cfg1(f2, ctx, po):
+    """BASELINE config 1: 4096^2, p=0.5, seed 1 — full bit-exact compare."""
+    a = po.random_dense(4096, 4096, 0.5, 1)
+    check_decomp(f2, ctx, po, a, 4096, 4096)
+
+
+@pytest.mark.parametrize("n,m", [(300, 700), (700, 300), (64, 4096), (1000, 1000), (5, 3000)])
+def test_rank(f2, ctx, po, n, m):
+    a = po.random_dense(n, m, 0.5, 21)
+    assert f2.rank(bm(f2, a, n, m), ctx=ctx) == po.rank_ge(a, n, m)
+
+
+def test_rank_low(f2, ctx, po):
+    x = po.random_dense(900, 37, 0.5, 1)
+    y = po.random_dense(37, 1200, 0.5, 2)
+    a = po.m4rm_mult(x, 900, 37, y, 1200)
+    assert f2.rank(bm(f2, a, 900, 1200), ctx=ctx) == po.rank_ge(a, 900, 1200) <= 37
+
+
+@pytest.mark.parametrize("n,m", [(64, 64), (100, 37), (37, 100), (1000, 4097), (130, 1)])
+def test_transpose(f2, ctx, po, n, m):
+    import ctypes as C
+    from paper_1209_5198_b200 import _lib
+
+    a = po.random_dense(n, m, 0.5, 3)
+    want = po.transpose(a, n, m)
+    da = f2.DeviceMatrix.from_host(bm(f2, a, n, m), ctx)
+    dt = f2.DeviceMatrix(m, n, ctx)
+    _lib.check(_lib.load().f2gpu_mat_transpose(ctx.handle, da.handle, dt.handle))
+    assert same(dt.download().words, want, m)
