@@ -45,7 +45,8 @@ int set_err(int code, const std::string& msg) {
     } while (0)
 
 size_t ceil64(size_t x) { return (x + 63) / 64; }
-size_t dev_stride(size_t rows) { return std::max<size_t>(32, (rows + 31) / 32 * 32); }
+// 128-row (1 KiB) granularity: the bulk-copy update kernel moves 128-row column segments
+size_t dev_stride(size_t rows) { return std::max<size_t>(128, (rows + 127) / 128 * 128); }
 
 // ---- NCCL, loaded at run time --------------------------------------------
 struct Id128 { char b[128]; };  // ncclUniqueId (NCCL_UNIQUE_ID_BYTES = 128), passed by value
@@ -406,8 +407,11 @@ int alloc_shard_aux(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, std::deque<DevB
     F2_TRY(keep.back().alloc(n * 4));
     s.perm = keep.back().as<uint32_t>();
     keep.emplace_back(c);
-    F2_TRY(keep.back().alloc(kBcastHdr + n * 8));
+    // landing column padded to the full stride (the bulk-copy update reads
+    // 128-row segments of it) and zeroed once; broadcasts fill rows < n
+    F2_TRY(keep.back().alloc(kBcastHdr + s.w.stride * 8));
     s.bcast = keep.back().as<uint64_t>();
+    CUDA_TRY(cudaMemsetAsync(s.bcast, 0, kBcastHdr + s.w.stride * 8, c->stream));
     return F2GPU_OK;
 }
 

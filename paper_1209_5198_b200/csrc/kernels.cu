@@ -265,8 +265,379 @@ __global__ void __launch_bounds__(kUpdThreads, 1) k_update(UpdateArgs p) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// K2 v2: fused table build + XOR update with C staged by bulk-async copies
+// ---------------------------------------------------------------------------
+// ncu on k_update (v1) showed the L1TEX data pipe at 91% of peak with half of
+// its wavefronts spent on LSU global traffic (one wavefront per 32-byte
+// sector).  v2 moves C through shared memory with cp.async.bulk (the TMA
+// engine, not the LSU): a producer warp streams 128-row x 16-column tiles of C
+// (16 x 1 KiB column segments, padded to 1040 B so 128-bit shared loads of the
+// consumers are bank-conflict free) plus the 128 driving words into a 3-stage
+// mbarrier ring, and writes finished tiles back with bulk stores.  16 consumer
+// warps keep the v1 lookup pattern (lane = (row half, column), one 128-byte
+// table row per half-warp lookup).  Requires 128-row aligned strides and a
+// 16-byte aligned driving column (device matrices and the decomposition).
+constexpr int kV2Warps = 16;
+constexpr int kV2Threads = (kV2Warps + 1) * 32;
+constexpr int kV2Rows = 128;
+constexpr int kV2Stages = 3;
+constexpr int kV2ColPitch = kV2Rows * 8 + 16;                      // 1040 B
+constexpr int kV2CBytes = kTabCols * kV2ColPitch;                  // 16640 B
+constexpr int kV2StageBytes = kV2CBytes + kV2Rows * 8;             // + driving words
+constexpr size_t kV2Smem = kTabBytes + size_t(kV2Stages) * kV2StageBytes + 64;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "W_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W_%=;\n}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void consumers_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(kV2Warps * 32) : "memory");
+}
+
+__global__ void __launch_bounds__(kV2Threads, 1) k_update_v2(UpdateArgs p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    uint64_t* tab = reinterpret_cast<uint64_t*>(smem_raw);
+    unsigned char* stage0 = smem_raw + kTabBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(stage0 + size_t(kV2Stages) * kV2StageBytes);
+    uint64_t* full = bars;               // [kV2Stages]
+    uint64_t* done = bars + kV2Stages;   // [kV2Stages]
+
+    size_t row_lo = p.row_lo, b_row0 = p.b_row0;
+    int k = p.k_bits;
+    if (p.st) {
+        const uint32_t R = p.st->R, r = p.st->r;
+        row_lo = size_t(R) + r;
+        k = int(r);
+        b_row0 = R;
+    }
+    const size_t row_hi = p.row_hi;
+    if (k <= 0 || row_lo >= row_hi || p.ncols <= 0) return;
+    const int nt = k > 56 ? 9 : (k + 6) / 7;
+    const size_t base = row_lo & ~size_t(kV2Rows - 1);
+    const size_t T = (row_hi - base + kV2Rows - 1) / kV2Rows;  // tiles per column group
+    const size_t ncg = (size_t(p.ncols) + kTabCols - 1) / kTabCols;
+    const size_t TU = T * ncg;
+    const size_t u0 = TU * blockIdx.x / gridDim.x;
+    const size_t u1 = TU * (blockIdx.x + 1) / gridDim.x;
+    if (u0 >= u1) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kV2Stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&done[s], kV2Warps);
+        }
+        fence_async_smem();
+    }
+    __syncthreads();
+
+    if (warp == kV2Warps) {
+        // ===== producer warp: bulk loads into the ring, bulk stores out of it =====
+        for (size_t u = u0; u < u1 + kV2Stages; ++u) {
+            const size_t it = u - u0;
+            const int s = int(it % kV2Stages);
+            unsigned char* sb = stage0 + size_t(s) * kV2StageBytes;
+            if (it >= size_t(kV2Stages)) {
+                // write back tile it - kV2Stages from stage s
+                const size_t uo = u - kV2Stages;
+                mbar_wait(&done[s], uint32_t(((it / kV2Stages) - 1) & 1));
+                const size_t g = uo / T, t = uo % T;
+                const int nvalid = min(kTabCols, int(size_t(p.ncols) - g * kTabCols));
+                const size_t r0 = base + t * kV2Rows;
+                if (lane < nvalid) {
+                    bulk_s2g(p.C + (p.c_wcol0 + g * kTabCols + lane) * p.sc + r0,
+                             sb + lane * kV2ColPitch, kV2Rows * 8);
+                    bulk_commit();
+                    bulk_wait_read0();
+                }
+                __syncwarp();
+            }
+            if (u >= u1) continue;
+            const size_t g = u / T, t = u % T;
+            const int nvalid = min(kTabCols, int(size_t(p.ncols) - g * kTabCols));
+            const size_t r0 = base + t * kV2Rows;
+            if (lane == 0) mbar_expect_tx(&full[s], uint32_t((nvalid + 1) * kV2Rows * 8));
+            __syncwarp();
+            if (lane < nvalid)
+                bulk_g2s(sb + lane * kV2ColPitch,
+                         p.C + (p.c_wcol0 + g * kTabCols + lane) * p.sc + r0, kV2Rows * 8,
+                         &full[s]);
+            if (lane == kTabCols)
+                bulk_g2s(sb + kV2CBytes, p.a + r0, kV2Rows * 8, &full[s]);
+        }
+        bulk_wait0();
+        return;
+    }
+
+    // ===== 16 consumer warps =====
+    const int h = lane >> 4, col = lane & 15;
+    const uint64_t* tl = tab + col;
+    const int rl = 8 * warp + 4 * h;  // this lane's 4 rows within the tile
+    size_t gcur = ~size_t(0);
+    for (size_t u = u0; u < u1; ++u) {
+        const size_t it = u - u0;
+        const int s = int(it % kV2Stages);
+        const size_t g = u / T, t = u % T;
+        if (g != gcur) {
+            consumers_sync();
+            const int nvalid = min(kTabCols, int(size_t(p.ncols) - g * kTabCols));
+            build_tables<kV2Warps * 32>(tab, p.B, p.sb, b_row0, p.b_wcol0 + g * kTabCols, nvalid,
+                                        k, nt);
+            consumers_sync();
+            gcur = g;
+        }
+        unsigned char* sb = stage0 + size_t(s) * kV2StageBytes;
+        mbar_wait(&full[s], uint32_t((it / kV2Stages) & 1));
+        uint64_t* cw = reinterpret_cast<uint64_t*>(sb + col * kV2ColPitch) + rl;
+        const uint64_t* aw = reinterpret_cast<const uint64_t*>(sb + kV2CBytes) + rl;
+        const ulonglong2 c01 = *reinterpret_cast<const ulonglong2*>(cw);
+        const ulonglong2 c23 = *reinterpret_cast<const ulonglong2*>(cw + 2);
+        const ulonglong2 a01 = *reinterpret_cast<const ulonglong2*>(aw);
+        const ulonglong2 a23 = *reinterpret_cast<const ulonglong2*>(aw + 2);
+        const size_t row = base + t * kV2Rows + rl;
+        uint64_t x[4] = {a01.x, a01.y, a23.x, a23.y};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (row + q < row_lo || row + q >= row_hi) x[q] = 0;
+        ulonglong2 o01, o23;
+        o01.x = c01.x ^ lookup(tl, x[0], nt);
+        o01.y = c01.y ^ lookup(tl, x[1], nt);
+        o23.x = c23.x ^ lookup(tl, x[2], nt);
+        o23.y = c23.y ^ lookup(tl, x[3], nt);
+        *reinterpret_cast<ulonglong2*>(cw) = o01;
+        *reinterpret_cast<ulonglong2*>(cw + 2) = o23;
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&done[s]);
+    }
+}
+
+bool update_v2_ok(const UpdateArgs& a) {
+    return (a.sc % kV2Rows) == 0 && (reinterpret_cast<uintptr_t>(a.C) % 16) == 0 &&
+           (reinterpret_cast<uintptr_t>(a.a) % 16) == 0 && a.row_hi <= a.sc;
+}
+
+// ---------------------------------------------------------------------------
+// K2 v3: table build + XOR sweep, C updated in place by bulk XOR-reduction
+// ---------------------------------------------------------------------------
+// ncu history: v1 (LSU loads/stores of C) is L1TEX-data-pipe bound, half of it
+// global traffic at one wavefront per 32-byte sector; v2 (bulk-async C staging)
+// was instruction/latency bound on the store-then-reload ring.  v3 never brings
+// C into the SM: the consumers compute only the update delta
+//   D[i, col] = XOR_t T_t[(y_i >> 7t) & mask][col]
+// into a shared-memory ring, and the producer warp applies it with
+// cp.reduce.async.bulk ... .xor.b64 (UBLKRED): the read-modify-write of C
+// happens in L2, so DRAM still sees C once in and once out while the SM's data
+// pipe carries only table lookups and the delta stores.  The 128 driving words
+// of each tile come through a separate 8-deep bulk-load ring.  Rows outside
+// [row_lo, row_hi) get a zero delta (the XOR leaves them unchanged).
+constexpr int kV3Warps = 16;                      // consumer warps
+constexpr int kV3Threads = (kV3Warps + 1) * 32;   // + producer warp
+constexpr int kV3Rows = 128;                      // tile rows (lane owns 4)
+constexpr int kV3DStages = 3;
+constexpr int kV3AStages = 8;
+constexpr int kV3ColPitch = kV3Rows * 8 + 16;     // 1040 B: conflict-free 128-bit smem access
+constexpr int kV3DBytes = kTabCols * kV3ColPitch; // 16640 B per delta tile
+constexpr int kV3ABytes = kV3Rows * 8;            // 1 KiB of driving words
+constexpr size_t kV3Smem =
+    kTabBytes + size_t(kV3DStages) * kV3DBytes + size_t(kV3AStages) * kV3ABytes + 256;
+
+__device__ __forceinline__ void bulk_red_xor(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.xor.b64 [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void v3_consumers_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(kV3Warps * 32) : "memory");
+}
+
+__global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    uint64_t* tab = reinterpret_cast<uint64_t*>(smem_raw);
+    unsigned char* dring = smem_raw + kTabBytes;
+    unsigned char* aring = dring + size_t(kV3DStages) * kV3DBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(aring + size_t(kV3AStages) * kV3ABytes);
+    uint64_t* a_full = bars;                       // [kV3AStages] tx barrier
+    uint64_t* a_empty = a_full + kV3AStages;       // [kV3AStages] 8 consumer warps
+    uint64_t* d_done = a_empty + kV3AStages;       // [kV3DStages] 8 consumer warps
+    uint64_t* d_free = d_done + kV3DStages;        // [kV3DStages] producer
+
+    size_t row_lo = p.row_lo, b_row0 = p.b_row0;
+    int k = p.k_bits;
+    if (p.st) {
+        const uint32_t R = p.st->R, r = p.st->r;
+        row_lo = size_t(R) + r;
+        k = int(r);
+        b_row0 = R;
+    }
+    const size_t row_hi = p.row_hi;
+    if (k <= 0 || row_lo >= row_hi || p.ncols <= 0) return;
+    const int nt = k > 56 ? 9 : (k + 6) / 7;
+    const size_t base = row_lo & ~size_t(kV3Rows - 1);
+    const size_t T = (row_hi - base + kV3Rows - 1) / kV3Rows;  // tiles per column group
+    const size_t ncg = (size_t(p.ncols) + kTabCols - 1) / kTabCols;
+    const size_t TU = T * ncg;
+    const size_t u0 = TU * blockIdx.x / gridDim.x;
+    const size_t u1 = TU * (blockIdx.x + 1) / gridDim.x;
+    if (u0 >= u1) return;
+    const size_t cnt = u1 - u0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kV3AStages; ++s) {
+            mbar_init(&a_full[s], 1);
+            mbar_init(&a_empty[s], kV3Warps);
+        }
+        for (int s = 0; s < kV3DStages; ++s) {
+            mbar_init(&d_done[s], kV3Warps);
+            mbar_init(&d_free[s], 1);
+        }
+        fence_async_smem();
+    }
+    __syncthreads();
+
+    if (warp == kV3Warps) {
+        // ===== producer warp =====
+        // tile cursors advance incrementally (no 64-bit divisions per tile)
+        size_t ag = u0 / T, at = u0 % T;   // next A tile to load
+        uint32_t a_stage = 0;
+        auto issue_a = [&]() {
+            if (lane == 0) {
+                mbar_expect_tx(&a_full[a_stage], kV3ABytes);
+                bulk_g2s(aring + size_t(a_stage) * kV3ABytes, p.a + base + at * kV3Rows, kV3ABytes,
+                         &a_full[a_stage]);
+            }
+            if (++at == T) { at = 0; ++ag; }
+            if (++a_stage == kV3AStages) a_stage = 0;
+        };
+        const size_t pre = cnt < size_t(kV3AStages) ? cnt : size_t(kV3AStages);
+        for (size_t i = 0; i < pre; ++i) issue_a();
+        size_t g = u0 / T, tt = u0 % T;
+        int s = 0, ae = 0;
+        uint32_t dph = 0, aph = 0;
+        for (size_t t = 0; t < cnt; ++t) {
+            const size_t r0 = base + tt * kV3Rows;
+            const int nvalid = min(kTabCols, int(size_t(p.ncols) - g * kTabCols));
+            mbar_wait(&d_done[s], dph);
+            if (lane < nvalid) {
+                bulk_red_xor(p.C + (p.c_wcol0 + g * kTabCols + lane) * p.sc + r0,
+                             dring + size_t(s) * kV3DBytes + lane * kV3ColPitch, kV3ABytes);
+                bulk_commit();
+                bulk_wait_read0();
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&d_free[s]);
+            if (t + kV3AStages < cnt) {
+                mbar_wait(&a_empty[ae], aph);
+                issue_a();
+            }
+            if (++ae == kV3AStages) { ae = 0; aph ^= 1; }
+            if (++s == kV3DStages) { s = 0; dph ^= 1; }
+            if (++tt == T) { tt = 0; ++g; }
+        }
+        bulk_wait0();
+        return;
+    }
+
+    // ===== consumer warps =====
+    const int h = lane >> 4, col = lane & 15;
+    const uint64_t* tl = tab + col;
+    const int rl = 8 * warp + 4 * h;  // this lane's 4 rows within the tile
+    size_t gcur = ~size_t(0);
+    size_t g = u0 / T, tt = u0 % T;
+    int as = 0, s = 0;
+    uint32_t aph = 0, dph = 0;
+    for (size_t t = 0; t < cnt; ++t) {
+        if (g != gcur) {
+            v3_consumers_sync();
+            const int nvalid = min(kTabCols, int(size_t(p.ncols) - g * kTabCols));
+            build_tables<kV3Warps * 32>(tab, p.B, p.sb, b_row0, p.b_wcol0 + g * kTabCols, nvalid,
+                                        k, nt);
+            v3_consumers_sync();
+            gcur = g;
+        }
+        mbar_wait(&a_full[as], aph);
+        const ulonglong2* ap = reinterpret_cast<const ulonglong2*>(aring + size_t(as) * kV3ABytes) + rl / 2;
+        uint64_t x[4];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const ulonglong2 v = ap[q];
+            x[2 * q] = v.x;
+            x[2 * q + 1] = v.y;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_empty[as]);
+        const size_t row = base + tt * kV3Rows + rl;
+        if (row < row_lo || row + 4 > row_hi) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (row + q < row_lo || row + q >= row_hi) x[q] = 0;
+        }
+        uint64_t d[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) d[q] = lookup(tl, x[q], nt);
+        if (t >= size_t(kV3DStages)) mbar_wait(&d_free[s], dph ^ 1);
+        ulonglong2* dp = reinterpret_cast<ulonglong2*>(dring + size_t(s) * kV3DBytes + col * kV3ColPitch) + rl / 2;
+        dp[0] = make_ulonglong2(d[0], d[1]);
+        dp[1] = make_ulonglong2(d[2], d[3]);
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&d_done[s]);
+        if (++as == kV3AStages) { as = 0; aph ^= 1; }
+        if (++s == kV3DStages) { s = 0; dph ^= 1; }
+        if (++tt == T) { tt = 0; ++g; }
+    }
+}
+
+bool update_v3_ok(const UpdateArgs& a) {
+    return (a.sc % kV3Rows) == 0 && (reinterpret_cast<uintptr_t>(a.C) % 16) == 0 &&
+           (reinterpret_cast<uintptr_t>(a.a) % 16) == 0 && a.row_hi <= a.sc;
+}
+
 cudaError_t launch_update(const UpdateArgs& a, int num_sms, cudaStream_t s) {
     if (a.ncols <= 0) return cudaSuccess;
+    if (update_v3_ok(a)) {
+        k_update_v3<<<num_sms, kV3Threads, kV3Smem, s>>>(a);
+        return cudaGetLastError();
+    }
     k_update<<<num_sms, kUpdThreads, kTabBytes, s>>>(a);
     return cudaGetLastError();
 }
@@ -367,18 +738,24 @@ cudaError_t launch_gemm(const GemmArgs& g, int num_sms, cudaStream_t s) {
 // ---------------------------------------------------------------------------
 // K4: panel kernel — Procedure buildZ
 // ---------------------------------------------------------------------------
-// One CTA of 512 threads.  The first kPanelWin rows of the panel are cached in
-// shared memory (loaded lazily, 512 rows at a time, only as far as the pivot
-// search reaches); rows beyond are read/written in place in global memory.
-// Each of the 64 sequential steps: warp 0 forms the mask c from M (two
-// ballots), the CTA finds the FIRST row i >= i_b with odd popcount(c & A_i)
-// (ballot + per-warp first index, min over warps) — the reference's
-// lowest-index tie-break — and warp 0 performs the swap and the
-// Gauss-Jordan update of Z and M with __reduce_xor_sync.  An orig[] array
-// tracks where each row came from, giving the composite permutation that the
-// swap kernel applies to every other word-column.
-constexpr int kPanelThreads = 512;
-constexpr int kPanelWin = 8192;
+// The 64 steps are strictly sequential, so the whole procedure runs in ONE
+// warp with no block barriers.  Z and M are held TRANSPOSED in registers: lane
+// l owns columns l and l+32 (zt_l bit j = bit l of Z_j).  In that form every
+// Gauss-Jordan update of the procedure is lane-local:
+//   c   = 2^k | (mt_k & low(k))                       (:989-992, one shuffle)
+//   M_k <- A_ib            : bit k of mt_l = bit l of A_ib              (:997)
+//   Z_k ^= sum_{j<k,y_j}Z_j: bit k of zt_l ^= parity(zt_l & y & low(k)) (:1001-1006)
+//   Z_j ^= Z_k (c_j, j<k)  : zt_l ^= c & low(k)  if bit k of zt_l      (:1007-1010)
+// and likewise for M.  The pivot search (:993-1000) tests 32 candidate rows
+// per ballot from a shared-memory window of the first kPanelWin rows (first
+// odd-parity row wins: the reference's lowest-index tie-break);
+// misses fall back to a 256-rows-per-iteration scan that also ORs the rows it
+// sees — when nothing nonzero remains, the remaining steps are insertions that
+// only touch bit positions the final compression removes, so the loop ends.
+// orig[] tracks the source row of every window slot, giving the composite
+// permutation that k_swaps mirrors on every other word-column.
+constexpr int kPanelThreads = 256;  // all warps load the window; warp 0 runs buildZ
+constexpr int kPanelWin = 2048;
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
 struct PanelSmem {
@@ -386,23 +763,29 @@ struct PanelSmem {
     uint32_t orig[kPanelWin];
     uint32_t ext_pos[64];
     uint32_t ext_orig[64];
-    uint32_t wfirst[2][kPanelThreads / 32];
-    uint64_t c;
-    uint32_t n_ext;
-    uint32_t npairs;
 };
 
-__device__ __forceinline__ uint64_t xor_reduce64(uint64_t v) {
-    const uint32_t lo = __reduce_xor_sync(0xffffffffu, uint32_t(v));
-    const uint32_t hi = __reduce_xor_sync(0xffffffffu, uint32_t(v >> 32));
-    return (uint64_t(hi) << 32) | lo;
+__device__ __forceinline__ uint64_t low_mask64(int k) {
+    return k >= 64 ? ~0ull : ((1ull << k) - 1);
+}
+
+// software pext: gather the bits of x at the set positions of sel (ascending)
+__device__ __forceinline__ uint64_t pext64(uint64_t x, uint64_t sel) {
+    uint64_t out = 0;
+    int cnt = 0;
+    while (sel) {
+        const int b = __ffsll(static_cast<long long>(sel)) - 1;
+        out |= ((x >> b) & 1ull) << cnt++;
+        sel &= sel - 1;
+    }
+    return out;
 }
 
 __global__ void __launch_bounds__(kPanelThreads, 1)
     k_panel(uint64_t* __restrict__ col, size_t n, PanelState* __restrict__ st_all, int j) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     PanelSmem& S = *reinterpret_cast<PanelSmem*>(smem_raw);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31;
     const size_t R = j == 0 ? 0 : size_t(st_all[j - 1].R) + st_all[j - 1].r;
     PanelState* st = st_all + j;
     const size_t rows = R < n ? n - R : 0;
@@ -412,137 +795,171 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
         return;
     }
     uint64_t* A = col + R;
-    if (tid == 0) { S.n_ext = 0; S.npairs = 0; }
+    const uint32_t winrows = rows < size_t(kPanelWin) ? uint32_t(rows) : uint32_t(kPanelWin);
+    for (uint32_t x = tid; x < winrows; x += kPanelThreads) {
+        S.win[x] = A[x];
+        S.orig[x] = x;
+    }
+    __syncthreads();
+    if (tid >= 32) return;
 
-    // warp-0 registers: Z_l, Z_{l+32}, M_l, M_{l+32}
-    uint64_t z0 = 1ull << lane, z1 = 1ull << (lane + 32);
-    uint64_t m0 = z0, m1 = z1;
-    uint64_t sel = 0;  // bit k set iff step k selected a row (P_k != -1)
-    size_t ib = 0, loaded = 0;
-    int par = 0;
-    const size_t winrows = rows < size_t(kPanelWin) ? rows : size_t(kPanelWin);
-
+    // transposed Z, M: lane owns columns lane (lo) and lane+32 (hi)
+    uint64_t zlo = 1ull << lane, zhi = 1ull << (lane + 32);
+    uint64_t mlo = zlo, mhi = zhi;
+    uint64_t sel = 0;        // bit k: step k selected a row (P_k != -1)
+    uint32_t ib = 0;         // next pivot slot (relative row)
+    uint32_t n_ext = 0;      // beyond-window rows touched (lane 0 bookkeeping, uniform count)
+    uint32_t max_touch = 0;  // highest window slot touched
     for (int k = 0; k < 64; ++k) {
-        if (warp == 0) {  // c = 2^k xor sum_{i<k, M_i bit k} 2^i   (:989-992)
-            const uint32_t lo = __ballot_sync(0xffffffffu, lane < k && ((m0 >> k) & 1));
-            const uint32_t hi = __ballot_sync(0xffffffffu, lane + 32 < k && ((m1 >> k) & 1));
-            if (lane == 0) S.c = (1ull << k) | lo | (uint64_t(hi) << 32);
-        }
-        __syncthreads();
-        const uint64_t c = S.c;
-        size_t found = kNone;
-        for (size_t base = ib; base < rows; base += kPanelThreads) {  // (:993-1000)
-            const size_t need = (base + kPanelThreads < winrows) ? base + kPanelThreads : winrows;
-            while (loaded < need) {
-                const size_t x = loaded + tid;
-                if (x < winrows) { S.win[x] = A[x]; S.orig[x] = uint32_t(x); }
-                loaded += kPanelThreads;
-                if (loaded > winrows) loaded = winrows;
-                __syncthreads();
-            }
-            const size_t i = base + tid;
-            bool hit = false;
-            if (i < rows) {
-                const uint64_t v = i < size_t(kPanelWin) ? S.win[i] : A[i];
-                hit = __popcll(c & v) & 1;
-            }
-            const uint32_t bal = __ballot_sync(0xffffffffu, hit);
-            if (lane == 0)
-                S.wfirst[par][warp] = bal ? uint32_t(base + warp * 32 + __ffs(bal) - 1) : kNone;
-            __syncthreads();
-            uint32_t f = kNone;
+        const uint64_t lowk = low_mask64(k);
+        const uint64_t mtk = __shfl_sync(0xffffffffu, k < 32 ? mlo : mhi, k & 31);
+        const uint64_t c = (1ull << k) | (mtk & lowk);
+        // ---- pivot search: first row i >= ib with odd popcount(c & A_i) ----
+        uint32_t found = kNone;
+        uint64_t newrow = 0;
+        {
+            const uint32_t i = ib + lane;
+            uint64_t v = 0;
+            uint32_t o = 0;
+            if (i < winrows) { v = S.win[i]; o = S.orig[i]; }
+            else if (i < rows) { v = A[i]; }
+            const uint32_t bal = __ballot_sync(0xffffffffu, i < rows && (__popcll(c & v) & 1));
+            if (bal) {
+                const int f = __ffs(bal) - 1;
+                found = ib + f;
+                newrow = __shfl_sync(0xffffffffu, v, f);
+                if (found < winrows) {  // fast path: both slots are in the window
+                    const uint64_t vb = __shfl_sync(0xffffffffu, v, 0);
+                    const uint32_t of = __shfl_sync(0xffffffffu, o, f);
+                    const uint32_t ob = __shfl_sync(0xffffffffu, o, 0);
+                    if (lane == 0) { S.win[ib] = newrow; S.orig[ib] = of; }
+                    if (lane == f && f != 0) { S.win[found] = vb; S.orig[found] = ob; }
+                    __syncwarp();
+                }
+            } else {
+                // slow path: scan the rest 256 rows at a time, OR-ing what we see
+                uint64_t orr = v;
+                for (size_t base = size_t(ib) + 32; base < rows && found == kNone; base += 256) {
+                    uint32_t hits[8];
 #pragma unroll
-            for (int w = 0; w < kPanelThreads / 32; ++w) f = min(f, S.wfirst[par][w]);
-            par ^= 1;
-            if (f != kNone) { found = f; break; }
-        }
-        if (warp == 0) {
-            const int kl = k & 31;
-            const bool khi = k >= 32;
-            if (found != kNone) {
-                if (lane == 0) {  // A_i <-> A_ib   (:996)
-                    const uint64_t vb = S.win[ib];
-                    uint32_t ob = S.orig[ib];
-                    if (found < size_t(kPanelWin)) {
-                        S.win[ib] = S.win[found];
-                        S.orig[ib] = S.orig[found];
-                        S.win[found] = vb;
-                        S.orig[found] = ob;
-                    } else {
-                        S.win[ib] = A[found];
-                        A[found] = vb;
-                        uint32_t e = 0;
-                        while (e < S.n_ext && S.ext_pos[e] != uint32_t(found)) ++e;
-                        if (e == S.n_ext) {
-                            S.ext_pos[e] = uint32_t(found);
-                            S.ext_orig[e] = uint32_t(found);
-                            S.n_ext = e + 1;
+                    for (int t = 0; t < 8; ++t) {
+                        const size_t ii = base + 32 * t + lane;
+                        uint64_t vv = 0;
+                        if (ii < winrows) vv = S.win[ii];
+                        else if (ii < rows) vv = A[ii];
+                        orr |= vv;
+                        hits[t] = __ballot_sync(0xffffffffu, ii < rows && (__popcll(c & vv) & 1));
+                    }
+#pragma unroll
+                    for (int t = 0; t < 8; ++t)
+                        if (found == kNone && hits[t]) found = uint32_t(base + 32 * t + __ffs(hits[t]) - 1);
+                }
+                if (found == kNone) {
+                    orr = __reduce_or_sync(0xffffffffu, uint32_t(orr)) |
+                          (uint64_t(__reduce_or_sync(0xffffffffu, uint32_t(orr >> 32))) << 32);
+                    if (orr == 0) break;  // only zero rows remain: no further selections
+                } else {
+                    if (lane == 0) {
+                        const uint64_t vb = S.win[ib];
+                        const uint32_t ob = S.orig[ib];
+                        if (found < winrows) {
+                            newrow = S.win[found];
+                            S.win[ib] = newrow;
+                            S.orig[ib] = S.orig[found];
+                            S.win[found] = vb;
+                            S.orig[found] = ob;
+                        } else {
+                            newrow = A[found];
+                            A[found] = vb;
+                            S.win[ib] = newrow;
+                            uint32_t e = 0;
+                            while (e < n_ext && S.ext_pos[e] != found) ++e;
+                            if (e == n_ext) { S.ext_pos[e] = found; S.ext_orig[e] = found; }
+                            S.orig[ib] = S.ext_orig[e];
+                            S.ext_orig[e] = ob;
                         }
-                        S.orig[ib] = S.ext_orig[e];
-                        S.ext_orig[e] = ob;
+                    }
+                    __syncwarp();
+                    newrow = __shfl_sync(0xffffffffu, newrow, 0);
+                    if (found >= winrows) {
+                        const uint32_t e0 = n_ext;  // uniform recount
+                        uint32_t present = 0;
+                        for (uint32_t e = 0; e < e0; ++e) present |= (S.ext_pos[e] == found);
+                        if (!present) ++n_ext;
                     }
                 }
-                __syncwarp();
-                const uint64_t newrow = S.win[ib];  // M_k <- A_ib   (:997)
-                if (lane == kl) { if (khi) m1 = newrow; else m0 = newrow; }
-                sel |= 1ull << k;
             }
-            // Z_k ^= sum_{j<k, y_j} Z_j ; M_k likewise   (:1001-1006)
-            const uint64_t y = __shfl_sync(0xffffffffu, khi ? m1 : m0, kl);
-            uint64_t zc = 0, mc = 0;
-            if (lane < k && ((y >> lane) & 1)) { zc ^= z0; mc ^= m0; }
-            if (lane + 32 < k && ((y >> (lane + 32)) & 1)) { zc ^= z1; mc ^= m1; }
-            const uint64_t zx = xor_reduce64(zc), mx = xor_reduce64(mc);
-            if (lane == kl) {
-                if (khi) { z1 ^= zx; m1 ^= mx; } else { z0 ^= zx; m0 ^= mx; }
-            }
-            const uint64_t zk = __shfl_sync(0xffffffffu, khi ? z1 : z0, kl);
-            const uint64_t mk = __shfl_sync(0xffffffffu, khi ? m1 : m0, kl);
-            // Z_j ^= Z_k, M_j ^= M_k for j<k with c_j   (:1007-1010)
-            if (lane < k && ((c >> lane) & 1)) { z0 ^= zk; m0 ^= mk; }
-            if (lane + 32 < k && ((c >> (lane + 32)) & 1)) { z1 ^= zk; m1 ^= mk; }
         }
-        if (found != kNone) ++ib;
+        if (found == kNone) {
+            // insertion (P_k = -1): M_k stays 2^k, y = 2^k -> only Z_j/M_j ^= 2^k for c_j
+            const uint64_t cm = c & lowk;
+            if ((zlo >> k) & 1) zlo ^= cm;
+            if ((zhi >> k) & 1) zhi ^= cm;
+            if ((mlo >> k) & 1) mlo ^= cm;
+            if ((mhi >> k) & 1) mhi ^= cm;
+            continue;
+        }
+        if (found < winrows && found > max_touch) max_touch = found;
+        sel |= 1ull << k;
+        // M_k <- newrow (bit k of mt_l = bit l of newrow; it was [l==k] before)
+        const uint64_t bk = 1ull << k;
+        mlo = (mlo & ~bk) | (((newrow >> lane) & 1ull) << k);
+        mhi = (mhi & ~bk) | (((newrow >> (lane + 32)) & 1ull) << k);
+        // Z_k ^= sum_{j<k, y_j} Z_j and M_k likewise, y = newrow
+        const uint64_t yk = newrow & lowk;
+        zlo ^= uint64_t(__popcll(zlo & yk) & 1) << k;
+        zhi ^= uint64_t(__popcll(zhi & yk) & 1) << k;
+        mlo ^= uint64_t(__popcll(mlo & yk) & 1) << k;
+        mhi ^= uint64_t(__popcll(mhi & yk) & 1) << k;
+        // Z_j ^= Z_k, M_j ^= M_k for j < k with c_j
+        const uint64_t cm = c & lowk;
+        if ((zlo >> k) & 1) zlo ^= cm;
+        if ((zhi >> k) & 1) zhi ^= cm;
+        if ((mlo >> k) & 1) mlo ^= cm;
+        if ((mhi >> k) & 1) mhi ^= cm;
+        ++ib;
     }
-    __syncthreads();
-    // write back touched window rows and collect the composite permutation
-    for (size_t x = tid; x < loaded; x += kPanelThreads) {
-        const uint32_t o = S.orig[x];
-        if (o != uint32_t(x)) {
+    // ---- composite permutation: window slots with orig != slot, then ext rows ----
+    uint32_t np = 0;
+    const uint32_t span = (ib > 0 ? max_touch + 1 : 0);
+    for (uint32_t x0 = 0; x0 < span; x0 += 32) {
+        const uint32_t x = x0 + lane;
+        const bool moved = x < span && S.orig[x] != x;
+        const uint32_t bal = __ballot_sync(0xffffffffu, moved);
+        if (moved) {
+            const uint32_t e = np + __popc(bal & ((1u << lane) - 1));
             A[x] = S.win[x];
-            const uint32_t e = atomicAdd(&S.npairs, 1u);
-            st->dst[e] = uint32_t(x);
-            st->src[e] = o;
+            st->dst[e] = x;
+            st->src[e] = S.orig[x];
         }
+        np += __popc(bal);
     }
-    __syncthreads();
-    if (tid < int(S.n_ext)) {
-        const uint32_t pos = S.ext_pos[tid], o = S.ext_orig[tid];
-        if (o != pos) {
-            const uint32_t e = atomicAdd(&S.npairs, 1u);
-            st->dst[e] = pos;
-            st->src[e] = o;
+    for (uint32_t e0 = 0; e0 < n_ext; e0 += 32) {
+        const uint32_t e = e0 + lane;
+        const bool moved = e < n_ext && S.ext_orig[e] != S.ext_pos[e];
+        const uint32_t bal = __ballot_sync(0xffffffffu, moved);
+        if (moved) {
+            const uint32_t d = np + __popc(bal & ((1u << lane) - 1));
+            st->dst[d] = S.ext_pos[e];
+            st->src[d] = S.ext_orig[e];
         }
+        np += __popc(bal);
     }
-    if (warp == 0) {
-        // compression: drop the bit positions of inserted rows   (:1011-1015)
-        uint64_t msk = 0;
-        for (int i = 0; i < 64; ++i) {
-            if (!((sel >> i) & 1)) {
-                z0 = ((z0 >> 1) & ~msk) ^ (z0 & msk);
-                z1 = ((z1 >> 1) & ~msk) ^ (z1 & msk);
-            } else {
-                msk = 2 * msk + 1;
-            }
-        }
-        st->Z[lane] = z0;
-        st->Z[lane + 32] = z1;
+    // ---- Z rows back from the transposed form, compressed (:1011-1015) ----
+    uint64_t zr0 = 0, zr1 = 0;  // rows lane, lane+32
+    for (int r = 0; r < 64; ++r) {
+        const uint64_t row = uint64_t(__ballot_sync(0xffffffffu, (zlo >> r) & 1)) |
+                             (uint64_t(__ballot_sync(0xffffffffu, (zhi >> r) & 1)) << 32);
+        if (r == lane) zr0 = row;
+        if (r == lane + 32) zr1 = row;
     }
-    __syncthreads();
-    if (tid == 0) {
+    if (sel != ~0ull) { zr0 = pext64(zr0, sel); zr1 = pext64(zr1, sel); }
+    st->Z[lane] = zr0;
+    st->Z[lane + 32] = zr1;
+    if (lane == 0) {
         st->R = uint32_t(R);
-        st->r = uint32_t(ib);
-        st->npairs = S.npairs;
+        st->r = ib;
+        st->npairs = np;
         st->flags = 0;
     }
 }
@@ -750,6 +1167,12 @@ cudaError_t launch_mask_cols(uint64_t* w, size_t stride, size_t n, size_t m, cud
 cudaError_t init_kernel_attrs() {
     cudaError_t e = cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(kTabBytes));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_update_v2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(kV2Smem));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_update_v3, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(kV3Smem));
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(kTabBytes));
