@@ -94,7 +94,77 @@ constexpr int kNcclUint8 = 1;  // ncclDataType_t ncclUint8 (nccl.h)
 }  // namespace
 
 // ---------------------------------------------------------------------------
+// Opt-in timeline (F2GPU_PROFILE=1): an event after every launch; per-kernel
+// device time = sum of the gaps ending at that kernel's event (so it includes
+// the launch gap in front of it).  Printed to stderr after each decomposition.
+struct Timeline {
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    std::vector<std::pair<cudaEvent_t, const char*>> marks;
+    void mark(cudaStream_t s, const char* what) {
+        if (!on) return;
+        if (marks.size() == pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            pool.push_back(e);
+        }
+        cudaEvent_t e = pool[marks.size()];
+        cudaEventRecord(e, s);
+        marks.emplace_back(e, what);
+    }
+    void report(const char* title) {
+        if (!on || marks.size() < 2) { marks.clear(); return; }
+        cudaEventSynchronize(marks.back().first);
+        std::vector<std::pair<std::string, std::pair<double, int>>> acc;
+        for (size_t i = 1; i < marks.size(); ++i) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, marks[i - 1].first, marks[i].first);
+            auto it = std::find_if(acc.begin(), acc.end(),
+                                   [&](const auto& x) { return x.first == marks[i].second; });
+            if (it == acc.end()) acc.push_back({marks[i].second, {ms, 1}});
+            else { it->second.first += ms; it->second.second += 1; }
+        }
+        float tot = 0;
+        cudaEventElapsedTime(&tot, marks.front().first, marks.back().first);
+        fprintf(stderr, "{\"f2gpu_profile\": \"%s\", \"total_ms\": %.3f", title, tot);
+        for (auto& x : acc)
+            fprintf(stderr, ", \"%s\": [%.3f, %d]", x.first.c_str(), x.second.first, x.second.second);
+        fprintf(stderr, "}\n");
+        marks.clear();
+    }
+    ~Timeline() { for (auto e : pool) cudaEventDestroy(e); }
+};
+
+// Replayable decomposition: the panel loop never synchronises with the host
+// (R and r_j live in device PanelStates), so for a repeated (matrix, shape) the
+// whole launch sequence is captured once into a CUDA graph and replayed.
+struct GraphCache {
+    uint64_t* w = nullptr;
+    size_t stride = 0, n = 0, mu = 0;
+    void* st = nullptr;
+    int seen = 0;                 // eager runs with this key
+    cudaGraphExec_t exec = nullptr;
+    uint64_t nodes = 0;
+    void reset() {
+        if (exec) cudaGraphExecDestroy(exec);
+        exec = nullptr;
+        seen = 0;
+        nodes = 0;
+        w = nullptr;
+    }
+    bool match(uint64_t* w_, size_t s_, size_t n_, size_t mu_, void* st_) const {
+        return w == w_ && stride == s_ && n == n_ && mu == mu_ && st == st_;
+    }
+};
+
 struct f2gpu_ctx {
+    Timeline tl;
+    GraphCache graph;
+    bool use_graphs = true;
+    void* scr_st = nullptr;   // persistent PanelState[mu]
+    size_t scr_st_cap = 0;
+    uint32_t* scr_perm = nullptr;
+    size_t scr_perm_cap = 0;
     int device = 0;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
@@ -132,6 +202,7 @@ int count(f2gpu_ctx* c, int n = 1) {
 
 int check_launch(f2gpu_ctx* c, cudaError_t e, const char* what) {
     if (e != cudaSuccess) return set_err(F2GPU_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    c->tl.mark(c->stream, what);
     return count(c);
 }
 
@@ -262,11 +333,9 @@ size_t first_local_after(size_t j, int g, int G) {
 int step_single(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t j) {
     uint64_t* colj = s.w.p + j * s.w.stride;
     F2_TRY(check_launch(c, f2::launch_panel(colj, n, s.st, int(j), c->stream), "k_panel"));
-    F2_TRY(check_launch(c, f2::launch_swaps(s.w.p, s.w.stride, int(mu), int(j), s.perm, s.st + j,
-                                            c->stream),
-                        "k_swaps"));
-    F2_TRY(check_launch(c, f2::launch_panel_y(colj, n, s.st + j, c->num_sms, c->stream),
-                        "k_panel_y"));
+    F2_TRY(check_launch(c, f2::launch_post(s.w.p, s.w.stride, int(mu), int(j), s.perm, n,
+                                           s.st + j, c->stream),
+                        "k_post"));
     if (j + 1 < mu) {
         f2::UpdateArgs u{};
         u.C = s.w.p; u.sc = s.w.stride; u.c_wcol0 = j + 1; u.ncols = int(mu - j - 1);
@@ -296,6 +365,32 @@ int read_results(f2gpu_ctx* c, const Shard& s, size_t n, size_t mu, uint32_t* pe
     return F2GPU_OK;
 }
 
+int ensure_scratch(f2gpu_ctx* c, size_t n, size_t mu) {
+    if (c->scr_st_cap < mu || c->scr_perm_cap < n) {
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        c->graph.reset();  // graphs hold the old pointers
+        if (c->scr_st_cap < mu) {
+            cudaFree(c->scr_st);
+            c->scr_st = nullptr;
+            CUDA_TRY(cudaMalloc(&c->scr_st, mu * kStateBytes));
+            c->scr_st_cap = mu;
+        }
+        if (c->scr_perm_cap < n) {
+            cudaFree(c->scr_perm);
+            c->scr_perm = nullptr;
+            CUDA_TRY(cudaMalloc(&c->scr_perm, n * 4));
+            c->scr_perm_cap = n;
+        }
+    }
+    return F2GPU_OK;
+}
+
+int enqueue_single(f2gpu_ctx* c, Shard& s, size_t n, size_t mu) {
+    F2_TRY(check_launch(c, f2::launch_iota(s.perm, n, c->stream), "k_iota"));
+    for (size_t j = 0; j < mu; ++j) F2_TRY(step_single(c, s, n, mu, j));
+    return F2GPU_OK;
+}
+
 int decompose_single(f2gpu_ctx* c, View w, uint32_t* perm, uint32_t* rj, size_t* rank) {
     const size_t n = w.rows, mu = w.wcols();
     if (n == 0 || mu == 0) {
@@ -304,13 +399,40 @@ int decompose_single(f2gpu_ctx* c, View w, uint32_t* perm, uint32_t* rj, size_t*
         if (perm) for (size_t i = 0; i < n; ++i) perm[i] = uint32_t(i);
         return F2GPU_OK;
     }
-    DevBuf stb(c), pb(c);
-    F2_TRY(stb.alloc(mu * kStateBytes));
-    F2_TRY(pb.alloc(n * 4));
+    F2_TRY(ensure_scratch(c, n, mu));
     Shard s;
-    s.w = w; s.lw = mu; s.st = stb.as<f2::PanelState>(); s.perm = pb.as<uint32_t>();
-    F2_TRY(check_launch(c, f2::launch_iota(s.perm, n, c->stream), "k_iota"));
-    for (size_t j = 0; j < mu; ++j) F2_TRY(step_single(c, s, n, mu, j));
+    s.w = w; s.lw = mu; s.st = static_cast<f2::PanelState*>(c->scr_st); s.perm = c->scr_perm;
+    GraphCache& g = c->graph;
+    const bool graphs = c->use_graphs && !c->tl.on;
+    if (graphs && g.match(w.p, w.stride, n, mu, s.st) && g.exec) {
+        CUDA_TRY(cudaGraphLaunch(g.exec, c->stream));
+        c->launches += g.nodes;
+    } else if (graphs && g.match(w.p, w.stride, n, mu, s.st) && g.seen >= 1) {
+        // second run with this key: capture the launch sequence once, then replay
+        cudaGraph_t graph = nullptr;
+        const uint64_t l0 = c->launches;
+        CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        int rc = enqueue_single(c, s, n, mu);
+        cudaError_t ec = cudaStreamEndCapture(c->stream, &graph);
+        if (rc != F2GPU_OK) { if (graph) cudaGraphDestroy(graph); return rc; }
+        if (ec != cudaSuccess) return set_err(F2GPU_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ec));
+        cudaError_t ei = cudaGraphInstantiate(&g.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ei != cudaSuccess) { g.exec = nullptr; return set_err(F2GPU_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei)); }
+        g.nodes = c->launches - l0;
+        CUDA_TRY(cudaGraphLaunch(g.exec, c->stream));
+    } else {
+        if (graphs) {
+            if (!g.match(w.p, w.stride, n, mu, s.st)) {
+                g.reset();
+                g.w = w.p; g.stride = w.stride; g.n = n; g.mu = mu; g.st = s.st;
+            }
+            g.seen += 1;
+        }
+        c->tl.mark(c->stream, "start");
+        F2_TRY(enqueue_single(c, s, n, mu));
+        c->tl.report("decompose_single");
+    }
     return read_results(c, s, n, mu, perm, rj, rank);
 }
 
@@ -362,11 +484,9 @@ int decompose_sharded(f2gpu_ctx* c, std::vector<Shard>& sh, int shard_base, int 
             Shard& o = sh[ol];
             uint64_t* colj = o.w.p + lj * o.w.stride;
             F2_TRY(check_launch(c, f2::launch_panel(colj, n, o.st, int(j), c->stream), "k_panel"));
-            F2_TRY(check_launch(c, f2::launch_swaps(o.w.p, o.w.stride, int(o.lw), int(lj), o.perm,
-                                                    o.st + j, c->stream),
-                                "k_swaps"));
-            F2_TRY(check_launch(c, f2::launch_panel_y(colj, n, o.st + j, c->num_sms, c->stream),
-                                "k_panel_y"));
+            F2_TRY(check_launch(c, f2::launch_post(o.w.p, o.w.stride, int(o.lw), int(lj), o.perm,
+                                                   n, o.st + j, c->stream),
+                                "k_post"));
             CUDA_TRY(cudaMemcpyAsync(o.bcast, o.st + j, kStateBytes, cudaMemcpyDeviceToDevice,
                                      c->stream));
             CUDA_TRY(cudaMemcpyAsync(o.bcast + kBcastHdr / 8, colj, n * 8,
@@ -440,6 +560,8 @@ int f2gpu_ctx_create(int device, f2gpu_ctx** out) {
     auto c = std::make_unique<f2gpu_ctx>();
     c->device = device;
     c->num_sms = prop.multiProcessorCount;
+    if (const char* pf = getenv("F2GPU_PROFILE")) c->tl.on = pf[0] == '1';
+    if (const char* gr = getenv("F2GPU_GRAPHS")) c->use_graphs = gr[0] != '0';
     CUDA_TRY(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
     c->stream = c->own_stream;
     CUDA_TRY(f2::init_kernel_attrs());
@@ -461,6 +583,9 @@ int f2gpu_ctx_destroy(f2gpu_ctx* c) {
     cudaSetDevice(c->device);
     if (c->comm && nccl().ok) nccl().commDestroy(c->comm);
     if (c->own_stream) cudaStreamSynchronize(c->own_stream);
+    c->graph.reset();
+    cudaFree(c->scr_st);
+    cudaFree(c->scr_perm);
     cudaFree(c->d_jump);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;

@@ -972,9 +972,9 @@ cudaError_t launch_panel(uint64_t* col, size_t n, PanelState* st_all, int j, cud
 // ---------------------------------------------------------------------------
 // Y = D*Z over D (rows R+r .. n of the panel column), written in place
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_panel_y(uint64_t* __restrict__ col, size_t n,
-                                                 const PanelState* __restrict__ st) {
-    __shared__ uint64_t zt[kTabEntries];
+__device__ __forceinline__ void panel_y_body(uint64_t* __restrict__ col, size_t n,
+                                             const PanelState* __restrict__ st, uint64_t* zt,
+                                             unsigned blk, unsigned nblk) {
     const size_t R = st->R, r = st->r;
     const size_t lo = R + r;
     if (r == 0 || lo >= n) return;
@@ -1001,8 +1001,8 @@ __global__ void __launch_bounds__(256) k_panel_y(uint64_t* __restrict__ col, siz
         for (int g = 0; g < 32; ++g) dst[g] = v[g];
     }
     __syncthreads();
-    for (size_t i = lo + size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += size_t(gridDim.x) * blockDim.x) {
+    for (size_t i = lo + size_t(blk) * blockDim.x + threadIdx.x; i < n;
+         i += size_t(nblk) * blockDim.x) {
         const uint64_t d = col[i];
         uint64_t y = 0;
 #pragma unroll
@@ -1010,6 +1010,12 @@ __global__ void __launch_bounds__(256) k_panel_y(uint64_t* __restrict__ col, siz
         y ^= zt[1024 + int(d >> 56)];
         col[i] = y;
     }
+}
+
+__global__ void __launch_bounds__(256) k_panel_y(uint64_t* __restrict__ col, size_t n,
+                                                 const PanelState* __restrict__ st) {
+    __shared__ uint64_t zt[kTabEntries];
+    panel_y_body(col, n, st, zt, blockIdx.x, gridDim.x);
 }
 
 cudaError_t launch_panel_y(uint64_t* col, size_t n, const PanelState* st, int num_sms,
@@ -1022,11 +1028,9 @@ cudaError_t launch_panel_y(uint64_t* col, size_t n, const PanelState* st, int nu
 // K6: apply the panel's composite row permutation to word-columns (+ perm)
 // ---------------------------------------------------------------------------
 // One warp per word-column; column index == ncols handles the uint32 perm.
-__global__ void __launch_bounds__(256) k_swaps(uint64_t* __restrict__ w, size_t stride,
-                                               int ncols, int skip_col,
-                                               uint32_t* __restrict__ perm,
-                                               const PanelState* __restrict__ st) {
-    const int gw = int((size_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+__device__ __forceinline__ void swaps_body(uint64_t* __restrict__ w, size_t stride, int ncols,
+                                           int skip_col, uint32_t* __restrict__ perm,
+                                           const PanelState* __restrict__ st, int gw) {
     const int lane = threadIdx.x & 31;
     if (gw > ncols || gw == skip_col) return;
     const uint32_t np = st->npairs;
@@ -1055,10 +1059,42 @@ __global__ void __launch_bounds__(256) k_swaps(uint64_t* __restrict__ w, size_t 
         if (lane + 32 * e < int(np)) cp[st->dst[lane + 32 * e]] = v[e];
 }
 
+__global__ void __launch_bounds__(256) k_swaps(uint64_t* __restrict__ w, size_t stride,
+                                               int ncols, int skip_col,
+                                               uint32_t* __restrict__ perm,
+                                               const PanelState* __restrict__ st) {
+    swaps_body(w, stride, ncols, skip_col, perm, st,
+               int((size_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5));
+}
+
 cudaError_t launch_swaps(uint64_t* w, size_t stride, int ncols, int skip_col, uint32_t* perm,
                          const PanelState* st, cudaStream_t s) {
     const int warps = ncols + 1;
     k_swaps<<<(warps + 7) / 8, 256, 0, s>>>(w, stride, ncols, skip_col, perm, st);
+    return cudaGetLastError();
+}
+
+// Swaps on every other word-column (+perm) and Y = D*Z on the panel column in
+// ONE launch: the two touch disjoint data (skip_col is the panel column).
+constexpr int kPostYBlocks = 64;
+__global__ void __launch_bounds__(256) k_post(uint64_t* __restrict__ w, size_t stride, int ncols,
+                                              int panel_col, uint32_t* __restrict__ perm,
+                                              size_t n, const PanelState* __restrict__ st,
+                                              int swap_blocks) {
+    __shared__ uint64_t zt[kTabEntries];
+    if (int(blockIdx.x) < swap_blocks) {
+        swaps_body(w, stride, ncols, panel_col, perm, st,
+                   int((size_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5));
+        return;
+    }
+    panel_y_body(w + size_t(panel_col) * stride, n, st, zt, blockIdx.x - swap_blocks, kPostYBlocks);
+}
+
+cudaError_t launch_post(uint64_t* w, size_t stride, int ncols, int panel_col, uint32_t* perm,
+                        size_t n, const PanelState* st, cudaStream_t s) {
+    const int swap_blocks = (ncols + 1 + 7) / 8;
+    k_post<<<swap_blocks + kPostYBlocks, 256, 0, s>>>(w, stride, ncols, panel_col, perm, n, st,
+                                                        swap_blocks);
     return cudaGetLastError();
 }
 

@@ -60,6 +60,9 @@ cudaError_t launch_panel_y(uint64_t* col, size_t n, const PanelState* st, int nu
                            cudaStream_t s);
 cudaError_t launch_swaps(uint64_t* w, size_t stride, int ncols, int skip_col, uint32_t* perm,
                          const PanelState* st, cudaStream_t s);
+// swaps on all columns but panel_col (+perm) and Y on panel_col, one launch
+cudaError_t launch_post(uint64_t* w, size_t stride, int ncols, int panel_col, uint32_t* perm,
+                        size_t n, const PanelState* st, cudaStream_t s);
 // dst = (acc ? dst : 0) ^ a ^ b ^ c ^ d over a rows x wcols block (any input may be null)
 cudaError_t launch_xor(uint64_t* dst, size_t sd, const uint64_t* a, size_t sa,
                        const uint64_t* b, size_t sb, const uint64_t* c, size_t scc,

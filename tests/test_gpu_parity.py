@@ -244,3 +244,29 @@ def test_transpose(f2, ctx, po, n, m):
     dt = f2.DeviceMatrix(m, n, ctx)
     _lib.check(_lib.load().f2gpu_mat_transpose(ctx.handle, da.handle, dt.handle))
     assert same(dt.download().words, want, m)
+
+
+def test_decompose_graph_replay(f2, ctx, po):
+    """Same matrix/shape three times: eager run, graph capture, graph replay —
+    all bit-identical to the oracle (the replay must not reuse stale state)."""
+    import ctypes as C
+
+    from paper_1209_5198_b200 import _lib
+
+    lib = _lib.load()
+    n, m = 3000, 2500
+    for seed in (1, 2):  # second seed: same shape, new content through the replayed graph
+        a = po.random_dense(n, m, 0.5, seed)
+        w, perm, rj, rank = po.decompose_block(a, n, m)
+        A = f2.DeviceMatrix.from_host(f2.BitMatrix(n, m, a), ctx)
+        W = f2.DeviceMatrix(n, m, ctx)
+        for it in range(3):
+            _lib.check(lib.f2gpu_mat_copy(ctx.handle, W.handle, A.handle))
+            p = np.zeros(n, np.uint32)
+            r = np.zeros((m + 63) // 64, np.uint32)
+            rk = C.c_size_t()
+            _lib.check(lib.f2gpu_decompose_block(ctx.handle, W.handle, p.ctypes.data,
+                                                 r.ctypes.data, C.byref(rk)))
+            got = W.download()
+            assert rk.value == rank and np.array_equal(p, perm) and np.array_equal(r, rj)
+            assert np.array_equal(got.words[:, :n], w[:, :n]), (seed, it)
