@@ -161,6 +161,11 @@ struct f2gpu_ctx {
     Timeline tl;
     GraphCache graph;
     bool use_graphs = true;
+    bool lookahead = true;
+    cudaStream_t side = nullptr;          // lookahead: panel kernels run here
+    cudaEvent_t ev_post = nullptr, ev_panel = nullptr;
+    uint32_t* scr_flags = nullptr;        // per-panel early-release counters
+    size_t scr_flags_cap = 0;
     void* scr_st = nullptr;   // persistent PanelState[mu]
     size_t scr_st_cap = 0;
     uint32_t* scr_perm = nullptr;
@@ -366,7 +371,7 @@ int read_results(f2gpu_ctx* c, const Shard& s, size_t n, size_t mu, uint32_t* pe
 }
 
 int ensure_scratch(f2gpu_ctx* c, size_t n, size_t mu) {
-    if (c->scr_st_cap < mu || c->scr_perm_cap < n) {
+    if (c->scr_st_cap < mu || c->scr_perm_cap < n || c->scr_flags_cap < mu) {
         CUDA_TRY(cudaStreamSynchronize(c->stream));
         c->graph.reset();  // graphs hold the old pointers
         if (c->scr_st_cap < mu) {
@@ -381,11 +386,59 @@ int ensure_scratch(f2gpu_ctx* c, size_t n, size_t mu) {
             CUDA_TRY(cudaMalloc(&c->scr_perm, n * 4));
             c->scr_perm_cap = n;
         }
+        if (c->scr_flags_cap < mu) {
+            cudaFree(c->scr_flags);
+            c->scr_flags = nullptr;
+            CUDA_TRY(cudaMalloc(&c->scr_flags, mu * 4));
+            c->scr_flags_cap = mu;
+        }
     }
     return F2GPU_OK;
 }
 
+// Lookahead schedule (two streams, capture-able):
+//   main: POST(j) -> U(j) [SMs-1 CTAs, column j+1 first, then release flag j]
+//   side: P(j+1) waits POST(j) (event) and then spins on flag j on the spare SM,
+//         so the panel factorisation of j+1 overlaps the bulk of update j.
+//   main waits P(j+1) (event) before POST(j+1).
+int enqueue_lookahead(f2gpu_ctx* c, Shard& s, size_t n, size_t mu) {
+    const int grid = c->num_sms - 1;
+    CUDA_TRY(cudaMemsetAsync(c->scr_flags, 0, mu * 4, c->stream));
+    F2_TRY(check_launch(c, f2::launch_iota(s.perm, n, c->stream), "k_iota"));
+    F2_TRY(check_launch(c, f2::launch_panel(s.w.p, n, s.st, 0, c->stream), "k_panel"));
+    for (size_t j = 0; j < mu; ++j) {
+        uint64_t* colj = s.w.p + j * s.w.stride;
+        if (j > 0) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_panel, 0));
+        F2_TRY(check_launch(c, f2::launch_post(s.w.p, s.w.stride, int(mu), int(j), s.perm, n,
+                                               s.st + j, c->stream),
+                            "k_post"));
+        if (j + 1 >= mu) break;
+        CUDA_TRY(cudaEventRecord(c->ev_post, c->stream));
+        f2::UpdateArgs u{};
+        u.C = s.w.p; u.sc = s.w.stride; u.c_wcol0 = j + 1; u.ncols = int(mu - j - 1);
+        u.row_lo = 0; u.row_hi = n; u.a = colj; u.k_bits = 0;
+        u.B = s.w.p; u.sb = s.w.stride; u.b_row0 = 0; u.b_wcol0 = j + 1;
+        u.st = s.st + j;
+        u.release = c->scr_flags + j;
+        F2_TRY(check_launch(c, f2::launch_update(u, grid, c->stream), "k_update"));
+        CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_post, 0));
+        F2_TRY(check_launch(c, f2::launch_panel(s.w.p + (j + 1) * s.w.stride, n, s.st, int(j + 1),
+                                                c->side, c->scr_flags + j, uint32_t(grid)),
+                            "k_panel"));
+        CUDA_TRY(cudaEventRecord(c->ev_panel, c->side));
+    }
+    return F2GPU_OK;
+}
+
+bool lookahead_ok(f2gpu_ctx* c, const Shard& s, size_t n) {
+    if (!c->lookahead || c->num_sms < 2 || !c->side) return false;
+    f2::UpdateArgs u{};
+    u.C = s.w.p; u.sc = s.w.stride; u.a = s.w.p; u.row_hi = n;
+    return f2::update_fast_ok(u);
+}
+
 int enqueue_single(f2gpu_ctx* c, Shard& s, size_t n, size_t mu) {
+    if (lookahead_ok(c, s, n)) return enqueue_lookahead(c, s, n, mu);
     F2_TRY(check_launch(c, f2::launch_iota(s.perm, n, c->stream), "k_iota"));
     for (size_t j = 0; j < mu; ++j) F2_TRY(step_single(c, s, n, mu, j));
     return F2GPU_OK;
@@ -562,6 +615,10 @@ int f2gpu_ctx_create(int device, f2gpu_ctx** out) {
     c->num_sms = prop.multiProcessorCount;
     if (const char* pf = getenv("F2GPU_PROFILE")) c->tl.on = pf[0] == '1';
     if (const char* gr = getenv("F2GPU_GRAPHS")) c->use_graphs = gr[0] != '0';
+    if (const char* la = getenv("F2GPU_LOOKAHEAD")) c->lookahead = la[0] != '0';
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_post, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_panel, cudaEventDisableTiming));
     CUDA_TRY(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
     c->stream = c->own_stream;
     CUDA_TRY(f2::init_kernel_attrs());
@@ -586,6 +643,10 @@ int f2gpu_ctx_destroy(f2gpu_ctx* c) {
     c->graph.reset();
     cudaFree(c->scr_st);
     cudaFree(c->scr_perm);
+    cudaFree(c->scr_flags);
+    if (c->side) { cudaStreamSynchronize(c->side); cudaStreamDestroy(c->side); }
+    if (c->ev_post) cudaEventDestroy(c->ev_post);
+    if (c->ev_panel) cudaEventDestroy(c->ev_panel);
     cudaFree(c->d_jump);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;

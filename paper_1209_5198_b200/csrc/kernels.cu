@@ -184,6 +184,61 @@ __device__ __forceinline__ uint64_t lookup(const uint64_t* __restrict__ tl, uint
     return acc;
 }
 
+// Lookup with the table at a FIXED shared-window address (kTabAddr): the byte
+// offset of entry g of table t for column col is t*16384 + g*128 + col*8, so a
+// lookup is one shift + one LOP3 ((x & 0x3F80) | col*8) + LDS [reg + t*16384 + kTabAddr].
+constexpr uint32_t kTabAddr = 0x10000;
+template <int T>
+__device__ __forceinline__ uint32_t tab_off(uint32_t lo, uint32_t hi, uint32_t colofs) {
+    // byte offset of the entry selected by group T of the 64-bit word (hi:lo)
+    uint32_t x;
+    if (T == 0) x = lo << 7;
+    else if (T == 1) x = lo;
+    else if (T == 2) x = lo >> 7;
+    else if (T == 3) x = lo >> 14;
+    else if (T == 4) x = __funnelshift_r(lo, hi, 21);
+    else if (T == 5) x = __funnelshift_r(lo, hi, 28);
+    else if (T == 6) x = hi >> 3;
+    else if (T == 7) x = hi >> 10;
+    else x = hi >> 17;  // 8-bit group at bit 56
+    return T == 8 ? ((x & 0x7F80u) | colofs) : ((x & 0x3F80u) | colofs);
+}
+template <int T>
+__device__ __forceinline__ void lds_tab(uint32_t off, uint32_t& a, uint32_t& b) {
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2 + %3];"
+                 : "=r"(a), "=r"(b)
+                 : "r"(off), "n"(kTabAddr + T * 16384));
+}
+// XOR of the nt (<= 9) entries addressed by the groups of word (hi:lo)
+__device__ __forceinline__ uint64_t lookup_fixed(uint32_t colofs, uint64_t w, int nt) {
+    const uint32_t lo = uint32_t(w), hi = uint32_t(w >> 32);
+    uint32_t a0, b0, a1, b1, a2, b2, a3, b3, a4, b4, a5, b5, a6, b6, a7, b7, a8, b8;
+    if (nt == 9) {
+        lds_tab<0>(tab_off<0>(lo, hi, colofs), a0, b0);
+        lds_tab<1>(tab_off<1>(lo, hi, colofs), a1, b1);
+        lds_tab<2>(tab_off<2>(lo, hi, colofs), a2, b2);
+        lds_tab<3>(tab_off<3>(lo, hi, colofs), a3, b3);
+        lds_tab<4>(tab_off<4>(lo, hi, colofs), a4, b4);
+        lds_tab<5>(tab_off<5>(lo, hi, colofs), a5, b5);
+        lds_tab<6>(tab_off<6>(lo, hi, colofs), a6, b6);
+        lds_tab<7>(tab_off<7>(lo, hi, colofs), a7, b7);
+        lds_tab<8>(tab_off<8>(lo, hi, colofs), a8, b8);
+        const uint32_t x = a0 ^ a1 ^ a2 ^ a3 ^ a4 ^ a5 ^ a6 ^ a7 ^ a8;
+        const uint32_t y = b0 ^ b1 ^ b2 ^ b3 ^ b4 ^ b5 ^ b6 ^ b7 ^ b8;
+        return (uint64_t(y) << 32) | x;
+    }
+    uint32_t x = 0, y = 0;
+#define F2_LK(T)                                                   \
+    if (T < nt) {                                                  \
+        lds_tab<T>(tab_off<T>(lo, hi, colofs), a##T, b##T);        \
+        x ^= a##T;                                                 \
+        y ^= b##T;                                                 \
+    }
+    F2_LK(0) F2_LK(1) F2_LK(2) F2_LK(3) F2_LK(4) F2_LK(5) F2_LK(6) F2_LK(7) F2_LK(8)
+#undef F2_LK
+    return (uint64_t(y) << 32) | x;
+}
+
 // ---------------------------------------------------------------------------
 // K2: fused table build + XOR update (the Schur update / mult_acc)
 // ---------------------------------------------------------------------------
@@ -478,8 +533,12 @@ constexpr int kV3AStages = 8;
 constexpr int kV3ColPitch = kV3Rows * 8 + 16;     // 1040 B: conflict-free 128-bit smem access
 constexpr int kV3DBytes = kTabCols * kV3ColPitch; // 16640 B per delta tile
 constexpr int kV3ABytes = kV3Rows * 8;            // 1 KiB of driving words
-constexpr size_t kV3Smem =
-    kTabBytes + size_t(kV3DStages) * kV3DBytes + size_t(kV3AStages) * kV3ABytes + 256;
+constexpr size_t kV3RingBytes = size_t(kV3DStages) * kV3DBytes + size_t(kV3AStages) * kV3ABytes + 256;
+// dynamic smem: [rings + barriers | pad] below kTabAddr, then the tables at kTabAddr
+// (the dynamic window starts at most 1 KiB into the shared address space)
+constexpr size_t kV3Smem = kTabAddr + kTabBytes;
+static_assert(kV3RingBytes + 1024 <= kTabAddr, "rings must fit below the table window");
+static_assert(kV3Smem <= 232448, "exceeds the 227 KiB per-CTA limit");
 
 __device__ __forceinline__ void bulk_red_xor(void* dst, const void* src, uint32_t bytes) {
     asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.xor.b64 [%0], [%1], %2;" ::"l"(dst),
@@ -490,15 +549,37 @@ __device__ __forceinline__ void v3_consumers_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(kV3Warps * 32) : "memory");
 }
 
+// per-CTA tile sequence: up to two contiguous segments of the flattened
+// (group, tile) space, walked with incremental cursors (no per-tile divides)
+struct TileCursor {
+    size_t T, g, tt, i, len0, s1;
+    __device__ void init(size_t T_, size_t s0, size_t len0_, size_t s1_) {
+        T = T_; i = 0; len0 = len0_; s1 = s1_;
+        const size_t u = len0 ? s0 : s1;
+        g = u / T; tt = u % T;
+    }
+    __device__ void next() {
+        if (++i == len0) { g = s1 / T; tt = s1 % T; }
+        else if (++tt == T) { tt = 0; ++g; }
+    }
+};
+
+__device__ __forceinline__ void release_signal(uint32_t* flag) {
+    __threadfence();
+    atomicAdd(flag, 1u);
+}
+
 __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    uint64_t* tab = reinterpret_cast<uint64_t*>(smem_raw);
-    unsigned char* dring = smem_raw + kTabBytes;
+    const uint32_t smem_base = smem_u32(smem_raw);
+    if (smem_base > kTabAddr - kV3RingBytes) __trap();  // layout assumption violated
+    uint64_t* tab = reinterpret_cast<uint64_t*>(smem_raw + (kTabAddr - smem_base));
+    unsigned char* dring = smem_raw;
     unsigned char* aring = dring + size_t(kV3DStages) * kV3DBytes;
     uint64_t* bars = reinterpret_cast<uint64_t*>(aring + size_t(kV3AStages) * kV3ABytes);
     uint64_t* a_full = bars;                       // [kV3AStages] tx barrier
-    uint64_t* a_empty = a_full + kV3AStages;       // [kV3AStages] 8 consumer warps
-    uint64_t* d_done = a_empty + kV3AStages;       // [kV3DStages] 8 consumer warps
+    uint64_t* a_empty = a_full + kV3AStages;       // [kV3AStages] consumer warps
+    uint64_t* d_done = a_empty + kV3AStages;       // [kV3DStages] consumer warps
     uint64_t* d_free = d_done + kV3DStages;        // [kV3DStages] producer
 
     size_t row_lo = p.row_lo, b_row0 = p.b_row0;
@@ -510,16 +591,34 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
         b_row0 = R;
     }
     const size_t row_hi = p.row_hi;
-    if (k <= 0 || row_lo >= row_hi || p.ncols <= 0) return;
+    if (k <= 0 || row_lo >= row_hi || p.ncols <= 0) {
+        if (p.release && threadIdx.x == 0) release_signal(p.release);
+        return;
+    }
     const int nt = k > 56 ? 9 : (k + 6) / 7;
     const size_t base = row_lo & ~size_t(kV3Rows - 1);
     const size_t T = (row_hi - base + kV3Rows - 1) / kV3Rows;  // tiles per column group
     const size_t ncg = (size_t(p.ncols) + kTabCols - 1) / kTabCols;
-    const size_t TU = T * ncg;
-    const size_t u0 = TU * blockIdx.x / gridDim.x;
-    const size_t u1 = TU * (blockIdx.x + 1) / gridDim.x;
-    if (u0 >= u1) return;
-    const size_t cnt = u1 - u0;
+    const size_t G = gridDim.x, b = blockIdx.x;
+    size_t s0, len0, s1, len1;
+    if (p.release) {  // group 0 spread over every CTA first, then the rest
+        s0 = T * b / G;
+        len0 = T * (b + 1) / G - s0;
+        const size_t TB = T * (ncg - 1);
+        s1 = T + TB * b / G;
+        len1 = T + TB * (b + 1) / G - s1;
+    } else {
+        const size_t TU = T * ncg;
+        s0 = TU * b / G;
+        len0 = TU * (b + 1) / G - s0;
+        s1 = s0 + len0;
+        len1 = 0;
+    }
+    const size_t cnt = len0 + len1;
+    if (cnt == 0) {
+        if (p.release && threadIdx.x == 0) release_signal(p.release);
+        return;
+    }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kV3AStages; ++s) {
@@ -536,34 +635,38 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
 
     if (warp == kV3Warps) {
         // ===== producer warp =====
-        // tile cursors advance incrementally (no 64-bit divisions per tile)
-        size_t ag = u0 / T, at = u0 % T;   // next A tile to load
+        TileCursor ac;
+        ac.init(T, s0, len0, s1);
         uint32_t a_stage = 0;
         auto issue_a = [&]() {
             if (lane == 0) {
                 mbar_expect_tx(&a_full[a_stage], kV3ABytes);
-                bulk_g2s(aring + size_t(a_stage) * kV3ABytes, p.a + base + at * kV3Rows, kV3ABytes,
-                         &a_full[a_stage]);
+                bulk_g2s(aring + size_t(a_stage) * kV3ABytes, p.a + base + ac.tt * kV3Rows,
+                         kV3ABytes, &a_full[a_stage]);
             }
-            if (++at == T) { at = 0; ++ag; }
+            ac.next();
             if (++a_stage == kV3AStages) a_stage = 0;
         };
+        if (p.release && len0 == 0 && lane == 0) release_signal(p.release);
         const size_t pre = cnt < size_t(kV3AStages) ? cnt : size_t(kV3AStages);
         for (size_t i = 0; i < pre; ++i) issue_a();
-        size_t g = u0 / T, tt = u0 % T;
+        TileCursor dc;
+        dc.init(T, s0, len0, s1);
         int s = 0, ae = 0;
         uint32_t dph = 0, aph = 0;
         for (size_t t = 0; t < cnt; ++t) {
-            const size_t r0 = base + tt * kV3Rows;
-            const int nvalid = min(kTabCols, int(size_t(p.ncols) - g * kTabCols));
+            const size_t r0 = base + dc.tt * kV3Rows;
+            const int nvalid = min(kTabCols, int(size_t(p.ncols) - dc.g * kTabCols));
             mbar_wait(&d_done[s], dph);
             if (lane < nvalid) {
-                bulk_red_xor(p.C + (p.c_wcol0 + g * kTabCols + lane) * p.sc + r0,
+                bulk_red_xor(p.C + (p.c_wcol0 + dc.g * kTabCols + lane) * p.sc + r0,
                              dring + size_t(s) * kV3DBytes + lane * kV3ColPitch, kV3ABytes);
                 bulk_commit();
-                bulk_wait_read0();
+                if (p.release && t + 1 == len0) bulk_wait0();  // group-0 writes complete
+                else bulk_wait_read0();
             }
             __syncwarp();
+            if (p.release && t + 1 == len0 && lane == 0) release_signal(p.release);
             if (lane == 0) mbar_arrive(&d_free[s]);
             if (t + kV3AStages < cnt) {
                 mbar_wait(&a_empty[ae], aph);
@@ -571,7 +674,7 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
             }
             if (++ae == kV3AStages) { ae = 0; aph ^= 1; }
             if (++s == kV3DStages) { s = 0; dph ^= 1; }
-            if (++tt == T) { tt = 0; ++g; }
+            dc.next();
         }
         bulk_wait0();
         return;
@@ -579,13 +682,15 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
 
     // ===== consumer warps =====
     const int h = lane >> 4, col = lane & 15;
-    const uint64_t* tl = tab + col;
+    const uint32_t colofs = uint32_t(col) * 8u;
     const int rl = 8 * warp + 4 * h;  // this lane's 4 rows within the tile
     size_t gcur = ~size_t(0);
-    size_t g = u0 / T, tt = u0 % T;
+    TileCursor cc;
+    cc.init(T, s0, len0, s1);
     int as = 0, s = 0;
     uint32_t aph = 0, dph = 0;
     for (size_t t = 0; t < cnt; ++t) {
+        const size_t g = cc.g;
         if (g != gcur) {
             v3_consumers_sync();
             const int nvalid = min(kTabCols, int(size_t(p.ncols) - g * kTabCols));
@@ -605,7 +710,7 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&a_empty[as]);
-        const size_t row = base + tt * kV3Rows + rl;
+        const size_t row = base + cc.tt * kV3Rows + rl;
         if (row < row_lo || row + 4 > row_hi) {
 #pragma unroll
             for (int q = 0; q < 4; ++q)
@@ -613,7 +718,7 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
         }
         uint64_t d[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) d[q] = lookup(tl, x[q], nt);
+        for (int q = 0; q < 4; ++q) d[q] = lookup_fixed(colofs, x[q], nt);
         if (t >= size_t(kV3DStages)) mbar_wait(&d_free[s], dph ^ 1);
         ulonglong2* dp = reinterpret_cast<ulonglong2*>(dring + size_t(s) * kV3DBytes + col * kV3ColPitch) + rl / 2;
         dp[0] = make_ulonglong2(d[0], d[1]);
@@ -623,17 +728,21 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
         if (lane == 0) mbar_arrive(&d_done[s]);
         if (++as == kV3AStages) { as = 0; aph ^= 1; }
         if (++s == kV3DStages) { s = 0; dph ^= 1; }
-        if (++tt == T) { tt = 0; ++g; }
+        cc.next();
     }
 }
 
+bool update_fast_ok(const UpdateArgs& a);
 bool update_v3_ok(const UpdateArgs& a) {
     return (a.sc % kV3Rows) == 0 && (reinterpret_cast<uintptr_t>(a.C) % 16) == 0 &&
            (reinterpret_cast<uintptr_t>(a.a) % 16) == 0 && a.row_hi <= a.sc;
 }
 
+bool update_fast_ok(const UpdateArgs& a) { return update_v3_ok(a); }
+
 cudaError_t launch_update(const UpdateArgs& a, int num_sms, cudaStream_t s) {
     if (a.ncols <= 0) return cudaSuccess;
+    if (a.release && !update_v3_ok(a)) return cudaErrorInvalidValue;
     if (update_v3_ok(a)) {
         k_update_v3<<<num_sms, kV3Threads, kV3Smem, s>>>(a);
         return cudaGetLastError();
@@ -782,10 +891,23 @@ __device__ __forceinline__ uint64_t pext64(uint64_t x, uint64_t sel) {
 }
 
 __global__ void __launch_bounds__(kPanelThreads, 1)
-    k_panel(uint64_t* __restrict__ col, size_t n, PanelState* __restrict__ st_all, int j) {
+    k_panel(uint64_t* __restrict__ col, size_t n, PanelState* __restrict__ st_all, int j,
+            const uint32_t* wait_flag, uint32_t wait_count) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     PanelSmem& S = *reinterpret_cast<PanelSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31;
+    if (wait_flag) {
+        // lookahead: the previous panel's update releases this column early
+        if (tid == 0) {
+            uint32_t v;
+            while (true) {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(wait_flag) : "memory");
+                if (v >= wait_count) break;
+                __nanosleep(64);
+            }
+        }
+        __syncthreads();
+    }
     const size_t R = j == 0 ? 0 : size_t(st_all[j - 1].R) + st_all[j - 1].r;
     PanelState* st = st_all + j;
     const size_t rows = R < n ? n - R : 0;
@@ -964,8 +1086,9 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
     }
 }
 
-cudaError_t launch_panel(uint64_t* col, size_t n, PanelState* st_all, int j, cudaStream_t s) {
-    k_panel<<<1, kPanelThreads, sizeof(PanelSmem), s>>>(col, n, st_all, j);
+cudaError_t launch_panel(uint64_t* col, size_t n, PanelState* st_all, int j, cudaStream_t s,
+                         const uint32_t* wait_flag, uint32_t wait_count) {
+    k_panel<<<1, kPanelThreads, sizeof(PanelSmem), s>>>(col, n, st_all, j, wait_flag, wait_count);
     return cudaGetLastError();
 }
 

@@ -42,6 +42,11 @@ struct UpdateArgs {
     int k_bits;
     const uint64_t* B; size_t sb; size_t b_row0; size_t b_wcol0;
     const PanelState* st;  // non-null: R,r from state -> row_lo=R+r, k=r, b_row0=R
+    // Early release (lookahead): when non-null, column group 0 (the next panel's
+    // column) is split over ALL CTAs and done first; each CTA then increments
+    // *release once its group-0 updates are complete in memory (exactly once per
+    // CTA, also when it has no work).  The next panel kernel waits for the count.
+    uint32_t* release;
 };
 
 struct GemmArgs {
@@ -55,7 +60,10 @@ cudaError_t launch_random_dense(uint64_t* w, size_t n, size_t m, size_t stride, 
                                 uint64_t seed, const uint64_t* d_jump, cudaStream_t s);
 cudaError_t launch_update(const UpdateArgs& a, int num_sms, cudaStream_t s);
 cudaError_t launch_gemm(const GemmArgs& g, int num_sms, cudaStream_t s);
-cudaError_t launch_panel(uint64_t* col, size_t n, PanelState* st_all, int j, cudaStream_t s);
+cudaError_t launch_panel(uint64_t* col, size_t n, PanelState* st_all, int j, cudaStream_t s,
+                         const uint32_t* wait_flag = nullptr, uint32_t wait_count = 0);
+// can launch_update take the bulk-reduction path (required for early release)?
+bool update_fast_ok(const UpdateArgs& a);
 cudaError_t launch_panel_y(uint64_t* col, size_t n, const PanelState* st, int num_sms,
                            cudaStream_t s);
 cudaError_t launch_swaps(uint64_t* w, size_t stride, int ncols, int skip_col, uint32_t* perm,
