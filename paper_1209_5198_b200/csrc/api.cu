@@ -192,13 +192,14 @@ namespace {
 struct View {  // non-owning device sub-block: rows x cols bits, word (i,q) at p[q*stride+i]
     uint64_t* p;
     size_t rows, cols, stride;
+    size_t cap;   // addressable rows from p within a column (stride - row offset)
     size_t wcols() const { return ceil64(cols); }
     View sub(size_t r0, size_t nr, size_t wc0, size_t nwc) const {
-        return View{p + wc0 * stride + r0, nr, nwc * 64, stride};
+        return View{p + wc0 * stride + r0, nr, nwc * 64, stride, cap - r0};
     }
 };
 
-View view_of(const f2gpu_mat* m) { return View{m->d, m->rows, m->cols, m->stride}; }
+View view_of(const f2gpu_mat* m) { return View{m->d, m->rows, m->cols, m->stride, m->stride}; }
 
 int count(f2gpu_ctx* c, int n = 1) {
     c->launches += uint64_t(n);
@@ -235,7 +236,8 @@ struct DevBuf {  // RAII stream-ordered allocation
 // C ^= A*B on views (stream-K M4RM kernel)
 int gemm_acc(f2gpu_ctx* c, View C, View A, View B) {
     if (A.rows == 0 || A.cols == 0 || B.cols == 0) return F2GPU_OK;
-    f2::GemmArgs g{A.p, A.stride, A.rows, B.p, B.stride, A.cols, C.p, C.stride, int(C.wcols())};
+    f2::GemmArgs g{A.p, A.stride, A.rows, B.p, B.stride, A.cols, C.p, C.stride, int(C.wcols()),
+                   A.cap, B.cap};
     return check_launch(c, f2::launch_gemm(g, c->num_sms, c->stream), "k_gemm");
 }
 
@@ -253,6 +255,7 @@ int xor_views(f2gpu_ctx* c, View dst, bool acc, const View* a, const View* b = n
 int zero_view(f2gpu_ctx* c, View v) {
     if (v.rows == 0 || v.wcols() == 0) return F2GPU_OK;
     CUDA_TRY(cudaMemset2DAsync(v.p, v.stride * 8, 0, v.rows * 8, v.wcols(), c->stream));
+    c->tl.mark(c->stream, "memset2d");
     return F2GPU_OK;
 }
 
@@ -277,8 +280,8 @@ int strassen_acc(f2gpu_ctx* c, View C, View A, View B, size_t cutover) {
     F2_TRY(sb.alloc(ss * kw * 8));
     F2_TRY(tb.alloc(ts * mw * 8));
     F2_TRY(qb.alloc(qs * mw * 8));
-    View S{sb.as<uint64_t>(), n2, k2, ss}, T{tb.as<uint64_t>(), k2, m2, ts},
-        Q{qb.as<uint64_t>(), n2, m2, qs};
+    View S{sb.as<uint64_t>(), n2, k2, ss, ss}, T{tb.as<uint64_t>(), k2, m2, ts, ts},
+        Q{qb.as<uint64_t>(), n2, m2, qs, qs};
     // Q = P1 = A11 B11 ; C11 ^= P1 ; C11 ^= P2 = A12 B21
     F2_TRY(zero_view(c, Q));
     F2_TRY(strassen_acc(c, Q, A11, B11, cutover));
@@ -840,8 +843,11 @@ int f2gpu_strassen_mult(f2gpu_ctx* c, const f2gpu_mat* a, const f2gpu_mat* b, f2
     if (cm->rows != a->rows || cm->cols != b->cols)
         return set_err(F2GPU_EINVAL, "strassen_mult: output shape mismatch");
     F2_TRY(f2gpu_mat_zero(c, cm));
-    return strassen_acc(c, view_of(cm), view_of(a), view_of(b),
-                        threshold ? threshold : c->strassen_cutover);
+    c->tl.mark(c->stream, "start");
+    F2_TRY(strassen_acc(c, view_of(cm), view_of(a), view_of(b),
+                        threshold ? threshold : c->strassen_cutover));
+    c->tl.report("strassen");
+    return F2GPU_OK;
 }
 
 // ---- decomposition ----
@@ -864,7 +870,7 @@ int f2gpu_decompose_block_sharded(f2gpu_ctx* c, f2gpu_mat* w, int G, uint32_t* p
         sh[g].lw = f2gpu_local_wcols(mu, g, G);
         keep.emplace_back(c);
         F2_TRY(keep.back().alloc(std::max<size_t>(1, sh[g].lw) * w->stride * 8));
-        sh[g].w = View{keep.back().as<uint64_t>(), n, sh[g].lw * 64, w->stride};
+        sh[g].w = View{keep.back().as<uint64_t>(), n, sh[g].lw * 64, w->stride, w->stride};
         for (size_t l = 0; l < sh[g].lw; ++l)
             CUDA_TRY(cudaMemcpyAsync(sh[g].w.p + l * w->stride, w->d + (g + l * G) * w->stride,
                                      w->stride * 8, cudaMemcpyDeviceToDevice, c->stream));
@@ -994,7 +1000,7 @@ int f2gpu_decompose_block_dist(f2gpu_ctx* c, f2gpu_mat* w_local, size_t m_global
     if (!c->comm) return set_err(F2GPU_ENCCL, "decompose_dist: communicator not initialised");
     std::deque<DevBuf> keep;
     std::vector<Shard> sh(1);
-    sh[0].w = View{w_local->d, n, lw * 64, w_local->stride};
+    sh[0].w = View{w_local->d, n, lw * 64, w_local->stride, w_local->stride};
     sh[0].lw = lw;
     F2_TRY(alloc_shard_aux(c, sh[0], n, mu, keep));
     NcclExchange ex;

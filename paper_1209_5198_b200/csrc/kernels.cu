@@ -11,6 +11,8 @@
 //   k_transpose     64x64 bit-tile transpose               (bit_matrix.hpp:59-70,220-238)
 #include "kernels.cuh"
 
+#include <algorithm>
+
 namespace f2 {
 
 // ---------------------------------------------------------------------------
@@ -209,6 +211,24 @@ __device__ __forceinline__ void lds_tab(uint32_t off, uint32_t& a, uint32_t& b) 
                  : "=r"(a), "=r"(b)
                  : "r"(off), "n"(kTabAddr + T * 16384));
 }
+// all 9 groups (full 64-bit k-block), branch-free
+__device__ __forceinline__ uint64_t lookup9(uint32_t colofs, uint64_t w) {
+    const uint32_t lo = uint32_t(w), hi = uint32_t(w >> 32);
+    uint32_t a0, b0, a1, b1, a2, b2, a3, b3, a4, b4, a5, b5, a6, b6, a7, b7, a8, b8;
+    lds_tab<0>(tab_off<0>(lo, hi, colofs), a0, b0);
+    lds_tab<1>(tab_off<1>(lo, hi, colofs), a1, b1);
+    lds_tab<2>(tab_off<2>(lo, hi, colofs), a2, b2);
+    lds_tab<3>(tab_off<3>(lo, hi, colofs), a3, b3);
+    lds_tab<4>(tab_off<4>(lo, hi, colofs), a4, b4);
+    lds_tab<5>(tab_off<5>(lo, hi, colofs), a5, b5);
+    lds_tab<6>(tab_off<6>(lo, hi, colofs), a6, b6);
+    lds_tab<7>(tab_off<7>(lo, hi, colofs), a7, b7);
+    lds_tab<8>(tab_off<8>(lo, hi, colofs), a8, b8);
+    const uint32_t x = a0 ^ a1 ^ a2 ^ a3 ^ a4 ^ a5 ^ a6 ^ a7 ^ a8;
+    const uint32_t y = b0 ^ b1 ^ b2 ^ b3 ^ b4 ^ b5 ^ b6 ^ b7 ^ b8;
+    return (uint64_t(y) << 32) | x;
+}
+
 // XOR of the nt (<= 9) entries addressed by the groups of word (hi:lo)
 __device__ __forceinline__ uint64_t lookup_fixed(uint32_t colofs, uint64_t w, int nt) {
     const uint32_t lo = uint32_t(w), hi = uint32_t(w >> 32);
@@ -595,7 +615,7 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
         if (p.release && threadIdx.x == 0) release_signal(p.release);
         return;
     }
-    const int nt = k > 56 ? 9 : (k + 6) / 7;
+    const int nt = 9;  // all tables built (rows >= k are zero); lookup9 is branch-free
     const size_t base = row_lo & ~size_t(kV3Rows - 1);
     const size_t T = (row_hi - base + kV3Rows - 1) / kV3Rows;  // tiles per column group
     const size_t ncg = (size_t(p.ncols) + kTabCols - 1) / kTabCols;
@@ -718,7 +738,7 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
         }
         uint64_t d[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) d[q] = lookup_fixed(colofs, x[q], nt);
+        for (int q = 0; q < 4; ++q) d[q] = lookup9(colofs, x[q]);
         if (t >= size_t(kV3DStages)) mbar_wait(&d_free[s], dph ^ 1);
         ulonglong2* dp = reinterpret_cast<ulonglong2*>(dring + size_t(s) * kV3DBytes + col * kV3ColPitch) + rl / 2;
         dp[0] = make_ulonglong2(d[0], d[1]);
@@ -834,12 +854,198 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm(GemmArgs p) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// K1+K2 v2 for products: producer-fed stream-K M4RM GEMM, C ^= A*B
+// ---------------------------------------------------------------------------
+// ncu on v1 (profiles/r1_gemm_r1_summary.txt): instruction-bound (3.55 G
+// instructions for 16384^3, issue 39%) on guarded lookups, with the global-load
+// latency of every k-block's table build exposed.  v2: a producer warp streams
+// each (tile, k-block) unit's A segment (1024 driving words) and B block
+// (64 rows x 16 word-columns) into a 3-stage shared ring with bulk copies; the
+// 16 consumer warps build the tables from shared memory at the fixed table
+// address and run the 3-instruction lookups; accumulators stay in registers
+// across the k-blocks of a tile (stream-K split, atomicXor for shared tiles).
+constexpr int kG2Warps = 16;
+constexpr int kG2Threads = kG2Warps * 32;
+constexpr int kG2Rows = 1024;                     // tile rows (lane owns 32)
+constexpr int kG2Stages = 3;
+constexpr int kG2ABytes = kG2Rows * 8;            // 8 KiB driving words
+constexpr int kG2BPitch = 64 * 8 + 16;            // 528 B: conflict-free 128-bit row-pair loads
+constexpr int kG2BBytes = kTabCols * kG2BPitch;   // 16 columns x 64 rows (padded)
+constexpr int kG2StageBytes = kG2ABytes + kG2BBytes;
+constexpr size_t kG2RingBytes = size_t(kG2Stages) * kG2StageBytes + 64;
+constexpr size_t kG2Smem = kTabAddr + kTabBytes;
+static_assert(kG2RingBytes + 1024 <= kTabAddr, "gemm ring must fit below the table window");
+
+// table build from a shared-memory B block (column c at bs + 64*c, k-row r)
+// 16-entry chunks (smaller register footprint: the GEMM keeps 32 accumulators live)
+__device__ __forceinline__ int tab_chunks16(int nt) { return nt <= 8 ? 8 * nt : 80; }
+
+template <int NTH>
+__device__ __forceinline__ void build_tables_smem(uint64_t* __restrict__ tab,
+                                                  const uint64_t* __restrict__ bs, int ncols_valid,
+                                                  int k_bits, int nt, int tid) {
+    const int total = tab_chunks16(nt) * kTabCols;
+    for (int it = tid; it < total; it += NTH) {
+        const int col = it & (kTabCols - 1);
+        const int cg = it >> 4;
+        const int t = cg < 64 ? (cg >> 3) : 8;
+        const int chunk = cg < 64 ? (cg & 7) : cg - 64;  // high bits (>= 4) of the entry index
+        const int sz = t < 8 ? 7 : 8;
+        uint64_t rows[8];
+        const bool cv = col < ncols_valid;
+        // rows 7t..7t+sz-1 of this column via 4 aligned 128-bit loads from row (7t & ~1)
+        const int r0 = (7 * t) & ~1, sh = (7 * t) & 1;
+        const ulonglong2* bp = reinterpret_cast<const ulonglong2*>(
+            reinterpret_cast<const unsigned char*>(bs) + col * kG2BPitch) + r0 / 2;
+        uint64_t raw[9];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const ulonglong2 v = bp[q];
+            raw[2 * q] = v.x;
+            raw[2 * q + 1] = v.y;
+        }
+        raw[8] = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+            const uint64_t x = sh ? raw[b + 1] : raw[b];
+            rows[b] = (b < sz && cv && 7 * t + b < k_bits) ? x : 0ull;
+        }
+        uint64_t cur = 0;
+#pragma unroll
+        for (int hb = 0; hb < 4; ++hb)
+            if ((chunk >> hb) & 1) cur ^= rows[4 + hb];
+        uint64_t* dst = tab + (size_t(128 * t + chunk * 16) * kTabCols + col);
+        uint64_t v[16];
+        v[0] = cur;
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+            for (int g = 1 << b; g < (2 << b); ++g) v[g] = v[g - (1 << b)] ^ rows[b];
+#pragma unroll
+        for (int g = 0; g < 16; ++g) dst[g * kTabCols] = v[g];
+    }
+}
+
+__global__ void __launch_bounds__(kG2Threads, 1) k_gemm_v2(GemmArgs p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const uint32_t smem_base = smem_u32(smem_raw);
+    if (smem_base > kTabAddr - kG2RingBytes) __trap();
+    uint64_t* tab = reinterpret_cast<uint64_t*>(smem_raw + (kTabAddr - smem_base));
+    unsigned char* ring = smem_raw;
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + size_t(kG2Stages) * kG2StageBytes);
+
+    const size_t KB = (p.k + 63) / 64;
+    const size_t ntr = (p.n + kG2Rows - 1) / kG2Rows;
+    const size_t ncg = (size_t(p.mcols) + kTabCols - 1) / kTabCols;
+    const size_t TU = ntr * ncg * KB;
+    const size_t u0 = TU * blockIdx.x / gridDim.x;
+    const size_t u1 = TU * (blockIdx.x + 1) / gridDim.x;
+    if (u0 >= u1) return;
+    const size_t cnt = u1 - u0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    // producer role (thread 0): bulk loads of unit `i` into stage i % kG2Stages.  A
+    // stage is reused only after the CTA-wide barrier that ends its previous unit.
+    size_t ptile = u0 / KB, pkb = u0 % KB;
+    auto produce = [&](size_t i) {
+        const int st = int(i % kG2Stages);
+        const size_t cg = ptile % ncg, rt = ptile / ncg;
+        const int nvalid = min(kTabCols, int(size_t(p.mcols) - cg * kTabCols));
+        const size_t row0 = rt * kG2Rows;
+        const size_t arows = min(size_t(kG2Rows), p.a_cap - row0);
+        const size_t brows = min(size_t(64), p.b_cap - pkb * 64);
+        unsigned char* sb = ring + size_t(st) * kG2StageBytes;
+        mbar_expect_tx(&full[st], uint32_t(arows * 8 + size_t(nvalid) * brows * 8));
+        bulk_g2s(sb, p.A + pkb * p.sa + row0, uint32_t(arows * 8), &full[st]);
+        for (int c = 0; c < nvalid; ++c)
+            bulk_g2s(sb + kG2ABytes + c * kG2BPitch, p.B + (cg * kTabCols + c) * p.sb + pkb * 64,
+                     uint32_t(brows * 8), &full[st]);
+        if (++pkb == KB) { pkb = 0; ++ptile; }
+    };
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kG2Stages; ++s) mbar_init(&full[s], 1);
+        fence_async_smem();
+        for (size_t i = 0; i < cnt && i + 1 < size_t(kG2Stages); ++i) produce(i);
+    }
+    __syncthreads();
+
+    const int h = lane >> 4, col = lane & 15;
+    const uint32_t colofs = uint32_t(col) * 8u;
+    const int rl = 64 * warp + 32 * h;  // lane's 32 rows within the tile
+    size_t tile = u0 / KB, kb0 = u0 % KB;
+    int s = 0;
+    uint32_t ph = 0;
+    for (size_t i = 0; i < cnt;) {
+        // one tile segment: k-blocks [kb0, kb0 + seg) of tile `tile`
+        const size_t seg = min(KB - kb0, cnt - i);
+        const size_t cg = tile % ncg, rt = tile / ncg;
+        const int nvalid = min(kTabCols, int(size_t(p.mcols) - cg * kTabCols));
+        uint64_t acc[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) acc[q] = 0;
+        for (size_t j = 0; j < seg; ++j, ++i) {
+            const size_t kb = kb0 + j;
+            const int kbits = int(p.k - kb * 64 < 64 ? p.k - kb * 64 : 64);
+            const unsigned char* sb = ring + size_t(s) * kG2StageBytes;
+            __syncthreads();  // every warp finished unit i-1: its stage and the tables are free
+            if (threadIdx.x == 0 && i + kG2Stages - 1 < cnt) produce(i + kG2Stages - 1);
+            mbar_wait(&full[s], ph);
+            build_tables_smem<kG2Threads>(tab, reinterpret_cast<const uint64_t*>(sb + kG2ABytes),
+                                          nvalid, kbits, 9, threadIdx.x);
+            __syncthreads();
+            // all 9 tables are always built (groups beyond k are all-zero tables and the
+            // driving words' bits beyond k are zero), so the lookup is branch-free
+            const ulonglong2* ap = reinterpret_cast<const ulonglong2*>(sb) + rl / 2;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const ulonglong2 v = ap[q];
+                acc[2 * q] ^= lookup9(colofs, v.x);
+                acc[2 * q + 1] ^= lookup9(colofs, v.y);
+            }
+            if (++s == kG2Stages) { s = 0; ph ^= 1; }
+        }
+        // epilogue: XOR into C (exclusive tile -> plain RMW, shared tile -> atomicXor)
+        const size_t row0 = rt * kG2Rows + rl;
+        if (col < nvalid && row0 < p.n) {
+            uint64_t* cp = p.C + (cg * kTabCols + col) * p.sc + row0;
+            const bool alone = (kb0 == 0 && seg == KB) && row0 + 32 <= p.n;
+#pragma unroll
+            for (int g4 = 0; g4 < 8; ++g4) {
+                if (alone) {
+                    uint64_t x0, x1, x2, x3;
+                    ld256(cp + 4 * g4, x0, x1, x2, x3);
+                    st256(cp + 4 * g4, x0 ^ acc[4 * g4], x1 ^ acc[4 * g4 + 1],
+                          x2 ^ acc[4 * g4 + 2], x3 ^ acc[4 * g4 + 3]);
+                } else {
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const int q = 4 * g4 + t;
+                        if (row0 + q < p.n && acc[q])
+                            atomicXor(reinterpret_cast<unsigned long long*>(cp + q),
+                                      (unsigned long long)acc[q]);
+                    }
+                }
+            }
+        }
+        kb0 = 0;
+        ++tile;
+    }
+}
+
 cudaError_t launch_gemm(const GemmArgs& g, int num_sms, cudaStream_t s) {
     if (g.n == 0 || g.k == 0 || g.mcols <= 0) return cudaSuccess;
     const size_t KB = (g.k + 63) / 64;
     const size_t units = ((g.n + kGemmRows - 1) / kGemmRows) *
                          ((size_t(g.mcols) + kTabCols - 1) / kTabCols) * KB;
     const int grid = int(units < size_t(num_sms) ? units : size_t(num_sms));
+    const bool v2 = g.a_cap >= g.n && g.b_cap >= g.k && (g.sa % 2) == 0 && (g.sb % 2) == 0 &&
+                    (reinterpret_cast<uintptr_t>(g.A) % 16) == 0 &&
+                    (reinterpret_cast<uintptr_t>(g.B) % 16) == 0;
+    if (v2) {
+        k_gemm_v2<<<grid, kG2Threads, kG2Smem, s>>>(g);
+        return cudaGetLastError();
+    }
     k_gemm<<<grid, kGemmThreads, kTabBytes, s>>>(g);
     return cudaGetLastError();
 }
@@ -1224,27 +1430,43 @@ cudaError_t launch_post(uint64_t* w, size_t stride, int ncols, int panel_col, ui
 // ---------------------------------------------------------------------------
 // block XOR (Strassen-Winograd additions)
 // ---------------------------------------------------------------------------
-__global__ void k_xor(uint64_t* __restrict__ dst, size_t sd, const uint64_t* __restrict__ a,
-                      size_t sa, const uint64_t* __restrict__ b, size_t sb,
-                      const uint64_t* __restrict__ c, size_t sc, const uint64_t* __restrict__ d,
-                      size_t sdd, size_t rows, size_t wcols, bool acc) {
-    const size_t rq = (rows + 3) / 4;  // 4-word (32 B) chunks per column
-    const size_t total = rq * wcols;
-    for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
-         e += size_t(gridDim.x) * blockDim.x) {
-        const size_t q = e / rq, i0 = (e % rq) * 4;
-        const int cnt = rows - i0 >= 4 ? 4 : int(rows - i0);
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            if (t >= cnt) break;
-            const size_t i = i0 + t;
-            uint64_t v = acc ? dst[q * sd + i] : 0ull;
-            if (a) v ^= a[q * sa + i];
-            if (b) v ^= b[q * sb + i];
-            if (c) v ^= c[q * sc + i];
-            if (d) v ^= d[q * sdd + i];
-            dst[q * sd + i] = v;
+// 2D grid: blockIdx.y = word-column, threads stride over 4-word (32 B) row chunks
+// with 256-bit accesses when every operand is 32-byte aligned (Strassen views are:
+// strides are multiples of 128 rows and quadrant offsets multiples of 64 rows).
+__global__ void __launch_bounds__(256) k_xor(uint64_t* __restrict__ dst, size_t sd,
+                                             const uint64_t* __restrict__ a, size_t sa,
+                                             const uint64_t* __restrict__ b, size_t sb,
+                                             const uint64_t* __restrict__ c, size_t sc,
+                                             const uint64_t* __restrict__ d, size_t sdd,
+                                             size_t rows, bool acc, bool vec) {
+    const size_t q = blockIdx.y;
+    uint64_t* dp = dst + q * sd;
+    const uint64_t* ap = a ? a + q * sa : nullptr;
+    const uint64_t* bp = b ? b + q * sb : nullptr;
+    const uint64_t* cp = c ? c + q * sc : nullptr;
+    const uint64_t* ep = d ? d + q * sdd : nullptr;
+    if (vec) {
+        const size_t nq = rows / 4;
+        for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nq;
+             i += size_t(gridDim.x) * blockDim.x) {
+            uint64_t v0 = 0, v1 = 0, v2 = 0, v3 = 0, x0, x1, x2, x3;
+            if (acc) ld256(dp + 4 * i, v0, v1, v2, v3);
+            if (ap) { ld256(ap + 4 * i, x0, x1, x2, x3); v0 ^= x0; v1 ^= x1; v2 ^= x2; v3 ^= x3; }
+            if (bp) { ld256(bp + 4 * i, x0, x1, x2, x3); v0 ^= x0; v1 ^= x1; v2 ^= x2; v3 ^= x3; }
+            if (cp) { ld256(cp + 4 * i, x0, x1, x2, x3); v0 ^= x0; v1 ^= x1; v2 ^= x2; v3 ^= x3; }
+            if (ep) { ld256(ep + 4 * i, x0, x1, x2, x3); v0 ^= x0; v1 ^= x1; v2 ^= x2; v3 ^= x3; }
+            st256(dp + 4 * i, v0, v1, v2, v3);
         }
+        return;
+    }
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < rows;
+         i += size_t(gridDim.x) * blockDim.x) {
+        uint64_t v = acc ? dp[i] : 0ull;
+        if (ap) v ^= ap[i];
+        if (bp) v ^= bp[i];
+        if (cp) v ^= cp[i];
+        if (ep) v ^= ep[i];
+        dp[i] = v;
     }
 }
 
@@ -1252,10 +1474,15 @@ cudaError_t launch_xor(uint64_t* dst, size_t sd, const uint64_t* a, size_t sa, c
                        size_t sb, const uint64_t* c, size_t scc, const uint64_t* d, size_t sdd,
                        size_t rows, size_t wcols, bool acc, cudaStream_t s) {
     if (rows == 0 || wcols == 0) return cudaSuccess;
-    const size_t total = (rows + 3) / 4 * wcols;
-    size_t blocks = (total + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
-    k_xor<<<unsigned(blocks), 256, 0, s>>>(dst, sd, a, sa, b, sb, c, scc, d, sdd, rows, wcols, acc);
+    auto al = [](const void* p, size_t st) {
+        return !p || ((reinterpret_cast<uintptr_t>(p) % 32) == 0 && st % 4 == 0);
+    };
+    const bool vec = rows % 4 == 0 && al(dst, sd) && al(a, sa) && al(b, sb) && al(c, scc) &&
+                     al(d, sdd);
+    const size_t work = vec ? rows / 4 : rows;
+    const unsigned bx = unsigned(std::min<size_t>((work + 255) / 256, 64));
+    dim3 grid(bx, unsigned(wcols));
+    k_xor<<<grid, 256, 0, s>>>(dst, sd, a, sa, b, sb, c, scc, d, sdd, rows, acc, vec);
     return cudaGetLastError();
 }
 
@@ -1335,6 +1562,9 @@ cudaError_t init_kernel_attrs() {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(kTabBytes));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_gemm_v2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(kG2Smem));
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(sizeof(PanelSmem)));

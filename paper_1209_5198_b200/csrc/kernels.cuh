@@ -53,6 +53,9 @@ struct GemmArgs {
     const uint64_t* A; size_t sa; size_t n;   // A: n rows, k bits
     const uint64_t* B; size_t sb; size_t k;   // B: k rows
     uint64_t* C; size_t sc; int mcols;        // C: n rows, mcols word-columns (XOR-accumulated)
+    // addressable rows from A / B base within a column (>= n / k); bulk loads of
+    // 1024-row A segments and 64-row B blocks are clamped to these
+    size_t a_cap = 0, b_cap = 0;
 };
 
 // launchers (return cudaError_t of the launch)

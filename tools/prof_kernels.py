@@ -32,6 +32,13 @@ elif what == "gemm":
     A.random_dense(0.5, 2); B.random_dense(0.5, 3)
     for _ in range(reps):
         _lib.check(lib.f2gpu_m4rm_mult(ctx.handle, A.handle, B.handle, Cm.handle, 0))
+elif what == "strassen":
+    n = 16384
+    cut = int(sys.argv[3]) if len(sys.argv) > 3 else 8192
+    A, B, Cm = (f2.DeviceMatrix(n, n, ctx) for _ in range(3))
+    A.random_dense(0.5, 2); B.random_dense(0.5, 3)
+    for _ in range(reps):
+        _lib.check(lib.f2gpu_strassen_mult(ctx.handle, A.handle, B.handle, Cm.handle, cut))
 elif what == "decompose":
     n = int(sys.argv[3]) if len(sys.argv) > 3 else 65536
     A = f2.DeviceMatrix(n, n, ctx); A.random_dense(0.5, 6)
