@@ -430,7 +430,7 @@ def measure_gemm(f2, lib, _lib, ctx, stream, torch) -> dict:
     Bm.random_dense(0.5, 3)
     out = {}
     variants = [("m4rm", lambda: _lib.check(lib.f2gpu_m4rm_mult(ctx.handle, Am.handle, Bm.handle, Cm.handle, 0)))]
-    for cut in (8192, 4096):
+    for cut in (16384, 8192, 4096):
         variants.append((f"strassen_cut{cut}", lambda cut=cut: _lib.check(
             lib.f2gpu_strassen_mult(ctx.handle, Am.handle, Bm.handle, Cm.handle, cut))))
     for name, fn in variants:

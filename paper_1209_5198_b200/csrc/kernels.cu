@@ -927,29 +927,28 @@ __device__ __forceinline__ void build_tables_smem(uint64_t* __restrict__ tab,
     }
 }
 
-__global__ void __launch_bounds__(kG2Threads, 1) k_gemm_v2(GemmArgs p) {
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    const uint32_t smem_base = smem_u32(smem_raw);
-    if (smem_base > kTabAddr - kG2RingBytes) __trap();
-    uint64_t* tab = reinterpret_cast<uint64_t*>(smem_raw + (kTabAddr - smem_base));
-    unsigned char* ring = smem_raw;
-    uint64_t* full = reinterpret_cast<uint64_t*>(ring + size_t(kG2Stages) * kG2StageBytes);
+__device__ __forceinline__ size_t gemm_units(const GemmArgs& p) {
+    return ((p.n + kG2Rows - 1) / kG2Rows) * ((size_t(p.mcols) + kTabCols - 1) / kTabCols) *
+           ((p.k + 63) / 64);
+}
 
+// units [u0, u1) of problem p; the ring stage/phase cursor (s, ph) carries over
+// between calls (every stage is drained at the end of a call)
+__device__ __forceinline__ void gemm_range(const GemmArgs& p, size_t u0, size_t u1,
+                                           unsigned char* ring, uint64_t* full, uint64_t* tab,
+                                           int& s, uint32_t& ph) {
     const size_t KB = (p.k + 63) / 64;
-    const size_t ntr = (p.n + kG2Rows - 1) / kG2Rows;
     const size_t ncg = (size_t(p.mcols) + kTabCols - 1) / kTabCols;
-    const size_t TU = ntr * ncg * KB;
-    const size_t u0 = TU * blockIdx.x / gridDim.x;
-    const size_t u1 = TU * (blockIdx.x + 1) / gridDim.x;
     if (u0 >= u1) return;
     const size_t cnt = u1 - u0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s0 = s;
 
     // producer role (thread 0): bulk loads of unit `i` into stage i % kG2Stages.  A
     // stage is reused only after the CTA-wide barrier that ends its previous unit.
     size_t ptile = u0 / KB, pkb = u0 % KB;
     auto produce = [&](size_t i) {
-        const int st = int(i % kG2Stages);
+        const int st = int((size_t(s0) + i) % kG2Stages);
         const size_t cg = ptile % ncg, rt = ptile / ncg;
         const int nvalid = min(kTabCols, int(size_t(p.mcols) - cg * kTabCols));
         const size_t row0 = rt * kG2Rows;
@@ -963,19 +962,14 @@ __global__ void __launch_bounds__(kG2Threads, 1) k_gemm_v2(GemmArgs p) {
                      uint32_t(brows * 8), &full[st]);
         if (++pkb == KB) { pkb = 0; ++ptile; }
     };
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kG2Stages; ++s) mbar_init(&full[s], 1);
-        fence_async_smem();
+    __syncthreads();  // previous range fully consumed
+    if (threadIdx.x == 0)
         for (size_t i = 0; i < cnt && i + 1 < size_t(kG2Stages); ++i) produce(i);
-    }
-    __syncthreads();
 
     const int h = lane >> 4, col = lane & 15;
     const uint32_t colofs = uint32_t(col) * 8u;
     const int rl = 64 * warp + 32 * h;  // lane's 32 rows within the tile
     size_t tile = u0 / KB, kb0 = u0 % KB;
-    int s = 0;
-    uint32_t ph = 0;
     for (size_t i = 0; i < cnt;) {
         // one tile segment: k-blocks [kb0, kb0 + seg) of tile `tile`
         const size_t seg = min(KB - kb0, cnt - i);
@@ -1031,6 +1025,111 @@ __global__ void __launch_bounds__(kG2Threads, 1) k_gemm_v2(GemmArgs p) {
         kb0 = 0;
         ++tile;
     }
+}
+
+__device__ __forceinline__ uint64_t* g2_setup(unsigned char* smem_raw, unsigned char*& ring,
+                                               uint64_t*& full) {
+    const uint32_t smem_base = smem_u32(smem_raw);
+    if (smem_base > kTabAddr - kG2RingBytes) __trap();
+    ring = smem_raw;
+    full = reinterpret_cast<uint64_t*>(ring + size_t(kG2Stages) * kG2StageBytes);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kG2Stages; ++s) mbar_init(&full[s], 1);
+        fence_async_smem();
+    }
+    __syncthreads();
+    return reinterpret_cast<uint64_t*>(smem_raw + (kTabAddr - smem_base));
+}
+
+__global__ void __launch_bounds__(kG2Threads, 1) k_gemm_v2(GemmArgs p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const size_t TU = gemm_units(p);
+    const size_t u0 = TU * blockIdx.x / gridDim.x;
+    const size_t u1 = TU * (blockIdx.x + 1) / gridDim.x;
+    if (u0 >= u1) return;
+    unsigned char* ring;
+    uint64_t* full;
+    uint64_t* tab = g2_setup(smem_raw, ring, full);
+    int s = 0;
+    uint32_t ph = 0;
+    gemm_range(p, u0, u1, ring, full, tab, s, ph);
+}
+
+// Batched products (Strassen-Winograd leaves): the concatenated unit spaces of
+// nprob problems are split evenly over the CTAs (one launch, no tail effects
+// per leaf).  offs[q] = first unit of problem q, offs[nprob] = total.
+__global__ void __launch_bounds__(kG2Threads, 1)
+    k_gemm_batched(const GemmArgs* __restrict__ probs, const size_t* __restrict__ offs, int nprob) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const size_t TU = offs[nprob];
+    const size_t u0 = TU * blockIdx.x / gridDim.x;
+    const size_t u1 = TU * (blockIdx.x + 1) / gridDim.x;
+    if (u0 >= u1) return;
+    unsigned char* ring;
+    uint64_t* full;
+    uint64_t* tab = g2_setup(smem_raw, ring, full);
+    int s = 0;
+    uint32_t ph = 0;
+    int q = 0;
+    while (q + 1 < nprob && offs[q + 1] <= u0) ++q;
+    for (; q < nprob && offs[q] < u1; ++q) {
+        const GemmArgs p = probs[q];
+        const size_t a = u0 > offs[q] ? u0 - offs[q] : 0;
+        const size_t b = (u1 < offs[q + 1] ? u1 : offs[q + 1]) - offs[q];
+        gemm_range(p, a, b, ring, full, tab, s, ph);
+    }
+}
+
+// Batched XOR jobs: dst = (acc ? dst : 0) ^ src0 ^ src1 ^ src2 ^ src3 (null srcs
+// skipped); blockIdx.y = job, blockIdx.z = word-column, 32-byte vector accesses.
+__global__ void __launch_bounds__(256) k_xor_batched(const XorJob* __restrict__ jobs) {
+    const XorJob& J = jobs[blockIdx.y];
+    const size_t q = blockIdx.z;
+    if (q >= J.wcols) return;
+    uint64_t* dp = J.dst + q * J.sd;
+    const uint64_t* sp[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) sp[t] = J.src[t] ? J.src[t] + q * J.ss[t] : nullptr;
+    const size_t nq = J.rows / 4;
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nq;
+         i += size_t(gridDim.x) * blockDim.x) {
+        uint64_t v0 = 0, v1 = 0, v2 = 0, v3 = 0, x0, x1, x2, x3;
+        if (J.acc) ld256(dp + 4 * i, v0, v1, v2, v3);
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (sp[t]) {
+                ld256(sp[t] + 4 * i, x0, x1, x2, x3);
+                v0 ^= x0; v1 ^= x1; v2 ^= x2; v3 ^= x3;
+            }
+        st256(dp + 4 * i, v0, v1, v2, v3);
+    }
+}
+
+cudaError_t launch_xor_batched(const XorJob* d_jobs, int njobs, size_t max_rows, size_t max_wcols,
+                               cudaStream_t s) {
+    if (njobs == 0) return cudaSuccess;
+    const unsigned bx = unsigned(std::min<size_t>((max_rows / 4 + 255) / 256, 16));
+    dim3 grid(bx ? bx : 1, unsigned(njobs), unsigned(max_wcols));
+    k_xor_batched<<<grid, 256, 0, s>>>(d_jobs);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gemm_batched(const GemmArgs* d_probs, const size_t* d_offs, int nprob,
+                                size_t total_units, int num_sms, cudaStream_t s) {
+    if (nprob == 0 || total_units == 0) return cudaSuccess;
+    const int grid = int(total_units < size_t(num_sms) ? total_units : size_t(num_sms));
+    k_gemm_batched<<<grid, kG2Threads, kG2Smem, s>>>(d_probs, d_offs, nprob);
+    return cudaGetLastError();
+}
+
+size_t gemm_units_host(const GemmArgs& p) {
+    return ((p.n + kG2Rows - 1) / kG2Rows) * ((size_t(p.mcols) + kTabCols - 1) / kTabCols) *
+           ((p.k + 63) / 64);
+}
+
+bool gemm_fast_ok(const GemmArgs& g) {
+    return g.a_cap >= g.n && g.b_cap >= g.k && (g.sa % 2) == 0 && (g.sb % 2) == 0 &&
+           (reinterpret_cast<uintptr_t>(g.A) % 16) == 0 && (reinterpret_cast<uintptr_t>(g.B) % 16) == 0;
 }
 
 cudaError_t launch_gemm(const GemmArgs& g, int num_sms, cudaStream_t s) {
@@ -1564,6 +1663,9 @@ cudaError_t init_kernel_attrs() {
                                  int(kTabBytes));
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_gemm_v2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(kG2Smem));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_gemm_batched, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(kG2Smem));
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,

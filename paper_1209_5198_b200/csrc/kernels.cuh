@@ -58,6 +58,13 @@ struct GemmArgs {
     size_t a_cap = 0, b_cap = 0;
 };
 
+struct XorJob {  // dst = (acc ? dst : 0) ^ src[0..3] over rows x wcols (rows % 4 == 0, 32-B aligned)
+    uint64_t* dst; size_t sd;
+    const uint64_t* src[4]; size_t ss[4];
+    size_t rows, wcols;
+    int acc;
+};
+
 // launchers (return cudaError_t of the launch)
 cudaError_t launch_random_dense(uint64_t* w, size_t n, size_t m, size_t stride, double density,
                                 uint64_t seed, const uint64_t* d_jump, cudaStream_t s);
@@ -83,6 +90,14 @@ cudaError_t launch_transpose(const uint64_t* a, size_t n, size_t m, size_t sa, u
                              size_t so, cudaStream_t s);
 cudaError_t launch_iota(uint32_t* p, size_t n, cudaStream_t s);
 cudaError_t launch_mask_cols(uint64_t* w, size_t stride, size_t n, size_t m, cudaStream_t s);
+
+// batched products / XORs (device arrays of descriptors)
+cudaError_t launch_gemm_batched(const GemmArgs* d_probs, const size_t* d_offs, int nprob,
+                                size_t total_units, int num_sms, cudaStream_t s);
+cudaError_t launch_xor_batched(const XorJob* d_jobs, int njobs, size_t max_rows, size_t max_wcols,
+                               cudaStream_t s);
+size_t gemm_units_host(const GemmArgs& p);
+bool gemm_fast_ok(const GemmArgs& g);
 
 // per-device one-time setup (dynamic shared memory opt-in)
 cudaError_t init_kernel_attrs();
