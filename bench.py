@@ -194,6 +194,7 @@ def cfg_json(cfg, gpus):
             "n": cfg["n"], "m": cfg["m"], "density": cfg["p"], "seed": cfg["seed"],
             "word_bits": 64, "tables": "9 groups (7x8+8 bits), 16 word-cols/CTA",
             "parallelism": f"column-round-robin x{gpus}" if gpus > 1 else "single GPU",
+            "variant": "decompose_block (lookahead 1, CUDA-graph replay)",
             "l2": "inputs (512 MiB) larger than L2 (126 MB); no flush needed"}
 
 
@@ -208,6 +209,9 @@ def main() -> None:
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--gemm", action="store_true", help="also time the cfg2 16384^2 GEMM")
+    ap.add_argument("--variant", default="block", choices=["block", "recursive"],
+                    help="decompose_block or decompose_recursive (bit-identical factors)")
+    ap.add_argument("--min-cols", type=int, default=0, help="recursive leaf width in bits (0 = default)")
     args = ap.parse_args()
     cfg = {"n": args.n, "m": args.n, "p": 0.5, "seed": 6}
 
@@ -256,6 +260,9 @@ def main() -> None:
         if world > 1:
             _lib.check(lib.f2gpu_decompose_block_dist(ctx.handle, W.handle, m, perm.ctypes.data,
                                                       rj.ctypes.data, C.byref(rk)))
+        elif args.variant == "recursive":
+            _lib.check(lib.f2gpu_decompose_recursive(ctx.handle, W.handle, args.min_cols,
+                                                     perm.ctypes.data, rj.ctypes.data, C.byref(rk)))
         else:
             _lib.check(lib.f2gpu_decompose_block(ctx.handle, W.handle, perm.ctypes.data,
                                                  rj.ctypes.data, C.byref(rk)))

@@ -115,6 +115,13 @@ int f2gpu_strassen_mult(f2gpu_ctx *ctx, const f2gpu_mat *a, const f2gpu_mat *b, 
  * written to HOST arrays (either may be NULL), *rank = sum rj. */
 int f2gpu_decompose_block(f2gpu_ctx *ctx, f2gpu_mat *w, uint32_t *perm, uint32_t *rj,
                           size_t *rank);
+/* decompose_recursive: split the columns,
+ * factor the left half, update the right half with a block TRSM + one
+ * Strassen-Winograd GEMM (A' = D ^ L21 L11^-1 C), recurse.  Exact arithmetic and
+ * 64-aligned splits make the result bit-identical to decompose_block.
+ * min_cols = 0 -> 128 panels (8192 columns) per leaf. */
+int f2gpu_decompose_recursive(f2gpu_ctx *ctx, f2gpu_mat *w, size_t min_cols, uint32_t *perm,
+                              uint32_t *rj, size_t *rank);
 /* Same algorithm, column blocks distributed round-robin over `shards` logical
  * shards that live on this device (testing the sharded driver on one GPU). */
 int f2gpu_decompose_block_sharded(f2gpu_ctx *ctx, f2gpu_mat *w, int shards, uint32_t *perm,

@@ -27,7 +27,8 @@ from ._lib import F2GpuError
 
 __all__ = [
     "BitMatrix", "RowPermutation", "LUFactors", "Context", "DeviceMatrix", "M4rmTables",
-    "m4rm_mult", "strassen_mult", "build_tables", "mult_acc", "decompose_block", "rank",
+    "m4rm_mult", "strassen_mult", "build_tables", "mult_acc", "decompose_block",
+    "decompose_recursive", "rank",
     "make_splits", "tuning", "F2GpuError", "default_context",
 ]
 
@@ -452,6 +453,27 @@ def decompose_block(a, ctx: Context | None = None, shards: int = 1) -> LUFactors
         rc = lib.f2gpu_decompose_block_sharded(ctx.handle, w.handle, int(shards), _ptr(perm),
                                                _ptr(rj), C.byref(rank_))
     _lib.check(rc, "decompose_block")
+    W = w.download()
+    return LUFactors(RowPermutation(perm[:n].copy()), W, int(rank_.value),
+                     rj[: (m + 63) // 64].copy())
+
+
+def decompose_recursive(a, min_cols: int = 0, ctx: Context | None = None) -> LUFactors:
+    """Recursive column-split variant: left
+    half recursively, right half brought up to date by a block TRSM and one
+    Strassen-Winograd GEMM (A' = D + L21 L11^-1 C), then recursion.  Exact
+    arithmetic with 64-aligned splits: the factors equal decompose_block's
+    bit-for-bit.  min_cols = 0 picks the device default (8192 columns per leaf)."""
+    ctx = ctx or (a.ctx if isinstance(a, DeviceMatrix) else default_context())
+    host = a.download() if isinstance(a, DeviceMatrix) else a
+    n, m = host.rows(), host.cols()
+    w = DeviceMatrix.from_host(host, ctx)
+    perm = np.zeros(max(n, 1), dtype=np.uint32)
+    rj = np.zeros(max((m + 63) // 64, 1), dtype=np.uint32)
+    rank_ = C.c_size_t()
+    _lib.check(_lib.load().f2gpu_decompose_recursive(ctx.handle, w.handle, int(min_cols),
+                                                     _ptr(perm), _ptr(rj), C.byref(rank_)),
+               "decompose_recursive")
     W = w.download()
     return LUFactors(RowPermutation(perm[:n].copy()), W, int(rank_.value),
                      rj[: (m + 63) // 64].copy())

@@ -482,26 +482,42 @@ int ensure_scratch(f2gpu_ctx* c, size_t n, size_t mu) {
 //   side: P(j+1) waits POST(j) (event) and then spins on flag j on the spare SM,
 //         so the panel factorisation of j+1 overlaps the bulk of update j.
 //   main waits P(j+1) (event) before POST(j+1).
-int enqueue_lookahead(f2gpu_ctx* c, Shard& s, size_t n, size_t mu) {
-    const int grid = c->num_sms - 1;
-    CUDA_TRY(cudaMemsetAsync(c->scr_flags, 0, mu * 4, c->stream));
-    F2_TRY(check_launch(c, f2::launch_iota(s.perm, n, c->stream), "k_iota"));
-    F2_TRY(check_launch(c, f2::launch_panel(s.w.p, n, s.st, 0, c->stream), "k_panel"));
-    for (size_t j = 0; j < mu; ++j) {
-        uint64_t* colj = s.w.p + j * s.w.stride;
-        if (j > 0) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_panel, 0));
+// Panels [c0, c1) with their Schur updates restricted to word-columns < c1
+// (c1 = mu for the block algorithm; a leaf range for the recursive one).  The
+// swaps of every panel are applied to all mu word-columns.
+int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_t c1, bool la) {
+    const int grid = la ? c->num_sms - 1 : c->num_sms;
+    auto upd = [&](size_t j, uint32_t* release) {
+        f2::UpdateArgs u{};
+        u.C = s.w.p; u.sc = s.w.stride; u.c_wcol0 = j + 1; u.ncols = int(c1 - j - 1);
+        u.row_lo = 0; u.row_hi = n; u.a = s.w.p + j * s.w.stride; u.k_bits = 0;
+        u.B = s.w.p; u.sb = s.w.stride; u.b_row0 = 0; u.b_wcol0 = j + 1;
+        u.st = s.st + j;
+        u.release = release;
+        return check_launch(c, f2::launch_update(u, grid, c->stream), "k_update");
+    };
+    if (!la) {
+        for (size_t j = c0; j < c1; ++j) {
+            F2_TRY(check_launch(c, f2::launch_panel(s.w.p + j * s.w.stride, n, s.st, int(j),
+                                                    c->stream),
+                                "k_panel"));
+            F2_TRY(check_launch(c, f2::launch_post(s.w.p, s.w.stride, int(mu), int(j), s.perm, n,
+                                                   s.st + j, c->stream),
+                                "k_post"));
+            if (j + 1 < c1) F2_TRY(upd(j, nullptr));
+        }
+        return F2GPU_OK;
+    }
+    F2_TRY(check_launch(c, f2::launch_panel(s.w.p + c0 * s.w.stride, n, s.st, int(c0), c->stream),
+                        "k_panel"));
+    for (size_t j = c0; j < c1; ++j) {
+        if (j > c0) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_panel, 0));
         F2_TRY(check_launch(c, f2::launch_post(s.w.p, s.w.stride, int(mu), int(j), s.perm, n,
                                                s.st + j, c->stream),
                             "k_post"));
-        if (j + 1 >= mu) break;
+        if (j + 1 >= c1) break;
         CUDA_TRY(cudaEventRecord(c->ev_post, c->stream));
-        f2::UpdateArgs u{};
-        u.C = s.w.p; u.sc = s.w.stride; u.c_wcol0 = j + 1; u.ncols = int(mu - j - 1);
-        u.row_lo = 0; u.row_hi = n; u.a = colj; u.k_bits = 0;
-        u.B = s.w.p; u.sb = s.w.stride; u.b_row0 = 0; u.b_wcol0 = j + 1;
-        u.st = s.st + j;
-        u.release = c->scr_flags + j;
-        F2_TRY(check_launch(c, f2::launch_update(u, grid, c->stream), "k_update"));
+        F2_TRY(upd(j, c->scr_flags + j));
         CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_post, 0));
         F2_TRY(check_launch(c, f2::launch_panel(s.w.p + (j + 1) * s.w.stride, n, s.st, int(j + 1),
                                                 c->side, c->scr_flags + j, uint32_t(grid)),
@@ -509,6 +525,17 @@ int enqueue_lookahead(f2gpu_ctx* c, Shard& s, size_t n, size_t mu) {
         CUDA_TRY(cudaEventRecord(c->ev_panel, c->side));
     }
     return F2GPU_OK;
+}
+
+// Lookahead schedule (two streams, capture-able):
+//   main: POST(j) -> U(j) [SMs-1 CTAs, column j+1 first, then release flag j]
+//   side: P(j+1) waits POST(j) (event) and then spins on flag j on the spare SM,
+//         so the panel factorisation of j+1 overlaps the bulk of update j.
+//   main waits P(j+1) (event) before POST(j+1).
+int enqueue_lookahead(f2gpu_ctx* c, Shard& s, size_t n, size_t mu) {
+    CUDA_TRY(cudaMemsetAsync(c->scr_flags, 0, mu * 4, c->stream));
+    F2_TRY(check_launch(c, f2::launch_iota(s.perm, n, c->stream), "k_iota"));
+    return enqueue_panels(c, s, n, mu, 0, mu, true);
 }
 
 bool lookahead_ok(f2gpu_ctx* c, const Shard& s, size_t n) {
@@ -523,6 +550,115 @@ int enqueue_single(f2gpu_ctx* c, Shard& s, size_t n, size_t mu) {
     F2_TRY(check_launch(c, f2::launch_iota(s.perm, n, c->stream), "k_iota"));
     for (size_t j = 0; j < mu; ++j) F2_TRY(step_single(c, s, n, mu, j));
     return F2GPU_OK;
+}
+
+// ---- decompose_recursive -------------
+// Column split at cm: factor the left half recursively, then bring the right
+// half up to date with the left panels in two big steps instead of one rank-64
+// update per panel:
+//   X  = L11^-1 C   (in place on the left pivot rows of the right half; L11 has
+//                    identity 64x64 diagonal blocks, so a recursive block TRSM of
+//                    rank-64 updates + GEMMs)
+//   A' = D ^ L21 X  (one Strassen-Winograd/M4RM GEMM)
+// then recurse on the right half.  Deferred updates commute with the later row
+// swaps (SURVEY Probe P5), so W, perm and r_j are bit-identical to
+// decompose_block.  The fast path needs the left half at full rank (R_j = R0 +
+// 64(j-c0), 64-aligned); otherwise the left panels' updates are applied to the
+// right half as rank-r_j updates (always exact).
+struct RecRun {
+    f2gpu_ctx* c;
+    Shard* s;
+    size_t n, mu, base;
+    bool la;
+    size_t cut;    // Strassen cutover inside the recursion (XOR traffic vs multiply)
+    size_t tbase;  // TRSM base (panels solved by rank-64 updates)
+};
+
+int rec_state(RecRun& r, size_t j, size_t* R, size_t* rr) {
+    f2::PanelState h;
+    CUDA_TRY(cudaStreamSynchronize(r.c->stream));
+    CUDA_TRY(cudaMemcpy(&h, r.s->st + j, 16, cudaMemcpyDeviceToHost));
+    *R = h.R;
+    *rr = h.r;
+    return F2GPU_OK;
+}
+
+// panels [a, b) applied to word-cols [col0, col1), rows (R_j + r_j) .. row_hi
+int rank_updates(RecRun& r, size_t a, size_t b, size_t col0, size_t col1, size_t row_hi) {
+    Shard& s = *r.s;
+    for (size_t j = a; j < b; ++j) {
+        f2::UpdateArgs u{};
+        u.C = s.w.p; u.sc = s.w.stride; u.c_wcol0 = col0; u.ncols = int(col1 - col0);
+        u.row_lo = 0; u.row_hi = row_hi; u.a = s.w.p + j * s.w.stride; u.k_bits = 0;
+        u.B = s.w.p; u.sb = s.w.stride; u.b_row0 = 0; u.b_wcol0 = col0;
+        u.st = s.st + j;
+        F2_TRY(check_launch(r.c, f2::launch_update(u, r.c->num_sms, r.c->stream), "k_update"));
+    }
+    return F2GPU_OK;
+}
+
+View wview(const Shard& s, size_t r0, size_t nr, size_t wc0, size_t nwc) {
+    return View{s.w.p + wc0 * s.w.stride + r0, nr, nwc * 64, s.w.stride, s.w.stride - r0};
+}
+
+// full-rank block TRSM: panels [a, b) own pivot rows [Ra, Ra + 64(b-a)); solve in
+// place on word-cols [col0, col1) of those rows.
+int rec_trsm(RecRun& r, size_t a, size_t b, size_t Ra, size_t col0, size_t col1) {
+    const size_t Rb = Ra + 64 * (b - a);
+    if (b - a <= r.tbase) return rank_updates(r, a, b, col0, col1, Rb);
+    const size_t m = a + (b - a) / 2, Rm = Ra + 64 * (m - a);
+    F2_TRY(rec_trsm(r, a, m, Ra, col0, col1));
+    F2_TRY(strassen_acc(r.c, wview(*r.s, Rm, Rb - Rm, col0, col1 - col0),
+                        wview(*r.s, Rm, Rb - Rm, a, m - a), wview(*r.s, Ra, Rm - Ra, col0, col1 - col0),
+                        r.cut));
+    return rec_trsm(r, m, b, Rm, col0, col1);
+}
+
+int rec_decompose(RecRun& r, size_t c0, size_t c1) {
+    if (c1 - c0 <= r.base) return enqueue_panels(r.c, *r.s, r.n, r.mu, c0, c1, r.la);
+    const size_t cm = c0 + (c1 - c0) / 2;
+    F2_TRY(rec_decompose(r, c0, cm));
+    size_t R0, r0, Rl, rl;
+    F2_TRY(rec_state(r, c0, &R0, &r0));
+    F2_TRY(rec_state(r, cm - 1, &Rl, &rl));
+    const size_t R1 = Rl + rl;
+    const bool full = R1 - R0 == 64 * (cm - c0) && R0 % 64 == 0;
+    if (full) {
+        F2_TRY(rec_trsm(r, c0, cm, R0, cm, c1));
+        if (R1 < r.n)
+            F2_TRY(strassen_acc(r.c, wview(*r.s, R1, r.n - R1, cm, c1 - cm),
+                                wview(*r.s, R1, r.n - R1, c0, cm - c0),
+                                wview(*r.s, R0, R1 - R0, cm, c1 - cm), r.cut));
+    } else {
+        F2_TRY(rank_updates(r, c0, cm, cm, c1, r.n));
+    }
+    return rec_decompose(r, cm, c1);
+}
+
+int decompose_recursive(f2gpu_ctx* c, View w, size_t min_cols, uint32_t* perm, uint32_t* rj,
+                        size_t* rank) {
+    const size_t n = w.rows, mu = w.wcols();
+    if (n == 0 || mu == 0) {
+        if (rank) *rank = 0;
+        if (rj) std::fill(rj, rj + mu, 0u);
+        if (perm) for (size_t i = 0; i < n; ++i) perm[i] = uint32_t(i);
+        return F2GPU_OK;
+    }
+    F2_TRY(ensure_scratch(c, n, mu));
+    Shard s;
+    s.w = w; s.lw = mu; s.st = static_cast<f2::PanelState*>(c->scr_st); s.perm = c->scr_perm;
+    // defaults from a sweep at 65536^2 (Strassen cutover 4096..65536, TRSM base 8..64,
+    // leaves 1024..8192 columns): wide leaves + shallow Strassen win, see DESIGN.md
+    RecRun r{c, &s, n, mu, std::max<size_t>(1, (min_cols ? min_cols : 128 * 64) / 64),
+             lookahead_ok(c, s, n), 16384, 64};
+    if (const char* e = getenv("F2GPU_REC_CUT")) r.cut = size_t(atol(e));
+    if (const char* e = getenv("F2GPU_REC_TBASE")) r.tbase = std::max<size_t>(1, size_t(atol(e)));
+    CUDA_TRY(cudaMemsetAsync(c->scr_flags, 0, mu * 4, c->stream));
+    c->tl.mark(c->stream, "start");
+    F2_TRY(check_launch(c, f2::launch_iota(s.perm, n, c->stream), "k_iota"));
+    F2_TRY(rec_decompose(r, 0, mu));
+    c->tl.report("decompose_recursive");
+    return read_results(c, s, n, mu, perm, rj, rank);
 }
 
 int decompose_single(f2gpu_ctx* c, View w, uint32_t* perm, uint32_t* rj, size_t* rank) {
@@ -933,6 +1069,13 @@ int f2gpu_decompose_block(f2gpu_ctx* c, f2gpu_mat* w, uint32_t* perm, uint32_t* 
     if (!c || !w) return set_err(F2GPU_EINVAL, "null argument");
     if (w->rows > 0xFFFFFFF0ull) return set_err(F2GPU_ERANGE, "decompose: too many rows for uint32 perm");
     return decompose_single(c, view_of(w), perm, rj, rank);
+}
+
+int f2gpu_decompose_recursive(f2gpu_ctx* c, f2gpu_mat* w, size_t min_cols, uint32_t* perm,
+                              uint32_t* rj, size_t* rank) {
+    if (!c || !w) return set_err(F2GPU_EINVAL, "null argument");
+    if (w->rows > 0xFFFFFFF0ull) return set_err(F2GPU_ERANGE, "decompose: too many rows for uint32 perm");
+    return decompose_recursive(c, view_of(w), min_cols, perm, rj, rank);
 }
 
 int f2gpu_decompose_block_sharded(f2gpu_ctx* c, f2gpu_mat* w, int G, uint32_t* perm, uint32_t* rj,

@@ -128,3 +128,20 @@ def test_cfg5_tall_sparse(f2, ctx, po):
     assert po.digest(a_host.words, n, m) == g["input_digest"]
     w, perm, rj, rank = run_decomp(f2, ctx, A)
     check_against(po, g, a_host, w, perm, rj, rank, n, m, freivalds=False)
+
+
+def test_cfg4_decompose_recursive_65536(f2, ctx, po):
+    """decompose_recursive at full size: same digests as the block algorithm."""
+    from paper_1209_5198_b200 import _lib
+
+    g = digests()["cfg4"]
+    n = g["n"]
+    lib = _lib.load()
+    A = f2.DeviceMatrix(n, n, ctx)
+    A.random_dense(0.5, g["seed"])
+    perm = np.zeros(n, np.uint32)
+    rj = np.zeros(n // 64, np.uint32)
+    rk = C.c_size_t()
+    _lib.check(lib.f2gpu_decompose_recursive(ctx.handle, A.handle, 0, perm.ctypes.data,
+                                             rj.ctypes.data, C.byref(rk)))
+    check_against(po, g, None, A.download(), perm, rj, int(rk.value), n, n, freivalds=False)

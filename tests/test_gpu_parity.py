@@ -270,3 +270,32 @@ def test_decompose_graph_replay(f2, ctx, po):
             got = W.download()
             assert rk.value == rank and np.array_equal(p, perm) and np.array_equal(r, rj)
             assert np.array_equal(got.words[:, :n], w[:, :n]), (seed, it)
+
+
+# ---------------------------------------------------------------------------
+# decompose_recursive: bit-identical to the block algorithm (oracle)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("n,m,p,min_cols", [(1000, 1000, 0.5, 64), (2048, 2048, 0.5, 128),
+                                            (3000, 2500, 0.5, 64), (700, 1300, 0.1, 64),
+                                            (1300, 700, 0.5, 128), (4096, 4096, 0.5, 256),
+                                            (2000, 2000, 0.01, 64), (640, 1000, 0.5, 64)])
+def test_decompose_recursive(f2, ctx, po, n, m, p, min_cols):
+    a = po.random_dense(n, m, p, n + 3 * m)
+    w, perm, rj, rank = po.decompose_block(a, n, m)
+    got = f2.decompose_recursive(bm(f2, a, n, m), min_cols=min_cols, ctx=ctx)
+    assert got.rank == rank
+    assert np.array_equal(got.block_ranks, rj)
+    assert np.array_equal(got.P.perm, perm)
+    assert same(got.overlay.words, w, n)
+
+
+def test_decompose_recursive_rank_deficient(f2, ctx, po):
+    """Left halves below full rank take the exact rank-r_j fallback."""
+    x = po.random_dense(3000, 900, 0.5, 4)
+    y = po.random_dense(900, 4000, 0.5, 5)
+    a = po.m4rm_mult(x, 3000, 900, y, 4000)
+    w, perm, rj, rank = po.decompose_block(a, 3000, 4000)
+    got = f2.decompose_recursive(bm(f2, a, 3000, 4000), min_cols=128, ctx=ctx)
+    assert got.rank == rank == 900
+    assert np.array_equal(got.P.perm, perm) and np.array_equal(got.block_ranks, rj)
+    assert same(got.overlay.words, w, 3000)

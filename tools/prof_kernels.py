@@ -39,6 +39,14 @@ elif what == "strassen":
     A.random_dense(0.5, 2); B.random_dense(0.5, 3)
     for _ in range(reps):
         _lib.check(lib.f2gpu_strassen_mult(ctx.handle, A.handle, B.handle, Cm.handle, cut))
+elif what == "decompose_rec":
+    n = int(sys.argv[3]) if len(sys.argv) > 3 else 65536
+    mc = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+    A = f2.DeviceMatrix(n, n, ctx); A.random_dense(0.5, 6)
+    import numpy as np
+    perm = np.zeros(n, np.uint32); rj = np.zeros(n // 64, np.uint32); rk = C.c_size_t()
+    for _ in range(reps):
+        _lib.check(lib.f2gpu_decompose_recursive(ctx.handle, A.handle, mc, perm.ctypes.data, rj.ctypes.data, C.byref(rk)))
 elif what == "decompose":
     n = int(sys.argv[3]) if len(sys.argv) > 3 else 65536
     A = f2.DeviceMatrix(n, n, ctx); A.random_dense(0.5, 6)
