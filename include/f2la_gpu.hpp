@@ -7,6 +7,7 @@
 //   strassen_mult(A, B, thr, c)    SPEC.md:192-200    f2la::gpu::strassen_mult(A, B, thr, c)
 //   decompose_block(A)->LUFactors  SPEC.md:319-327    f2la::gpu::decompose_block(A)
 //   rank(A)                        SPEC.md:346-353    f2la::gpu::rank(A)
+//   decompose_recursive(A, mc)     SPEC.md:328-345    f2la::gpu::decompose_recursive(A, mc)
 //
 // Matrices are passed in the reference layout (PackedMatrix<uint64_t>:
 // col_block(q) + col_stride(), bit_matrix.hpp:74-81).  Errors are rethrown as
@@ -111,6 +112,41 @@ LUFactors<Matrix> decompose_block(const Matrix& a) {
             xor_bits_at(f.L, i, R, bits);  // reference helper, bit_matrix.hpp:402-413
         }
         for (std::size_t q = j; q < mu; ++q)
+            for (std::size_t t = 0; t < r; ++t) f.U.word(R + t, q) = f.overlay.word(R + t, q);
+        R += r;
+    }
+    return f;
+}
+
+/// decompose_recursive(A, min_cols): same LUFactors contract;
+/// exact arithmetic and 64-aligned splits make it bit-identical to decompose_block.
+template <class Matrix>
+LUFactors<Matrix> decompose_recursive(const Matrix& a, std::size_t min_cols = 0) {
+    const std::size_t n = a.rows(), m = a.cols();
+    LUFactors<Matrix> f;
+    f2gpu_mat* w = nullptr;
+    check(f2gpu_mat_alloc(context(), n, m, &w), "mat_alloc");
+    struct Free { f2gpu_mat* p; ~Free() { f2gpu_mat_free(p); } } guard{w};
+    if (n && m) check(f2gpu_mat_upload(context(), w, a.col_block(0), a.col_stride()), "upload");
+    f.overlay = Matrix(n, m);
+    f.P.resize(n);
+    std::vector<std::uint32_t> rj(a.word_cols());
+    std::size_t rank = 0;
+    check(f2gpu_decompose_recursive(context(), w, min_cols, f.P.data(), rj.data(), &rank),
+          "decompose_recursive");
+    if (n && m) check(f2gpu_mat_download(context(), w, f.overlay.col_block(0), f.overlay.col_stride()),
+                      "download");
+    f.rank = rank;
+    f.block_ranks.assign(rj.begin(), rj.end());
+    f.L = Matrix(n, rank);
+    f.U = Matrix(rank, m);
+    std::size_t R = 0;
+    for (std::size_t j = 0; j < a.word_cols(); ++j) {
+        const std::size_t r = rj[j];
+        if (!r) continue;
+        for (std::size_t i = R; i < n; ++i)
+            xor_bits_at(f.L, i, R, i < R + r ? (std::uint64_t(1) << (i - R)) : f.overlay.word(i, j));
+        for (std::size_t q = j; q < a.word_cols(); ++q)
             for (std::size_t t = 0; t < r; ++t) f.U.word(R + t, q) = f.overlay.word(R + t, q);
         R += r;
     }

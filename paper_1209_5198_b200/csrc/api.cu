@@ -157,8 +157,10 @@ struct GraphCache {
     }
 };
 
+struct f2gpu_mat;
 struct f2gpu_ctx {
     Timeline tl;
+    f2gpu_mat* stage = nullptr;           // reusable device matrix for host-buffer calls
     GraphCache graph;
     bool use_graphs = true;
     bool lookahead = true;
@@ -858,6 +860,7 @@ int f2gpu_ctx_destroy(f2gpu_ctx* c) {
     if (c->comm && nccl().ok) nccl().commDestroy(c->comm);
     if (c->own_stream) cudaStreamSynchronize(c->own_stream);
     c->graph.reset();
+    if (c->stage) { f2gpu_mat_free(c->stage); c->stage = nullptr; }
     cudaFree(c->scr_st);
     cudaFree(c->scr_perm);
     cudaFree(c->scr_flags);
@@ -1157,14 +1160,27 @@ int f2gpu_strassen_mult_host(f2gpu_ctx* c, const uint64_t* a, size_t n, size_t k
     return f2gpu_mat_download(c, C.m, out, sc);
 }
 
+// Host-buffer calls stage through a context-owned device matrix that is reused
+// while the shape stays the same (no per-call 0.5 GiB cudaMalloc/cudaFree, and a
+// stable pointer keeps the decomposition's CUDA graph cache warm).
+int staging(f2gpu_ctx* c, size_t n, size_t m, f2gpu_mat** out) {
+    if (c->stage && (c->stage->rows != n || c->stage->cols != m)) {
+        f2gpu_mat_free(c->stage);
+        c->stage = nullptr;
+    }
+    if (!c->stage) F2_TRY(f2gpu_mat_alloc(c, n, m, &c->stage));
+    *out = c->stage;
+    return F2GPU_OK;
+}
+
 int f2gpu_decompose_block_host(f2gpu_ctx* c, const uint64_t* a, size_t n, size_t m, size_t stride,
                                uint64_t* w_out, uint32_t* perm, uint32_t* rj, size_t* rank) {
     if (!c) return set_err(F2GPU_EINVAL, "null ctx");
-    MatGuard W;
-    F2_TRY(f2gpu_mat_alloc(c, n, m, &W.m));
-    F2_TRY(f2gpu_mat_upload(c, W.m, a, stride));
-    F2_TRY(f2gpu_decompose_block(c, W.m, perm, rj, rank));
-    if (w_out) F2_TRY(f2gpu_mat_download(c, W.m, w_out, stride));
+    f2gpu_mat* W = nullptr;
+    F2_TRY(staging(c, n, m, &W));
+    F2_TRY(f2gpu_mat_upload(c, W, a, stride));
+    F2_TRY(f2gpu_decompose_block(c, W, perm, rj, rank));
+    if (w_out) F2_TRY(f2gpu_mat_download(c, W, w_out, stride));
     return F2GPU_OK;
 }
 

@@ -27,6 +27,9 @@ int main() {
     const BitMatrix pa = f2la::gather_rows(a, std::span<const std::uint32_t>(f.P));
     const bool lu_ok = f2la::m4rm_mult(f.L, f.U, 8) == pa;
     const bool rank_ok = f2la::gpu::rank(a) == f.rank && f.rank == 777;
-    std::printf("mult %d  plu %d  rank %d (%zu)\n", mult_ok, lu_ok, rank_ok, f.rank);
-    return (mult_ok && lu_ok && rank_ok) ? 0 : 1;
+    const auto g = f2la::gpu::decompose_recursive(a, 128);
+    const bool rec_ok = g.P == f.P && g.overlay == f.overlay && g.L == f.L && g.U == f.U;
+    std::printf("mult %d  plu %d  rank %d (%zu)  recursive %d\n", mult_ok, lu_ok, rank_ok, f.rank,
+                rec_ok);
+    return (mult_ok && lu_ok && rank_ok && rec_ok) ? 0 : 1;
 }

@@ -105,7 +105,7 @@ def test_cpp_shim_compiles_against_reference():
     if not ref.is_dir():
         pytest.skip("reference headers not present")
     src = ROOT / "tests" / "cpp" / "shim_example.cpp"
-    out = Path("/tmp/f2gpu_shim_example")
+    out = ROOT / "tests" / "cpp" / "shim_example.bin"  # travels to the GPU box (git-ignored)
     from paper_1209_5198_b200 import _lib
 
     _lib.load()
