@@ -13,6 +13,13 @@
 
 #include <algorithm>
 
+#ifndef F2_PIPELINED_WRITEBACK
+#define F2_PIPELINED_WRITEBACK 0
+#endif
+#ifndef F2_FENCE_IN_PRODUCER
+#define F2_FENCE_IN_PRODUCER 0
+#endif
+
 namespace f2 {
 
 // ---------------------------------------------------------------------------
@@ -401,6 +408,9 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
+__device__ __forceinline__ void bulk_wait_read1() {
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -674,20 +684,46 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
         dc.init(T, s0, len0, s1);
         int s = 0, ae = 0;
         uint32_t dph = 0, aph = 0;
+        // Pipelined write-back: tile t's reductions are committed, and the stage of
+        // tile t-1 is released once ITS reductions have read shared memory
+        // (wait_group.read 1), so the producer never blocks on the tile it just issued.
+        int sprev = -1;
         for (size_t t = 0; t < cnt; ++t) {
             const size_t r0 = base + dc.tt * kV3Rows;
             const int nvalid = min(kTabCols, int(size_t(p.ncols) - dc.g * kTabCols));
             mbar_wait(&d_done[s], dph);
-            if (lane < nvalid) {
+            // consumers' generic-proxy smem writes (released by their d_done arrivals,
+            // acquired by the wait above) -> ordered before the async-proxy reads of
+            // the bulk reductions by one cumulative proxy fence here
+#if F2_FENCE_IN_PRODUCER
+            fence_async_smem();
+#endif
+            const bool issued = lane < nvalid;
+            if (issued) {
                 bulk_red_xor(p.C + (p.c_wcol0 + dc.g * kTabCols + lane) * p.sc + r0,
                              dring + size_t(s) * kV3DBytes + lane * kV3ColPitch, kV3ABytes);
                 bulk_commit();
-                if (p.release && t + 1 == len0) bulk_wait0();  // group-0 writes complete
-                else bulk_wait_read0();
             }
+            const bool rel_point = p.release && t + 1 == len0;
+#if F2_PIPELINED_WRITEBACK
+            if (rel_point) bulk_wait0();          // group-0 writes complete in memory
+            else if (issued) bulk_wait_read1();   // previous tile's reads done
+            else bulk_wait_read0();
             __syncwarp();
-            if (p.release && t + 1 == len0 && lane == 0) release_signal(p.release);
+            if (rel_point && lane == 0) release_signal(p.release);
+            if (lane == 0) {
+                if (rel_point) mbar_arrive(&d_free[s]);  // everything drained
+                if (sprev >= 0) mbar_arrive(&d_free[sprev]);
+            }
+            sprev = rel_point ? -1 : s;
+#else
+            if (rel_point) bulk_wait0();          // group-0 writes complete in memory
+            else bulk_wait_read0();               // this tile's reads done
+            __syncwarp();
+            if (rel_point && lane == 0) release_signal(p.release);
             if (lane == 0) mbar_arrive(&d_free[s]);
+            (void)sprev;
+#endif
             if (t + kV3AStages < cnt) {
                 mbar_wait(&a_empty[ae], aph);
                 issue_a();
@@ -697,6 +733,7 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
             dc.next();
         }
         bulk_wait0();
+        // (the last tile's stage needs no release: no consumer waits for it)
         return;
     }
 
@@ -743,7 +780,9 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
         ulonglong2* dp = reinterpret_cast<ulonglong2*>(dring + size_t(s) * kV3DBytes + col * kV3ColPitch) + rl / 2;
         dp[0] = make_ulonglong2(d[0], d[1]);
         dp[1] = make_ulonglong2(d[2], d[3]);
-        fence_async_smem();
+#if !F2_FENCE_IN_PRODUCER
+        fence_async_smem();  // generic-proxy smem writes -> async-proxy bulk reductions
+#endif
         __syncwarp();
         if (lane == 0) mbar_arrive(&d_done[s]);
         if (++as == kV3AStages) { as = 0; aph ^= 1; }
