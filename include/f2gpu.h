@@ -103,6 +103,10 @@ int f2gpu_m4rm_mult_acc(f2gpu_ctx *ctx, const f2gpu_mat *a, const f2gpu_mat *b, 
 int f2gpu_mult_acc(f2gpu_ctx *ctx, f2gpu_mat *c, size_t c_row0, size_t c_wcol0,
                    size_t n_wcols, const uint64_t *d_a_words, size_t n_rows, size_t k_bits,
                    const f2gpu_mat *b, size_t b_row0, size_t b_wcol0);
+/* The evaluated alternative leaf (north_star): C = A*B (acc=0) or C ^= A*B on the
+ * tensor cores, tcgen05.mma kind::i8 on bit->byte expanded operands, parity of the
+ * s32 accumulators.  Requires n % 256 == 0, m % 128 == 0, k % 64 == 0. */
+int f2gpu_gemm_tc(f2gpu_ctx *ctx, const f2gpu_mat *a, const f2gpu_mat *b, f2gpu_mat *c, int acc);
 /* Strassen-Winograd over device sub-blocks, M4RM leaves
  * below the cutover. threshold = 0 -> context cutover. C = A*B. */
 int f2gpu_strassen_mult(f2gpu_ctx *ctx, const f2gpu_mat *a, const f2gpu_mat *b, f2gpu_mat *c,

@@ -1033,6 +1033,30 @@ int f2gpu_m4rm_mult(f2gpu_ctx* c, const f2gpu_mat* a, const f2gpu_mat* b, f2gpu_
     return gemm_acc(c, view_of(cm), view_of(a), view_of(b));
 }
 
+int f2gpu_gemm_tc(f2gpu_ctx* c, const f2gpu_mat* a, const f2gpu_mat* b, f2gpu_mat* cm, int acc) {
+    if (!c || !a || !b || !cm) return set_err(F2GPU_EINVAL, "null argument");
+    if (a->cols != b->rows || cm->rows != a->rows || cm->cols != b->cols)
+        return set_err(F2GPU_EINVAL, "gemm_tc: shape mismatch");
+    if (!f2::gemm_tc_ok(a->rows, a->cols, b->cols))
+        return set_err(F2GPU_EINVAL, "gemm_tc: needs n % 256 == 0, m % 128 == 0, k % 64 == 0");
+    if (f2::gemm_tc2_ok(a->rows, a->cols, b->cols)) {
+        // B^T once (m x k), then the 256x256-tile kernel reads both operands as k-rows
+        const size_t sbt = (b->cols + 127) / 128 * 128;
+        DevBuf bt(c);
+        if (int e = bt.alloc(sbt * ceil64(b->rows) * 8)) return e;
+        if (int e = check_launch(c, f2::launch_transpose(b->d, b->rows, b->cols, b->stride, bt.as<uint64_t>(),
+                                                         sbt, c->stream),
+                                 "k_transpose"))
+            return e;
+        return check_launch(c, f2::launch_gemm_tc2(a->d, a->stride, bt.as<uint64_t>(), sbt, cm->d, cm->stride,
+                                                   a->rows, a->cols, b->cols, acc != 0, c->stream),
+                            "k_gemm_tc2");
+    }
+    return check_launch(c, f2::launch_gemm_tc(a->d, a->stride, b->d, b->stride, cm->d, cm->stride,
+                                              a->rows, a->cols, b->cols, acc != 0, c->stream),
+                        "k_gemm_tc");
+}
+
 int f2gpu_mult_acc(f2gpu_ctx* c, f2gpu_mat* cm, size_t c_row0, size_t c_wcol0, size_t n_wcols,
                    const uint64_t* d_a, size_t n_rows, size_t k_bits, const f2gpu_mat* b,
                    size_t b_row0, size_t b_wcol0) {

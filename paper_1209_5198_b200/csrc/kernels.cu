@@ -765,8 +765,6 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
             x[2 * q] = v.x;
             x[2 * q + 1] = v.y;
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&a_empty[as]);
         const size_t row = base + cc.tt * kV3Rows + rl;
         if (row < row_lo || row + 4 > row_hi) {
 #pragma unroll
@@ -776,6 +774,11 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
         uint64_t d[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) d[q] = lookup9(colofs, x[q]);
+        // release the A stage only once every lane has CONSUMED its words: an
+        // mbarrier arrive is not ordered behind the warp's outstanding shared loads,
+        // so arriving right after the LDS could let the next bulk load overwrite them
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_empty[as]);
         if (t >= size_t(kV3DStages)) mbar_wait(&d_free[s], dph ^ 1);
         ulonglong2* dp = reinterpret_cast<ulonglong2*>(dring + size_t(s) * kV3DBytes + col * kV3ColPitch) + rl / 2;
         dp[0] = make_ulonglong2(d[0], d[1]);

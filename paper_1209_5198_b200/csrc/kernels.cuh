@@ -99,6 +99,17 @@ cudaError_t launch_xor_batched(const XorJob* d_jobs, int njobs, size_t max_rows,
 size_t gemm_units_host(const GemmArgs& p);
 bool gemm_fast_ok(const GemmArgs& g);
 
+// evaluated tensor-core leaf (tc_leaf.cu): int8 tcgen05 GF(2) product,
+// n % 256 == 0, m % 128 == 0, k % 64 == 0
+bool gemm_tc_ok(size_t n, size_t k, size_t m);
+cudaError_t launch_gemm_tc(const uint64_t* A, size_t sa, const uint64_t* B, size_t sb, uint64_t* C,
+                           size_t sc, size_t n, size_t k, size_t m, bool acc, cudaStream_t s);
+// 256x256-tile variant on a pre-transposed B (BT = B^T, m x k):
+// n % 256 == 0, m % 256 == 0, k % 64 == 0
+bool gemm_tc2_ok(size_t n, size_t k, size_t m);
+cudaError_t launch_gemm_tc2(const uint64_t* A, size_t sa, const uint64_t* BT, size_t sbt, uint64_t* C,
+                            size_t sc, size_t n, size_t k, size_t m, bool acc, cudaStream_t s);
+
 // per-device one-time setup (dynamic shared memory opt-in)
 cudaError_t init_kernel_attrs();
 

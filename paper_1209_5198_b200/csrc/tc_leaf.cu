@@ -1,0 +1,540 @@
+// tc_leaf.cu — the evaluated alternative GEMM leaf (north_star): GF(2) products
+// on the 5th-generation tensor cores.
+//
+// sm_100a has no binary (b1) MMA: mma.sync .b1 is emulated with IMMA and tcgen05
+// has no b1 kind (SURVEY Probe P6).  The leaf therefore expands bits to 0/1
+// bytes and runs tcgen05.mma.cta_group::1.kind::i8 with s32 accumulation in
+// TMEM; the parity of each accumulator is the GF(2) result.
+//
+// Transposed formulation D^T = B^T * A^T: the MMA's M dimension (TMEM lanes) is
+// the output COLUMN, N (TMEM columns) the output ROW.  After tcgen05.ld each
+// thread holds one output column for 32 consecutive rows, so one __ballot_sync
+// of the accumulator LSBs yields 32 packed output bits of one row: the epilogue
+// costs two instructions per 32 output bits.
+//
+// Tile: 128 output columns x 256 output rows per CTA, k-blocks of 64 bits
+// (two K=32 MMAs), operands expanded in registers into a double-buffered
+// canonical K-major no-swizzle layout ((8,n),2):((16B,SBO),LBO) with LBO=128 B,
+// SBO=512 B, MMA completion tracked with tcgen05.commit -> mbarrier.
+#include <cstdint>
+#include <cstdlib>
+
+#include "kernels.cuh"
+
+namespace f2 {
+
+namespace {
+
+constexpr int kTcThreads = 256;  // 8 warps: expansion; thread 0 issues MMAs; warps 0-3 epilogue
+constexpr int kTcM = 128;        // output columns per CTA (TMEM lanes)
+constexpr int kTcN = 256;        // output rows per CTA (TMEM columns)
+constexpr int kTcABytes = kTcM * 64;  // B^T tile: 128 x 64 bytes
+constexpr int kTcBBytes = kTcN * 64;  // A^T tile: 256 x 64 bytes
+constexpr int kTcStage = kTcABytes + kTcBBytes;
+constexpr size_t kTcSmem = 2 * size_t(kTcStage) + 64;
+
+__device__ __forceinline__ uint32_t sm_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 8 bits -> 8 bytes of 0/1 (byte j = bit j)
+__device__ __forceinline__ uint64_t expand8(uint32_t x) {
+    uint64_t y = (uint64_t(x & 0xFFu) * 0x0101010101010101ull) & 0x8040201008040201ull;
+    return ((y + 0x7F7F7F7F7F7F7F7Full) >> 7) & 0x0101010101010101ull;
+}
+
+#ifndef F2_TC_SWIZZLE64
+#define F2_TC_SWIZZLE64 1
+#endif
+// canonical K-major offset of (row r, 16-byte k-chunk c) in a tile.
+// SWIZZLE_64B: 8-row atoms of 64-byte rows (SBO = 512 B), chunk index XOR-ed
+// with address bits [7,9) = (r >> 1) & 3 (Swizzle<2,4,3>).
+// SWIZZLE_NONE: core matrices of 8 rows x 16 B, LBO = 128 B, SBO = 512 B.
+__device__ __forceinline__ uint32_t kmaj_off(int r, int c) {
+#if F2_TC_SWIZZLE64
+    return uint32_t((r >> 3) * 512 + (r & 7) * 64 + ((c ^ ((r >> 1) & 3)) * 16));
+#else
+    return uint32_t((r >> 3) * 512 + c * 128 + (r & 7) * 16);
+#endif
+}
+
+// 4 bits -> 4 bytes of 0/1: the shifted copies x, x<<7, x<<14, x<<21 do not
+// overlap, so one multiply places bit i at bit 8i
+__device__ __forceinline__ uint32_t expand4(uint32_t x) { return ((x & 0xFu) * 0x00204081u) & 0x01010101u; }
+
+// store the 64 0/1 bytes of word w as row r of a K-major tile
+__device__ __forceinline__ void store_row(unsigned char* tile, int r, uint64_t w) {
+    const uint32_t lo = uint32_t(w), hi = uint32_t(w >> 32);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const uint32_t x = (c < 2) ? (lo >> (16 * c)) : (hi >> (16 * (c - 2)));
+        uint4 v;
+        v.x = expand4(x);
+        v.y = expand4(x >> 4);
+        v.z = expand4(x >> 8);
+        v.w = expand4(x >> 12);
+        *reinterpret_cast<uint4*>(tile + kmaj_off(r, c)) = v;
+    }
+}
+
+// smem descriptor; the K=32 second half of a k-block advances the start address
+// by 256 B (no swizzle: 2 k-chunks of LBO) or 32 B (inside the 64-byte swizzled row)
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= uint64_t((saddr >> 4) & 0x3FFF);        // start address
+#if F2_TC_SWIZZLE64
+    d |= uint64_t(1) << 16;                      // LBO (unused for swizzled K-major)
+    d |= uint64_t(512 >> 4) << 32;               // SBO: next 8-row atom
+    d |= uint64_t(1) << 46;                      // version (Blackwell)
+    d |= uint64_t(4) << 61;                      // SWIZZLE_64B
+#else
+    d |= uint64_t(128 >> 4) << 16;               // LBO: next 16-byte k-chunk
+    d |= uint64_t(512 >> 4) << 32;               // SBO: next group of 8 rows
+    d |= uint64_t(1) << 46;                      // version (Blackwell)
+#endif
+    return d;
+}
+constexpr uint32_t kKHalf = F2_TC_SWIZZLE64 ? 32u : 256u;
+
+// kind::i8, A=u8, B=u8, D=s32, both K-major, M=128, N=256
+constexpr uint32_t kIdesc = (2u << 4) | (0u << 7) | (0u << 10) | (uint32_t(kTcN >> 3) << 17) |
+                            (uint32_t(kTcM >> 4) << 24);
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+    const uint32_t z = 0;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %5, %5, %5}, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(kIdesc), "r"(acc), "r"(z));
+}
+
+__device__ __forceinline__ void mbar_init1(uint64_t* b) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm_u32(b)));
+}
+__device__ __forceinline__ void mbar_wait1(uint64_t* b, uint32_t ph) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "L_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra L_%=;\n}" ::"r"(sm_u32(b)),
+        "r"(ph)
+        : "memory");
+}
+
+}  // namespace
+
+// C (n x m) = A (n x k) * B (k x m) over GF(2); n % 256 == 0, m % 128 == 0, k % 64 == 0.
+// acc != 0: C ^= A*B.
+__global__ void __launch_bounds__(kTcThreads, 1)
+    k_gemm_tc(const uint64_t* __restrict__ A, size_t sa, const uint64_t* __restrict__ B, size_t sb,
+              uint64_t* __restrict__ C, size_t sc, size_t n, size_t k, size_t m, int acc) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + 2 * kTcStage);  // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 2);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const size_t c0 = size_t(blockIdx.x) * kTcM;  // output column base
+    const size_t i0 = size_t(blockIdx.y) * kTcN;  // output row base
+    const size_t q0 = c0 / 64;
+    const size_t KB = k / 64;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         sm_u32(tmem_slot)),
+                     "r"(uint32_t(kTcN)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        mbar_init1(&mbar[0]);
+        mbar_init1(&mbar[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    uint32_t ph[2] = {0, 0};
+    // operand words of the NEXT k-block are prefetched into registers while the
+    // current one is expanded (the L2 latency is off the critical path)
+    const bool bt_warp = warp < 2;                 // warps 0,1: B^T (transpose + expand)
+    const int ar0 = tid - 64, ar1 = tid + 128;     // warps 2..7: A^T rows (1-2 per thread)
+    const bool has_ar1 = !bt_warp && ar1 < kTcN;
+    uint64_t pa0 = 0, pa1 = 0, pb0 = 0, pb1 = 0;
+    auto fetch = [&](size_t kb) {
+        if (bt_warp) {
+            const uint64_t* bp = B + (q0 + warp) * sb + kb * 64;
+            pb0 = bp[lane];
+            pb1 = bp[lane + 32];
+        } else {
+            pa0 = A[kb * sa + i0 + ar0];
+            if (has_ar1) pa1 = A[kb * sa + i0 + ar1];
+        }
+    };
+    fetch(0);
+    for (size_t kb = 0; kb < KB; ++kb) {
+        const int s = int(kb & 1);
+        unsigned char* ta = smem + s * kTcStage;  // B^T tile (MMA A operand)
+        unsigned char* tb = ta + kTcABytes;       // A^T tile (MMA B operand)
+        const uint64_t a0 = pa0, a1 = pa1;
+        uint64_t x0 = pb0, x1 = pb1;
+        if (kb + 1 < KB) fetch(kb + 1);
+        if (kb >= 2) {  // the MMA that last read this stage has completed
+            mbar_wait1(&mbar[s], ph[s]);
+            ph[s] ^= 1;
+        }
+        if (!bt_warp) {
+            store_row(tb, ar0, a0);
+            if (has_ar1) store_row(tb, ar1, a1);
+        } else {
+            // B^T: transpose the 64x64 bit tile of word-column q0+warp (rows k -> columns)
+            {   // stage 32 (in-lane)
+                const uint64_t t = ((x0 >> 32) ^ x1) & 0x00000000FFFFFFFFull;
+                x1 ^= t;
+                x0 ^= t << 32;
+            }
+            const uint64_t masks[5] = {0x0000FFFF0000FFFFull, 0x00FF00FF00FF00FFull,
+                                       0x0F0F0F0F0F0F0F0Full, 0x3333333333333333ull,
+                                       0x5555555555555555ull};
+#pragma unroll
+            for (int st = 0; st < 5; ++st) {
+                const int j = 16 >> st;
+                const uint64_t msk = masks[st];
+                const uint64_t y0 = __shfl_xor_sync(0xffffffffu, x0, j);
+                const uint64_t y1 = __shfl_xor_sync(0xffffffffu, x1, j);
+                if (!(lane & j)) {
+                    x0 ^= (((x0 >> j) ^ y0) & msk) << j;
+                    x1 ^= (((x1 >> j) ^ y1) & msk) << j;
+                } else {
+                    x0 ^= ((y0 >> j) ^ x0) & msk;
+                    x1 ^= ((y1 >> j) ^ x1) & msk;
+                }
+            }
+            store_row(ta, 64 * warp + lane, x0);       // output column c0 + 64w + lane
+            store_row(ta, 64 * warp + lane + 32, x1);  // output column c0 + 64w + lane + 32
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t sa_ = sm_u32(ta), sb_ = sm_u32(tb);
+            mma_i8(tmem, umma_desc(sa_), umma_desc(sb_), kb > 0 ? 1u : 0u);
+            mma_i8(tmem, umma_desc(sa_ + kKHalf), umma_desc(sb_ + kKHalf), 1u);
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             sm_u32(&mbar[s]))
+                         : "memory");
+        }
+    }
+    // wait for the last MMA (tcgen05.commit tracks all prior MMAs of this thread)
+    {
+        const int s = int((KB - 1) & 1);
+        mbar_wait1(&mbar[s], ph[s]);
+    }
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    // epilogue: warp w (0..3) owns TMEM lanes 32w..32w+31 = output columns c0+32w+lane
+    const size_t q = q0 + ((warp & 3) >> 1);
+    uint32_t* crow = reinterpret_cast<uint32_t*>(C + q * sc + i0) + (warp & 1);
+#pragma unroll 1
+    for (int chunk = 0; chunk < (warp < 4 ? kTcN / 32 : 0); ++chunk) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem + (uint32_t(32 * warp) << 16) + uint32_t(32 * chunk);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+            "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+            "%28, %29, %30, %31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+              "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+              "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+              "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+              "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        uint32_t mine = 0;
+#pragma unroll
+        for (int r = 0; r < 32; ++r) {
+            const uint32_t bits = __ballot_sync(0xffffffffu, v[r] & 1u);
+            if (lane == r) mine = bits;
+        }
+        const size_t row = size_t(32 * chunk + lane);
+        uint32_t* dst = crow + 2 * row;  // 32-bit half of word (i0+row, q)
+        if (acc) mine ^= *dst;
+        *dst = mine;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"(uint32_t(kTcN)));
+}
+
+// ---- v2: 256x256 output tiles, warp-specialised, pre-transposed B ----
+// B is transposed once beforehand (B^T: m x k, one pass over B), so both
+// operands arrive as "rows of 64 k-bits": word (r, kb) at X[kb * s + r].  Per
+// k-block the load warp bulk-copies 256 B^T words + 256 A words (4 KB) into an
+// 8-deep raw ring; 16 expansion warps turn one word each into a 64-byte 0/1
+// row of the SWIZZLE_64B K-major tiles; the MMA warp issues 4 x (M=128, N=256,
+// K=32) int8 MMAs into two TMEM accumulators (all 512 columns) and commits the
+// stage release.  The k order inside a k-block is permuted identically for both
+// operands ((x >> t) & 0x01010101 spreads bits t, t+8, t+16, t+24 of a 32-bit
+// half into one 4-byte word), which a dot product does not see and which costs
+// two instructions per 4 output bytes.
+constexpr int kT2Exp = 512;                  // expansion threads (warps 0-15)
+constexpr int kT2Mma = kT2Exp / 32;          // warp 16: MMA issuer
+constexpr int kT2Load = kT2Mma + 1;          // warp 17: bulk loads
+constexpr int kT2Threads = kT2Exp + 64;
+constexpr int kT2Cols = 256;                 // output columns per CTA (2 x M=128)
+constexpr int kT2Rows = 256;                 // output rows per CTA (N=256)
+constexpr int kT2ABytes = kT2Cols * 64;      // expanded B^T tile (MMA A operand)
+constexpr int kT2BBytes = kT2Rows * 64;      // expanded A^T tile (MMA B operand)
+constexpr int kT2Slot = kT2ABytes + kT2BBytes;  // one expanded k-block
+constexpr int kT2Kps = 2;                        // k-blocks per pipeline stage
+constexpr int kT2Stage = kT2Kps * kT2Slot;
+constexpr int kT2Stages = 3;
+constexpr int kT2RawBytes = (kT2Rows + kT2Cols) * 8;  // packed words of one k-block
+constexpr int kT2Raw = 4;
+constexpr size_t kT2Smem = size_t(kT2Stages) * kT2Stage + size_t(kT2Raw) * kT2RawBytes + 256;
+
+__device__ __forceinline__ void mbar_init_n(uint64_t* b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_u32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_arrive1(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            sm_u32(dst)),
+        "l"(src), "r"(bytes), "r"(sm_u32(bar))
+        : "memory");
+}
+
+// 64 bits -> 64 bytes of 0/1 in the permuted k order, row r of a K-major tile
+__device__ __forceinline__ void store_row_perm(unsigned char* tile, int r, uint64_t w) {
+    const uint32_t h[2] = {uint32_t(w), uint32_t(w >> 32)};
+    constexpr uint32_t M = 0x01010101u;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const uint32_t x = h[c >> 1] >> (4 * (c & 1));
+        uint4 v;
+        v.x = x & M;
+        v.y = (x >> 1) & M;
+        v.z = (x >> 2) & M;
+        v.w = (x >> 3) & M;
+        *reinterpret_cast<uint4*>(tile + kmaj_off(r, c)) = v;
+    }
+}
+
+// MODE (diagnostic, F2GPU_TC_MODE): 0 normal; 1 expansion warps skip the
+// expanded stores (MMA-bound rate); 2 the MMA warp skips the MMAs (expansion rate);
+// 3 = 2 without the proxy fence; 4 = full kernel without the proxy fence (timing only)
+template <int MODE>
+__global__ void __launch_bounds__(kT2Threads, 1)
+    k_gemm_tc2(const uint64_t* __restrict__ A, size_t sa, const uint64_t* __restrict__ BT, size_t sbt,
+               uint64_t* __restrict__ C, size_t sc, size_t k, int acc) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    unsigned char* raw = smem + size_t(kT2Stages) * kT2Stage;
+    uint64_t* full = reinterpret_cast<uint64_t*>(raw + size_t(kT2Raw) * kT2RawBytes);
+    uint64_t* empty = full + kT2Stages;
+    uint64_t* rfull = empty + kT2Stages;
+    uint64_t* rempty = rfull + kT2Raw;
+    uint64_t* done = rempty + kT2Raw;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const size_t c0 = size_t(blockIdx.x) * kT2Cols;
+    const size_t i0 = size_t(blockIdx.y) * kT2Rows;
+    const size_t KB = k / 64;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         sm_u32(tmem_slot)),
+                     "r"(512u));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int s = 0; s < kT2Stages; ++s) {
+            mbar_init_n(&full[s], kT2Exp / 32);  // one arrive per expansion warp
+            mbar_init_n(&empty[s], 1);
+        }
+        for (int s = 0; s < kT2Raw; ++s) {
+            mbar_init_n(&rfull[s], 1);
+            mbar_init_n(&rempty[s], kT2Exp / 32);
+        }
+        mbar_init_n(done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == kT2Load) {
+        // ===== load warp: raw operand words, kT2Raw k-blocks ahead =====
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (size_t kb = 0; kb < KB; ++kb) {
+                if (kb >= size_t(kT2Raw)) mbar_wait1(&rempty[s], ph ^ 1);
+                unsigned char* r = raw + size_t(s) * kT2RawBytes;
+                mbar_expect(&rfull[s], kT2RawBytes);
+                bulk_g2s(r, BT + kb * sbt + c0, kT2Cols * 8, &rfull[s]);
+                bulk_g2s(r + kT2Cols * 8, A + kb * sa + i0, kT2Rows * 8, &rfull[s]);
+                if (++s == kT2Raw) { s = 0; ph ^= 1; }
+            }
+        }
+        __syncwarp();
+    } else if (warp == kT2Mma) {
+        // ===== MMA issuer =====
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (size_t kb = 0; kb < KB; kb += kT2Kps) {
+                mbar_wait1(&full[s], ph);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+                for (int j = 0; j < kT2Kps; ++j) {
+                    if (kb + j >= KB) break;
+                    const uint32_t ta = sm_u32(smem + size_t(s) * kT2Stage + j * kT2Slot);
+                    const uint32_t tb = ta + kT2ABytes;
+                    const uint32_t a0 = kb + j > 0 ? 1u : 0u;
+                    if (MODE != 2 && MODE != 3) {
+                        mma_i8(tmem, umma_desc(ta), umma_desc(tb), a0);
+                        mma_i8(tmem, umma_desc(ta + kKHalf), umma_desc(tb + kKHalf), 1u);
+                        mma_i8(tmem + 256, umma_desc(ta + 128 * 64), umma_desc(tb), a0);
+                        mma_i8(tmem + 256, umma_desc(ta + 128 * 64 + kKHalf), umma_desc(tb + kKHalf), 1u);
+                    }
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 sm_u32(&empty[s]))
+                             : "memory");
+                if (++s == kT2Stages) { s = 0; ph ^= 1; }
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             sm_u32(done))
+                         : "memory");
+        }
+        __syncwarp();
+    } else {
+        // ===== expansion warps 0-15: thread t expands raw word t =====
+        // t < 256: B^T row t (output column c0 + t); t >= 256: A^T row t - 256
+        const int region = tid < kT2Cols ? 0 : kT2ABytes;
+        const int r = tid & 255;
+        int s = 0, rs = 0;
+        uint32_t ph = 0, rph = 0;
+        for (size_t kb = 0, st = 0; kb < KB; kb += kT2Kps, ++st) {
+            if (st >= size_t(kT2Stages)) mbar_wait1(&empty[s], ph ^ 1);
+#pragma unroll
+            for (int j = 0; j < kT2Kps; ++j) {
+                if (kb + j >= KB) break;
+                mbar_wait1(&rfull[rs], rph);
+                const uint64_t x = reinterpret_cast<const uint64_t*>(raw + size_t(rs) * kT2RawBytes)[tid];
+                unsigned char* tile = smem + size_t(s) * kT2Stage + j * kT2Slot + region;
+                if (MODE == 1) {
+                    if (x == 0x123456789ull) tile[r] = 1;  // keep the load alive
+                } else {
+                    store_row_perm(tile, r, x);
+                }
+                // the raw slot is released only after x was consumed by the stores
+                // above: an arrive right after the LDS can overtake it (the mbarrier
+                // unit is not ordered behind outstanding shared loads) and let the
+                // next bulk load overwrite a word not yet read
+                __syncwarp();
+                if (lane == 0) mbar_arrive1(&rempty[rs]);
+                if (++rs == kT2Raw) { rs = 0; rph ^= 1; }
+            }
+            if (MODE < 3) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive1(&full[s]);
+            if (++s == kT2Stages) { s = 0; ph ^= 1; }
+        }
+        // ===== epilogue: warp w -> accumulator (w>>2)&1, TMEM lanes 32(w&3).., row half w>>3 =====
+        mbar_wait1(done, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const int accn = (warp >> 2) & 1, lq = warp & 3, rh = warp >> 3;
+        const size_t col = c0 + size_t(accn) * 128 + size_t(lq) * 32;  // first output column
+        uint32_t* crow = reinterpret_cast<uint32_t*>(C + (col / 64) * sc + i0) + ((col / 32) & 1);
+#pragma unroll 1
+        for (int chunk = 4 * rh; chunk < 4 * rh + 4; ++chunk) {
+            uint32_t v[32];
+            const uint32_t taddr = tmem + (uint32_t(32 * lq) << 16) + uint32_t(256 * accn + 32 * chunk);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+                "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+                "%28, %29, %30, %31}, [%32];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                  "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+                  "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+                  "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+                  "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+                  "=r"(v[31])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            uint32_t mine = 0;
+#pragma unroll
+            for (int q = 0; q < 32; ++q) {
+                const uint32_t bits = __ballot_sync(0xffffffffu, v[q] & 1u);
+                if (lane == q) mine = bits;
+            }
+            uint32_t* dst = crow + 2 * size_t(32 * chunk + lane);
+            if (acc) mine ^= *dst;
+            *dst = mine;
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
+}
+
+bool gemm_tc_ok(size_t n, size_t k, size_t m) {
+    return n > 0 && k > 0 && m > 0 && n % kTcN == 0 && m % kTcM == 0 && k % 64 == 0;
+}
+bool gemm_tc2_ok(size_t n, size_t k, size_t m) {
+    return n > 0 && k > 0 && m > 0 && n % kT2Rows == 0 && m % kT2Cols == 0 && k % 64 == 0;
+}
+
+// C (n x m) (^)= A (n x k) * B (k x m) given BT = B^T (m x k, stride sbt)
+cudaError_t launch_gemm_tc2(const uint64_t* A, size_t sa, const uint64_t* BT, size_t sbt, uint64_t* C,
+                            size_t sc, size_t n, size_t k, size_t m, bool acc, cudaStream_t s) {
+    static bool attr = false;
+    static int mode = 0;
+    if (!attr) {
+        for (auto fn : {k_gemm_tc2<0>, k_gemm_tc2<1>, k_gemm_tc2<2>, k_gemm_tc2<3>, k_gemm_tc2<4>}) {
+            cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 int(kT2Smem));
+            if (e != cudaSuccess) return e;
+        }
+        const char* env = getenv("F2GPU_TC_MODE");
+        mode = env ? atoi(env) : 0;
+        attr = true;
+    }
+    if (!gemm_tc2_ok(n, k, m) || (sbt % 2) || (sa % 2) ||
+        (reinterpret_cast<uintptr_t>(A) % 16) || (reinterpret_cast<uintptr_t>(BT) % 16))
+        return cudaErrorInvalidValue;
+    dim3 grid(unsigned(m / kT2Cols), unsigned(n / kT2Rows));
+    auto fn = mode == 1 ? k_gemm_tc2<1> : mode == 2 ? k_gemm_tc2<2> : mode == 3 ? k_gemm_tc2<3>
+            : mode == 4 ? k_gemm_tc2<4> : k_gemm_tc2<0>;
+    fn<<<grid, kT2Threads, kT2Smem, s>>>(A, sa, BT, sbt, C, sc, k, acc ? 1 : 0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gemm_tc(const uint64_t* A, size_t sa, const uint64_t* B, size_t sb, uint64_t* C,
+                           size_t sc, size_t n, size_t k, size_t m, bool acc, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(kTcSmem));
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    if (!gemm_tc_ok(n, k, m)) return cudaErrorInvalidValue;
+    dim3 grid(unsigned(m / kTcM), unsigned(n / kTcN));
+    k_gemm_tc<<<grid, kTcThreads, kTcSmem, s>>>(A, sa, B, sb, C, sc, n, k, m, acc ? 1 : 0);
+    return cudaGetLastError();
+}
+
+}  // namespace f2

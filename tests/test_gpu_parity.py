@@ -105,6 +105,58 @@ def test_strassen_cfg2(f2, ctx, po):
     assert same(got.words, want, n)
 
 
+# tensor-core leaf (evaluated alternative, tc_leaf.cu): 256x256 tiles on a
+# pre-transposed B when m % 256 == 0, else the 128-column v1 kernel
+TC_SHAPES = [(256, 64, 128), (256, 128, 256), (512, 64, 256), (256, 640, 384), (512, 192, 512),
+             (1024, 1024, 1024), (2048, 4096, 1536), (768, 4160, 512)]
+
+
+def _tc(f2, ctx, lib, a, b, n, k, m, acc, c0=None):
+    A = f2.DeviceMatrix.from_host(f2.BitMatrix(n, k, a), ctx)
+    B = f2.DeviceMatrix.from_host(f2.BitMatrix(k, m, b), ctx)
+    C = f2.DeviceMatrix.from_host(f2.BitMatrix(n, m, c0), ctx) if c0 is not None else f2.DeviceMatrix(n, m, ctx)
+    f2._lib.check(lib.f2gpu_gemm_tc(ctx.handle, A.handle, B.handle, C.handle, acc))
+    return C.download().words
+
+
+@pytest.mark.parametrize("n,k,m", TC_SHAPES)
+def test_gemm_tc(f2, ctx, po, n, k, m):
+    lib = f2._lib.load()
+    a = po.random_dense(n, k, 0.5, n + 3 * k)
+    b = po.random_dense(k, m, 0.5, k + 5 * m)
+    assert same(_tc(f2, ctx, lib, a, b, n, k, m, 0), po.m4rm_mult(a, n, k, b, m), n)
+
+
+def test_gemm_tc_accumulate(f2, ctx, po):
+    lib = f2._lib.load()
+    n, k, m = 512, 384, 512
+    a, b, c = po.random_dense(n, k, 0.5, 1), po.random_dense(k, m, 0.5, 2), po.random_dense(n, m, 0.5, 3)
+    want = po.m4rm_mult(a, n, k, b, m) ^ c
+    assert same(_tc(f2, ctx, lib, a, b, n, k, m, 1, c0=c), want, n)
+
+
+def test_gemm_tc_multiwave_matches_m4rm(f2, ctx):
+    """4096^3: 256 CTAs over 148 SMs, 64 k-blocks (the raw/expanded rings wrap many
+    times) -- the configuration that exposed a release-before-consume race."""
+    lib = f2._lib.load()
+    n = 4096
+    A, B, Ct, Cm = (f2.DeviceMatrix(n, n, ctx) for _ in range(4))
+    A.random_dense(0.5, 11)
+    B.random_dense(0.5, 12)
+    f2._lib.check(lib.f2gpu_m4rm_mult(ctx.handle, A.handle, B.handle, Cm.handle, 0))
+    want = Cm.download().words
+    for _ in range(3):
+        f2._lib.check(lib.f2gpu_gemm_tc(ctx.handle, A.handle, B.handle, Ct.handle, 0))
+        assert np.array_equal(Ct.download().words[:, :n], want[:, :n])
+
+
+def test_gemm_tc_rejects_shapes(f2, ctx):
+    lib = f2._lib.load()
+    A, B, C = f2.DeviceMatrix(200, 64, ctx), f2.DeviceMatrix(64, 128, ctx), f2.DeviceMatrix(200, 128, ctx)
+    with pytest.raises(ValueError):
+        f2._lib.check(lib.f2gpu_gemm_tc(ctx.handle, A.handle, B.handle, C.handle, 0))
+
+
 @pytest.mark.parametrize("k", [1, 7, 13, 56, 57, 64])
 def test_mult_acc(f2, ctx, po, k):
     """C[r0.., w0..w0+nw) ^= a * B[b0..b0+k, bw0..] (m4rm.hpp:93-172 semantics)."""
