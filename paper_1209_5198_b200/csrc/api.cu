@@ -1037,8 +1037,25 @@ int f2gpu_gemm_tc(f2gpu_ctx* c, const f2gpu_mat* a, const f2gpu_mat* b, f2gpu_ma
     if (!c || !a || !b || !cm) return set_err(F2GPU_EINVAL, "null argument");
     if (a->cols != b->rows || cm->rows != a->rows || cm->cols != b->cols)
         return set_err(F2GPU_EINVAL, "gemm_tc: shape mismatch");
+    static const int kind = [] {
+        const char* e = getenv("F2GPU_TC_KIND");  // evaluation switch: "i8" selects the int8 leaf
+        return (e && e[0] == 'i') ? 8 : 4;
+    }();
+    if (kind == 4 && f2::gemm_tc3_ok(a->rows, a->cols, b->cols)) {
+        const size_t sbt = (b->cols + 127) / 128 * 128;
+        DevBuf bt(c);
+        if (int e = bt.alloc(sbt * ceil64(b->rows) * 8)) return e;
+        if (int e = check_launch(c, f2::launch_transpose(b->d, b->rows, b->cols, b->stride, bt.as<uint64_t>(),
+                                                         sbt, c->stream),
+                                 "k_transpose"))
+            return e;
+        return check_launch(c, f2::launch_gemm_tc3(a->d, a->stride, a->rows, bt.as<uint64_t>(), sbt, cm->d,
+                                                   cm->stride, a->cols, b->cols, acc != 0, c->stream),
+                            "k_gemm_tc3");
+    }
     if (!f2::gemm_tc_ok(a->rows, a->cols, b->cols))
-        return set_err(F2GPU_EINVAL, "gemm_tc: needs n % 256 == 0, m % 128 == 0, k % 64 == 0");
+        return set_err(F2GPU_EINVAL, kind == 4 ? "gemm_tc: needs m % 256 == 0"
+                                               : "gemm_tc: needs n % 256 == 0, m % 128 == 0, k % 64 == 0");
     if (f2::gemm_tc2_ok(a->rows, a->cols, b->cols)) {
         // B^T once (m x k), then the 256x256-tile kernel reads both operands as k-rows
         const size_t sbt = (b->cols + 127) / 128 * 128;

@@ -109,6 +109,10 @@ cudaError_t launch_gemm_tc(const uint64_t* A, size_t sa, const uint64_t* B, size
 bool gemm_tc2_ok(size_t n, size_t k, size_t m);
 cudaError_t launch_gemm_tc2(const uint64_t* A, size_t sa, const uint64_t* BT, size_t sbt, uint64_t* C,
                             size_t sc, size_t n, size_t k, size_t m, bool acc, cudaStream_t s);
+// block-scaled FP4 variant: n, k arbitrary (B^T bits past k zero), m % 256 == 0
+bool gemm_tc3_ok(size_t n, size_t k, size_t m);
+cudaError_t launch_gemm_tc3(const uint64_t* A, size_t sa, size_t n, const uint64_t* BT, size_t sbt,
+                            uint64_t* C, size_t sc, size_t k, size_t m, bool acc, cudaStream_t s);
 
 // per-device one-time setup (dynamic shared memory opt-in)
 cudaError_t init_kernel_attrs();

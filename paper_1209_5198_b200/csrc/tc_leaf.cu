@@ -490,6 +490,248 @@ __global__ void __launch_bounds__(kT2Threads, 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
 }
 
+// ---- v3: block-scaled FP4 (kind::mxf4) on the same warp-specialised pipeline ----
+// A bit becomes the E2M1 nibble 0x2 (= 1.0) or 0x0, two elements per byte, so a
+// 64-bit k-block is one 32-byte K=64 row slice: half the expansion stores and
+// half the operand reads of the int8 leaf, at twice the int8 MMA rate.  The
+// E8M0 scale factors are all 1.0: 32 TMEM columns are filled with 0x7F bytes,
+// so the result does not depend on the scale-factor layout.  Accumulators are
+// f32 (exact: every sum is an integer <= k < 2^23); parity = LSB of v + 2^23.
+// TMEM: two M=128 x N=240 accumulators (480 columns) + the 32 scale columns.
+// Output rows are tiled by 240 (ragged last tile); B is pre-transposed.
+constexpr int kT3Exp = 512;                 // expansion threads (warps 0-15)
+constexpr int kT3Mma = kT3Exp / 32;         // warp 16
+constexpr int kT3Load = kT3Mma + 1;         // warp 17
+constexpr int kT3Threads = kT3Exp + 64;
+constexpr int kT3Cols = 256;                // output columns per CTA (2 x M=128)
+constexpr int kT3Rows = 240;                // output rows per CTA (N)
+constexpr int kT3ABytes = kT3Cols * 64;     // B^T slot: 2 k-blocks x 32 B per row
+constexpr int kT3BBytes = kT3Rows * 64;     // A^T slot
+constexpr int kT3Slot = kT3ABytes + kT3BBytes;  // 2 k-blocks
+constexpr int kT3Slots = 2;                 // slots per stage -> 4 k-blocks per stage
+constexpr int kT3Kps = 2 * kT3Slots;
+constexpr int kT3Stage = kT3Slots * kT3Slot;
+constexpr int kT3Stages = 3;
+constexpr int kT3RawWords = kT3Cols + kT3Rows;
+constexpr int kT3RawBytes = kT3RawWords * 8;
+constexpr int kT3Raw = 4;
+constexpr uint32_t kT3SfCol = 480;
+constexpr size_t kT3Smem = size_t(kT3Stages) * kT3Stage + size_t(kT3Raw) * kT3RawBytes + 256;
+// kind::mxf4: a/b E2M1 (1), K-major, N=240, scale E8M0, M=128, sf ids 0, K=64
+constexpr uint32_t kIdescF4 = (1u << 7) | (1u << 10) | (uint32_t(kT3Rows >> 3) << 17) | (1u << 23) |
+                              (uint32_t(128 >> 4) << 24);
+
+__device__ __forceinline__ void mma_f4(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc,
+                                       uint32_t tsf) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%5], [%5], p;\n\t}\n" ::"r"(
+            tmem_d),
+        "l"(da), "l"(db), "r"(kIdescF4), "r"(acc), "r"(tsf));
+}
+
+// 64 bits -> 64 E2M1 nibbles (0x2 / 0x0), row r, k-block j of a 2-k-block slot
+__device__ __forceinline__ void store_row_f4(unsigned char* tile, int r, int j, uint64_t w) {
+    constexpr uint32_t M = 0x22222222u;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const uint32_t x = uint32_t(w >> (32 * h));
+        uint4 v;  // nibble q of word t <- bit 4q + t (moved to the nibble's bit 1)
+        v.x = (x << 1) & M;
+        v.y = x & M;
+        v.z = (x >> 1) & M;
+        v.w = (x >> 2) & M;
+        *reinterpret_cast<uint4*>(tile + kmaj_off(r, 2 * j + h)) = v;
+    }
+}
+
+__device__ __forceinline__ void ld_shared_u64(uint64_t& v, const void* p) { v = *reinterpret_cast<const uint64_t*>(p); }
+
+template <int MODE>
+__global__ void __launch_bounds__(kT3Threads, 1)
+    k_gemm_tc3(const uint64_t* __restrict__ A, size_t sa, size_t n, const uint64_t* __restrict__ BT,
+               size_t sbt, uint64_t* __restrict__ C, size_t sc, size_t k, int acc) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    unsigned char* raw = smem + size_t(kT3Stages) * kT3Stage;
+    uint64_t* full = reinterpret_cast<uint64_t*>(raw + size_t(kT3Raw) * kT3RawBytes);
+    uint64_t* empty = full + kT3Stages;
+    uint64_t* rfull = empty + kT3Stages;
+    uint64_t* rempty = rfull + kT3Raw;
+    uint64_t* done = rempty + kT3Raw;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const size_t c0 = size_t(blockIdx.x) * kT3Cols;
+    const size_t i0 = size_t(blockIdx.y) * kT3Rows;
+    const int nvalid = int(min(size_t(kT3Rows), n - i0));
+    const size_t KB = (k + 63) / 64;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         sm_u32(tmem_slot)),
+                     "r"(512u));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int s = 0; s < kT3Stages; ++s) {
+            mbar_init_n(&full[s], kT3Exp / 32);
+            mbar_init_n(&empty[s], 1);
+        }
+        for (int s = 0; s < kT3Raw; ++s) {
+            mbar_init_n(&rfull[s], 1);
+            mbar_init_n(&rempty[s], kT3Exp / 32);
+        }
+        mbar_init_n(done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+    if (warp < 4) {  // scale factors: every byte of columns 480..511 = E8M0 1.0
+        const uint32_t one = 0x7F7F7F7Fu;
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, "
+            "%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(
+                tmem + (uint32_t(32 * warp) << 16) + kT3SfCol),
+            "r"(one)
+            : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+
+    if (warp == kT3Load) {
+        if (lane == 0) {
+            // rows past n: the bulk copy moves an even number of rows (16-byte
+            // granule); an odd last row is stored by this thread before the arrive
+            const int nb = nvalid & ~1;
+            int s = 0;
+            uint32_t ph = 0;
+            for (size_t kb = 0; kb < KB; ++kb) {
+                if (kb >= size_t(kT3Raw)) mbar_wait1(&rempty[s], ph ^ 1);
+                unsigned char* r = raw + size_t(s) * kT3RawBytes;
+                if (nvalid & 1)
+                    reinterpret_cast<uint64_t*>(r)[kT3Cols + nb] = A[kb * sa + i0 + nb];
+                mbar_expect(&rfull[s], uint32_t(kT3Cols + nb) * 8);
+                bulk_g2s(r, BT + kb * sbt + c0, kT3Cols * 8, &rfull[s]);
+                if (nb) bulk_g2s(r + kT3Cols * 8, A + kb * sa + i0, uint32_t(nb) * 8, &rfull[s]);
+                if (++s == kT3Raw) { s = 0; ph ^= 1; }
+            }
+        }
+        __syncwarp();
+    } else if (warp == kT3Mma) {
+        if (lane == 0) {
+            const uint32_t tsf = tmem + kT3SfCol;
+            int s = 0;
+            uint32_t ph = 0;
+            for (size_t kb = 0; kb < KB; kb += kT3Kps) {
+                mbar_wait1(&full[s], ph);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+                for (int j = 0; j < kT3Kps; ++j) {
+                    if (kb + j >= KB) break;
+                    const uint32_t ta = sm_u32(smem + size_t(s) * kT3Stage + (j >> 1) * kT3Slot) + (j & 1) * 32;
+                    const uint32_t tb = ta + kT3ABytes;
+                    const uint32_t a0 = kb + j > 0 ? 1u : 0u;
+                    if (MODE != 2) {
+                        mma_f4(tmem, umma_desc(ta), umma_desc(tb), a0, tsf);
+                        mma_f4(tmem + kT3Rows, umma_desc(ta + 128 * 64), umma_desc(tb), a0, tsf);
+                    }
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 sm_u32(&empty[s]))
+                             : "memory");
+                if (++s == kT3Stages) { s = 0; ph ^= 1; }
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             sm_u32(done))
+                         : "memory");
+        }
+        __syncwarp();
+    } else {
+        // thread t < 256: B^T row t; 256 <= t < 496: A^T row t - 256 (zero past n)
+        const bool active = tid < kT3RawWords;
+        const int region = tid < kT3Cols ? 0 : kT3ABytes;
+        const int r = tid < kT3Cols ? tid : tid - kT3Cols;
+        const bool live = active && (tid < kT3Cols || r < nvalid);
+        int s = 0, rs = 0;
+        uint32_t ph = 0, rph = 0;
+        for (size_t kb = 0, st = 0; kb < KB; kb += kT3Kps, ++st) {
+            if (st >= size_t(kT3Stages)) mbar_wait1(&empty[s], ph ^ 1);
+#pragma unroll
+            for (int j = 0; j < kT3Kps; ++j) {
+                if (kb + j >= KB) break;
+                mbar_wait1(&rfull[rs], rph);
+                uint64_t x = 0;
+                if (live) ld_shared_u64(x, raw + size_t(rs) * kT3RawBytes + size_t(tid) * 8);
+                if (active) {
+                    unsigned char* tile = smem + size_t(s) * kT3Stage + (j >> 1) * kT3Slot + region;
+                    if (MODE == 1) {
+                        if (x == 0x123456789ull) tile[r] = 1;
+                    } else {
+                        store_row_f4(tile, r, j & 1, x);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive1(&rempty[rs]);
+                if (++rs == kT3Raw) { rs = 0; rph ^= 1; }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive1(&full[s]);
+            if (++s == kT3Stages) { s = 0; ph ^= 1; }
+        }
+        // epilogue: lane quarter lq = w & 3; 16-column chunks c = (w >> 2) + 4i of the
+        // 2 x 15 chunks; a ballot per row packs the 32 output columns of the quarter
+        mbar_wait1(done, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const int lq = warp & 3;
+#pragma unroll 1
+        for (int ch = warp >> 2; ch < 2 * (kT3Rows / 16); ch += 4) {
+            const int accn = ch / (kT3Rows / 16), cc = ch % (kT3Rows / 16);
+            uint32_t v[16];
+            const uint32_t taddr = tmem + (uint32_t(32 * lq) << 16) + uint32_t(kT3Rows * accn + 16 * cc);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+                "%11, %12, %13, %14, %15}, [%16];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                  "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+                  "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (MODE == 3) {  // debug: raw accumulators of the first tile, [column][row] f32
+                if (blockIdx.x == 0 && blockIdx.y == 0) {
+                    uint32_t* dump = reinterpret_cast<uint32_t*>(C);
+                    const int colx = accn * 128 + lq * 32 + lane;
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) dump[colx * kT3Rows + 16 * cc + q] = v[q];
+                }
+                continue;
+            }
+            uint32_t mine = 0;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const uint32_t par = __float_as_uint(__uint_as_float(v[q]) + 8388608.0f) & 1u;
+                const uint32_t bits = __ballot_sync(0xffffffffu, par);
+                if (lane == q) mine = bits;
+            }
+            const int row = 16 * cc + lane;
+            const size_t col = c0 + size_t(accn) * 128 + size_t(lq) * 32;
+            if (lane < 16 && row < nvalid) {
+                uint32_t* dst = reinterpret_cast<uint32_t*>(C + (col / 64) * sc + i0 + row) + ((col / 32) & 1);
+                if (acc) mine ^= *dst;
+                *dst = mine;
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
+}
+
 bool gemm_tc_ok(size_t n, size_t k, size_t m) {
     return n > 0 && k > 0 && m > 0 && n % kTcN == 0 && m % kTcM == 0 && k % 64 == 0;
 }
@@ -519,6 +761,33 @@ cudaError_t launch_gemm_tc2(const uint64_t* A, size_t sa, const uint64_t* BT, si
     auto fn = mode == 1 ? k_gemm_tc2<1> : mode == 2 ? k_gemm_tc2<2> : mode == 3 ? k_gemm_tc2<3>
             : mode == 4 ? k_gemm_tc2<4> : k_gemm_tc2<0>;
     fn<<<grid, kT2Threads, kT2Smem, s>>>(A, sa, BT, sbt, C, sc, k, acc ? 1 : 0);
+    return cudaGetLastError();
+}
+
+bool gemm_tc3_ok(size_t n, size_t k, size_t m) { return n > 0 && k > 0 && m > 0 && m % kT3Cols == 0; }
+
+// fp4 leaf: C (n x m) (^)= A (n x k) * B (k x m) given BT = B^T (m x k, stride sbt,
+// bits past k zero); n and k arbitrary, m % 256 == 0
+cudaError_t launch_gemm_tc3(const uint64_t* A, size_t sa, size_t n, const uint64_t* BT, size_t sbt,
+                            uint64_t* C, size_t sc, size_t k, size_t m, bool acc, cudaStream_t s) {
+    static bool attr = false;
+    static int mode = 0;
+    if (!attr) {
+        for (auto fn : {k_gemm_tc3<0>, k_gemm_tc3<1>, k_gemm_tc3<2>, k_gemm_tc3<3>}) {
+            cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 int(kT3Smem));
+            if (e != cudaSuccess) return e;
+        }
+        const char* env = getenv("F2GPU_TC_MODE");
+        mode = env ? atoi(env) : 0;
+        attr = true;
+    }
+    if (!gemm_tc3_ok(n, k, m) || (sbt % 2) || (sa % 2) ||
+        (reinterpret_cast<uintptr_t>(A) % 16) || (reinterpret_cast<uintptr_t>(BT) % 16))
+        return cudaErrorInvalidValue;
+    dim3 grid(unsigned(m / kT3Cols), unsigned((n + kT3Rows - 1) / kT3Rows));
+    auto fn = mode == 1 ? k_gemm_tc3<1> : mode == 2 ? k_gemm_tc3<2> : mode == 3 ? k_gemm_tc3<3> : k_gemm_tc3<0>;
+    fn<<<grid, kT3Threads, kT3Smem, s>>>(A, sa, n, BT, sbt, C, sc, k, acc ? 1 : 0);
     return cudaGetLastError();
 }
 

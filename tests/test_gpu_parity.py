@@ -108,7 +108,10 @@ def test_strassen_cfg2(f2, ctx, po):
 # tensor-core leaf (evaluated alternative, tc_leaf.cu): 256x256 tiles on a
 # pre-transposed B when m % 256 == 0, else the 128-column v1 kernel
 TC_SHAPES = [(256, 64, 128), (256, 128, 256), (512, 64, 256), (256, 640, 384), (512, 192, 512),
-             (1024, 1024, 1024), (2048, 4096, 1536), (768, 4160, 512)]
+             (1024, 1024, 1024), (2048, 4096, 1536), (768, 4160, 512),
+             # block-scaled fp4 leaf: ragged n (240-row tiles) and ragged k
+             (240, 64, 256), (1, 1, 256), (7, 100, 512), (1000, 777, 768), (4097, 130, 256),
+             (3000, 5000, 1024)]
 
 
 def _tc(f2, ctx, lib, a, b, n, k, m, acc, c0=None):
@@ -152,7 +155,7 @@ def test_gemm_tc_multiwave_matches_m4rm(f2, ctx):
 
 def test_gemm_tc_rejects_shapes(f2, ctx):
     lib = f2._lib.load()
-    A, B, C = f2.DeviceMatrix(200, 64, ctx), f2.DeviceMatrix(64, 128, ctx), f2.DeviceMatrix(200, 128, ctx)
+    A, B, C = f2.DeviceMatrix(200, 60, ctx), f2.DeviceMatrix(60, 128, ctx), f2.DeviceMatrix(200, 128, ctx)
     with pytest.raises(ValueError):
         f2._lib.check(lib.f2gpu_gemm_tc(ctx.handle, A.handle, B.handle, C.handle, 0))
 

@@ -19,8 +19,14 @@ stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 ctx.set_stream(stream.cuda_stream)
 ok = True
-for (n, k, m) in [(256, 64, 128), (256, 128, 128), (512, 64, 256), (256, 640, 384), (256, 64, 256), (512, 192, 512), (1024, 1024, 1024),
-                  (2048, 4096, 1536)]:
+import os  # noqa: E402
+
+SH = [(256, 64, 128), (256, 128, 128), (512, 64, 256), (256, 640, 384), (256, 64, 256), (512, 192, 512), (1024, 1024, 1024),
+      (2048, 4096, 1536)]
+if os.environ.get("F2GPU_TC_KIND", "f4")[0] != "i":  # fp4 leaf: ragged n and k, m % 256 == 0
+    SH = [(240, 64, 256), (1, 1, 256), (7, 100, 512), (480, 320, 256), (1000, 777, 768), (2048, 4096, 1536),
+          (4097, 130, 256), (3000, 5000, 1024)]
+for (n, k, m) in SH:
     a = po.random_dense(n, k, 0.5, n + k)
     b = po.random_dense(k, m, 0.5, k + m)
     want = po.m4rm_mult(a, n, k, b, m)
@@ -35,8 +41,6 @@ for (n, k, m) in [(256, 64, 128), (256, 128, 128), (512, 64, 256), (256, 640, 38
     if not eq:
         d = got.words[:, :n] ^ want[:, :n]
         print("  mismatching words:", int(np.count_nonzero(d)), "of", d.size)
-import os  # noqa: E402
-
 if not ok and not os.environ.get("F2GPU_TC_MODE"):
     sys.exit(1)
 n = 16384
