@@ -1445,35 +1445,31 @@ cudaError_t launch_panel(uint64_t* col, size_t n, PanelState* st_all, int j, cud
 __device__ __forceinline__ void panel_y_body(uint64_t* __restrict__ col, size_t n,
                                              const PanelState* __restrict__ st, uint64_t* zt,
                                              unsigned blk, unsigned nblk) {
-    const size_t R = st->R, r = st->r;
-    const size_t lo = R + r;
+    // every load this block needs up front: the state header, Z, and the block's
+    // first row word (one round trip instead of a chain)
+    __shared__ uint64_t zs[64];
+    const uint32_t R = st->R, r = st->r;
+    if (threadIdx.x < 64) zs[threadIdx.x] = st->Z[threadIdx.x];
+    const size_t lo = size_t(R) + r;
+    const size_t i0 = lo + size_t(blk) * blockDim.x + threadIdx.x;
+    const uint64_t d0 = (r != 0 && i0 < n) ? col[i0] : 0;
+    __syncthreads();
     if (r == 0 || lo >= n) return;
-    // single-column tables over the 64 Z words
-    for (int it = threadIdx.x; it < 40; it += blockDim.x) {
-        const int t = it < 32 ? (it >> 2) : 8;
-        const int chunk = it < 32 ? (it & 3) : it - 32;
-        const int sz = t < 8 ? 7 : 8;
-        uint64_t rows[8];
+    // single-column tables over the 64 Z words, all entries in parallel:
+    // groups 0-7 cover bits 7t..7t+6 (128 entries), group 8 bits 56..63 (256)
+    for (int e = threadIdx.x; e < kTabEntries; e += blockDim.x) {
+        const int t = e < 1024 ? e >> 7 : 8;
+        const int idx = e < 1024 ? e & 127 : e - 1024;
+        uint64_t v = 0;
 #pragma unroll
-        for (int b = 0; b < 8; ++b) rows[b] = b < sz ? st->Z[7 * t + b] : 0ull;
-        uint64_t cur = 0;
-#pragma unroll
-        for (int hb = 0; hb < 3; ++hb)
-            if ((chunk >> hb) & 1) cur ^= rows[5 + hb];
-        uint64_t* dst = zt + 128 * t + chunk * 32;
-        uint64_t v[32];
-        v[0] = cur;
-#pragma unroll
-        for (int b = 0; b < 5; ++b)
-#pragma unroll
-            for (int g = 1 << b; g < (2 << b); ++g) v[g] = v[g - (1 << b)] ^ rows[b];
-#pragma unroll
-        for (int g = 0; g < 32; ++g) dst[g] = v[g];
+        for (int b = 0; b < 8; ++b)
+            if ((idx >> b) & 1) v ^= zs[7 * t + b];
+        zt[e] = v;
     }
     __syncthreads();
-    for (size_t i = lo + size_t(blk) * blockDim.x + threadIdx.x; i < n;
-         i += size_t(nblk) * blockDim.x) {
-        const uint64_t d = col[i];
+    uint64_t d = d0;
+    for (size_t i = i0; i < n; i += size_t(nblk) * blockDim.x) {
+        if (i != i0) d = col[i];
         uint64_t y = 0;
 #pragma unroll
         for (int t = 0; t < 8; ++t) y ^= zt[128 * t + int((d >> (7 * t)) & 127)];
@@ -1503,30 +1499,38 @@ __device__ __forceinline__ void swaps_body(uint64_t* __restrict__ w, size_t stri
                                            const PanelState* __restrict__ st, int gw) {
     const int lane = threadIdx.x & 31;
     if (gw > ncols || gw == skip_col) return;
+    // header and pair lists are loaded together (independent addresses), so the
+    // swap costs two dependent global round trips: state, then the rows
     const uint32_t np = st->npairs;
+    const uint32_t R = st->R;
+    uint32_t sidx[4], didx[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        sidx[e] = st->src[lane + 32 * e];
+        didx[e] = st->dst[lane + 32 * e];
+    }
     if (np == 0) return;
-    const size_t R = st->R;
     if (gw == ncols) {
         if (!perm) return;
         uint32_t v[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e)
-            if (lane + 32 * e < int(np)) v[e] = perm[R + st->src[lane + 32 * e]];
+            if (lane + 32 * e < int(np)) v[e] = perm[R + sidx[e]];
         __syncwarp();
 #pragma unroll
         for (int e = 0; e < 4; ++e)
-            if (lane + 32 * e < int(np)) perm[R + st->dst[lane + 32 * e]] = v[e];
+            if (lane + 32 * e < int(np)) perm[R + didx[e]] = v[e];
         return;
     }
     uint64_t* cp = w + size_t(gw) * stride + R;
     uint64_t v[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e)
-        if (lane + 32 * e < int(np)) v[e] = cp[st->src[lane + 32 * e]];
+        if (lane + 32 * e < int(np)) v[e] = cp[sidx[e]];
     __syncwarp();
 #pragma unroll
     for (int e = 0; e < 4; ++e)
-        if (lane + 32 * e < int(np)) cp[st->dst[lane + 32 * e]] = v[e];
+        if (lane + 32 * e < int(np)) cp[didx[e]] = v[e];
 }
 
 __global__ void __launch_bounds__(256) k_swaps(uint64_t* __restrict__ w, size_t stride,
@@ -1550,21 +1554,23 @@ constexpr int kPostYBlocks = 64;
 __global__ void __launch_bounds__(256) k_post(uint64_t* __restrict__ w, size_t stride, int ncols,
                                               int panel_col, uint32_t* __restrict__ perm,
                                               size_t n, const PanelState* __restrict__ st,
-                                              int swap_blocks) {
+                                              int swap_blocks, int yblocks) {
     __shared__ uint64_t zt[kTabEntries];
     if (int(blockIdx.x) < swap_blocks) {
         swaps_body(w, stride, ncols, panel_col, perm, st,
                    int((size_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5));
         return;
     }
-    panel_y_body(w + size_t(panel_col) * stride, n, st, zt, blockIdx.x - swap_blocks, kPostYBlocks);
+    panel_y_body(w + size_t(panel_col) * stride, n, st, zt, blockIdx.x - swap_blocks, yblocks);
 }
 
 cudaError_t launch_post(uint64_t* w, size_t stride, int ncols, int panel_col, uint32_t* perm,
                         size_t n, const PanelState* st, cudaStream_t s) {
     const int swap_blocks = (ncols + 1 + 7) / 8;
-    k_post<<<swap_blocks + kPostYBlocks, 256, 0, s>>>(w, stride, ncols, panel_col, perm, n, st,
-                                                        swap_blocks);
+    // Y blocks: about one row per thread (latency-bound), at least kPostYBlocks
+    const int yblocks = int(std::min<size_t>(1024, std::max<size_t>(kPostYBlocks, (n + 255) / 256)));
+    k_post<<<swap_blocks + yblocks, 256, 0, s>>>(w, stride, ncols, panel_col, perm, n, st,
+                                                   swap_blocks, yblocks);
     return cudaGetLastError();
 }
 
