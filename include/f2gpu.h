@@ -104,9 +104,19 @@ int f2gpu_mult_acc(f2gpu_ctx *ctx, f2gpu_mat *c, size_t c_row0, size_t c_wcol0,
                    size_t n_wcols, const uint64_t *d_a_words, size_t n_rows, size_t k_bits,
                    const f2gpu_mat *b, size_t b_row0, size_t b_wcol0);
 /* The evaluated alternative leaf (north_star): C = A*B (acc=0) or C ^= A*B on the
- * tensor cores, tcgen05.mma kind::i8 on bit->byte expanded operands, parity of the
- * s32 accumulators.  Requires n % 256 == 0, m % 128 == 0, k % 64 == 0. */
+ * tensor cores.  Default: tcgen05.mma kind::mxf4 (bits as E2M1 1.0/0.0, unit
+ * E8M0 scales, exact f32 sums, parity), any n and k, m % 256 == 0.  With
+ * F2GPU_TC_KIND=i8 (or m % 256 != 0): kind::i8 on 0/1 bytes, n % 256 == 0,
+ * m % 128 == 0, k % 64 == 0. */
 int f2gpu_gemm_tc(f2gpu_ctx *ctx, const f2gpu_mat *a, const f2gpu_mat *b, f2gpu_mat *c, int acc);
+/* Tensor-core trailing update (the blocked decomposition's GEMM step):
+ *   C[row_lo, row_hi) x word-cols [c_wcol0, c_wcol0 + n_wcols)
+ *     ^= A[same rows] x word-cols [a_wcol0, a_wcol0 + kwords)  *  BT^T
+ * with BT an (n_wcols*64) x (kwords*64) matrix holding B transposed, kwords <= 2
+ * (rank <= 128).  Rows of A outside [row_lo, row_hi) do not contribute. */
+int f2gpu_update_tc(f2gpu_ctx *ctx, f2gpu_mat *c, size_t row_lo, size_t row_hi, size_t c_wcol0,
+                    size_t n_wcols, const f2gpu_mat *a, size_t a_wcol0, size_t kwords,
+                    const f2gpu_mat *bt);
 /* Strassen-Winograd over device sub-blocks, M4RM leaves
  * below the cutover. threshold = 0 -> context cutover. C = A*B. */
 int f2gpu_strassen_mult(f2gpu_ctx *ctx, const f2gpu_mat *a, const f2gpu_mat *b, f2gpu_mat *c,

@@ -31,6 +31,7 @@ SYMBOLS = [
     "f2gpu_mat_copy", "f2gpu_mat_select_wcols", "f2gpu_mat_xor", "f2gpu_mat_transpose",
     "f2gpu_m4rm_mult", "f2gpu_m4rm_mult_acc", "f2gpu_mult_acc", "f2gpu_strassen_mult",
     "f2gpu_gemm_tc",
+    "f2gpu_update_tc",
     "f2gpu_decompose_block", "f2gpu_decompose_recursive", "f2gpu_decompose_block_sharded",
     "f2gpu_rank",
     "f2gpu_m4rm_mult_host", "f2gpu_strassen_mult_host", "f2gpu_decompose_block_host",
@@ -70,6 +71,7 @@ _SIG = {
     "f2gpu_mult_acc": ([vp, vp, sz, sz, sz, vp, sz, sz, vp, sz, sz], C.c_int),
     "f2gpu_strassen_mult": ([vp, vp, vp, vp, sz], C.c_int),
     "f2gpu_gemm_tc": ([vp, vp, vp, vp, C.c_int], C.c_int),
+    "f2gpu_update_tc": ([vp, vp, sz, sz, sz, sz, vp, sz, sz, vp], C.c_int),
     "f2gpu_decompose_block": ([vp, vp, vp, vp, C.POINTER(sz)], C.c_int),
     "f2gpu_decompose_block_sharded": ([vp, vp, C.c_int, vp, vp, C.POINTER(sz)], C.c_int),
     "f2gpu_decompose_recursive": ([vp, vp, sz, vp, vp, C.POINTER(sz)], C.c_int),

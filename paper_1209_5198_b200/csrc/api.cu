@@ -1074,6 +1074,32 @@ int f2gpu_gemm_tc(f2gpu_ctx* c, const f2gpu_mat* a, const f2gpu_mat* b, f2gpu_ma
                         "k_gemm_tc");
 }
 
+int f2gpu_update_tc(f2gpu_ctx* c, f2gpu_mat* cm, size_t row_lo, size_t row_hi, size_t c_wcol0,
+                    size_t n_wcols, const f2gpu_mat* a, size_t a_wcol0, size_t kwords, const f2gpu_mat* bt) {
+    if (!c || !cm || !a || !bt) return set_err(F2GPU_EINVAL, "null argument");
+    if (kwords < 1 || kwords > 2) return set_err(F2GPU_EINVAL, "update_tc: kwords must be 1 or 2");
+    if (row_lo > row_hi || row_hi > cm->rows || a->rows != cm->rows)
+        return set_err(F2GPU_ERANGE, "update_tc: row range outside C / A");
+    if (c_wcol0 + n_wcols > ceil64(cm->cols) || a_wcol0 + kwords > ceil64(a->cols))
+        return set_err(F2GPU_ERANGE, "update_tc: word-columns outside C / A");
+    if (bt->rows < n_wcols * 64 || bt->cols < kwords * 64)
+        return set_err(F2GPU_EINVAL, "update_tc: BT must be (n_wcols*64) x (kwords*64)");
+    if (n_wcols == 0 || row_lo == row_hi) return F2GPU_OK;
+    // B^T with the row padding the kernel's 192-row bulk loads read
+    const size_t sbt = (f2::update_tc_bt_rows(int(n_wcols)) + 127) / 128 * 128;
+    DevBuf pad(c);
+    F2_TRY(pad.alloc(sbt * kwords * 8));
+    CUDA_TRY(cudaMemcpy2DAsync(pad.p, sbt * 8, bt->d, bt->stride * 8, n_wcols * 64 * 8, kwords,
+                               cudaMemcpyDeviceToDevice, c->stream));
+    f2::TcUpdateArgs u{};
+    u.C = cm->d; u.sc = cm->stride; u.q0 = c_wcol0; u.ncols = int(n_wcols);
+    u.row_lo = row_lo; u.row_hi = row_hi;
+    u.a = a->d + a_wcol0 * a->stride; u.sa = a->stride; u.kwords = int(kwords);
+    u.bt = pad.as<uint64_t>(); u.sbt = sbt;
+    if (!f2::update_tc_ok(u)) return set_err(F2GPU_EINVAL, "update_tc: operands not aligned");
+    return check_launch(c, f2::launch_update_tc(u, c->num_sms, c->stream), "k_update_tc");
+}
+
 int f2gpu_mult_acc(f2gpu_ctx* c, f2gpu_mat* cm, size_t c_row0, size_t c_wcol0, size_t n_wcols,
                    const uint64_t* d_a, size_t n_rows, size_t k_bits, const f2gpu_mat* b,
                    size_t b_row0, size_t b_wcol0) {

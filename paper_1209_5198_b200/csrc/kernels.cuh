@@ -114,6 +114,25 @@ bool gemm_tc3_ok(size_t n, size_t k, size_t m);
 cudaError_t launch_gemm_tc3(const uint64_t* A, size_t sa, size_t n, const uint64_t* BT, size_t sbt,
                             uint64_t* C, size_t sc, size_t k, size_t m, bool acc, cudaStream_t s);
 
+// tensor-core trailing update (tc_update.cu): C[lo..hi) x [q0, q0+ncols) ^= A * B,
+// A = kwords (<= 2) word-columns at a (stride sa), B^T = ncols*64 rows x kwords
+// words at bt (stride sbt >= update_tc_bt_rows(ncols)); lo = st->R + st->r when
+// st is set.  release: lookahead counter, update_tc_release_count() increments
+// once column tile 0 (the next block's panel columns) is complete in memory.
+struct TcUpdateArgs {
+    uint64_t* C; size_t sc; size_t q0; int ncols;
+    size_t row_lo, row_hi;
+    const uint64_t* a; size_t sa; int kwords;
+    const uint64_t* bt; size_t sbt;
+    const PanelState* st;
+    uint32_t* release;
+};
+bool update_tc_ok(const TcUpdateArgs& a);
+int update_tc_segments(const TcUpdateArgs& a, int grid);
+int update_tc_release_count(const TcUpdateArgs& a, int grid);
+size_t update_tc_bt_rows(int ncols);
+cudaError_t launch_update_tc(const TcUpdateArgs& a, int grid, cudaStream_t s);
+
 // per-device one-time setup (dynamic shared memory opt-in)
 cudaError_t init_kernel_attrs();
 

@@ -20,6 +20,7 @@
 #include <cstdlib>
 
 #include "kernels.cuh"
+#include "tc_common.cuh"
 
 namespace f2 {
 
@@ -33,29 +34,10 @@ constexpr int kTcBBytes = kTcN * 64;  // A^T tile: 256 x 64 bytes
 constexpr int kTcStage = kTcABytes + kTcBBytes;
 constexpr size_t kTcSmem = 2 * size_t(kTcStage) + 64;
 
-__device__ __forceinline__ uint32_t sm_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
 // 8 bits -> 8 bytes of 0/1 (byte j = bit j)
 __device__ __forceinline__ uint64_t expand8(uint32_t x) {
     uint64_t y = (uint64_t(x & 0xFFu) * 0x0101010101010101ull) & 0x8040201008040201ull;
     return ((y + 0x7F7F7F7F7F7F7F7Full) >> 7) & 0x0101010101010101ull;
-}
-
-#ifndef F2_TC_SWIZZLE64
-#define F2_TC_SWIZZLE64 1
-#endif
-// canonical K-major offset of (row r, 16-byte k-chunk c) in a tile.
-// SWIZZLE_64B: 8-row atoms of 64-byte rows (SBO = 512 B), chunk index XOR-ed
-// with address bits [7,9) = (r >> 1) & 3 (Swizzle<2,4,3>).
-// SWIZZLE_NONE: core matrices of 8 rows x 16 B, LBO = 128 B, SBO = 512 B.
-__device__ __forceinline__ uint32_t kmaj_off(int r, int c) {
-#if F2_TC_SWIZZLE64
-    return uint32_t((r >> 3) * 512 + (r & 7) * 64 + ((c ^ ((r >> 1) & 3)) * 16));
-#else
-    return uint32_t((r >> 3) * 512 + c * 128 + (r & 7) * 16);
-#endif
 }
 
 // 4 bits -> 4 bytes of 0/1: the shifted copies x, x<<7, x<<14, x<<21 do not
@@ -77,25 +59,6 @@ __device__ __forceinline__ void store_row(unsigned char* tile, int r, uint64_t w
     }
 }
 
-// smem descriptor; the K=32 second half of a k-block advances the start address
-// by 256 B (no swizzle: 2 k-chunks of LBO) or 32 B (inside the 64-byte swizzled row)
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
-    uint64_t d = 0;
-    d |= uint64_t((saddr >> 4) & 0x3FFF);        // start address
-#if F2_TC_SWIZZLE64
-    d |= uint64_t(1) << 16;                      // LBO (unused for swizzled K-major)
-    d |= uint64_t(512 >> 4) << 32;               // SBO: next 8-row atom
-    d |= uint64_t(1) << 46;                      // version (Blackwell)
-    d |= uint64_t(4) << 61;                      // SWIZZLE_64B
-#else
-    d |= uint64_t(128 >> 4) << 16;               // LBO: next 16-byte k-chunk
-    d |= uint64_t(512 >> 4) << 32;               // SBO: next group of 8 rows
-    d |= uint64_t(1) << 46;                      // version (Blackwell)
-#endif
-    return d;
-}
-constexpr uint32_t kKHalf = F2_TC_SWIZZLE64 ? 32u : 256u;
-
 // kind::i8, A=u8, B=u8, D=s32, both K-major, M=128, N=256
 constexpr uint32_t kIdesc = (2u << 4) | (0u << 7) | (0u << 10) | (uint32_t(kTcN >> 3) << 17) |
                             (uint32_t(kTcM >> 4) << 24);
@@ -107,19 +70,6 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %5, %5, %5}, p;\n\t}\n" ::"r"(tmem_d),
         "l"(da), "l"(db), "r"(kIdesc), "r"(acc), "r"(z));
-}
-
-__device__ __forceinline__ void mbar_init1(uint64_t* b) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm_u32(b)));
-}
-__device__ __forceinline__ void mbar_wait1(uint64_t* b, uint32_t ph) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "L_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra L_%=;\n}" ::"r"(sm_u32(b)),
-        "r"(ph)
-        : "memory");
 }
 
 }  // namespace
@@ -145,8 +95,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
-        mbar_init1(&mbar[0]);
-        mbar_init1(&mbar[1]);
+        mbar_init_n(&mbar[0], 1);
+        mbar_init_n(&mbar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -294,24 +244,6 @@ constexpr int kT2Stages = 3;
 constexpr int kT2RawBytes = (kT2Rows + kT2Cols) * 8;  // packed words of one k-block
 constexpr int kT2Raw = 4;
 constexpr size_t kT2Smem = size_t(kT2Stages) * kT2Stage + size_t(kT2Raw) * kT2RawBytes + 256;
-
-__device__ __forceinline__ void mbar_init_n(uint64_t* b, uint32_t n) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_u32(b)), "r"(n));
-}
-__device__ __forceinline__ void mbar_arrive1(uint64_t* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm_u32(b)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            sm_u32(dst)),
-        "l"(src), "r"(bytes), "r"(sm_u32(bar))
-        : "memory");
-}
 
 // 64 bits -> 64 bytes of 0/1 in the permuted k order, row r of a K-major tile
 __device__ __forceinline__ void store_row_perm(unsigned char* tile, int r, uint64_t w) {
@@ -517,34 +449,7 @@ constexpr int kT3RawBytes = kT3RawWords * 8;
 constexpr int kT3Raw = 4;
 constexpr uint32_t kT3SfCol = 480;
 constexpr size_t kT3Smem = size_t(kT3Stages) * kT3Stage + size_t(kT3Raw) * kT3RawBytes + 256;
-// kind::mxf4: a/b E2M1 (1), K-major, N=240, scale E8M0, M=128, sf ids 0, K=64
-constexpr uint32_t kIdescF4 = (1u << 7) | (1u << 10) | (uint32_t(kT3Rows >> 3) << 17) | (1u << 23) |
-                              (uint32_t(128 >> 4) << 24);
-
-__device__ __forceinline__ void mma_f4(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc,
-                                       uint32_t tsf) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%5], [%5], p;\n\t}\n" ::"r"(
-            tmem_d),
-        "l"(da), "l"(db), "r"(kIdescF4), "r"(acc), "r"(tsf));
-}
-
-// 64 bits -> 64 E2M1 nibbles (0x2 / 0x0), row r, k-block j of a 2-k-block slot
-__device__ __forceinline__ void store_row_f4(unsigned char* tile, int r, int j, uint64_t w) {
-    constexpr uint32_t M = 0x22222222u;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const uint32_t x = uint32_t(w >> (32 * h));
-        uint4 v;  // nibble q of word t <- bit 4q + t (moved to the nibble's bit 1)
-        v.x = (x << 1) & M;
-        v.y = x & M;
-        v.z = (x >> 1) & M;
-        v.w = (x >> 2) & M;
-        *reinterpret_cast<uint4*>(tile + kmaj_off(r, 2 * j + h)) = v;
-    }
-}
+constexpr uint32_t kIdescF4 = idesc_f4(128, kT3Rows);
 
 __device__ __forceinline__ void ld_shared_u64(uint64_t& v, const void* p) { v = *reinterpret_cast<const uint64_t*>(p); }
 
@@ -636,8 +541,8 @@ __global__ void __launch_bounds__(kT3Threads, 1)
                     const uint32_t tb = ta + kT3ABytes;
                     const uint32_t a0 = kb + j > 0 ? 1u : 0u;
                     if (MODE != 2) {
-                        mma_f4(tmem, umma_desc(ta), umma_desc(tb), a0, tsf);
-                        mma_f4(tmem + kT3Rows, umma_desc(ta + 128 * 64), umma_desc(tb), a0, tsf);
+                        mma_f4(tmem, umma_desc(ta), umma_desc(tb), kIdescF4, a0, tsf);
+                        mma_f4(tmem + kT3Rows, umma_desc(ta + 128 * 64), umma_desc(tb), kIdescF4, a0, tsf);
                     }
                 }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(

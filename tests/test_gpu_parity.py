@@ -160,6 +160,33 @@ def test_gemm_tc_rejects_shapes(f2, ctx):
         f2._lib.check(lib.f2gpu_gemm_tc(ctx.handle, A.handle, B.handle, C.handle, 0))
 
 
+# tensor-core trailing update (tc_update.cu): C[lo, hi) x [q0, q0+nwc) ^= A * BT^T
+UPD_TC_CASES = [  # n, m, lo, hi, q0, nwc, kwords
+    (300, 640, 5, 290, 1, 7, 2), (1000, 192, 0, 1000, 0, 3, 1), (4096, 1280, 1000, 4096, 3, 17, 2),
+    (129, 256, 128, 129, 0, 4, 2), (20000, 3200, 777, 19999, 2, 47, 2), (640, 128, 0, 640, 0, 1, 2),
+    (5000, 4096, 4999, 5000, 10, 54, 1)]
+
+
+@pytest.mark.parametrize("n,m,lo,hi,q0,nwc,kw", UPD_TC_CASES)
+def test_update_tc(f2, ctx, po, n, m, lo, hi, q0, nwc, kw):
+    lib = f2._lib.load()
+    seed = n + m + lo
+    c = po.random_dense(n, m, 0.5, seed)
+    a = po.random_dense(n, kw * 64, 0.5, seed + 1)
+    bt = po.random_dense(nwc * 64, kw * 64, 0.5, seed + 2)
+    am = a.copy()
+    am[:, :lo] = 0
+    am[:, hi:] = 0
+    prod = po.m4rm_mult(am, n, kw * 64, po.transpose(bt, nwc * 64, kw * 64), nwc * 64)
+    want = c.copy()
+    want[q0:q0 + nwc, :n] ^= prod[:, :n]
+    C = f2.DeviceMatrix.from_host(f2.BitMatrix(n, m, c), ctx)
+    A = f2.DeviceMatrix.from_host(f2.BitMatrix(n, kw * 64, a), ctx)
+    BT = f2.DeviceMatrix.from_host(f2.BitMatrix(nwc * 64, kw * 64, bt), ctx)
+    f2._lib.check(lib.f2gpu_update_tc(ctx.handle, C.handle, lo, hi, q0, nwc, A.handle, 0, kw, BT.handle))
+    assert same(C.download().words, want, n)
+
+
 @pytest.mark.parametrize("k", [1, 7, 13, 56, 57, 64])
 def test_mult_acc(f2, ctx, po, k):
     """C[r0.., w0..w0+nw) ^= a * B[b0..b0+k, bw0..] (m4rm.hpp:93-172 semantics)."""
