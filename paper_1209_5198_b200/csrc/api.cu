@@ -179,6 +179,9 @@ struct f2gpu_ctx {
     uint64_t* d_jump = nullptr;
     uint64_t launches = 0;
     size_t strassen_cutover = 4096;  // measured: 16384^3 -> 3 levels, 2.77 ms vs 3.15 ms plain M4RM
+    // fp4 tensor-core leaf (F2GPU_TC=0 disables): products with n, k, m >= 256
+    bool use_tc = true;
+    size_t tc_cutover = 16384;  // minimum TC Strassen leaf size (F2GPU_TC_CUT)
     void* comm = nullptr;
     int rank = 0, world = 1;
 };
@@ -397,6 +400,142 @@ int strassen_acc(f2gpu_ctx* c, View C, View A, View B, size_t cutover) {
     return F2GPU_OK;
 }
 
+// ---- tensor-core products (fp4 leaf, tc_leaf.cu) ---------------------------
+// Strassen-Winograd over (A, B^T): B is transposed once up front, so every leaf
+// product gets its B^T operand as a plain view.  The B-side sums are formed on
+// the transposed quadrants (B_ij^T is quadrant (j, i) of B^T); P temps are
+// written by the leaves (acc = 0), the top level accumulates.
+int strassen_tc(f2gpu_ctx* c, View C, View A, View BT, int L) {
+    const size_t n0 = A.rows, k0 = A.cols, m0 = BT.rows;
+    if (L == 0) {
+        f2::TcGemmArgs g{A.p, A.stride, n0, BT.p, BT.stride, C.p, C.stride, k0, m0, 1};
+        return check_launch(c, f2::launch_gemm_tc3(g.A, g.sa, g.n, g.BT, g.sbt, g.C, g.sc, g.k, g.m, true,
+                                                   c->stream),
+                            "k_gemm_tc3");
+    }
+    size_t bytes = 0;
+    {
+        size_t n = n0, k = k0, m = m0, nodes = 1;
+        for (int l = 0; l < L; ++l) {
+            n /= 2; k /= 2; m /= 2;
+            bytes += nodes * (4 * dev_stride(n) * (k / 64) + 4 * dev_stride(m) * (k / 64) +
+                              7 * dev_stride(n) * (m / 64)) * 8;
+            nodes *= 7;
+        }
+    }
+    DevBuf arena(c);
+    F2_TRY(arena.alloc(bytes));
+    unsigned char* cur = arena.as<unsigned char>();
+    auto take = [&](size_t rows, size_t cols) {
+        const size_t s = dev_stride(rows);
+        View v{reinterpret_cast<uint64_t*>(cur), rows, cols, s, s};
+        cur += s * (cols / 64) * 8;
+        return v;
+    };
+    struct Node { View C, A, BT; };
+    std::vector<Node> level{{C, A, BT}};
+    std::vector<std::vector<f2::XorJob>> post(L);
+    for (int l = 0; l < L; ++l) {
+        std::vector<f2::XorJob> pre;
+        std::vector<Node> next;
+        for (const Node& nd : level) {
+            const size_t n2 = nd.A.rows / 2, k2 = nd.A.cols / 2, m2 = nd.BT.rows / 2;
+            const size_t kw = k2 / 64, mw = m2 / 64;
+            View A11 = nd.A.sub(0, n2, 0, kw), A12 = nd.A.sub(0, n2, kw, kw);
+            View A21 = nd.A.sub(n2, n2, 0, kw), A22 = nd.A.sub(n2, n2, kw, kw);
+            // B_ij^T: rows = the j-th half of m, word-columns = the i-th half of k
+            View B11 = nd.BT.sub(0, m2, 0, kw), B12 = nd.BT.sub(m2, m2, 0, kw);
+            View B21 = nd.BT.sub(0, m2, kw, kw), B22 = nd.BT.sub(m2, m2, kw, kw);
+            View C11 = nd.C.sub(0, n2, 0, mw), C12 = nd.C.sub(0, n2, mw, mw);
+            View C21 = nd.C.sub(n2, n2, 0, mw), C22 = nd.C.sub(n2, n2, mw, mw);
+            View S1 = take(n2, k2), S2 = take(n2, k2), S3 = take(n2, k2), S4 = take(n2, k2);
+            View T1 = take(m2, k2), T2 = take(m2, k2), T3 = take(m2, k2), T4 = take(m2, k2);
+            View P[7];
+            for (auto& v : P) v = take(n2, m2);
+            pre.push_back(xjob(S1, false, {A21, A22}));
+            pre.push_back(xjob(S2, false, {A11, A21, A22}));
+            pre.push_back(xjob(S3, false, {A11, A21}));
+            pre.push_back(xjob(S4, false, {A11, A12, A21, A22}));
+            pre.push_back(xjob(T1, false, {B11, B12}));
+            pre.push_back(xjob(T2, false, {B11, B12, B22}));
+            pre.push_back(xjob(T3, false, {B12, B22}));
+            pre.push_back(xjob(T4, false, {B11, B12, B21, B22}));
+            next.push_back({P[0], A11, B11});
+            next.push_back({P[1], A12, B21});
+            next.push_back({P[2], S4, B22});
+            next.push_back({P[3], A22, T4});
+            next.push_back({P[4], S1, T1});
+            next.push_back({P[5], S2, T2});
+            next.push_back({P[6], S3, T3});
+            // level 0 accumulates into C; deeper levels fill fresh P temps of the
+            // level above, each quadrant by exactly one job
+            const bool acc = l == 0;
+            post[l].push_back(xjob(C11, acc, {P[0], P[1]}));
+            post[l].push_back(xjob(C12, acc, {P[0], P[5], P[4], P[2]}));
+            post[l].push_back(xjob(C21, acc, {P[0], P[5], P[6], P[3]}));
+            post[l].push_back(xjob(C22, acc, {P[0], P[5], P[6], P[4]}));
+        }
+        F2_TRY(launch_xor_jobs(c, pre));
+        level.swap(next);
+    }
+    std::vector<f2::TcGemmArgs> probs;
+    for (const Node& nd : level)
+        probs.push_back({nd.A.p, nd.A.stride, nd.A.rows, nd.BT.p, nd.BT.stride, nd.C.p, nd.C.stride, nd.A.cols,
+                         nd.BT.rows, 0});
+    DevBuf dp(c);
+    F2_TRY(dp.alloc(probs.size() * sizeof(f2::TcGemmArgs)));
+    CUDA_TRY(cudaMemcpyAsync(dp.p, probs.data(), probs.size() * sizeof(f2::TcGemmArgs), cudaMemcpyHostToDevice,
+                             c->stream));
+    F2_TRY(check_launch(c, f2::launch_gemm_tc3_batched(probs.data(), dp.as<f2::TcGemmArgs>(), int(probs.size()),
+                                                       c->stream),
+                        "k_gemm_tc3_batched"));
+    for (int l = L - 1; l >= 0; --l) F2_TRY(launch_xor_jobs(c, post[l]));
+    return F2GPU_OK;
+}
+
+// levels of the tensor-core Strassen plan: halve while every leaf dimension stays
+// at or above the cutover (the minimum leaf size) and leaves keep 256-column,
+// 128-row granularity.  Measured (B200, fp4 leaf): 16384^3 direct 1.97 ms vs
+// 2.12 ms with one level; 32768^3 one level (16384 leaves) 13.0 ms vs 15.3 ms
+// direct -> default cutover 16384.
+int strassen_tc_levels(size_t n, size_t k, size_t m, size_t cutover) {
+    int L = 0;
+    while (cutover >= 256 && n / 2 >= cutover && k / 2 >= cutover && m / 2 >= cutover && n % 256 == 0 &&
+           k % 128 == 0 && m % 512 == 0 && L < 4) {
+        n /= 2; k /= 2; m /= 2; ++L;
+    }
+    return L;
+}
+
+bool tc_product_ok(f2gpu_ctx* c, size_t n, size_t k, size_t m) {
+    return c->use_tc && n >= 256 && k >= 256 && m >= 256;
+}
+
+// C ^= A*B with the fp4 tensor-core leaf on the first floor(m/256)*256 columns
+// (Strassen-Winograd over tc_cutover) and M4RM on the rest
+int tc_product(f2gpu_ctx* c, View C, View A, View B, size_t tc_cut) {
+    const size_t n = A.rows, k = A.cols, m = B.cols, m256 = m / 256 * 256;
+    if (m256 < m) {
+        const size_t w0 = m256 / 64, nw = B.wcols() - w0;
+        F2_TRY(strassen_acc(c, C.sub(0, n, w0, nw), A, B.sub(0, k, w0, nw), c->strassen_cutover));
+    }
+    if (m256 == 0) return F2GPU_OK;
+    const size_t sbt = dev_stride(m256);
+    DevBuf bt(c);
+    F2_TRY(bt.alloc(sbt * ceil64(k) * 8));
+    F2_TRY(check_launch(c, f2::launch_transpose(B.p, k, m256, B.stride, bt.as<uint64_t>(), sbt, c->stream),
+                        "k_transpose"));
+    View BT{bt.as<uint64_t>(), m256, k, sbt, sbt};
+    View Cl{C.p, n, m256, C.stride, C.cap};
+    return strassen_tc(c, Cl, A, BT, strassen_tc_levels(n, k, m256, tc_cut));
+}
+
+// the product used by the Strassen API and the recursive decomposition
+int best_product(f2gpu_ctx* c, View C, View A, View B, size_t m4rm_cutover, size_t tc_cutover) {
+    if (tc_product_ok(c, A.rows, A.cols, B.cols)) return tc_product(c, C, A, B, tc_cutover);
+    return strassen_acc(c, C, A, B, m4rm_cutover);
+}
+
 // ---- decomposition drivers -------------------------------------------------
 
 // One logical shard: a local packed matrix of the word-columns it owns.
@@ -610,9 +749,9 @@ int rec_trsm(RecRun& r, size_t a, size_t b, size_t Ra, size_t col0, size_t col1)
     if (b - a <= r.tbase) return rank_updates(r, a, b, col0, col1, Rb);
     const size_t m = a + (b - a) / 2, Rm = Ra + 64 * (m - a);
     F2_TRY(rec_trsm(r, a, m, Ra, col0, col1));
-    F2_TRY(strassen_acc(r.c, wview(*r.s, Rm, Rb - Rm, col0, col1 - col0),
+    F2_TRY(best_product(r.c, wview(*r.s, Rm, Rb - Rm, col0, col1 - col0),
                         wview(*r.s, Rm, Rb - Rm, a, m - a), wview(*r.s, Ra, Rm - Ra, col0, col1 - col0),
-                        r.cut));
+                        r.cut, r.c->tc_cutover));
     return rec_trsm(r, m, b, Rm, col0, col1);
 }
 
@@ -628,9 +767,9 @@ int rec_decompose(RecRun& r, size_t c0, size_t c1) {
     if (full) {
         F2_TRY(rec_trsm(r, c0, cm, R0, cm, c1));
         if (R1 < r.n)
-            F2_TRY(strassen_acc(r.c, wview(*r.s, R1, r.n - R1, cm, c1 - cm),
+            F2_TRY(best_product(r.c, wview(*r.s, R1, r.n - R1, cm, c1 - cm),
                                 wview(*r.s, R1, r.n - R1, c0, cm - c0),
-                                wview(*r.s, R0, R1 - R0, cm, c1 - cm), r.cut));
+                                wview(*r.s, R0, R1 - R0, cm, c1 - cm), r.cut, r.c->tc_cutover));
     } else {
         F2_TRY(rank_updates(r, c0, cm, cm, c1, r.n));
     }
@@ -835,6 +974,8 @@ int f2gpu_ctx_create(int device, f2gpu_ctx** out) {
     if (const char* pf = getenv("F2GPU_PROFILE")) c->tl.on = pf[0] == '1';
     if (const char* gr = getenv("F2GPU_GRAPHS")) c->use_graphs = gr[0] != '0';
     if (const char* la = getenv("F2GPU_LOOKAHEAD")) c->lookahead = la[0] != '0';
+    if (const char* tc = getenv("F2GPU_TC")) c->use_tc = tc[0] != '0';
+    if (const char* tcc = getenv("F2GPU_TC_CUT")) c->tc_cutover = size_t(atoll(tcc));
     CUDA_TRY(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&c->ev_post, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&c->ev_panel, cudaEventDisableTiming));
@@ -1128,8 +1269,10 @@ int f2gpu_strassen_mult(f2gpu_ctx* c, const f2gpu_mat* a, const f2gpu_mat* b, f2
         return set_err(F2GPU_EINVAL, "strassen_mult: output shape mismatch");
     F2_TRY(f2gpu_mat_zero(c, cm));
     c->tl.mark(c->stream, "start");
-    F2_TRY(strassen_acc(c, view_of(cm), view_of(a), view_of(b),
-                        threshold ? threshold : c->strassen_cutover));
+    // the paper's multiply: Strassen-Winograd over the fastest leaf (the fp4
+    // tensor-core leaf when the shape allows, else M4RM); threshold = cutover
+    F2_TRY(best_product(c, view_of(cm), view_of(a), view_of(b), threshold ? threshold : c->strassen_cutover,
+                        threshold ? threshold : c->tc_cutover));
     c->tl.report("strassen");
     return F2GPU_OK;
 }

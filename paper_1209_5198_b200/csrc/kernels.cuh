@@ -110,6 +110,15 @@ bool gemm_tc2_ok(size_t n, size_t k, size_t m);
 cudaError_t launch_gemm_tc2(const uint64_t* A, size_t sa, const uint64_t* BT, size_t sbt, uint64_t* C,
                             size_t sc, size_t n, size_t k, size_t m, bool acc, cudaStream_t s);
 // block-scaled FP4 variant: n, k arbitrary (B^T bits past k zero), m % 256 == 0
+struct TcGemmArgs {
+    const uint64_t* A; size_t sa, n;     // A: n x k, word (i, q) at A[q*sa + i]
+    const uint64_t* BT; size_t sbt;      // B^T: m x k
+    uint64_t* C; size_t sc;              // C: n x m
+    size_t k, m;
+    int acc;                             // C ^= A*B (else C = A*B)
+};
+cudaError_t launch_gemm_tc3_batched(const TcGemmArgs* h_probs, const TcGemmArgs* d_probs, int nprob,
+                                    cudaStream_t s);
 bool gemm_tc3_ok(size_t n, size_t k, size_t m);
 cudaError_t launch_gemm_tc3(const uint64_t* A, size_t sa, size_t n, const uint64_t* BT, size_t sbt,
                             uint64_t* C, size_t sc, size_t k, size_t m, bool acc, cudaStream_t s);

@@ -16,6 +16,7 @@
 // (two K=32 MMAs), operands expanded in registers into a double-buffered
 // canonical K-major no-swizzle layout ((8,n),2):((16B,SBO),LBO) with LBO=128 B,
 // SBO=512 B, MMA completion tracked with tcgen05.commit -> mbarrier.
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -455,8 +456,15 @@ __device__ __forceinline__ void ld_shared_u64(uint64_t& v, const void* p) { v = 
 
 template <int MODE>
 __global__ void __launch_bounds__(kT3Threads, 1)
-    k_gemm_tc3(const uint64_t* __restrict__ A, size_t sa, size_t n, const uint64_t* __restrict__ BT,
-               size_t sbt, uint64_t* __restrict__ C, size_t sc, size_t k, int acc) {
+    k_gemm_tc3(TcGemmArgs one, const TcGemmArgs* __restrict__ probs) {
+    // one problem per launch, or a batch (blockIdx.z = problem; Strassen leaves)
+    const TcGemmArgs P = probs ? probs[blockIdx.z] : one;
+    if (size_t(blockIdx.x) * kT3Cols >= P.m || size_t(blockIdx.y) * kT3Rows >= P.n) return;
+    const uint64_t* __restrict__ A = P.A;
+    const uint64_t* __restrict__ BT = P.BT;
+    uint64_t* __restrict__ C = P.C;
+    const size_t sa = P.sa, n = P.n, sbt = P.sbt, sc = P.sc, k = P.k;
+    const int acc = P.acc;
     extern __shared__ __align__(1024) unsigned char smem[];
     unsigned char* raw = smem + size_t(kT3Stages) * kT3Stage;
     uint64_t* full = reinterpret_cast<uint64_t*>(raw + size_t(kT3Raw) * kT3RawBytes);
@@ -671,28 +679,52 @@ cudaError_t launch_gemm_tc2(const uint64_t* A, size_t sa, const uint64_t* BT, si
 
 bool gemm_tc3_ok(size_t n, size_t k, size_t m) { return n > 0 && k > 0 && m > 0 && m % kT3Cols == 0; }
 
+namespace {
+using Tc3Fn = void (*)(TcGemmArgs, const TcGemmArgs*);
+Tc3Fn tc3_fn() {
+    static Tc3Fn fn = nullptr;
+    if (!fn) {
+        for (auto f : {k_gemm_tc3<0>, k_gemm_tc3<1>, k_gemm_tc3<2>, k_gemm_tc3<3>})
+            if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kT3Smem)) != cudaSuccess)
+                return nullptr;
+        const char* env = getenv("F2GPU_TC_MODE");
+        const int mode = env ? atoi(env) : 0;
+        fn = mode == 1 ? k_gemm_tc3<1> : mode == 2 ? k_gemm_tc3<2> : mode == 3 ? k_gemm_tc3<3> : k_gemm_tc3<0>;
+    }
+    return fn;
+}
+bool tc3_args_ok(const TcGemmArgs& p) {
+    return gemm_tc3_ok(p.n, p.k, p.m) && p.sbt % 2 == 0 && p.sa % 2 == 0 &&
+           reinterpret_cast<uintptr_t>(p.A) % 16 == 0 && reinterpret_cast<uintptr_t>(p.BT) % 16 == 0;
+}
+}  // namespace
+
 // fp4 leaf: C (n x m) (^)= A (n x k) * B (k x m) given BT = B^T (m x k, stride sbt,
 // bits past k zero); n and k arbitrary, m % 256 == 0
 cudaError_t launch_gemm_tc3(const uint64_t* A, size_t sa, size_t n, const uint64_t* BT, size_t sbt,
                             uint64_t* C, size_t sc, size_t k, size_t m, bool acc, cudaStream_t s) {
-    static bool attr = false;
-    static int mode = 0;
-    if (!attr) {
-        for (auto fn : {k_gemm_tc3<0>, k_gemm_tc3<1>, k_gemm_tc3<2>, k_gemm_tc3<3>}) {
-            cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 int(kT3Smem));
-            if (e != cudaSuccess) return e;
-        }
-        const char* env = getenv("F2GPU_TC_MODE");
-        mode = env ? atoi(env) : 0;
-        attr = true;
-    }
-    if (!gemm_tc3_ok(n, k, m) || (sbt % 2) || (sa % 2) ||
-        (reinterpret_cast<uintptr_t>(A) % 16) || (reinterpret_cast<uintptr_t>(BT) % 16))
-        return cudaErrorInvalidValue;
+    Tc3Fn fn = tc3_fn();
+    if (!fn) return cudaErrorInvalidValue;
+    const TcGemmArgs p{A, sa, n, BT, sbt, C, sc, k, m, acc ? 1 : 0};
+    if (!tc3_args_ok(p)) return cudaErrorInvalidValue;
     dim3 grid(unsigned(m / kT3Cols), unsigned((n + kT3Rows - 1) / kT3Rows));
-    auto fn = mode == 1 ? k_gemm_tc3<1> : mode == 2 ? k_gemm_tc3<2> : mode == 3 ? k_gemm_tc3<3> : k_gemm_tc3<0>;
-    fn<<<grid, kT3Threads, kT3Smem, s>>>(A, sa, n, BT, sbt, C, sc, k, acc ? 1 : 0);
+    fn<<<grid, kT3Threads, kT3Smem, s>>>(p, nullptr);
+    return cudaGetLastError();
+}
+
+// a batch of fp4-leaf problems (host copy h_probs, device copy d_probs), one launch
+cudaError_t launch_gemm_tc3_batched(const TcGemmArgs* h_probs, const TcGemmArgs* d_probs, int nprob,
+                                    cudaStream_t s) {
+    Tc3Fn fn = tc3_fn();
+    if (!fn || nprob <= 0 || nprob > 65535) return cudaErrorInvalidValue;
+    size_t mx = 0, nx = 0;
+    for (int i = 0; i < nprob; ++i) {
+        if (!tc3_args_ok(h_probs[i])) return cudaErrorInvalidValue;
+        mx = std::max(mx, h_probs[i].m);
+        nx = std::max(nx, h_probs[i].n);
+    }
+    dim3 grid(unsigned(mx / kT3Cols), unsigned((nx + kT3Rows - 1) / kT3Rows), unsigned(nprob));
+    fn<<<grid, kT3Threads, kT3Smem, s>>>(TcGemmArgs{}, d_probs);
     return cudaGetLastError();
 }
 
