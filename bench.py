@@ -181,20 +181,27 @@ def run_reference(args, cfg) -> None:
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 1),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (random_dense seed %d, p=%g)" % (cfg["seed"], cfg["p"]),
-        "config": cfg_json(cfg, args.gpus),
+        "config": cfg_json(cfg, args.gpus, args.variant),
         "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def cfg_json(cfg, gpus):
-    return {"workload": f"decompose_block {cfg['n']}x{cfg['m']} dense F2, Bernoulli({cfg['p']}), "
+VARIANTS = {
+    "block": "decompose_block (lookahead 1, CUDA-graph replay)",
+    "recursive": "decompose_recursive (256-panel block leaves with lookahead; TRSM + products on the fp4 "
+                 "tensor-core leaf, Strassen-Winograd over 16384 leaves)",
+}
+
+
+def cfg_json(cfg, gpus, variant="block"):
+    return {"workload": f"decompose {cfg['n']}x{cfg['m']} dense F2, Bernoulli({cfg['p']}), "
                         f"seed {cfg['seed']} (BASELINE configs[3])",
             "n": cfg["n"], "m": cfg["m"], "density": cfg["p"], "seed": cfg["seed"],
             "word_bits": 64, "tables": "9 groups (7x8+8 bits), 16 word-cols/CTA",
             "parallelism": f"column-round-robin x{gpus}" if gpus > 1 else "single GPU",
-            "variant": "decompose_block (lookahead 1, CUDA-graph replay)",
+            "variant": VARIANTS[variant] if gpus == 1 else VARIANTS["block"],
             "l2": "inputs (512 MiB) larger than L2 (126 MB); no flush needed"}
 
 
@@ -209,8 +216,8 @@ def main() -> None:
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--gemm", action="store_true", help="also time the cfg2 16384^2 GEMM")
-    ap.add_argument("--variant", default="block", choices=["block", "recursive"],
-                    help="decompose_block or decompose_recursive (bit-identical factors)")
+    ap.add_argument("--variant", default="recursive", choices=["block", "recursive"],
+                    help="decompose_recursive (default, fastest) or decompose_block; bit-identical factors")
     ap.add_argument("--min-cols", type=int, default=0, help="recursive leaf width in bits (0 = default)")
     args = ap.parse_args()
     cfg = {"n": args.n, "m": args.n, "p": 0.5, "seed": 6}
@@ -304,7 +311,7 @@ def main() -> None:
     e2e = None
     if not args.no_e2e:
         e2e = measure_e2e(f2, lib, _lib, ctx, torch, A, n, m, mu, world, rank, dist,
-                          steps=min(args.steps, 3))
+                          steps=min(args.steps, 3), variant=args.variant, min_cols=args.min_cols)
 
     gemm = None
     if args.gemm and rank == 0:
@@ -321,7 +328,7 @@ def main() -> None:
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
             "data": f"synthetic (random_dense seed {cfg['seed']}, p={cfg['p']}, generated on device)",
-            "config": cfg_json(cfg, world),
+            "config": cfg_json(cfg, world, args.variant),
             "rank": rank_found,
             "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": ck,
             "gpu_launches": launches,
@@ -379,7 +386,8 @@ def measure_update_roofline(f2, lib, _lib, ctx, stream, torch, n: int) -> dict:
             "bitops_per_s": round(n * 64 * n / t, 1), "peak_source": src}
 
 
-def measure_e2e(f2, lib, _lib, ctx, torch, A, n, m, mu, world, rank, dist, steps: int) -> dict:
+def measure_e2e(f2, lib, _lib, ctx, torch, A, n, m, mu, world, rank, dist, steps: int,
+                variant: str = "block", min_cols: int = 0) -> dict:
     """Same metric through the public C-ABI host entry point with host buffers:
     H2D of A (pinned) + decomposition + D2H of W, perm, r_j inside the region."""
     host_stride = (n + 7) // 8 * 8
@@ -403,6 +411,10 @@ def measure_e2e(f2, lib, _lib, ctx, torch, A, n, m, mu, world, rank, dist, steps
             _lib.check(lib.f2gpu_mat_download(ctx.handle, Wd.handle, C.c_void_p(hW.ctypes.data),
                                               host_stride))
             Wd.free()
+        elif variant == "recursive":
+            _lib.check(lib.f2gpu_decompose_recursive_host(
+                ctx.handle, C.c_void_p(hA.ctypes.data), n, m, host_stride, min_cols,
+                C.c_void_p(hW.ctypes.data), perm.ctypes.data, rj.ctypes.data, C.byref(rk)))
         else:
             _lib.check(lib.f2gpu_decompose_block_host(
                 ctx.handle, C.c_void_p(hA.ctypes.data), n, m, host_stride,
@@ -425,8 +437,9 @@ def measure_e2e(f2, lib, _lib, ctx, torch, A, n, m, mu, world, rank, dist, steps
     return {"value": round(n * n * min(n, m) / dt / 1e9, 1), "unit": UNIT,
             "h2d_bytes_per_step": hbytes * world,
             "d2h_bytes_per_step": hbytes * world + 4 * n + 4 * mu,
-            "ms_per_step": round(dt * 1e3, 2), "api": "f2gpu_decompose_block_host" if world == 1
-            else "f2gpu_decompose_block_dist + host upload/download"}
+            "ms_per_step": round(dt * 1e3, 2),
+            "api": (f"f2gpu_decompose_{variant}_host" if world == 1
+                    else "f2gpu_decompose_block_dist + host upload/download")}
 
 
 def measure_gemm(f2, lib, _lib, ctx, stream, torch) -> dict:
@@ -436,10 +449,18 @@ def measure_gemm(f2, lib, _lib, ctx, stream, torch) -> dict:
     Am.random_dense(0.5, 2)
     Bm.random_dense(0.5, 3)
     out = {}
+    def smult(tc, cut):
+        def run():
+            ctx.set_tc(tc)
+            _lib.check(lib.f2gpu_strassen_mult(ctx.handle, Am.handle, Bm.handle, Cm.handle, cut))
+        return run
+
     variants = [("m4rm", lambda: _lib.check(lib.f2gpu_m4rm_mult(ctx.handle, Am.handle, Bm.handle, Cm.handle, 0)))]
     for cut in (16384, 8192, 4096):
-        variants.append((f"strassen_cut{cut}", lambda cut=cut: _lib.check(
-            lib.f2gpu_strassen_mult(ctx.handle, Am.handle, Bm.handle, Cm.handle, cut))))
+        variants.append((f"strassen_m4rm_cut{cut}", smult(False, cut)))
+    variants.append(("tc_fp4_leaf", lambda: _lib.check(lib.f2gpu_gemm_tc(ctx.handle, Am.handle, Bm.handle,
+                                                                         Cm.handle, 0))))
+    variants.append(("strassen_mult_default", smult(True, 0)))
     for name, fn in variants:
         for _ in range(3):
             fn()
@@ -452,6 +473,7 @@ def measure_gemm(f2, lib, _lib, ctx, stream, torch) -> dict:
         torch.cuda.synchronize()
         t = e0.elapsed_time(e1) / 5 * 1e-3
         out[name] = {"ms": round(t * 1e3, 3), "Gbitop_s": round(n ** 3 / t / 1e9, 1)}
+    ctx.set_tc(True)
     return {"metric": "M4RM GEMM Gbitop/s (n^3/t), 16384^2 (BASELINE configs[1])", **out}
 
 

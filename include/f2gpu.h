@@ -60,6 +60,11 @@ uint64_t f2gpu_ctx_launches(const f2gpu_ctx *ctx);
  * Strassen cutover (minimum dimension in bits below which the M4RM leaf runs;
  * 0 = default) replaces tuning::strassen_threshold (tuning.hpp:30). */
 int f2gpu_ctx_set_strassen_cutover(f2gpu_ctx *ctx, size_t min_dim_bits);
+/* Product leaf: on != 0 (default) lets strassen_mult and the recursive
+ * decomposition use the fp4 tensor-core leaf where the shape allows (n, k, m
+ * >= 256); tc_min_leaf_bits = minimum Strassen leaf size over that leaf
+ * (0 = default 16384).  Results are bit-identical either way. */
+int f2gpu_ctx_set_tc(f2gpu_ctx *ctx, int on, size_t tc_min_leaf_bits);
 
 /* ---- device matrix store (replaces PackedMatrix<uint64_t> storage,
  *      bit_matrix.hpp:82-346) ------------------------------------------------- */
@@ -154,6 +159,10 @@ int f2gpu_strassen_mult_host(f2gpu_ctx *ctx, const uint64_t *a, size_t n, size_t
 int f2gpu_decompose_block_host(f2gpu_ctx *ctx, const uint64_t *a, size_t n, size_t m,
                                size_t stride, uint64_t *w_out, uint32_t *perm, uint32_t *rj,
                                size_t *rank);
+/* the same through decompose_recursive (min_cols = 0: default leaf width) */
+int f2gpu_decompose_recursive_host(f2gpu_ctx *ctx, const uint64_t *a, size_t n, size_t m,
+                                   size_t stride, size_t min_cols, uint64_t *w_out, uint32_t *perm,
+                                   uint32_t *rj, size_t *rank);
 int f2gpu_rank_host(f2gpu_ctx *ctx, const uint64_t *a, size_t n, size_t m, size_t stride,
                     size_t *rank);
 

@@ -240,6 +240,10 @@ class Context:
     def set_strassen_cutover(self, bits: int) -> None:
         _lib.check(_lib.load().f2gpu_ctx_set_strassen_cutover(self._h, int(bits)))
 
+    def set_tc(self, on: bool, min_leaf_bits: int = 0) -> None:
+        """Allow the fp4 tensor-core product leaf (bit-identical results)."""
+        _lib.check(_lib.load().f2gpu_ctx_set_tc(self._h, 1 if on else 0, int(min_leaf_bits)))
+
     def init_comm(self, rank: int, world: int, uid: bytes) -> None:
         buf = C.create_string_buffer(bytes(uid), 128)
         _lib.check(_lib.load().f2gpu_ctx_init_comm(self._h, rank, world, buf), "init_comm")

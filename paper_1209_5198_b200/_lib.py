@@ -25,7 +25,7 @@ class F2GpuError(RuntimeError):
 SYMBOLS = [
     "f2gpu_last_error", "f2gpu_version",
     "f2gpu_ctx_create", "f2gpu_ctx_destroy", "f2gpu_ctx_set_stream", "f2gpu_ctx_sync",
-    "f2gpu_ctx_launches", "f2gpu_ctx_set_strassen_cutover",
+    "f2gpu_ctx_launches", "f2gpu_ctx_set_strassen_cutover", "f2gpu_ctx_set_tc",
     "f2gpu_mat_alloc", "f2gpu_mat_free", "f2gpu_mat_shape", "f2gpu_mat_device_ptr",
     "f2gpu_mat_zero", "f2gpu_mat_upload", "f2gpu_mat_download", "f2gpu_mat_random_dense",
     "f2gpu_mat_copy", "f2gpu_mat_select_wcols", "f2gpu_mat_xor", "f2gpu_mat_transpose",
@@ -35,6 +35,7 @@ SYMBOLS = [
     "f2gpu_decompose_block", "f2gpu_decompose_recursive", "f2gpu_decompose_block_sharded",
     "f2gpu_rank",
     "f2gpu_m4rm_mult_host", "f2gpu_strassen_mult_host", "f2gpu_decompose_block_host",
+    "f2gpu_decompose_recursive_host",
     "f2gpu_rank_host",
     "f2gpu_nccl_unique_id", "f2gpu_ctx_init_comm", "f2gpu_decompose_block_dist",
     "f2gpu_local_wcols",
@@ -54,6 +55,7 @@ _SIG = {
     "f2gpu_ctx_sync": ([vp], C.c_int),
     "f2gpu_ctx_launches": ([vp], C.c_uint64),
     "f2gpu_ctx_set_strassen_cutover": ([vp, sz], C.c_int),
+    "f2gpu_ctx_set_tc": ([vp, C.c_int, sz], C.c_int),
     "f2gpu_mat_alloc": ([vp, sz, sz, C.POINTER(vp)], C.c_int),
     "f2gpu_mat_free": ([vp], C.c_int),
     "f2gpu_mat_shape": ([vp, C.POINTER(sz), C.POINTER(sz), C.POINTER(sz)], C.c_int),
@@ -79,6 +81,7 @@ _SIG = {
     "f2gpu_m4rm_mult_host": ([vp, vp, sz, sz, sz, vp, sz, sz, vp, sz, C.c_uint], C.c_int),
     "f2gpu_strassen_mult_host": ([vp, vp, sz, sz, sz, vp, sz, sz, vp, sz, sz], C.c_int),
     "f2gpu_decompose_block_host": ([vp, vp, sz, sz, sz, vp, vp, vp, C.POINTER(sz)], C.c_int),
+    "f2gpu_decompose_recursive_host": ([vp, vp, sz, sz, sz, sz, vp, vp, vp, C.POINTER(sz)], C.c_int),
     "f2gpu_rank_host": ([vp, vp, sz, sz, sz, C.POINTER(sz)], C.c_int),
     "f2gpu_nccl_unique_id": ([vp], C.c_int),
     "f2gpu_ctx_init_comm": ([vp, C.c_int, C.c_int, vp], C.c_int),

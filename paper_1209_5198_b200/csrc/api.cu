@@ -788,10 +788,11 @@ int decompose_recursive(f2gpu_ctx* c, View w, size_t min_cols, uint32_t* perm, u
     F2_TRY(ensure_scratch(c, n, mu));
     Shard s;
     s.w = w; s.lw = mu; s.st = static_cast<f2::PanelState*>(c->scr_st); s.perm = c->scr_perm;
-    // defaults from a sweep at 65536^2 (Strassen cutover 4096..65536, TRSM base 8..64,
-    // leaves 1024..8192 columns): wide leaves + shallow Strassen win, see DESIGN.md
-    RecRun r{c, &s, n, mu, std::max<size_t>(1, (min_cols ? min_cols : 128 * 64) / 64),
-             lookahead_ok(c, s, n), 16384, 64};
+    // defaults from a sweep at 65536^2 with the fp4 tensor-core products (leaves
+    // 2048..32768 columns x TRSM base 4..64 panels): 16384-column leaves, base 16
+    // -> 87.6 ms (8192: 93.4, 32768: 88.9), see DESIGN.md
+    RecRun r{c, &s, n, mu, std::max<size_t>(1, (min_cols ? min_cols : 256 * 64) / 64),
+             lookahead_ok(c, s, n), 16384, 16};
     if (const char* e = getenv("F2GPU_REC_CUT")) r.cut = size_t(atol(e));
     if (const char* e = getenv("F2GPU_REC_TBASE")) r.tbase = std::max<size_t>(1, size_t(atol(e)));
     CUDA_TRY(cudaMemsetAsync(c->scr_flags, 0, mu * 4, c->stream));
@@ -1031,6 +1032,13 @@ uint64_t f2gpu_ctx_launches(const f2gpu_ctx* c) { return c ? c->launches : 0; }
 int f2gpu_ctx_set_strassen_cutover(f2gpu_ctx* c, size_t v) {
     if (!c) return set_err(F2GPU_EINVAL, "null ctx");
     c->strassen_cutover = v ? v : 4096;
+    return F2GPU_OK;
+}
+
+int f2gpu_ctx_set_tc(f2gpu_ctx* c, int on, size_t leaf) {
+    if (!c) return set_err(F2GPU_EINVAL, "null ctx");
+    c->use_tc = on != 0;
+    c->tc_cutover = leaf ? leaf : 16384;
     return F2GPU_OK;
 }
 
@@ -1390,6 +1398,18 @@ int f2gpu_decompose_block_host(f2gpu_ctx* c, const uint64_t* a, size_t n, size_t
     F2_TRY(staging(c, n, m, &W));
     F2_TRY(f2gpu_mat_upload(c, W, a, stride));
     F2_TRY(f2gpu_decompose_block(c, W, perm, rj, rank));
+    if (w_out) F2_TRY(f2gpu_mat_download(c, W, w_out, stride));
+    return F2GPU_OK;
+}
+
+int f2gpu_decompose_recursive_host(f2gpu_ctx* c, const uint64_t* a, size_t n, size_t m, size_t stride,
+                                   size_t min_cols, uint64_t* w_out, uint32_t* perm, uint32_t* rj,
+                                   size_t* rank) {
+    if (!c) return set_err(F2GPU_EINVAL, "null ctx");
+    f2gpu_mat* W = nullptr;
+    F2_TRY(staging(c, n, m, &W));
+    F2_TRY(f2gpu_mat_upload(c, W, a, stride));
+    F2_TRY(f2gpu_decompose_recursive(c, W, min_cols, perm, rj, rank));
     if (w_out) F2_TRY(f2gpu_mat_download(c, W, w_out, stride));
     return F2GPU_OK;
 }

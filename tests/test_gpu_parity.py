@@ -381,3 +381,48 @@ def test_decompose_recursive_rank_deficient(f2, ctx, po):
     assert got.rank == rank == 900
     assert np.array_equal(got.P.perm, perm) and np.array_equal(got.block_ranks, rj)
     assert same(got.overlay.words, w, 3000)
+
+
+# ---------------------------------------------------------------------------
+# product leaf selection: the fp4 tensor-core Strassen plan (B transposed once,
+# batched leaves) against M4RM and the oracle, 0-2 Strassen levels
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("n,k,m,leaf", [(2048, 2048, 2048, 512), (1024, 1536, 2048, 512), (2048, 1024, 1024, 256),
+                                        (1000, 700, 1300, 256), (4096, 4096, 4096, 1024)])
+def test_strassen_tc_plan(f2, ctx, po, n, k, m, leaf):
+    lib = f2._lib.load()
+    a = po.random_dense(n, k, 0.5, n + 1)
+    b = po.random_dense(k, m, 0.5, m + 2)
+    A = f2.DeviceMatrix.from_host(f2.BitMatrix(n, k, a), ctx)
+    B = f2.DeviceMatrix.from_host(f2.BitMatrix(k, m, b), ctx)
+    C1, C2 = f2.DeviceMatrix(n, m, ctx), f2.DeviceMatrix(n, m, ctx)
+    try:
+        ctx.set_tc(True, leaf)
+        f2._lib.check(lib.f2gpu_strassen_mult(ctx.handle, A.handle, B.handle, C1.handle, 0))
+        ctx.set_tc(False)
+        f2._lib.check(lib.f2gpu_strassen_mult(ctx.handle, A.handle, B.handle, C2.handle, 0))
+    finally:
+        ctx.set_tc(True)
+    got = C1.download().words
+    assert same(got, C2.download().words, n)
+    if n * k * m <= 2048 ** 3:
+        assert same(got, po.m4rm_mult(a, n, k, b, m), n)
+
+
+def test_decompose_recursive_host(f2, ctx, po):
+    import ctypes as C
+    lib = f2._lib.load()
+    n, m = 1500, 2300
+    a = po.random_dense(n, m, 0.5, 77)
+    w, perm, rj, rank = po.decompose_block(a, n, m)
+    stride = a.shape[1]
+    wout = np.zeros_like(a)
+    p = np.zeros(n, np.uint32)
+    r = np.zeros((m + 63) // 64, np.uint32)
+    rk = C.c_size_t()
+    f2._lib.check(lib.f2gpu_decompose_recursive_host(ctx.handle, a.ctypes.data, n, m, stride, 256,
+                                                     wout.ctypes.data, p.ctypes.data, r.ctypes.data,
+                                                     C.byref(rk)))
+    assert rk.value == rank
+    assert np.array_equal(p, perm) and np.array_equal(r, rj)
+    assert same(wout, w, n)
