@@ -712,7 +712,8 @@ struct RecRun {
     size_t n, mu, base;
     bool la;
     size_t cut;    // Strassen cutover inside the recursion (XOR traffic vs multiply)
-    size_t tbase;  // TRSM base (panels solved by rank-64 updates)
+    size_t tbase;  // TRSM base (panels solved in one k_trsm_block launch)
+    bool trsm_kernel = true;  // F2GPU_REC_TRSM=0: rank-64 updates instead (A/B check)
 };
 
 int rec_state(RecRun& r, size_t j, size_t* R, size_t* rr) {
@@ -725,7 +726,8 @@ int rec_state(RecRun& r, size_t j, size_t* R, size_t* rr) {
 }
 
 // panels [a, b) applied to word-cols [col0, col1), rows (R_j + r_j) .. row_hi
-int rank_updates(RecRun& r, size_t a, size_t b, size_t col0, size_t col1, size_t row_hi) {
+int rank_updates(RecRun& r, size_t a, size_t b, size_t col0, size_t col1, size_t row_hi,
+                 const char* what = "k_update") {
     Shard& s = *r.s;
     for (size_t j = a; j < b; ++j) {
         f2::UpdateArgs u{};
@@ -733,7 +735,7 @@ int rank_updates(RecRun& r, size_t a, size_t b, size_t col0, size_t col1, size_t
         u.row_lo = 0; u.row_hi = row_hi; u.a = s.w.p + j * s.w.stride; u.k_bits = 0;
         u.B = s.w.p; u.sb = s.w.stride; u.b_row0 = 0; u.b_wcol0 = col0;
         u.st = s.st + j;
-        F2_TRY(check_launch(r.c, f2::launch_update(u, r.c->num_sms, r.c->stream), "k_update"));
+        F2_TRY(check_launch(r.c, f2::launch_update(u, r.c->num_sms, r.c->stream), what));
     }
     return F2GPU_OK;
 }
@@ -746,7 +748,13 @@ View wview(const Shard& s, size_t r0, size_t nr, size_t wc0, size_t nwc) {
 // place on word-cols [col0, col1) of those rows.
 int rec_trsm(RecRun& r, size_t a, size_t b, size_t Ra, size_t col0, size_t col1) {
     const size_t Rb = Ra + 64 * (b - a);
-    if (b - a <= r.tbase) return rank_updates(r, a, b, col0, col1, Rb);
+    if (b - a <= r.tbase) {
+        if (b - a <= 16 && r.trsm_kernel)
+            return check_launch(r.c, f2::launch_trsm_block(r.s->w.p, r.s->w.stride, int(a), int(b - a), Ra, col0,
+                                                           int(col1 - col0), r.c->stream),
+                                "k_trsm_block");
+        return rank_updates(r, a, b, col0, col1, Rb, "k_update(trsm)");
+    }
     const size_t m = a + (b - a) / 2, Rm = Ra + 64 * (m - a);
     F2_TRY(rec_trsm(r, a, m, Ra, col0, col1));
     F2_TRY(best_product(r.c, wview(*r.s, Rm, Rb - Rm, col0, col1 - col0),
@@ -795,6 +803,7 @@ int decompose_recursive(f2gpu_ctx* c, View w, size_t min_cols, uint32_t* perm, u
              lookahead_ok(c, s, n), 16384, 16};
     if (const char* e = getenv("F2GPU_REC_CUT")) r.cut = size_t(atol(e));
     if (const char* e = getenv("F2GPU_REC_TBASE")) r.tbase = std::max<size_t>(1, size_t(atol(e)));
+    if (const char* e = getenv("F2GPU_REC_TRSM")) r.trsm_kernel = e[0] != '0';
     CUDA_TRY(cudaMemsetAsync(c->scr_flags, 0, mu * 4, c->stream));
     c->tl.mark(c->stream, "start");
     F2_TRY(check_launch(c, f2::launch_iota(s.perm, n, c->stream), "k_iota"));

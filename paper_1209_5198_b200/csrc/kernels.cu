@@ -1575,6 +1575,74 @@ cudaError_t launch_post(uint64_t* w, size_t stride, int ncols, int panel_col, ui
 }
 
 // ---------------------------------------------------------------------------
+// block TRSM base case of decompose_recursive (full rank): panels a .. a+P-1
+// own pivot rows Ra .. Ra+64P; on word-columns [col0, col0+ncols) of those rows
+//   for t = 0..P-1:  rows of panel u > t  ^=  Y_t[row] * (pivot rows of t)
+// (the in-place X = L11^-1 C of SPEC.md:328-345 restricted to a 64P-row block).
+// One 128-thread CTA per word-column: the column segment (<= 1024 words) sits in
+// shared memory; per panel a 4-bit lookup table of its 64 final pivot words (16
+// groups x 16 entries, one 128-byte group per lookup step -> conflict-free)
+// turns each row update into 16 lookups, and each thread loads all of its
+// multiplier words for the panel at once.  Replaces P launches of the rank-64
+// update.
+// ---------------------------------------------------------------------------
+constexpr int kTrsmThreads = 128;  // one CTA per word-column
+constexpr int kTrsmMaxP = 16;
+constexpr int kTrsmRowsPerThread = 64 * kTrsmMaxP / kTrsmThreads;
+__global__ void __launch_bounds__(kTrsmThreads) k_trsm_block(uint64_t* __restrict__ W, size_t stride, int a,
+                                                             int P, size_t Ra, size_t col0) {
+    __shared__ uint64_t cs[64 * kTrsmMaxP];
+    __shared__ uint64_t tb[256];
+    const int tid = threadIdx.x;
+    uint64_t* col = W + (col0 + blockIdx.x) * stride + Ra;
+    const int rows = 64 * P;
+    for (int i = tid; i < rows; i += kTrsmThreads) cs[i] = col[i];
+    __syncthreads();
+    for (int t = 0; t < P; ++t) {
+        // all multiplier words this thread needs for panel t, loaded together
+        const uint64_t* Y = W + size_t(a + t) * stride + Ra;
+        const int r0 = 64 * (t + 1) + tid;
+        uint64_t y[kTrsmRowsPerThread];
+#pragma unroll
+        for (int i = 0; i < kTrsmRowsPerThread; ++i) {
+            const int r = r0 + kTrsmThreads * i;
+            y[i] = r < rows ? Y[r] : 0;
+        }
+        // 4-bit table of panel t's final pivot words (2 entries per thread)
+        const uint64_t* B = cs + 64 * t;
+#pragma unroll
+        for (int e2 = 0; e2 < 2; ++e2) {
+            const int e = tid + kTrsmThreads * e2, g = e >> 4, v = e & 15;
+            uint64_t x = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if ((v >> i) & 1) x ^= B[4 * g + i];
+            tb[e] = x;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < kTrsmRowsPerThread; ++i) {
+            const int r = r0 + kTrsmThreads * i;
+            if (r < rows) {
+                uint64_t x = 0;
+#pragma unroll
+                for (int g = 0; g < 16; ++g) x ^= tb[16 * g + int((y[i] >> (4 * g)) & 15)];
+                cs[r] ^= x;
+            }
+        }
+        __syncthreads();
+    }
+    for (int i = 64 + tid; i < rows; i += kTrsmThreads) col[i] = cs[i];  // panel 0's rows are unchanged
+}
+
+cudaError_t launch_trsm_block(uint64_t* W, size_t stride, int a, int P, size_t Ra, size_t col0, int ncols,
+                              cudaStream_t s) {
+    if (P < 1 || P > kTrsmMaxP || ncols < 1) return cudaErrorInvalidValue;
+    k_trsm_block<<<ncols, kTrsmThreads, 0, s>>>(W, stride, a, P, Ra, col0);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // block XOR (Strassen-Winograd additions)
 // ---------------------------------------------------------------------------
 // 2D grid: blockIdx.y = word-column, threads stride over 4-word (32 B) row chunks
@@ -1636,39 +1704,71 @@ cudaError_t launch_xor(uint64_t* dst, size_t sd, const uint64_t* a, size_t sa, c
 // ---------------------------------------------------------------------------
 // bit transpose: one warp per 64x64 tile (transpose_tile, bit_matrix.hpp:59-70)
 // ---------------------------------------------------------------------------
+// 64x64 bit-matrix transpose held in a warp: lane L holds rows L (x0) and L+32
+// (x1) on entry and columns L / L+32 on exit.  One register swap for the 32-bit
+// halves, then five shuffle butterflies -- no shared memory, no bank conflicts.
+__device__ __forceinline__ void warp_transpose64(uint64_t& x0, uint64_t& x1, int lane) {
+    {
+        const uint64_t t = ((x0 >> 32) ^ x1) & 0x00000000FFFFFFFFull;
+        x1 ^= t;
+        x0 ^= t << 32;
+    }
+    const uint64_t masks[5] = {0x0000FFFF0000FFFFull, 0x00FF00FF00FF00FFull, 0x0F0F0F0F0F0F0F0Full,
+                               0x3333333333333333ull, 0x5555555555555555ull};
+#pragma unroll
+    for (int st = 0; st < 5; ++st) {
+        const int j = 16 >> st;
+        const uint64_t msk = masks[st];
+        const uint64_t y0 = __shfl_xor_sync(0xffffffffu, x0, j);
+        const uint64_t y1 = __shfl_xor_sync(0xffffffffu, x1, j);
+        if (!(lane & j)) {
+            x0 ^= (((x0 >> j) ^ y0) & msk) << j;
+            x1 ^= (((x1 >> j) ^ y1) & msk) << j;
+        } else {
+            x0 ^= ((y0 >> j) ^ x0) & msk;
+            x1 ^= ((y1 >> j) ^ x1) & msk;
+        }
+    }
+}
+
+// out (m x n) = a (n x m)^T.  Grid: blockIdx.y = input word-column q, each warp
+// transposes kTrTilesPerWarp consecutive 64-row tiles of it (loads issued
+// together); no integer division in the kernel.
+constexpr int kTrTilesPerWarp = 2;
 __global__ void __launch_bounds__(256) k_transpose(const uint64_t* __restrict__ a, size_t n,
                                                    size_t m, size_t sa, uint64_t* __restrict__ out,
                                                    size_t so) {
-    __shared__ uint64_t tiles[8][64];
-    const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const size_t mu = (m + 63) / 64, mt = (n + 63) / 64;
-    const size_t tile = size_t(blockIdx.x) * 8 + wl;
-    if (tile >= mu * mt) return;
-    const size_t q = tile / mt, tr = tile % mt;
-    uint64_t* x = tiles[wl];
-    const size_t i0 = tr * 64;
-    x[lane] = (i0 + lane < n) ? a[q * sa + i0 + lane] : 0ull;
-    x[lane + 32] = (i0 + lane + 32 < n) ? a[q * sa + i0 + lane + 32] : 0ull;
-    __syncwarp();
-    uint64_t msk = 0x00000000FFFFFFFFull;
-    for (int jj = 32; jj != 0; jj >>= 1, msk ^= (msk << jj)) {
-        const int k = ((lane & ~(jj - 1)) << 1) | (lane & (jj - 1));
-        const uint64_t t = ((x[k] >> jj) ^ x[k + jj]) & msk;
-        __syncwarp();
-        x[k + jj] ^= t;
-        x[k] ^= t << jj;
-        __syncwarp();
+    const int lane = threadIdx.x & 31;
+    const size_t q = blockIdx.y, mt = (n + 63) / 64;
+    const size_t tr0 = (size_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * kTrTilesPerWarp;
+    const uint64_t* col = a + q * sa;
+    uint64_t x0[kTrTilesPerWarp], x1[kTrTilesPerWarp];
+#pragma unroll
+    for (int u = 0; u < kTrTilesPerWarp; ++u) {
+        const size_t i0 = (tr0 + u) * 64;
+        x0[u] = (i0 + lane < n) ? col[i0 + lane] : 0;
+        x1[u] = (i0 + lane + 32 < n) ? col[i0 + lane + 32] : 0;
     }
     const size_t orow = q * 64;
-    if (orow + lane < m) out[tr * so + orow + lane] = x[lane];
-    if (orow + lane + 32 < m) out[tr * so + orow + lane + 32] = x[lane + 32];
+#pragma unroll
+    for (int u = 0; u < kTrTilesPerWarp; ++u) {
+        const size_t tr = tr0 + u;
+        if (tr >= mt) break;  // warp-uniform
+        warp_transpose64(x0[u], x1[u], lane);
+        uint64_t* o = out + tr * so + orow;
+        if (orow + lane < m) o[lane] = x0[u];
+        if (orow + lane + 32 < m) o[lane + 32] = x1[u];
+    }
 }
 
 cudaError_t launch_transpose(const uint64_t* a, size_t n, size_t m, size_t sa, uint64_t* out,
                              size_t so, cudaStream_t s) {
-    const size_t tiles = ((m + 63) / 64) * ((n + 63) / 64);
-    if (tiles == 0) return cudaSuccess;
-    k_transpose<<<unsigned((tiles + 7) / 8), 256, 0, s>>>(a, n, m, sa, out, so);
+    const size_t mu = (m + 63) / 64, mt = (n + 63) / 64;
+    if (mu == 0 || mt == 0) return cudaSuccess;
+    if (mu > 65535) return cudaErrorInvalidValue;
+    const size_t per_block = 8 * kTrTilesPerWarp;
+    dim3 grid(unsigned((mt + per_block - 1) / per_block), unsigned(mu));
+    k_transpose<<<grid, 256, 0, s>>>(a, n, m, sa, out, so);
     return cudaGetLastError();
 }
 

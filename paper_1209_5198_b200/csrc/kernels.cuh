@@ -142,6 +142,11 @@ int update_tc_release_count(const TcUpdateArgs& a, int grid);
 size_t update_tc_bt_rows(int ncols);
 cudaError_t launch_update_tc(const TcUpdateArgs& a, int grid, cudaStream_t s);
 
+// block TRSM base (decompose_recursive, full rank): P <= 16 panels a.., pivot
+// rows Ra .. Ra+64P, in place on word-columns [col0, col0+ncols)
+cudaError_t launch_trsm_block(uint64_t* W, size_t stride, int a, int P, size_t Ra, size_t col0, int ncols,
+                              cudaStream_t s);
+
 // per-device one-time setup (dynamic shared memory opt-in)
 cudaError_t init_kernel_attrs();
 
