@@ -981,6 +981,17 @@ int f2gpu_ctx_create(int device, f2gpu_ctx** out) {
     auto c = std::make_unique<f2gpu_ctx>();
     c->device = device;
     c->num_sms = prop.multiProcessorCount;
+    {
+        // scratch (B^T, Strassen arenas, broadcast buffers) comes from the stream-
+        // ordered pool; keep freed blocks cached instead of returning them to the
+        // OS at every synchronisation (release threshold 0 made each large scratch
+        // allocation a fresh OS allocation inside the decomposition)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t keep = ~uint64_t(0);
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    }
     if (const char* pf = getenv("F2GPU_PROFILE")) c->tl.on = pf[0] == '1';
     if (const char* gr = getenv("F2GPU_GRAPHS")) c->use_graphs = gr[0] != '0';
     if (const char* la = getenv("F2GPU_LOOKAHEAD")) c->lookahead = la[0] != '0';
