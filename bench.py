@@ -51,6 +51,19 @@ def peaks() -> tuple[float, str]:
     return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
 
 
+def tensor_peak() -> tuple[float, str]:
+    """Dense fp4 tensor peak in TFLOP/s: the measured bf16 burst GEMM figure x 4
+    (fp4 : bf16 = 9 : 2.25 PFLOP/s dense, B200_PROFILING.md nominal table)."""
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            bf16 = float(json.loads(p.read_text())["bf16_tflops"])
+            return 4 * bf16, "derived: 4 x measured bf16 burst (MEASURED_PEAKS.json bf16_tflops)"
+        except Exception:
+            pass
+    return 4 * 1590.0, "derived: 4 x fallback bf16 1.59 PFLOP/s (B200_PROFILING.md)"
+
+
 # ---------------------------------------------------------------------------
 # clocks sampler (nvidia-smi during the timed region)
 # ---------------------------------------------------------------------------
@@ -303,9 +316,11 @@ def main() -> None:
     rank_found = int(rk.value)
 
     # ---- roofline: the dominant kernel, measured live (north-star unit) ----
-    roof = None
+    roof = roof_tc = None
     if rank == 0:
         roof = measure_update_roofline(f2, lib, _lib, ctx, stream, torch, n)
+        if args.variant == "recursive" and world == 1:
+            roof_tc = measure_tensor_roofline(f2, lib, _lib, ctx, stream, torch)
 
     # ---- e2e through the C-ABI host entry point (pinned host buffers) ----
     e2e = None
@@ -330,7 +345,7 @@ def main() -> None:
             "data": f"synthetic (random_dense seed {cfg['seed']}, p={cfg['p']}, generated on device)",
             "config": cfg_json(cfg, world, args.variant),
             "rank": rank_found,
-            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": ck,
+            "e2e": e2e, "roofline": roof, "roofline_tensor": roof_tc, "cpu_baseline": cpu, "clocks": ck,
             "gpu_launches": launches,
         }
         if gemm:
@@ -383,7 +398,50 @@ def measure_update_roofline(f2, lib, _lib, ctx, stream, torch, n: int) -> dict:
             "kernel": "k_update (fused M4RM table build + XOR sweep)",
             "unit_workload": f"C({n}x{n}) ^= A({n}x64)*B(64x{n})",
             "algorithmic_bytes": alg, "us_per_launch": round(t * 1e6, 1),
-            "bitops_per_s": round(n * 64 * n / t, 1), "peak_source": src}
+            "bitops_per_s": round(n * 64 * n / t, 1),
+            "share_of_step": "33% of the decomposition (profiles/r1_launches_rec_summary.txt)",
+            "peak_source": src}
+
+
+def measure_tensor_roofline(f2, lib, _lib, ctx, stream, torch, n: int = 16384) -> dict:
+    """The fp4 tensor-core product leaf (k_gemm_tc3) on C = A*B, n^3 (BASELINE
+    configs[1] shape): fp4 MACs executed = one per (i, j, k), 2 FLOP each.  The
+    timed call includes the B^T staging transpose (~2% of it)."""
+    Am, Bm, Cm = (f2.DeviceMatrix(n, n, ctx) for _ in range(3))
+    Am.random_dense(0.5, 2)
+    Bm.random_dense(0.5, 3)
+
+    def launch():
+        _lib.check(lib.f2gpu_gemm_tc(ctx.handle, Am.handle, Bm.handle, Cm.handle, 0))
+
+    for _ in range(3):
+        launch()
+    torch.cuda.synchronize()
+    reps = 10
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        launch()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / reps * 1e-3
+    peak, src = tensor_peak()
+    ach = 2.0 * n ** 3 / t / 1e12
+    traffic = None
+    tp = ROOT / "profiles" / "tc3_traffic.json"
+    if tp.exists():
+        try:
+            traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    Am.free(); Bm.free(); Cm.free()
+    return {"bound": "tensor", "achieved": round(ach, 1), "peak": round(peak, 1), "unit": "TFLOP/s",
+            "frac": round(ach / peak, 4), "traffic": traffic,
+            "kernel": "k_gemm_tc3 (fp4 kind::mxf4 GF(2) product leaf)",
+            "unit_workload": f"C({n}x{n}) = A({n}x{n})*B({n}x{n}), 2*n^3 fp4 FLOP",
+            "us_per_launch": round(t * 1e6, 1), "bitops_per_s": round(n ** 3 / t, 1),
+            "share_of_step": "35% of the decomposition (profiles/r1_launches_rec_summary.txt)",
+            "peak_source": src}
 
 
 def measure_e2e(f2, lib, _lib, ctx, torch, A, n, m, mu, world, rank, dist, steps: int,
