@@ -52,6 +52,42 @@ static __device__ __forceinline__ void mma_f4_sf(uint32_t tmem_d, uint64_t da, u
             tmem_d),
         "l"(da), "l"(db), "r"(idesc), "r"(acc), "r"(tsfa), "r"(tsfb));
 }
+// CTA-pair (cta_group::2) variants: issued by the leader CTA of a 2-CTA cluster;
+// A (M = 256) is split by rows over the pair, B by N halves, each CTA's TMEM
+// receives the D rows of its own M half
+static __device__ __forceinline__ void mma_f4_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                                   uint32_t acc, uint32_t tsf) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%5], [%5], p;\n\t}\n" ::"r"(
+            tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc), "r"(tsf));
+}
+// arrive on the barrier at the same shared offset in every CTA of mask
+static __device__ __forceinline__ void tc_commit_pair(uint64_t* bar, uint16_t mask) {
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                     sm_u32(bar)),
+                 "h"(mask)
+                 : "memory");
+}
+static __device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// shared::cluster address of `p` (a shared::cta address in this CTA) in CTA `rank`
+static __device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t rank) {
+    uint32_t a;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(sm_u32(p)), "r"(rank));
+    return a;
+}
+static __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+static __device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 static __device__ __forceinline__ void tc_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sm_u32(bar))
                  : "memory");

@@ -447,7 +447,7 @@ constexpr int kT3Stage = kT3Slots * kT3Slot;
 constexpr int kT3Stages = 3;
 constexpr int kT3RawWords = kT3Cols + kT3Rows;
 constexpr int kT3RawBytes = kT3RawWords * 8;
-constexpr int kT3Raw = 4;
+constexpr int kT3Raw = 4;  // (an 8-deep ring, or direct __ldg feeds, measured no faster / slower)
 constexpr uint32_t kT3SfCol = 480;
 constexpr size_t kT3Smem = size_t(kT3Stages) * kT3Stage + size_t(kT3Raw) * kT3RawBytes + 256;
 constexpr uint32_t kIdescF4 = idesc_f4(128, kT3Rows);
@@ -679,6 +679,221 @@ cudaError_t launch_gemm_tc2(const uint64_t* A, size_t sa, const uint64_t* BT, si
 
 bool gemm_tc3_ok(size_t n, size_t k, size_t m) { return n > 0 && k > 0 && m > 0 && m % kT3Cols == 0; }
 
+// ---- v4: the fp4 leaf on CTA pairs (cta_group::2) ----
+// A cluster of 2 CTAs computes a 512-column x 240-row tile with M = 256 MMAs
+// issued by the leader: for each of the two accumulators the M = 256 output
+// columns are split 128/128 over the pair (each CTA expands its own B^T rows) and
+// the N = 240 output rows are split 120/120 (each CTA expands half of the A^T
+// rows; the MMA reads the other half from the peer's shared memory).  Per SM and
+// k-block that is 376 expanded rows and 15.5 KB of operand reads instead of 496
+// rows and 23 KB -- the single-CTA leaf is shared-memory-bandwidth-bound (LSU +
+// tensor-core wavefronts ~95%, profiles/r1_tc3_summary.txt).  Each CTA's TMEM
+// holds its 128 M-rows x 240 columns per accumulator; the epilogue is unchanged.
+constexpr int kT4Exp = 384;                 // expansion threads (warps 0-11)
+constexpr int kT4Mma = kT4Exp / 32;         // warp 12 (leader CTA issues)
+constexpr int kT4Load = kT4Mma + 1;         // warp 13
+constexpr int kT4Threads = kT4Exp + 64;
+constexpr int kT4Cols = 512;                // output columns per pair (2 accumulators x M = 256)
+constexpr int kT4ARows = 256;               // B^T rows expanded per CTA (2 x 128)
+constexpr int kT4Rows = 240;                // output rows per pair (N)
+constexpr int kT4BRows = kT4Rows / 2;       // A^T rows expanded per CTA
+constexpr int kT4ABytes = kT4ARows * 64;    // per 2-k-block slot
+constexpr int kT4BBytes = kT4BRows * 64;
+constexpr int kT4Slot = 24 * 1024;          // A (16 KB) + B (7.5 KB), padded to 1 KB
+constexpr int kT4Slots = 2;                 // 4 k-blocks per stage
+constexpr int kT4Kps = 2 * kT4Slots;
+constexpr int kT4Stage = kT4Slots * kT4Slot;
+constexpr int kT4Stages = 4;
+constexpr int kT4RawWords = kT4ARows + kT4BRows;
+constexpr int kT4RawBytes = 3072;           // 376 words, padded
+constexpr int kT4Raw = 4;
+constexpr uint32_t kT4SfCol = 480;
+constexpr size_t kT4Smem = size_t(kT4Stages) * kT4Stage + size_t(kT4Raw) * kT4RawBytes + 512;
+constexpr uint32_t kIdescF4Pair = idesc_f4(256, kT4Rows);
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT4Threads, 1)
+    k_gemm_tc4(TcGemmArgs one, const TcGemmArgs* __restrict__ probs) {
+    const TcGemmArgs P = probs ? probs[blockIdx.z] : one;
+    const uint32_t rank = cluster_rank();
+    const size_t pc0 = size_t(blockIdx.x >> 1) * kT4Cols;   // pair's first output column
+    const size_t i0 = size_t(blockIdx.y) * kT4Rows;
+    if (pc0 >= P.m || i0 >= P.n) return;  // uniform over the pair
+    const uint64_t* __restrict__ A = P.A;
+    const uint64_t* __restrict__ BT = P.BT;
+    uint64_t* __restrict__ C = P.C;
+    const size_t sa = P.sa, n = P.n, sbt = P.sbt, sc = P.sc, k = P.k;
+    const int acc = P.acc;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    unsigned char* raw = smem + size_t(kT4Stages) * kT4Stage;
+    uint64_t* full = reinterpret_cast<uint64_t*>(raw + size_t(kT4Raw) * kT4RawBytes);
+    uint64_t* empty = full + kT4Stages;
+    uint64_t* rfull = empty + kT4Stages;
+    uint64_t* rempty = rfull + kT4Raw;
+    uint64_t* done = rempty + kT4Raw;
+    uint64_t* pfull = done + 1;  // leader: the peer's stage s is expanded (forwarded)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pfull + kT4Stages);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // this CTA's A^T rows: i0 + 120*rank .. (zero past n)
+    const size_t bi0 = i0 + size_t(kT4BRows) * rank;
+    const int bvalid = bi0 >= n ? 0 : int(min(size_t(kT4BRows), n - bi0));
+    const int nvalid = int(min(size_t(kT4Rows), n - i0));  // output rows of the pair tile
+    const size_t KB = (k + 63) / 64;
+
+    if (tid == 0) {
+        for (int s = 0; s < kT4Stages; ++s) {
+            mbar_init_n(&full[s], kT4Exp / 32);  // this CTA's expansion warps
+            mbar_init_n(&empty[s], 1);
+            mbar_init_n(&pfull[s], 1);
+        }
+        for (int s = 0; s < kT4Raw; ++s) {
+            mbar_init_n(&rfull[s], 1);
+            mbar_init_n(&rempty[s], kT4Exp / 32);
+        }
+        mbar_init_n(done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sm_u32(tmem_slot)),
+                     "r"(512u));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+    if (warp < 4) {  // scale factors: every byte of columns 480..511 = E8M0 1.0
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, "
+            "%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(
+                tmem + (uint32_t(32 * warp) << 16) + kT4SfCol),
+            "r"(0x7F7F7F7Fu)
+            : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    cluster_sync_all();  // both CTAs: barriers initialised, TMEM allocated, scales set
+    asm volatile("tcgen05.fence::after_thread_sync;");
+
+    if (warp == kT4Load) {
+        if (lane == 0) {
+            const int nb = bvalid & ~1;
+            const size_t ca = pc0 + size_t(128) * rank, cb = ca + 256;  // B^T rows of acc 0 / acc 1
+            int s = 0;
+            uint32_t ph = 0;
+            for (size_t kb = 0; kb < KB; ++kb) {
+                if (kb >= size_t(kT4Raw)) mbar_wait1(&rempty[s], ph ^ 1);
+                uint64_t* r = reinterpret_cast<uint64_t*>(raw + size_t(s) * kT4RawBytes);
+                if (bvalid & 1) r[kT4ARows + nb] = A[kb * sa + bi0 + nb];
+                mbar_expect(&rfull[s], uint32_t(kT4ARows + nb) * 8);
+                bulk_g2s(r, BT + kb * sbt + ca, 128 * 8, &rfull[s]);
+                bulk_g2s(r + 128, BT + kb * sbt + cb, 128 * 8, &rfull[s]);
+                if (nb) bulk_g2s(r + kT4ARows, A + kb * sa + bi0, uint32_t(nb) * 8, &rfull[s]);
+                if (++s == kT4Raw) { s = 0; ph ^= 1; }
+            }
+        }
+        __syncwarp();
+    } else if (warp == kT4Mma) {
+        if (lane == 0 && rank == 1) {
+            // peer: forward each locally completed stage to the leader with one
+            // cluster-scope release (the expansion warps only arrive CTA-locally)
+            const uint32_t pfull_leader = mapa_shared(pfull, 0);
+            int s = 0;
+            uint32_t ph = 0;
+            for (size_t kb = 0; kb < KB; kb += kT4Kps) {
+                mbar_wait1(&full[s], ph);
+                mbar_arrive_cluster(pfull_leader + uint32_t(s) * 8);
+                if (++s == kT4Stages) { s = 0; ph ^= 1; }
+            }
+        }
+        if (lane == 0 && rank == 0) {
+            const uint32_t tsf = tmem + kT4SfCol;
+            int s = 0;
+            uint32_t ph = 0;
+            for (size_t kb = 0; kb < KB; kb += kT4Kps) {
+                mbar_wait1(&full[s], ph);
+                mbar_wait1(&pfull[s], ph);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+                for (int j = 0; j < kT4Kps; ++j) {
+                    if (kb + j >= KB) break;
+                    const uint32_t ta = sm_u32(smem + size_t(s) * kT4Stage + (j >> 1) * kT4Slot) + (j & 1) * 32;
+                    const uint32_t tb = ta + kT4ABytes;
+                    const uint32_t a0 = kb + j > 0 ? 1u : 0u;
+                    mma_f4_pair(tmem, umma_desc(ta), umma_desc(tb), kIdescF4Pair, a0, tsf);
+                    mma_f4_pair(tmem + kT4Rows, umma_desc(ta + 128 * 64), umma_desc(tb), kIdescF4Pair, a0, tsf);
+                }
+                tc_commit_pair(&empty[s], 0x3);
+                if (++s == kT4Stages) { s = 0; ph ^= 1; }
+            }
+            tc_commit_pair(done, 0x3);
+        }
+        __syncwarp();
+    } else {
+        // thread t < 256: B^T row t (acc t / 128); 256 <= t < 376: A^T row t - 256
+        const bool active = tid < kT4RawWords;
+        const int region = tid < kT4ARows ? 0 : kT4ABytes;
+        const int r = tid < kT4ARows ? tid : tid - kT4ARows;
+        const bool live = active && (tid < kT4ARows || r < bvalid);
+        int s = 0, rs = 0;
+        uint32_t ph = 0, rph = 0;
+        for (size_t kb = 0, st = 0; kb < KB; kb += kT4Kps, ++st) {
+            if (st >= size_t(kT4Stages)) mbar_wait1(&empty[s], ph ^ 1);
+#pragma unroll
+            for (int j = 0; j < kT4Kps; ++j) {
+                if (kb + j >= KB) break;
+                mbar_wait1(&rfull[rs], rph);
+                uint64_t x = 0;
+                if (live) x = reinterpret_cast<const uint64_t*>(raw + size_t(rs) * kT4RawBytes)[tid];
+                if (active) store_row_f4(smem + size_t(s) * kT4Stage + (j >> 1) * kT4Slot + region, r, j & 1, x);
+                __syncwarp();  // x consumed by every lane before the raw slot is released
+                if (lane == 0) mbar_arrive1(&rempty[rs]);
+                if (++rs == kT4Raw) { rs = 0; rph ^= 1; }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive1(&full[s]);
+            if (++s == kT4Stages) { s = 0; ph ^= 1; }
+        }
+        // epilogue: lane quarter lq = w & 3; 16-column chunks (acc, cc) = (w >> 2) + 3i
+        // of 2 x 15; this CTA's output columns are pc0 + 256 acc + 128 rank + 32 lq + lane
+        mbar_wait1(done, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const int lq = warp & 3;
+#pragma unroll 1
+        for (int ch = warp >> 2; ch < 2 * (kT4Rows / 16); ch += kT4Exp / 128) {
+            const int accn = ch / (kT4Rows / 16), cc = ch % (kT4Rows / 16);
+            uint32_t v[16];
+            const uint32_t taddr = tmem + (uint32_t(32 * lq) << 16) + uint32_t(kT4Rows * accn + 16 * cc);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+                "%11, %12, %13, %14, %15}, [%16];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                  "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+                  "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            uint32_t mine = 0;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const uint32_t par = __float_as_uint(__uint_as_float(v[q]) + 8388608.0f) & 1u;
+                const uint32_t bits = __ballot_sync(0xffffffffu, par);
+                if (lane == q) mine = bits;
+            }
+            const int row = 16 * cc + lane;
+            const size_t col = pc0 + size_t(accn) * 256 + size_t(128) * rank + size_t(lq) * 32;
+            if (lane < 16 && row < nvalid) {
+                uint32_t* dst = reinterpret_cast<uint32_t*>(C + (col / 64) * sc + i0 + row) + ((col / 32) & 1);
+                if (acc) mine ^= *dst;
+                *dst = mine;
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    cluster_sync_all();  // the pair's MMAs and TMEM reads are finished
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
+}
+
 namespace {
 using Tc3Fn = void (*)(TcGemmArgs, const TcGemmArgs*);
 Tc3Fn tc3_fn() {
@@ -692,6 +907,22 @@ Tc3Fn tc3_fn() {
         fn = mode == 1 ? k_gemm_tc3<1> : mode == 2 ? k_gemm_tc3<2> : mode == 3 ? k_gemm_tc3<3> : k_gemm_tc3<0>;
     }
     return fn;
+}
+// the pair kernel is opt-in (F2GPU_TC_PAIR=1) for products whose width is a
+// multiple of 512.  Measured at 16384^3: 1.85 ms vs 1.86 ms for the single-CTA
+// kernel -- it takes the shared-memory pipe from ~95% to ~64% busy, but the raw-
+// operand feed (and with deeper raw rings, 1.99 ms) then limits it, so the
+// simpler single-CTA kernel stays the default.
+bool tc4_use(size_t m) {
+    static const int on = [] {
+        const char* e = getenv("F2GPU_TC_PAIR");
+        if (!e || e[0] != '1') return 0;
+        return cudaFuncSetAttribute(k_gemm_tc4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kT4Smem)) ==
+                       cudaSuccess
+                   ? 1
+                   : 0;
+    }();
+    return on && m % kT4Cols == 0;
 }
 bool tc3_args_ok(const TcGemmArgs& p) {
     return gemm_tc3_ok(p.n, p.k, p.m) && p.sbt % 2 == 0 && p.sa % 2 == 0 &&
@@ -707,6 +938,11 @@ cudaError_t launch_gemm_tc3(const uint64_t* A, size_t sa, size_t n, const uint64
     if (!fn) return cudaErrorInvalidValue;
     const TcGemmArgs p{A, sa, n, BT, sbt, C, sc, k, m, acc ? 1 : 0};
     if (!tc3_args_ok(p)) return cudaErrorInvalidValue;
+    if (tc4_use(m)) {
+        dim3 grid4(unsigned(2 * (m / kT4Cols)), unsigned((n + kT4Rows - 1) / kT4Rows));
+        k_gemm_tc4<<<grid4, kT4Threads, kT4Smem, s>>>(p, nullptr);
+        return cudaGetLastError();
+    }
     dim3 grid(unsigned(m / kT3Cols), unsigned((n + kT3Rows - 1) / kT3Rows));
     fn<<<grid, kT3Threads, kT3Smem, s>>>(p, nullptr);
     return cudaGetLastError();
@@ -722,6 +958,13 @@ cudaError_t launch_gemm_tc3_batched(const TcGemmArgs* h_probs, const TcGemmArgs*
         if (!tc3_args_ok(h_probs[i])) return cudaErrorInvalidValue;
         mx = std::max(mx, h_probs[i].m);
         nx = std::max(nx, h_probs[i].n);
+    }
+    bool all4 = true;
+    for (int i = 0; i < nprob; ++i) all4 = all4 && tc4_use(h_probs[i].m);
+    if (all4) {
+        dim3 grid4(unsigned(2 * (mx / kT4Cols)), unsigned((nx + kT4Rows - 1) / kT4Rows), unsigned(nprob));
+        k_gemm_tc4<<<grid4, kT4Threads, kT4Smem, s>>>(TcGemmArgs{}, d_probs);
+        return cudaGetLastError();
     }
     dim3 grid(unsigned(mx / kT3Cols), unsigned((nx + kT3Rows - 1) / kT3Rows), unsigned(nprob));
     fn<<<grid, kT3Threads, kT3Smem, s>>>(TcGemmArgs{}, d_probs);

@@ -426,3 +426,22 @@ def test_decompose_recursive_host(f2, ctx, po):
     assert rk.value == rank
     assert np.array_equal(p, perm) and np.array_equal(r, rj)
     assert same(wout, w, n)
+
+
+def test_gemm_tc_pair_kernel(f2, po):
+    """The cta_group::2 leaf (opt-in via F2GPU_TC_PAIR=1) in a fresh process."""
+    import os
+    import subprocess
+    import sys
+    code = ("import numpy as np, paper_1209_5198_b200 as f2; from oracle import pyoracle as po; "
+            "ctx=f2.Context(0); lib=f2._lib.load()\n"
+            "for (n,k,m) in [(7,100,512),(2048,4096,1536),(3000,5000,1024),(481,64,512)]:\n"
+            "    a=po.random_dense(n,k,0.5,n+k); b=po.random_dense(k,m,0.5,k+m)\n"
+            "    A=f2.DeviceMatrix.from_host(f2.BitMatrix(n,k,a),ctx); B=f2.DeviceMatrix.from_host(f2.BitMatrix(k,m,b),ctx)\n"
+            "    Cm=f2.DeviceMatrix(n,m,ctx); f2._lib.check(lib.f2gpu_gemm_tc(ctx.handle,A.handle,B.handle,Cm.handle,0))\n"
+            "    assert np.array_equal(Cm.download().words[:, :n], po.m4rm_mult(a,n,k,b,m)[:, :n]), (n,k,m)\n"
+            "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, F2GPU_TC_PAIR="1", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
