@@ -168,6 +168,26 @@ def cpu_baseline(n: int, m: int, p: float, seed: int, panels: int, reps: int = 1
     }
 
 
+def gemm_cpu_baseline(n: int) -> dict:
+    """The reference's own m4rm_mult (m4rm.hpp:177-196, compiled from the reference
+    headers into oracle/_ref, OpenMP over output word-columns) on the full n^3
+    product with the same seeds, on all host cores."""
+    from oracle import pyoracle as po
+
+    threads = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
+    po.build(ref=False)
+    if not po.ref_available():
+        return {"unavailable": "oracle/_ref not built"}
+    a = po.random_dense(n, n, 0.5, 2)
+    b = po.random_dense(n, n, 0.5, 3)
+    t0 = time.perf_counter()
+    po.ref_m4rm_mult(a, n, n, b, n, tc=0)  # c = 0: the reference's cost-model table size
+    dt = time.perf_counter() - t0
+    return {"value": round(n ** 3 / dt / 1e9, 1), "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"full {n}^3 reference m4rm_mult (table size from tuning, c=0), one run, {dt:.2f} s"}
+
+
 # ---------------------------------------------------------------------------
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
@@ -329,8 +349,10 @@ def main() -> None:
                           steps=min(args.steps, 3), variant=args.variant, min_cols=args.min_cols)
 
     gemm = None
-    if args.gemm and rank == 0:
+    if args.gemm and world == 1:
         gemm = measure_gemm(f2, lib, _lib, ctx, stream, torch)
+    elif args.gemm:
+        gemm = measure_gemm_dist(f2, lib, _lib, ctx, stream, torch, rank, world, dist)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -500,6 +522,43 @@ def measure_e2e(f2, lib, _lib, ctx, torch, A, n, m, mu, world, rank, dist, steps
                     else "f2gpu_decompose_block_dist + host upload/download")}
 
 
+def measure_gemm_dist(f2, lib, _lib, ctx, stream, torch, rank, world, dist, n: int = 16384) -> dict:
+    """BASELINE configs[1] on G GPUs: B and C word-columns round-robin,
+    A broadcast from rank 0 (inside the timed region), local strassen_mult; the
+    time is the max over ranks, the value the whole job's n^3 / t."""
+    mu = n // 64
+    lw = int(lib.f2gpu_local_wcols(mu, rank, world))
+    Am = f2.DeviceMatrix(n, n, ctx)
+    if rank == 0:
+        Am.random_dense(0.5, 2)
+    Bm = f2.DeviceMatrix(n, n, ctx)
+    Bm.random_dense(0.5, 3)
+    Bl, Cl = f2.DeviceMatrix(n, 64 * lw, ctx), f2.DeviceMatrix(n, 64 * lw, ctx)
+    _lib.check(lib.f2gpu_mat_select_wcols(ctx.handle, Bl.handle, Bm.handle, rank, world, 0))
+    Bm.free()
+
+    def run():
+        _lib.check(lib.f2gpu_strassen_mult_dist(ctx.handle, Am.handle, Bl.handle, Cl.handle, 0))
+
+    for _ in range(3):
+        run()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(5):
+        run()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / 5], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    Am.free(); Bl.free(); Cl.free()
+    return {"metric": f"GF(2) multiply Gbitop/s (n^3/t), {n}^2, column-sharded over {world} GPUs "
+                      "(A broadcast + local strassen_mult, max over ranks)",
+            "ms": round(ms, 3), "Gbitop_s": round(n ** 3 / (ms * 1e-3) / 1e9, 1)}
+
+
 def measure_gemm(f2, lib, _lib, ctx, stream, torch) -> dict:
     """BASELINE configs[1]: C = A*B, A, B 16384^2 (seeds 2, 3), M4RM and Strassen-Winograd."""
     n = 16384
@@ -532,6 +591,7 @@ def measure_gemm(f2, lib, _lib, ctx, stream, torch) -> dict:
         t = e0.elapsed_time(e1) / 5 * 1e-3
         out[name] = {"ms": round(t * 1e3, 3), "Gbitop_s": round(n ** 3 / t / 1e9, 1)}
     ctx.set_tc(True)
+    out["cpu_baseline"] = gemm_cpu_baseline(n)
     return {"metric": "M4RM GEMM Gbitop/s (n^3/t), 16384^2 (BASELINE configs[1])", **out}
 
 

@@ -180,6 +180,14 @@ int f2gpu_decompose_block_dist(f2gpu_ctx *ctx, f2gpu_mat *w_local, size_t n_cols
                                uint32_t *perm, uint32_t *rj, size_t *rank);
 /* number of local word-columns rank `rank` owns out of mu */
 size_t f2gpu_local_wcols(size_t mu, int rank, int world);
+/* NCCL broadcast of a whole device matrix from `root` (no-op at world 1). */
+int f2gpu_mat_broadcast(f2gpu_ctx *ctx, f2gpu_mat *m, int root);
+/* Multiply sharded by column blocks (BASELINE configs[1] on G GPUs):
+ * rank r holds word-columns q = r, r+G, ... of B and C (f2gpu_mat_select_wcols);
+ * A is broadcast from rank 0 into every rank's `a`, then c_local = a * b_local
+ * (strassen_mult semantics; threshold 0 = default).  No per-step exchange. */
+int f2gpu_strassen_mult_dist(f2gpu_ctx *ctx, f2gpu_mat *a, const f2gpu_mat *b_local, f2gpu_mat *c_local,
+                             size_t threshold);
 
 #ifdef __cplusplus
 }

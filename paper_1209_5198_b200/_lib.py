@@ -38,7 +38,7 @@ SYMBOLS = [
     "f2gpu_decompose_recursive_host",
     "f2gpu_rank_host",
     "f2gpu_nccl_unique_id", "f2gpu_ctx_init_comm", "f2gpu_decompose_block_dist",
-    "f2gpu_local_wcols",
+    "f2gpu_local_wcols", "f2gpu_mat_broadcast", "f2gpu_strassen_mult_dist",
 ]
 
 sz = C.c_size_t
@@ -87,6 +87,8 @@ _SIG = {
     "f2gpu_ctx_init_comm": ([vp, C.c_int, C.c_int, vp], C.c_int),
     "f2gpu_decompose_block_dist": ([vp, vp, sz, vp, vp, C.POINTER(sz)], C.c_int),
     "f2gpu_local_wcols": ([sz, C.c_int, C.c_int], sz),
+    "f2gpu_mat_broadcast": ([vp, vp, C.c_int], C.c_int),
+    "f2gpu_strassen_mult_dist": ([vp, vp, vp, vp, sz], C.c_int),
 }
 
 _lib = None

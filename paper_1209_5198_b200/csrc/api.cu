@@ -1476,6 +1476,30 @@ int f2gpu_ctx_init_comm(f2gpu_ctx* c, int rank, int world, const void* id) {
     return F2GPU_OK;
 }
 
+int f2gpu_mat_broadcast(f2gpu_ctx* c, f2gpu_mat* m, int root) {
+    if (!c || !m) return set_err(F2GPU_EINVAL, "null argument");
+    if (root < 0 || root >= c->world) return set_err(F2GPU_ERANGE, "broadcast: root rank");
+    if (c->world == 1 && !c->comm) return F2GPU_OK;
+    if (!c->comm) return set_err(F2GPU_ENCCL, "broadcast: communicator not initialised");
+    NcclApi& api = nccl();
+    const size_t bytes = ceil64(m->cols) * m->stride * 8;
+    if (bytes == 0) return F2GPU_OK;
+    int rc = api.broadcast(m->d, m->d, bytes, kNcclUint8, root, c->comm, c->stream);
+    if (rc != 0)
+        return set_err(F2GPU_ENCCL, std::string("ncclBroadcast: ") + (api.getErrorString ? api.getErrorString(rc) : "?"));
+    return F2GPU_OK;
+}
+
+// Multiply sharded by column blocks: B and C word-columns are
+// round-robin over the ranks, A is replicated by one broadcast from rank 0, and
+// every rank computes its own C columns -- no per-step exchange.
+int f2gpu_strassen_mult_dist(f2gpu_ctx* c, f2gpu_mat* a, const f2gpu_mat* b_local, f2gpu_mat* c_local,
+                             size_t threshold) {
+    if (!c || !a || !b_local || !c_local) return set_err(F2GPU_EINVAL, "null argument");
+    F2_TRY(f2gpu_mat_broadcast(c, a, 0));
+    return f2gpu_strassen_mult(c, a, b_local, c_local, threshold);
+}
+
 int f2gpu_decompose_block_dist(f2gpu_ctx* c, f2gpu_mat* w_local, size_t m_global, uint32_t* perm,
                                uint32_t* rj, size_t* rank) {
     if (!c || !w_local) return set_err(F2GPU_EINVAL, "null argument");

@@ -143,3 +143,45 @@ def test_local_column_bookkeeping():
                 for j in range(mu):
                     l0 = first_local_after(j, g, G)
                     assert [q for q in owned if q > j] == owned[l0:]
+
+
+def mult_worker(rank, world, port, n, k, m, q):
+    """Rank r owns word-columns q = r, r+G, ... of B and C; A comes from rank 0 by
+    one broadcast (f2gpu_strassen_mult_dist's exchange), then C_local = A * B_local."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import pyoracle as po
+    a = po.random_dense(n, k, 0.5, 21) if rank == 0 else np.zeros((po.wcols(k), po.stride_for(n)), np.uint64)
+    t = torch.from_numpy(a.view(np.int64))
+    dist.broadcast(t, src=0)
+    a = t.numpy().view(np.uint64)
+    b = po.random_dense(k, m, 0.5, 22)          # every rank can generate B; it keeps its columns only
+    mine = list(range(rank, po.wcols(m), world))
+    b_local = np.ascontiguousarray(b[mine])
+    c_local = po.m4rm_mult(a, n, k, b_local, 64 * len(mine)) if mine else np.zeros((0, 1), np.uint64)
+    q.put((rank, mine, c_local))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,k,m", [(300, 200, 640), (130, 700, 130)])
+def test_sharded_multiply_protocol(po, n, k, m):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=mult_worker, args=(r, world, port, n, k, m, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    want = po.m4rm_mult(po.random_dense(n, k, 0.5, 21), n, k, po.random_dense(k, m, 0.5, 22), m)
+    seen = set()
+    for _, mine, c_local in res:
+        for l, qcol in enumerate(mine):
+            # the last word-column's padding bits past m are zero in both
+            assert np.array_equal(c_local[l, :n], want[qcol, :n]), qcol
+            seen.add(qcol)
+    assert seen == set(range(po.wcols(m)))

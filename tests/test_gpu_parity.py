@@ -445,3 +445,25 @@ def test_gemm_tc_pair_kernel(f2, po):
     env = dict(os.environ, F2GPU_TC_PAIR="1", PYTHONPATH=root)
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_strassen_mult_dist_shards(f2, ctx, po, G):
+    """The column-sharded multiply at world 1 (broadcast = no-op), G shards emulated
+    with f2gpu_mat_select_wcols: every shard's C columns equal the global product."""
+    lib = f2._lib.load()
+    n, k, m = 1500, 1200, 64 * 40
+    a = po.random_dense(n, k, 0.5, 31)
+    b = po.random_dense(k, m, 0.5, 32)
+    want = po.m4rm_mult(a, n, k, b, m)
+    A = f2.DeviceMatrix.from_host(f2.BitMatrix(n, k, a), ctx)
+    B = f2.DeviceMatrix.from_host(f2.BitMatrix(k, m, b), ctx)
+    C = f2.DeviceMatrix(n, m, ctx)
+    mu = m // 64
+    for g in range(G):
+        lw = int(lib.f2gpu_local_wcols(mu, g, G))
+        Bl, Cl = f2.DeviceMatrix(k, 64 * lw, ctx), f2.DeviceMatrix(n, 64 * lw, ctx)
+        f2._lib.check(lib.f2gpu_mat_select_wcols(ctx.handle, Bl.handle, B.handle, g, G, 0))
+        f2._lib.check(lib.f2gpu_strassen_mult_dist(ctx.handle, A.handle, Bl.handle, Cl.handle, 0))
+        f2._lib.check(lib.f2gpu_mat_select_wcols(ctx.handle, C.handle, Cl.handle, g, G, 1))
+    assert same(C.download().words, want, n)
