@@ -166,6 +166,17 @@ int f2gpu_decompose_recursive_host(f2gpu_ctx *ctx, const uint64_t *a, size_t n, 
 int f2gpu_rank_host(f2gpu_ctx *ctx, const uint64_t *a, size_t n, size_t m, size_t stride,
                     size_t *rank);
 
+/* ---- null space and linear systems ------
+ * Partial block decomposition of [A^T | I]: the A^T panels are eliminated exactly
+ * as decompose_block does, the identity part records the row operations.
+ * null_space: *basis = new m x (m - rank) matrix, A * N = 0, columns independent
+ *             (free with f2gpu_mat_free); *nullity = m - rank.
+ * solve:      rhs = ceil(n/64) host words (bit i = b_i); on *solvable = 1, x =
+ *             ceil(m/64) host words with A x = b; *solvable = 0 signals an
+ *             inconsistent system (not an error). */
+int f2gpu_null_space(f2gpu_ctx *ctx, const f2gpu_mat *a, f2gpu_mat **basis, size_t *nullity);
+int f2gpu_solve(f2gpu_ctx *ctx, const f2gpu_mat *a, const uint64_t *rhs, uint64_t *x, int *solvable);
+
 /* ---- multi-GPU (one process per GPU, NCCL over NVLink) ---------------------- */
 /* 128-byte ncclUniqueId, produced on rank 0 and shared by the caller (e.g. via
  * torch.distributed); NCCL is loaded at run time (dlopen libnccl.so.2). */

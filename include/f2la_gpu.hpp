@@ -8,6 +8,7 @@
 //   decompose_block(A)->LUFactors  SPEC.md:319-327    f2la::gpu::decompose_block(A)
 //   rank(A)                        SPEC.md:346-353    f2la::gpu::rank(A)
 //   decompose_recursive(A, mc)     SPEC.md:328-345    f2la::gpu::decompose_recursive(A, mc)
+//   null_space(A), solve(A, rhs)   SPEC.md:354-362    f2la::gpu::null_space(A), f2la::gpu::solve(A, rhs)
 //
 // Matrices are passed in the reference layout (PackedMatrix<uint64_t>:
 // col_block(q) + col_stride(), bit_matrix.hpp:74-81).  Errors are rethrown as
@@ -17,6 +18,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -161,6 +163,56 @@ std::size_t rank(const Matrix& a) {
         check(f2gpu_rank_host(context(), a.col_block(0), a.rows(), a.cols(), a.col_stride(), &r),
               "rank");
     return r;
+}
+
+namespace detail {
+template <class Matrix>
+f2gpu_mat* upload(const Matrix& a) {
+    f2gpu_mat* d = nullptr;
+    check(f2gpu_mat_alloc(context(), a.rows(), a.cols(), &d), "mat_alloc");
+    if (a.rows() && a.cols()) {
+        const int rc = f2gpu_mat_upload(context(), d, a.col_block(0), a.col_stride());
+        if (rc != F2GPU_OK) {
+            f2gpu_mat_free(d);
+            check(rc, "mat_upload");
+        }
+    }
+    return d;
+}
+struct MatFree {
+    f2gpu_mat* m;
+    ~MatFree() { f2gpu_mat_free(m); }
+};
+}  // namespace detail
+
+/// m x (m - rank) basis N with A*N = 0 and independent columns.
+template <class Matrix>
+Matrix null_space(const Matrix& a) {
+    detail::MatFree A{detail::upload(a)};
+    f2gpu_mat* n = nullptr;
+    std::size_t nul = 0;
+    check(f2gpu_null_space(context(), A.m, &n, &nul), "null_space");
+    detail::MatFree N{n};
+    Matrix out(a.cols(), nul);
+    if (a.cols() && nul) check(f2gpu_mat_download(context(), n, out.col_block(0), out.col_stride()), "download");
+    return out;
+}
+
+/// x with A x = rhs over F2 (one bit per element), or nullopt for an inconsistent
+/// system -- signalled, not an error.
+template <class Matrix>
+std::optional<std::vector<std::uint8_t>> solve(const Matrix& a, const std::vector<std::uint8_t>& rhs) {
+    if (rhs.size() != a.rows()) throw std::invalid_argument("solve: rhs length must equal rows");
+    detail::MatFree A{detail::upload(a)};
+    std::vector<std::uint64_t> b((a.rows() + 63) / 64 + 1, 0), x((a.cols() + 63) / 64 + 1, 0);
+    for (std::size_t i = 0; i < rhs.size(); ++i)
+        if (rhs[i] & 1) b[i / 64] |= std::uint64_t(1) << (i % 64);
+    int ok = 0;
+    check(f2gpu_solve(context(), A.m, b.data(), x.data(), &ok), "solve");
+    if (!ok) return std::nullopt;
+    std::vector<std::uint8_t> out(a.cols());
+    for (std::size_t j = 0; j < out.size(); ++j) out[j] = std::uint8_t((x[j / 64] >> (j % 64)) & 1);
+    return out;
 }
 
 }  // namespace f2la::gpu

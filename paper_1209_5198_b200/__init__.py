@@ -29,8 +29,7 @@ __all__ = [
     "BitMatrix", "RowPermutation", "LUFactors", "Context", "DeviceMatrix", "M4rmTables",
     "m4rm_mult", "strassen_mult", "build_tables", "mult_acc", "decompose_block",
     "decompose_recursive", "rank",
-    "make_splits", "tuning", "F2GpuError", "default_context",
-]
+    "make_splits", "tuning", "F2GpuError", "default_context", "null_space", "solve"]
 
 
 def _ptr(a: np.ndarray) -> C.c_void_p:
@@ -297,6 +296,16 @@ class DeviceMatrix:
         return self._h
 
     @classmethod
+    def _adopt(cls, h: C.c_void_p, ctx: Context) -> "DeviceMatrix":
+        """Wrap a matrix handle the library allocated (e.g. f2gpu_null_space's basis)."""
+        d = cls.__new__(cls)
+        d.ctx, d._h = ctx, h
+        r, c, st = C.c_size_t(), C.c_size_t(), C.c_size_t()
+        _lib.load().f2gpu_mat_shape(h, C.byref(r), C.byref(c), C.byref(st))
+        d.n, d.m, d.stride = int(r.value), int(c.value), int(st.value)
+        return d
+
+    @classmethod
     def from_host(cls, a: BitMatrix, ctx: Context | None = None) -> "DeviceMatrix":
         d = cls(a.rows(), a.cols(), ctx)
         d.upload(a)
@@ -481,6 +490,48 @@ def decompose_recursive(a, min_cols: int = 0, ctx: Context | None = None) -> LUF
     W = w.download()
     return LUFactors(RowPermutation(perm[:n].copy()), W, int(rank_.value),
                      rj[: (m + 63) // 64].copy())
+
+
+def _pack_bits(bits, n: int) -> np.ndarray:
+    v = np.zeros(max(1, (n + 63) // 64), np.uint64)
+    b = np.asarray(bits, dtype=np.uint8).reshape(-1)[:n]
+    for i in np.nonzero(b)[0]:
+        v[i // 64] |= np.uint64(1) << np.uint64(i % 64)
+    return v
+
+
+def _unpack_bits(words: np.ndarray, n: int) -> np.ndarray:
+    idx = np.arange(n)
+    return ((words[idx // 64] >> (idx % 64).astype(np.uint64)) & np.uint64(1)).astype(np.uint8)
+
+
+def null_space(a, ctx: Context | None = None) -> BitMatrix:
+    """m x (m - rank) basis N with A*N = 0, computed on the device by a
+    partial block decomposition of [A^T | I]."""
+    ctx = ctx or (a.ctx if isinstance(a, DeviceMatrix) else default_context())
+    d = _as_dev(a, ctx)
+    h, nul = C.c_void_p(), C.c_size_t()
+    _lib.check(_lib.load().f2gpu_null_space(ctx.handle, d.handle, C.byref(h), C.byref(nul)), "null_space")
+    N = DeviceMatrix._adopt(h, ctx)
+    try:
+        return N.download()
+    finally:
+        N.free()
+
+
+def solve(a, rhs, ctx: Context | None = None) -> np.ndarray | None:
+    """x (m bits, uint8) with A x = rhs over F2, or None when the system is inconsistent
+    (signalled, not an error)."""
+    ctx = ctx or (a.ctx if isinstance(a, DeviceMatrix) else default_context())
+    d = _as_dev(a, ctx)
+    n, m = d.n, d.m
+    if len(np.asarray(rhs).reshape(-1)) != n:
+        raise ValueError("solve: rhs length must equal the number of rows")
+    b = _pack_bits(rhs, n)
+    x = np.zeros(max(1, (m + 63) // 64), np.uint64)
+    ok = C.c_int()
+    _lib.check(_lib.load().f2gpu_solve(ctx.handle, d.handle, _ptr(b), _ptr(x), C.byref(ok)), "solve")
+    return _unpack_bits(x, m) if ok.value else None
 
 
 def rank(a, ctx: Context | None = None) -> int:

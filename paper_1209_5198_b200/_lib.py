@@ -35,7 +35,7 @@ SYMBOLS = [
     "f2gpu_decompose_block", "f2gpu_decompose_recursive", "f2gpu_decompose_block_sharded",
     "f2gpu_rank",
     "f2gpu_m4rm_mult_host", "f2gpu_strassen_mult_host", "f2gpu_decompose_block_host",
-    "f2gpu_decompose_recursive_host",
+    "f2gpu_decompose_recursive_host", "f2gpu_null_space", "f2gpu_solve",
     "f2gpu_rank_host",
     "f2gpu_nccl_unique_id", "f2gpu_ctx_init_comm", "f2gpu_decompose_block_dist",
     "f2gpu_local_wcols", "f2gpu_mat_broadcast", "f2gpu_strassen_mult_dist",
@@ -83,6 +83,8 @@ _SIG = {
     "f2gpu_decompose_block_host": ([vp, vp, sz, sz, sz, vp, vp, vp, C.POINTER(sz)], C.c_int),
     "f2gpu_decompose_recursive_host": ([vp, vp, sz, sz, sz, sz, vp, vp, vp, C.POINTER(sz)], C.c_int),
     "f2gpu_rank_host": ([vp, vp, sz, sz, sz, C.POINTER(sz)], C.c_int),
+    "f2gpu_null_space": ([vp, vp, C.POINTER(vp), C.POINTER(sz)], C.c_int),
+    "f2gpu_solve": ([vp, vp, vp, vp, C.POINTER(C.c_int)], C.c_int),
     "f2gpu_nccl_unique_id": ([vp], C.c_int),
     "f2gpu_ctx_init_comm": ([vp, C.c_int, C.c_int, vp], C.c_int),
     "f2gpu_decompose_block_dist": ([vp, vp, sz, vp, vp, C.POINTER(sz)], C.c_int),

@@ -1362,6 +1362,97 @@ int f2gpu_rank(f2gpu_ctx* c, const f2gpu_mat* a, size_t* rank) {
     return decompose_single(c, view_of(t), nullptr, nullptr, rank);
 }
 
+// ---- null space / solve ---------------------------------
+// Both are a PARTIAL block decomposition of an augmented matrix: the P panels of
+// its left part are factored exactly as in decompose_block (buildZ, swaps on
+// every word-column, Schur updates on every trailing word-column), the identity
+// on the right records the row operations.  Non-pivot rows end with a zero left
+// part, so their identity parts span the left null space of the left part.
+//   null_space(A): left part A^T (m rows)        -> those rows, transposed, are N
+//   solve(A, b):   left part [A^T; b^T] (m+1 rows) -> a null vector c with c_m = 1
+//                                                    gives A * c[0..m) = b
+namespace {
+int partial_eliminate(f2gpu_ctx* c, f2gpu_mat* w, size_t panels, size_t* rank) {
+    const size_t n = w->rows, mu = ceil64(w->cols);
+    F2_TRY(ensure_scratch(c, n, mu));
+    Shard s;
+    s.w = view_of(w); s.lw = mu; s.st = static_cast<f2::PanelState*>(c->scr_st); s.perm = c->scr_perm;
+    F2_TRY(check_launch(c, f2::launch_iota(s.perm, n, c->stream), "k_iota"));
+    for (size_t j = 0; j < panels; ++j) F2_TRY(step_single(c, s, n, mu, j));
+    return read_results(c, s, n, panels, nullptr, nullptr, rank);
+}
+
+// W (rows x (P + ceil64(rows)) word-cols): A^T in word-cols [0, P), I_rows after
+int build_augmented(f2gpu_ctx* c, const f2gpu_mat* a, size_t rows, size_t P, f2gpu_mat** out) {
+    F2_TRY(f2gpu_mat_alloc(c, rows, (P + ceil64(rows)) * 64, out));
+    F2_TRY(f2gpu_mat_zero(c, *out));
+    if (a->rows && a->cols)
+        F2_TRY(check_launch(c, f2::launch_transpose(a->d, a->rows, a->cols, a->stride, (*out)->d, (*out)->stride,
+                                                    c->stream),
+                            "k_transpose"));
+    return check_launch(c, f2::launch_set_diag((*out)->d, (*out)->stride, rows, P, c->stream), "k_set_diag");
+}
+}  // namespace
+
+int f2gpu_null_space(f2gpu_ctx* c, const f2gpu_mat* a, f2gpu_mat** basis, size_t* nullity) {
+    if (!c || !a || !basis) return set_err(F2GPU_EINVAL, "null argument");
+    *basis = nullptr;
+    const size_t n = a->rows, m = a->cols, P = ceil64(n);
+    if (m > 0xFFFFFFF0ull) return set_err(F2GPU_ERANGE, "null_space: too many columns");
+    f2gpu_mat* W = nullptr;
+    F2_TRY(build_augmented(c, a, m, P, &W));
+    std::unique_ptr<f2gpu_mat, int (*)(f2gpu_mat*)> guard(W, f2gpu_mat_free);
+    size_t r = 0;
+    if (m) F2_TRY(partial_eliminate(c, W, P, &r));
+    const size_t nul = m - r;
+    F2_TRY(f2gpu_mat_alloc(c, m, nul, basis));
+    if (nul)
+        F2_TRY(check_launch(c, f2::launch_transpose(W->d + P * W->stride + r, nul, m, W->stride, (*basis)->d,
+                                                    (*basis)->stride, c->stream),
+                            "k_transpose"));
+    if (nullity) *nullity = nul;
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return F2GPU_OK;
+}
+
+int f2gpu_solve(f2gpu_ctx* c, const f2gpu_mat* a, const uint64_t* rhs, uint64_t* x, int* solvable) {
+    if (!c || !a || !solvable || (!rhs && a->rows) || (!x && a->cols)) return set_err(F2GPU_EINVAL, "null argument");
+    const size_t n = a->rows, m = a->cols, P = ceil64(n), m1 = m + 1;
+    if (m1 > 0xFFFFFFF0ull) return set_err(F2GPU_ERANGE, "solve: too many columns");
+    f2gpu_mat* W = nullptr;
+    F2_TRY(build_augmented(c, a, m1, P, &W));  // row m of the A^T part stays 0 ...
+    std::unique_ptr<f2gpu_mat, int (*)(f2gpu_mat*)> guard(W, f2gpu_mat_free);
+    if (P) {  // ... and receives b^T (bits past n cleared)
+        std::vector<uint64_t> b(rhs, rhs + P);
+        if (n % 64) b[P - 1] &= (uint64_t(1) << (n % 64)) - 1;
+        CUDA_TRY(cudaMemcpy2DAsync(W->d + m, W->stride * 8, b.data(), 8, 8, P, cudaMemcpyHostToDevice, c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));  // b is a local
+    }
+    size_t r = 0;
+    F2_TRY(partial_eliminate(c, W, P, &r));
+    *solvable = 0;
+    const size_t mw = ceil64(m);
+    if (x) std::fill(x, x + mw, 0ull);
+    if (r >= m1) return F2GPU_OK;  // only the trivial combination: b not in the column space
+    // the c_m bits of the null rows r .. m
+    std::vector<uint64_t> tag(m1 - r);
+    CUDA_TRY(cudaMemcpyAsync(tag.data(), W->d + (P + m / 64) * W->stride + r, tag.size() * 8, cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    for (size_t i = 0; i < tag.size(); ++i) {
+        if (!((tag[i] >> (m % 64)) & 1)) continue;
+        std::vector<uint64_t> row(ceil64(m1));
+        CUDA_TRY(cudaMemcpy2DAsync(row.data(), 8, W->d + P * W->stride + r + i, W->stride * 8, 8, row.size(),
+                                   cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        for (size_t q = 0; q < mw; ++q) x[q] = row[q];
+        if (m % 64) x[mw - 1] &= (uint64_t(1) << (m % 64)) - 1;  // drop c_m (and padding)
+        *solvable = 1;
+        break;
+    }
+    return F2GPU_OK;
+}
+
 // ---- host-buffer entry points ----
 namespace {
 struct MatGuard {

@@ -1772,6 +1772,17 @@ cudaError_t launch_transpose(const uint64_t* a, size_t n, size_t m, size_t sa, u
     return cudaGetLastError();
 }
 
+// identity block: bit (i, 64*wcol0 + i) = 1 for i < rows (the matrix is zeroed)
+__global__ void k_set_diag(uint64_t* w, size_t stride, size_t rows, size_t wcol0) {
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < rows; i += size_t(gridDim.x) * blockDim.x)
+        w[(wcol0 + i / 64) * stride + i] |= uint64_t(1) << (i % 64);
+}
+cudaError_t launch_set_diag(uint64_t* w, size_t stride, size_t rows, size_t wcol0, cudaStream_t s) {
+    if (rows == 0) return cudaSuccess;
+    k_set_diag<<<256, 256, 0, s>>>(w, stride, rows, wcol0);
+    return cudaGetLastError();
+}
+
 __global__ void k_iota(uint32_t* p, size_t n) {
     for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += size_t(gridDim.x) * blockDim.x)

@@ -29,7 +29,23 @@ int main() {
     const bool rank_ok = f2la::gpu::rank(a) == f.rank && f.rank == 777;
     const auto g = f2la::gpu::decompose_recursive(a, 128);
     const bool rec_ok = g.P == f.P && g.overlay == f.overlay && g.L == f.L && g.U == f.U;
-    std::printf("mult %d  plu %d  rank %d (%zu)  recursive %d\n", mult_ok, lu_ok, rank_ok, f.rank,
-                rec_ok);
-    return (mult_ok && lu_ok && rank_ok && rec_ok) ? 0 : 1;
+    // null space of a rank-deficient product, checked with the reference's own product
+    const BitMatrix x = BitMatrix::random_dense(300, 90, 0.5, 3), y = BitMatrix::random_dense(90, 500, 0.5, 4);
+    const BitMatrix xy = f2la::m4rm_mult(x, y, 8);
+    const BitMatrix ns = f2la::gpu::null_space(xy);
+    const bool ns_ok = ns.cols() == 500 - f2la::gpu::rank(xy) && f2la::m4rm_mult(xy, ns, 8) == BitMatrix(300, ns.cols());
+    // solve a consistent system b = A * e_0 (column 0 of A)
+    std::vector<std::uint8_t> rhs(a.rows());
+    for (std::size_t i = 0; i < a.rows(); ++i) rhs[i] = std::uint8_t(a.get(i, 0));
+    const auto sol = f2la::gpu::solve(a, rhs);
+    bool solve_ok = sol.has_value();
+    if (solve_ok) {
+        BitMatrix xv(a.cols(), 1);
+        for (std::size_t j = 0; j < a.cols(); ++j) xv.set(j, 0, (*sol)[j]);
+        const BitMatrix ax = f2la::m4rm_mult(a, xv, 8);
+        for (std::size_t i = 0; i < a.rows(); ++i) solve_ok = solve_ok && ax.get(i, 0) == bool(rhs[i]);
+    }
+    std::printf("mult %d  plu %d  rank %d (%zu)  recursive %d  null_space %d  solve %d\n", mult_ok, lu_ok,
+                rank_ok, f.rank, rec_ok, ns_ok, solve_ok);
+    return (mult_ok && lu_ok && rank_ok && rec_ok && ns_ok && solve_ok) ? 0 : 1;
 }

@@ -467,3 +467,62 @@ def test_strassen_mult_dist_shards(f2, ctx, po, G):
         f2._lib.check(lib.f2gpu_strassen_mult_dist(ctx.handle, A.handle, Bl.handle, Cl.handle, 0))
         f2._lib.check(lib.f2gpu_mat_select_wcols(ctx.handle, C.handle, Cl.handle, g, G, 1))
     assert same(C.download().words, want, n)
+
+
+# ---------------------------------------------------------------------------
+# null space / solve: properties against the oracle
+# ---------------------------------------------------------------------------
+def _xy(po, n, k, m, seed):
+    x, y = po.random_dense(n, k, 0.5, seed), po.random_dense(k, m, 0.5, seed + 1)
+    return po.m4rm_mult(x, n, k, y, m)
+
+
+NS_CASES = [("dense", 300, 300), ("dense", 100, 700), ("dense", 700, 100), ("xy", 500, 640), ("xy", 640, 500),
+            ("zero", 70, 130), ("ident", 128, 128), ("dense", 1, 1), ("dense", 1, 65), ("xy", 2000, 3000)]
+
+
+@pytest.mark.parametrize("kind,n,m", NS_CASES)
+def test_null_space(f2, ctx, po, kind, n, m):
+    if kind == "dense":
+        a = po.random_dense(n, m, 0.5, n + 3 * m)
+    elif kind == "xy":
+        a = _xy(po, n, min(n, m) // 3, m, n + m)
+    elif kind == "zero":
+        a = po.zeros(n, m)
+    else:
+        a = po.from_dense(np.eye(n, dtype=np.uint8))
+    r = po.rank_ge(a, n, m)
+    N = f2.null_space(f2.BitMatrix(n, m, a), ctx=ctx)
+    assert N.rows() == m and N.cols() == m - r
+    if N.cols():
+        assert not po.m4rm_mult(a, n, m, N.words, N.cols())[:, :n].any()   # A * N = 0
+        assert po.rank_ge(N.words, m, N.cols()) == N.cols()                 # independent columns
+
+
+def _matvec(po, a, n, m, x):
+    xm = po.zeros(m, 1)
+    xm[0, :m] = x.astype(np.uint64)
+    return (po.m4rm_mult(a, n, m, xm, 1)[0, :n] & np.uint64(1)).astype(np.uint8)
+
+
+@pytest.mark.parametrize("kind,n,m", [("dense", 300, 300), ("dense", 200, 500), ("xy", 400, 300),
+                                      ("xy", 300, 700), ("dense", 700, 100)])
+def test_solve(f2, ctx, po, kind, n, m):
+    a = po.random_dense(n, m, 0.5, 5 * n + m) if kind == "dense" else _xy(po, n, min(n, m) // 4, m, n)
+    A = f2.BitMatrix(n, m, a)
+    rng = np.random.default_rng(n * m)
+    # consistent: b = A x0
+    x0 = rng.integers(0, 2, m, dtype=np.uint8)
+    b = _matvec(po, a, n, m, x0)
+    x = f2.solve(A, b, ctx=ctx)
+    assert x is not None and np.array_equal(_matvec(po, a, n, m, x), b)
+    # random rhs: solvable exactly when rank([A | b]) == rank(A)
+    b2 = rng.integers(0, 2, n, dtype=np.uint8)
+    ab = po.zeros(n, m + 1)
+    ab[: (m + 63) // 64, : a.shape[1]] = a
+    ab[m // 64, :n] |= b2.astype(np.uint64) << np.uint64(m % 64)
+    consistent = po.rank_ge(ab, n, m + 1) == po.rank_ge(a, n, m)
+    x2 = f2.solve(A, b2, ctx=ctx)
+    assert (x2 is not None) == consistent
+    if x2 is not None:
+        assert np.array_equal(_matvec(po, a, n, m, x2), b2)
