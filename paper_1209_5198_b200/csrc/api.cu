@@ -12,7 +12,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <map>
 #include <memory>
+#include <array>
 #include <string>
 #include <vector>
 
@@ -157,11 +159,27 @@ struct GraphCache {
     }
 };
 
+// decompose_recursive: one captured graph per leaf (matrix, shape, column range)
+struct LeafGraph {
+    int seen = 0;
+    cudaGraphExec_t exec = nullptr;
+    uint64_t nodes = 0;
+};
+struct LeafGraphs {
+    std::map<std::array<uintptr_t, 7>, LeafGraph> m;
+    void clear() {
+        for (auto& kv : m)
+            if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+        m.clear();
+    }
+};
+
 struct f2gpu_mat;
 struct f2gpu_ctx {
     Timeline tl;
     f2gpu_mat* stage = nullptr;           // reusable device matrix for host-buffer calls
     GraphCache graph;
+    LeafGraphs leaf_graphs;
     bool use_graphs = true;
     bool lookahead = true;
     cudaStream_t side = nullptr;          // lookahead: panel kernels run here
@@ -596,6 +614,7 @@ int ensure_scratch(f2gpu_ctx* c, size_t n, size_t mu) {
     if (c->scr_st_cap < mu || c->scr_perm_cap < n || c->scr_flags_cap < mu) {
         CUDA_TRY(cudaStreamSynchronize(c->stream));
         c->graph.reset();  // graphs hold the old pointers
+        c->leaf_graphs.clear();
         if (c->scr_st_cap < mu) {
             cudaFree(c->scr_st);
             c->scr_st = nullptr;
@@ -763,8 +782,44 @@ int rec_trsm(RecRun& r, size_t a, size_t b, size_t Ra, size_t col0, size_t col1)
     return rec_trsm(r, m, b, Rm, col0, col1);
 }
 
+// a leaf: the block algorithm (with lookahead) on panels [c0, c1), replayed from
+// a CUDA graph from the second call with the same matrix, shape and range
+int rec_leaf(RecRun& r, size_t c0, size_t c1) {
+    f2gpu_ctx* c = r.c;
+    Shard& s = *r.s;
+    if (!c->use_graphs || c->tl.on) return enqueue_panels(c, s, r.n, r.mu, c0, c1, r.la);
+    const std::array<uintptr_t, 7> key{uintptr_t(s.w.p), s.w.stride, r.n, r.mu, c0, c1,
+                                       uintptr_t(s.st) ^ (r.la ? 1u : 0u)};
+    LeafGraph& g = c->leaf_graphs.m[key];
+    if (g.exec) {
+        CUDA_TRY(cudaGraphLaunch(g.exec, c->stream));
+        c->launches += g.nodes;
+        return F2GPU_OK;
+    }
+    if (g.seen < 1) {
+        g.seen += 1;
+        return enqueue_panels(c, s, r.n, r.mu, c0, c1, r.la);
+    }
+    cudaGraph_t graph = nullptr;
+    const uint64_t l0 = c->launches;
+    CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    int rc = enqueue_panels(c, s, r.n, r.mu, c0, c1, r.la);
+    cudaError_t ec = cudaStreamEndCapture(c->stream, &graph);
+    if (rc != F2GPU_OK) { if (graph) cudaGraphDestroy(graph); return rc; }
+    if (ec != cudaSuccess) return set_err(F2GPU_ECUDA, std::string("leaf graph capture: ") + cudaGetErrorString(ec));
+    cudaError_t ei = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) {
+        g.exec = nullptr;
+        return set_err(F2GPU_ECUDA, std::string("leaf graph instantiate: ") + cudaGetErrorString(ei));
+    }
+    g.nodes = c->launches - l0;
+    CUDA_TRY(cudaGraphLaunch(g.exec, c->stream));
+    return F2GPU_OK;
+}
+
 int rec_decompose(RecRun& r, size_t c0, size_t c1) {
-    if (c1 - c0 <= r.base) return enqueue_panels(r.c, *r.s, r.n, r.mu, c0, c1, r.la);
+    if (c1 - c0 <= r.base) return rec_leaf(r, c0, c1);
     const size_t cm = c0 + (c1 - c0) / 2;
     F2_TRY(rec_decompose(r, c0, cm));
     size_t R0, r0, Rl, rl;
@@ -1022,6 +1077,7 @@ int f2gpu_ctx_destroy(f2gpu_ctx* c) {
     if (c->comm && nccl().ok) nccl().commDestroy(c->comm);
     if (c->own_stream) cudaStreamSynchronize(c->own_stream);
     c->graph.reset();
+    c->leaf_graphs.clear();
     if (c->stage) { f2gpu_mat_free(c->stage); c->stage = nullptr; }
     cudaFree(c->scr_st);
     cudaFree(c->scr_perm);
