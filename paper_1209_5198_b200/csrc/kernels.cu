@@ -1279,82 +1279,128 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
     uint32_t ib = 0;         // next pivot slot (relative row)
     uint32_t n_ext = 0;      // beyond-window rows touched (lane 0 bookkeeping, uniform count)
     uint32_t max_touch = 0;  // highest window slot touched
+    // Fast path: lane L holds candidate slot ib + L in registers (cv, co) and the
+    // window advances by one shuffle per selection instead of a shared-memory
+    // round trip; shared memory stays authoritative (the swaps are stored) and
+    // the search below is the slow path (pivot outside the 32 candidates, window
+    // exhausted).  Measured 20.5 -> 19.5 us per panel; the remaining ~17 us are
+    // the 64-step chain at ~180 instructions per step in one warp.
+    uint64_t cv = 0;
+    uint32_t co = 0;
+    bool regwin = false;
+    auto load_regwin = [&]() {
+        regwin = ib + 33u <= winrows;  // the slot entering after a selection must be in the window
+        if (regwin) {
+            cv = S.win[ib + lane];
+            co = S.orig[ib + lane];
+        }
+    };
+    load_regwin();
     for (int k = 0; k < 64; ++k) {
         const uint64_t lowk = low_mask64(k);
         const uint64_t mtk = __shfl_sync(0xffffffffu, k < 32 ? mlo : mhi, k & 31);
         const uint64_t c = (1ull << k) | (mtk & lowk);
-        // ---- pivot search: first row i >= ib with odd popcount(c & A_i) ----
         uint32_t found = kNone;
         uint64_t newrow = 0;
-        {
-            const uint32_t i = ib + lane;
-            uint64_t v = 0;
-            uint32_t o = 0;
-            if (i < winrows) { v = S.win[i]; o = S.orig[i]; }
-            else if (i < rows) { v = A[i]; }
-            const uint32_t bal = __ballot_sync(0xffffffffu, i < rows && (__popcll(c & v) & 1));
+        bool fast = false;
+        if (regwin) {
+            uint64_t pv = 0;
+            uint32_t po = 0;
+            if (lane == 31) {  // the slot entering the window after a selection
+                pv = S.win[ib + 32];
+                po = S.orig[ib + 32];
+            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, __popcll(c & cv) & 1);
             if (bal) {
+                fast = true;
                 const int f = __ffs(bal) - 1;
-                found = ib + f;
-                newrow = __shfl_sync(0xffffffffu, v, f);
-                if (found < winrows) {  // fast path: both slots are in the window
-                    const uint64_t vb = __shfl_sync(0xffffffffu, v, 0);
-                    const uint32_t of = __shfl_sync(0xffffffffu, o, f);
-                    const uint32_t ob = __shfl_sync(0xffffffffu, o, 0);
-                    if (lane == 0) { S.win[ib] = newrow; S.orig[ib] = of; }
-                    if (lane == f && f != 0) { S.win[found] = vb; S.orig[found] = ob; }
-                    __syncwarp();
-                }
-            } else {
-                // slow path: scan the rest 256 rows at a time, OR-ing what we see
-                uint64_t orr = v;
-                for (size_t base = size_t(ib) + 32; base < rows && found == kNone; base += 256) {
-                    uint32_t hits[8];
-#pragma unroll
-                    for (int t = 0; t < 8; ++t) {
-                        const size_t ii = base + 32 * t + lane;
-                        uint64_t vv = 0;
-                        if (ii < winrows) vv = S.win[ii];
-                        else if (ii < rows) vv = A[ii];
-                        orr |= vv;
-                        hits[t] = __ballot_sync(0xffffffffu, ii < rows && (__popcll(c & vv) & 1));
+                found = ib + uint32_t(f);
+                newrow = __shfl_sync(0xffffffffu, cv, f);
+                const uint32_t of = __shfl_sync(0xffffffffu, co, f);
+                const uint64_t vb = __shfl_sync(0xffffffffu, cv, 0);
+                const uint32_t ob = __shfl_sync(0xffffffffu, co, 0);
+                if (lane == 0) { S.win[ib] = newrow; S.orig[ib] = of; }
+                const bool mv = lane == f && f != 0;
+                if (mv) { S.win[found] = vb; S.orig[found] = ob; }
+                // slots ib+1 .. ib+32 (slot ib+f now holds the old slot ib)
+                cv = __shfl_down_sync(0xffffffffu, mv ? vb : cv, 1);
+                co = __shfl_down_sync(0xffffffffu, mv ? ob : co, 1);
+                if (lane == 31) { cv = pv; co = po; }
+            }
+        }
+        if (!fast) {
+            __syncwarp();  // the fast path's swap stores are visible to every lane
+            // ---- pivot search: first row i >= ib with odd popcount(c & A_i) ----
+            {
+                const uint32_t i = ib + lane;
+                uint64_t v = 0;
+                uint32_t o = 0;
+                if (i < winrows) { v = S.win[i]; o = S.orig[i]; }
+                else if (i < rows) { v = A[i]; }
+                const uint32_t bal = __ballot_sync(0xffffffffu, i < rows && (__popcll(c & v) & 1));
+                if (bal) {
+                    const int f = __ffs(bal) - 1;
+                    found = ib + f;
+                    newrow = __shfl_sync(0xffffffffu, v, f);
+                    if (found < winrows) {  // fast path: both slots are in the window
+                        const uint64_t vb = __shfl_sync(0xffffffffu, v, 0);
+                        const uint32_t of = __shfl_sync(0xffffffffu, o, f);
+                        const uint32_t ob = __shfl_sync(0xffffffffu, o, 0);
+                        if (lane == 0) { S.win[ib] = newrow; S.orig[ib] = of; }
+                        if (lane == f && f != 0) { S.win[found] = vb; S.orig[found] = ob; }
+                        __syncwarp();
                     }
-#pragma unroll
-                    for (int t = 0; t < 8; ++t)
-                        if (found == kNone && hits[t]) found = uint32_t(base + 32 * t + __ffs(hits[t]) - 1);
-                }
-                if (found == kNone) {
-                    orr = __reduce_or_sync(0xffffffffu, uint32_t(orr)) |
-                          (uint64_t(__reduce_or_sync(0xffffffffu, uint32_t(orr >> 32))) << 32);
-                    if (orr == 0) break;  // only zero rows remain: no further selections
                 } else {
-                    if (lane == 0) {
-                        const uint64_t vb = S.win[ib];
-                        const uint32_t ob = S.orig[ib];
-                        if (found < winrows) {
-                            newrow = S.win[found];
-                            S.win[ib] = newrow;
-                            S.orig[ib] = S.orig[found];
-                            S.win[found] = vb;
-                            S.orig[found] = ob;
-                        } else {
-                            newrow = A[found];
-                            A[found] = vb;
-                            S.win[ib] = newrow;
-                            uint32_t e = 0;
-                            while (e < n_ext && S.ext_pos[e] != found) ++e;
-                            if (e == n_ext) { S.ext_pos[e] = found; S.ext_orig[e] = found; }
-                            S.orig[ib] = S.ext_orig[e];
-                            S.ext_orig[e] = ob;
+                    // slow path: scan the rest 256 rows at a time, OR-ing what we see
+                    uint64_t orr = v;
+                    for (size_t base = size_t(ib) + 32; base < rows && found == kNone; base += 256) {
+                        uint32_t hits[8];
+    #pragma unroll
+                        for (int t = 0; t < 8; ++t) {
+                            const size_t ii = base + 32 * t + lane;
+                            uint64_t vv = 0;
+                            if (ii < winrows) vv = S.win[ii];
+                            else if (ii < rows) vv = A[ii];
+                            orr |= vv;
+                            hits[t] = __ballot_sync(0xffffffffu, ii < rows && (__popcll(c & vv) & 1));
                         }
+    #pragma unroll
+                        for (int t = 0; t < 8; ++t)
+                            if (found == kNone && hits[t]) found = uint32_t(base + 32 * t + __ffs(hits[t]) - 1);
                     }
-                    __syncwarp();
-                    newrow = __shfl_sync(0xffffffffu, newrow, 0);
-                    if (found >= winrows) {
-                        const uint32_t e0 = n_ext;  // uniform recount
-                        uint32_t present = 0;
-                        for (uint32_t e = 0; e < e0; ++e) present |= (S.ext_pos[e] == found);
-                        if (!present) ++n_ext;
+                    if (found == kNone) {
+                        orr = __reduce_or_sync(0xffffffffu, uint32_t(orr)) |
+                              (uint64_t(__reduce_or_sync(0xffffffffu, uint32_t(orr >> 32))) << 32);
+                        if (orr == 0) break;  // only zero rows remain: no further selections
+                    } else {
+                        if (lane == 0) {
+                            const uint64_t vb = S.win[ib];
+                            const uint32_t ob = S.orig[ib];
+                            if (found < winrows) {
+                                newrow = S.win[found];
+                                S.win[ib] = newrow;
+                                S.orig[ib] = S.orig[found];
+                                S.win[found] = vb;
+                                S.orig[found] = ob;
+                            } else {
+                                newrow = A[found];
+                                A[found] = vb;
+                                S.win[ib] = newrow;
+                                uint32_t e = 0;
+                                while (e < n_ext && S.ext_pos[e] != found) ++e;
+                                if (e == n_ext) { S.ext_pos[e] = found; S.ext_orig[e] = found; }
+                                S.orig[ib] = S.ext_orig[e];
+                                S.ext_orig[e] = ob;
+                            }
+                        }
+                        __syncwarp();
+                        newrow = __shfl_sync(0xffffffffu, newrow, 0);
+                        if (found >= winrows) {
+                            const uint32_t e0 = n_ext;  // uniform recount
+                            uint32_t present = 0;
+                            for (uint32_t e = 0; e < e0; ++e) present |= (S.ext_pos[e] == found);
+                            if (!present) ++n_ext;
+                        }
                     }
                 }
             }
@@ -1366,7 +1412,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
             if ((zhi >> k) & 1) zhi ^= cm;
             if ((mlo >> k) & 1) mlo ^= cm;
             if ((mhi >> k) & 1) mhi ^= cm;
-            continue;
+            continue;  // no swap happened: the register window is still valid
         }
         if (found < winrows && found > max_touch) max_touch = found;
         sel |= 1ull << k;
@@ -1387,7 +1433,14 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
         if ((mlo >> k) & 1) mlo ^= cm;
         if ((mhi >> k) & 1) mhi ^= cm;
         ++ib;
+        if (fast) {
+            regwin = ib + 33u <= winrows;
+            if (!regwin) __syncwarp();
+        } else {
+            load_regwin();
+        }
     }
+    __syncwarp();
     // ---- composite permutation: window slots with orig != slot, then ext rows ----
     uint32_t np = 0;
     const uint32_t span = (ib > 0 ? max_touch + 1 : 0);
