@@ -166,7 +166,7 @@ struct LeafGraph {
     uint64_t nodes = 0;
 };
 struct LeafGraphs {
-    std::map<std::array<uintptr_t, 7>, LeafGraph> m;
+    std::map<std::array<uintptr_t, 8>, LeafGraph> m;
     void clear() {
         for (auto& kv : m)
             if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
@@ -183,6 +183,10 @@ struct f2gpu_ctx {
     bool use_graphs = true;
     bool lookahead = true;
     cudaStream_t side = nullptr;          // lookahead: panel kernels run here
+    cudaStream_t copy = nullptr;          // decompose_recursive_host: chunked uploads
+    std::vector<cudaEvent_t> chunk_ev;    // one per uploaded column chunk
+    void* pend = nullptr;                 // uploaded, not yet materialised columns
+    size_t pend_bytes = 0;
     cudaEvent_t ev_post = nullptr, ev_panel = nullptr;
     uint32_t* scr_flags = nullptr;        // per-panel early-release counters
     size_t scr_flags_cap = 0;
@@ -645,7 +649,11 @@ int ensure_scratch(f2gpu_ctx* c, size_t n, size_t mu) {
 // Panels [c0, c1) with their Schur updates restricted to word-columns < c1
 // (c1 = mu for the block algorithm; a leaf range for the recursive one).  The
 // swaps of every panel are applied to all mu word-columns.
-int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_t c1, bool la) {
+// swap_cols: word-columns [0, swap_cols) receive the row swaps (default: all);
+// the recursive driver's upload overlap keeps not-yet-materialised columns out
+int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_t c1, bool la,
+                   size_t swap_cols = size_t(-1)) {
+    if (swap_cols > mu) swap_cols = mu;
     const int grid = la ? c->num_sms - 1 : c->num_sms;
     auto upd = [&](size_t j, uint32_t* release) {
         f2::UpdateArgs u{};
@@ -661,7 +669,7 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
             F2_TRY(check_launch(c, f2::launch_panel(s.w.p + j * s.w.stride, n, s.st, int(j),
                                                     c->stream),
                                 "k_panel"));
-            F2_TRY(check_launch(c, f2::launch_post(s.w.p, s.w.stride, int(mu), int(j), s.perm, n,
+            F2_TRY(check_launch(c, f2::launch_post(s.w.p, s.w.stride, int(swap_cols), int(j), s.perm, n,
                                                    s.st + j, c->stream),
                                 "k_post"));
             if (j + 1 < c1) F2_TRY(upd(j, nullptr));
@@ -672,7 +680,7 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
                         "k_panel"));
     for (size_t j = c0; j < c1; ++j) {
         if (j > c0) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_panel, 0));
-        F2_TRY(check_launch(c, f2::launch_post(s.w.p, s.w.stride, int(mu), int(j), s.perm, n,
+        F2_TRY(check_launch(c, f2::launch_post(s.w.p, s.w.stride, int(swap_cols), int(j), s.perm, n,
                                                s.st + j, c->stream),
                             "k_post"));
         if (j + 1 >= c1) break;
@@ -733,7 +741,30 @@ struct RecRun {
     size_t cut;    // Strassen cutover inside the recursion (XOR traffic vs multiply)
     size_t tbase;  // TRSM base (panels solved in one k_trsm_block launch)
     bool trsm_kernel = true;  // F2GPU_REC_TRSM=0: rank-64 updates instead (A/B check)
+    // upload overlap (f2gpu_decompose_recursive_host): word-columns >= frontier are
+    // still in `pend` (original row order, column q at pend + (q - frontier0) * ps),
+    // chunk i of `chunk` word-columns complete at event chunk_ev[i]
+    size_t frontier = size_t(-1), frontier0 = 0, chunk = 0, ps = 0;
+    const uint64_t* pend = nullptr;
 };
+
+// materialise word-columns up to c1: wait for their upload, gather them under the
+// current composite permutation (swaps of every panel factored so far)
+int ensure_cols(RecRun& r, size_t c1) {
+    f2gpu_ctx* c = r.c;
+    while (r.frontier < c1 && r.frontier < r.mu) {
+        const size_t idx = (r.frontier - r.frontier0) / r.chunk;
+        CUDA_TRY(cudaStreamWaitEvent(c->stream, c->chunk_ev[idx], 0));
+        const size_t nq = std::min(r.chunk, r.mu - r.frontier);
+        Shard& s = *r.s;
+        F2_TRY(check_launch(c, f2::launch_gather_rows(s.w.p + r.frontier * s.w.stride, s.w.stride,
+                                                      r.pend + (r.frontier - r.frontier0) * r.ps, r.ps, s.perm,
+                                                      r.n, nq, c->stream),
+                            "k_gather_rows"));
+        r.frontier += nq;
+    }
+    return F2GPU_OK;
+}
 
 int rec_state(RecRun& r, size_t j, size_t* R, size_t* rr) {
     f2::PanelState h;
@@ -787,9 +818,11 @@ int rec_trsm(RecRun& r, size_t a, size_t b, size_t Ra, size_t col0, size_t col1)
 int rec_leaf(RecRun& r, size_t c0, size_t c1) {
     f2gpu_ctx* c = r.c;
     Shard& s = *r.s;
-    if (!c->use_graphs || c->tl.on) return enqueue_panels(c, s, r.n, r.mu, c0, c1, r.la);
-    const std::array<uintptr_t, 7> key{uintptr_t(s.w.p), s.w.stride, r.n, r.mu, c0, c1,
-                                       uintptr_t(s.st) ^ (r.la ? 1u : 0u)};
+    F2_TRY(ensure_cols(r, c1));
+    const size_t sw = std::min(r.frontier, r.mu);
+    if (!c->use_graphs || c->tl.on) return enqueue_panels(c, s, r.n, r.mu, c0, c1, r.la, sw);
+    const std::array<uintptr_t, 8> key{uintptr_t(s.w.p), s.w.stride, r.n, r.mu, c0, c1,
+                                       uintptr_t(s.st) ^ (r.la ? 1u : 0u), sw};
     LeafGraph& g = c->leaf_graphs.m[key];
     if (g.exec) {
         CUDA_TRY(cudaGraphLaunch(g.exec, c->stream));
@@ -798,12 +831,12 @@ int rec_leaf(RecRun& r, size_t c0, size_t c1) {
     }
     if (g.seen < 1) {
         g.seen += 1;
-        return enqueue_panels(c, s, r.n, r.mu, c0, c1, r.la);
+        return enqueue_panels(c, s, r.n, r.mu, c0, c1, r.la, sw);
     }
     cudaGraph_t graph = nullptr;
     const uint64_t l0 = c->launches;
     CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    int rc = enqueue_panels(c, s, r.n, r.mu, c0, c1, r.la);
+    int rc = enqueue_panels(c, s, r.n, r.mu, c0, c1, r.la, sw);
     cudaError_t ec = cudaStreamEndCapture(c->stream, &graph);
     if (rc != F2GPU_OK) { if (graph) cudaGraphDestroy(graph); return rc; }
     if (ec != cudaSuccess) return set_err(F2GPU_ECUDA, std::string("leaf graph capture: ") + cudaGetErrorString(ec));
@@ -827,6 +860,7 @@ int rec_decompose(RecRun& r, size_t c0, size_t c1) {
     F2_TRY(rec_state(r, cm - 1, &Rl, &rl));
     const size_t R1 = Rl + rl;
     const bool full = R1 - R0 == 64 * (cm - c0) && R0 % 64 == 0;
+    F2_TRY(ensure_cols(r, c1));
     if (full) {
         F2_TRY(rec_trsm(r, c0, cm, R0, cm, c1));
         if (R1 < r.n)
@@ -840,7 +874,8 @@ int rec_decompose(RecRun& r, size_t c0, size_t c1) {
 }
 
 int decompose_recursive(f2gpu_ctx* c, View w, size_t min_cols, uint32_t* perm, uint32_t* rj,
-                        size_t* rank) {
+                        size_t* rank, size_t frontier = size_t(-1), const uint64_t* pend = nullptr,
+                        size_t ps = 0, size_t chunk = 0) {
     const size_t n = w.rows, mu = w.wcols();
     if (n == 0 || mu == 0) {
         if (rank) *rank = 0;
@@ -859,6 +894,12 @@ int decompose_recursive(f2gpu_ctx* c, View w, size_t min_cols, uint32_t* perm, u
     if (const char* e = getenv("F2GPU_REC_CUT")) r.cut = size_t(atol(e));
     if (const char* e = getenv("F2GPU_REC_TBASE")) r.tbase = std::max<size_t>(1, size_t(atol(e)));
     if (const char* e = getenv("F2GPU_REC_TRSM")) r.trsm_kernel = e[0] != '0';
+    if (pend && frontier < mu) {
+        r.frontier = r.frontier0 = frontier;
+        r.pend = pend;
+        r.ps = ps;
+        r.chunk = chunk;
+    }
     CUDA_TRY(cudaMemsetAsync(c->scr_flags, 0, mu * 4, c->stream));
     c->tl.mark(c->stream, "start");
     F2_TRY(check_launch(c, f2::launch_iota(s.perm, n, c->stream), "k_iota"));
@@ -1083,6 +1124,9 @@ int f2gpu_ctx_destroy(f2gpu_ctx* c) {
     cudaFree(c->scr_perm);
     cudaFree(c->scr_flags);
     if (c->side) { cudaStreamSynchronize(c->side); cudaStreamDestroy(c->side); }
+    if (c->copy) { cudaStreamSynchronize(c->copy); cudaStreamDestroy(c->copy); }
+    for (cudaEvent_t e : c->chunk_ev) cudaEventDestroy(e);
+    cudaFree(c->pend);
     if (c->ev_post) cudaEventDestroy(c->ev_post);
     if (c->ev_panel) cudaEventDestroy(c->ev_panel);
     cudaFree(c->d_jump);
@@ -1575,8 +1619,47 @@ int f2gpu_decompose_recursive_host(f2gpu_ctx* c, const uint64_t* a, size_t n, si
     if (!c) return set_err(F2GPU_EINVAL, "null ctx");
     f2gpu_mat* W = nullptr;
     F2_TRY(staging(c, n, m, &W));
-    F2_TRY(f2gpu_mat_upload(c, W, a, stride));
-    F2_TRY(f2gpu_decompose_recursive(c, W, min_cols, perm, rj, rank));
+    const size_t mu = ceil64(m);
+    // Upload overlap: the first leaf's word-columns go straight into W; the rest
+    // stream on the copy stream, chunk by chunk, into `pend` in the host's row
+    // order, and the recursion materialises each chunk under the row permutation
+    // of the panels factored so far when it first needs it (ensure_cols).
+    const size_t cw = std::max<size_t>(1, (min_cols ? min_cols : 256 * 64) / 64);
+    if (n == 0 || mu <= cw || !a || getenv("F2GPU_NO_UPLOAD_OVERLAP")) {
+        F2_TRY(f2gpu_mat_upload(c, W, a, stride));
+        F2_TRY(f2gpu_decompose_recursive(c, W, min_cols, perm, rj, rank));
+    } else {
+        if (n > 0xFFFFFFF0ull) return set_err(F2GPU_ERANGE, "decompose: too many rows for uint32 perm");
+        const size_t ps = W->stride, nchunks = (mu - cw + cw - 1) / cw;
+        const size_t bytes = (mu - cw) * ps * 8;
+        if (!c->copy) CUDA_TRY(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+        while (c->chunk_ev.size() < nchunks + 1) {
+            cudaEvent_t e;
+            CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            c->chunk_ev.push_back(e);
+        }
+        if (c->pend_bytes < bytes) {
+            CUDA_TRY(cudaStreamSynchronize(c->stream));
+            cudaFree(c->pend);
+            c->pend = nullptr;
+            c->pend_bytes = 0;
+            CUDA_TRY(cudaMalloc(&c->pend, bytes));
+            c->pend_bytes = bytes;
+        }
+        // the copy stream may overwrite `pend` once earlier work on it is done
+        CUDA_TRY(cudaEventRecord(c->chunk_ev[nchunks], c->stream));
+        CUDA_TRY(cudaStreamWaitEvent(c->copy, c->chunk_ev[nchunks], 0));
+        CUDA_TRY(cudaMemcpy2DAsync(W->d, W->stride * 8, a, stride * 8, n * 8, cw, cudaMemcpyHostToDevice,
+                                   c->stream));
+        uint64_t* pend = static_cast<uint64_t*>(c->pend);
+        for (size_t i = 0; i < nchunks; ++i) {
+            const size_t q0 = cw + i * cw, nq = std::min(cw, mu - q0);
+            CUDA_TRY(cudaMemcpy2DAsync(pend + (q0 - cw) * ps, ps * 8, a + q0 * stride, stride * 8, n * 8, nq,
+                                       cudaMemcpyHostToDevice, c->copy));
+            CUDA_TRY(cudaEventRecord(c->chunk_ev[i], c->copy));
+        }
+        F2_TRY(decompose_recursive(c, view_of(W), min_cols, perm, rj, rank, cw, pend, ps, cw));
+    }
     if (w_out) F2_TRY(f2gpu_mat_download(c, W, w_out, stride));
     return F2GPU_OK;
 }

@@ -1825,6 +1825,25 @@ cudaError_t launch_transpose(const uint64_t* a, size_t n, size_t m, size_t sa, u
     return cudaGetLastError();
 }
 
+// dst word-column q, row i  <-  src word-column q, row perm[i]   (i < n, q < nq):
+// materialises a column chunk uploaded in original row order under the
+// composite row permutation of the panels already factored
+__global__ void __launch_bounds__(256) k_gather_rows(uint64_t* __restrict__ dst, size_t sd,
+                                                     const uint64_t* __restrict__ src, size_t ss,
+                                                     const uint32_t* __restrict__ perm, size_t n) {
+    const size_t q = blockIdx.y;
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+        dst[q * sd + i] = src[q * ss + perm[i]];
+}
+cudaError_t launch_gather_rows(uint64_t* dst, size_t sd, const uint64_t* src, size_t ss, const uint32_t* perm,
+                               size_t n, size_t nq, cudaStream_t s) {
+    if (n == 0 || nq == 0) return cudaSuccess;
+    if (nq > 65535) return cudaErrorInvalidValue;
+    dim3 grid(unsigned(std::min<size_t>((n + 255) / 256, 64)), unsigned(nq));
+    k_gather_rows<<<grid, 256, 0, s>>>(dst, sd, src, ss, perm, n);
+    return cudaGetLastError();
+}
+
 // identity block: bit (i, 64*wcol0 + i) = 1 for i < rows (the matrix is zeroed)
 __global__ void k_set_diag(uint64_t* w, size_t stride, size_t rows, size_t wcol0) {
     for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < rows; i += size_t(gridDim.x) * blockDim.x)

@@ -90,6 +90,8 @@ cudaError_t launch_transpose(const uint64_t* a, size_t n, size_t m, size_t sa, u
                              size_t so, cudaStream_t s);
 cudaError_t launch_iota(uint32_t* p, size_t n, cudaStream_t s);
 cudaError_t launch_set_diag(uint64_t* w, size_t stride, size_t rows, size_t wcol0, cudaStream_t s);
+cudaError_t launch_gather_rows(uint64_t* dst, size_t sd, const uint64_t* src, size_t ss, const uint32_t* perm,
+                               size_t n, size_t nq, cudaStream_t s);
 cudaError_t launch_mask_cols(uint64_t* w, size_t stride, size_t n, size_t m, cudaStream_t s);
 
 // batched products / XORs (device arrays of descriptors)

@@ -409,18 +409,21 @@ def test_strassen_tc_plan(f2, ctx, po, n, k, m, leaf):
         assert same(got, po.m4rm_mult(a, n, k, b, m), n)
 
 
-def test_decompose_recursive_host(f2, ctx, po):
+@pytest.mark.parametrize("n,m,kind,mc", [(1500, 2300, "dense", 256), (4096, 8192, "dense", 1024),
+                                         (3000, 5000, "xy", 512), (777, 4160, "dense", 64)])
+def test_decompose_recursive_host(f2, ctx, po, n, m, kind, mc):
+    """Host entry with the overlapped chunked upload (chunks of mc columns are
+    materialised under the running row permutation when first needed)."""
     import ctypes as C
     lib = f2._lib.load()
-    n, m = 1500, 2300
-    a = po.random_dense(n, m, 0.5, 77)
+    a = po.random_dense(n, m, 0.5, 77) if kind == "dense" else _xy(po, n, 1000, m, 5)
     w, perm, rj, rank = po.decompose_block(a, n, m)
     stride = a.shape[1]
     wout = np.zeros_like(a)
     p = np.zeros(n, np.uint32)
     r = np.zeros((m + 63) // 64, np.uint32)
     rk = C.c_size_t()
-    f2._lib.check(lib.f2gpu_decompose_recursive_host(ctx.handle, a.ctypes.data, n, m, stride, 256,
+    f2._lib.check(lib.f2gpu_decompose_recursive_host(ctx.handle, a.ctypes.data, n, m, stride, mc,
                                                      wout.ctypes.data, p.ctypes.data, r.ctypes.data,
                                                      C.byref(rk)))
     assert rk.value == rank
