@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <functional>
 #include <map>
 #include <memory>
 #include <array>
@@ -746,6 +747,10 @@ struct RecRun {
     // chunk i of `chunk` word-columns complete at event chunk_ev[i]
     size_t frontier = size_t(-1), frontier0 = 0, chunk = 0, ps = 0;
     const uint64_t* pend = nullptr;
+    // download overlap: called (stream-ordered) when rows [0, R) are final in
+    // every word-column -- after a split's TRSM/update on the recursion's right
+    // spine: rows above R_J are never swapped or updated by a later panel
+    std::function<int(size_t)> on_final;
 };
 
 // materialise word-columns up to c1: wait for their upload, gather them under the
@@ -870,12 +875,13 @@ int rec_decompose(RecRun& r, size_t c0, size_t c1) {
     } else {
         F2_TRY(rank_updates(r, c0, cm, cm, c1, r.n));
     }
+    if (c1 == r.mu && r.on_final) F2_TRY(r.on_final(R1));
     return rec_decompose(r, cm, c1);
 }
 
 int decompose_recursive(f2gpu_ctx* c, View w, size_t min_cols, uint32_t* perm, uint32_t* rj,
                         size_t* rank, size_t frontier = size_t(-1), const uint64_t* pend = nullptr,
-                        size_t ps = 0, size_t chunk = 0) {
+                        size_t ps = 0, size_t chunk = 0, std::function<int(size_t)> on_final = {}) {
     const size_t n = w.rows, mu = w.wcols();
     if (n == 0 || mu == 0) {
         if (rank) *rank = 0;
@@ -894,6 +900,7 @@ int decompose_recursive(f2gpu_ctx* c, View w, size_t min_cols, uint32_t* perm, u
     if (const char* e = getenv("F2GPU_REC_CUT")) r.cut = size_t(atol(e));
     if (const char* e = getenv("F2GPU_REC_TBASE")) r.tbase = std::max<size_t>(1, size_t(atol(e)));
     if (const char* e = getenv("F2GPU_REC_TRSM")) r.trsm_kernel = e[0] != '0';
+    r.on_final = std::move(on_final);
     if (pend && frontier < mu) {
         r.frontier = r.frontier0 = frontier;
         r.pend = pend;
@@ -1658,7 +1665,26 @@ int f2gpu_decompose_recursive_host(f2gpu_ctx* c, const uint64_t* a, size_t n, si
                                        cudaMemcpyHostToDevice, c->copy));
             CUDA_TRY(cudaEventRecord(c->chunk_ev[i], c->copy));
         }
-        F2_TRY(decompose_recursive(c, view_of(W), min_cols, perm, rj, rank, cw, pend, ps, cw));
+        // download overlap: row blocks that are final go back on the copy stream
+        // while the rest of the matrix is factored
+        size_t done = 0;
+        auto on_final = [&](size_t R) -> int {
+            if (!w_out || R <= done) return F2GPU_OK;
+            CUDA_TRY(cudaEventRecord(c->chunk_ev[nchunks], c->stream));
+            CUDA_TRY(cudaStreamWaitEvent(c->copy, c->chunk_ev[nchunks], 0));
+            CUDA_TRY(cudaMemcpy2DAsync(w_out + done, stride * 8, W->d + done, W->stride * 8, (R - done) * 8, mu,
+                                       cudaMemcpyDeviceToHost, c->copy));
+            done = R;
+            return F2GPU_OK;
+        };
+        F2_TRY(decompose_recursive(c, view_of(W), min_cols, perm, rj, rank, cw, pend, ps, cw, on_final));
+        if (w_out && done < n) {
+            CUDA_TRY(cudaMemcpy2DAsync(w_out + done, stride * 8, W->d + done, W->stride * 8, (n - done) * 8, mu,
+                                       cudaMemcpyDeviceToHost, c->stream));
+        }
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->copy));
+        return F2GPU_OK;
     }
     if (w_out) F2_TRY(f2gpu_mat_download(c, W, w_out, stride));
     return F2GPU_OK;
