@@ -145,3 +145,44 @@ def test_cfg4_decompose_recursive_65536(f2, ctx, po):
     _lib.check(lib.f2gpu_decompose_recursive(ctx.handle, A.handle, 0, perm.ctypes.data,
                                              rj.ctypes.data, C.byref(rk)))
     check_against(po, g, None, A.download(), perm, rj, int(rk.value), n, n, freivalds=False)
+
+
+def _run_recursive(f2, ctx, A, n, m):
+    from paper_1209_5198_b200 import _lib
+    lib = _lib.load()
+    perm = np.zeros(n, np.uint32)
+    rj = np.zeros((m + 63) // 64, np.uint32)
+    rk = C.c_size_t()
+    _lib.check(lib.f2gpu_decompose_recursive(ctx.handle, A.handle, 0, perm.ctypes.data, rj.ctypes.data,
+                                             C.byref(rk)))
+    return A.download(), perm, rj, int(rk.value)
+
+
+def test_cfg3_decompose_recursive(f2, ctx, po):
+    """The recursive variant on the rank-deficient cfg3 input (rank-r_j fallback splits)."""
+    from paper_1209_5198_b200 import _lib
+
+    g = digests()["cfg3"]
+    lib = _lib.load()
+    X = f2.DeviceMatrix(16384, 12000, ctx)
+    Y = f2.DeviceMatrix(12000, 65536, ctx)
+    A = f2.DeviceMatrix(16384, 65536, ctx)
+    X.random_dense(0.5, g["seedX"])
+    Y.random_dense(0.5, g["seedY"])
+    _lib.check(lib.f2gpu_m4rm_mult(ctx.handle, X.handle, Y.handle, A.handle, 0))
+    a_host = A.download()
+    w, perm, rj, rank = _run_recursive(f2, ctx, A, 16384, 65536)
+    assert rank == 12000
+    check_against(po, g, a_host, w, perm, rj, rank, 16384, 65536)
+
+
+def test_cfg5_decompose_recursive(f2, ctx, po):
+    d = digests()
+    if "cfg5" not in d:
+        pytest.skip("cfg5 digest not generated")
+    g = d["cfg5"]
+    n, m = g["n"], g["m"]
+    A = f2.DeviceMatrix(n, m, ctx)
+    A.random_dense(g["p"], g["seed"])
+    w, perm, rj, rank = _run_recursive(f2, ctx, A, n, m)
+    check_against(po, g, None, w, perm, rj, rank, n, m, freivalds=False)
