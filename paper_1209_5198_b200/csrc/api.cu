@@ -183,6 +183,7 @@ struct f2gpu_ctx {
     LeafGraphs leaf_graphs;
     bool use_graphs = true;
     bool lookahead = true;
+    bool lookahead_col = true;  // F2GPU_LOOKAHEAD_COL=0: release from the update's column group 0 instead
     cudaStream_t side = nullptr;          // lookahead: panel kernels run here
     cudaStream_t copy = nullptr;          // decompose_recursive_host: chunked uploads
     std::vector<cudaEvent_t> chunk_ev;    // one per uploaded column chunk
@@ -656,15 +657,17 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
                    size_t swap_cols = size_t(-1)) {
     if (swap_cols > mu) swap_cols = mu;
     const int grid = la ? c->num_sms - 1 : c->num_sms;
-    auto upd = [&](size_t j, uint32_t* release) {
+    auto upd = [&](size_t j, uint32_t* release, size_t skip = 0) {
         f2::UpdateArgs u{};
-        u.C = s.w.p; u.sc = s.w.stride; u.c_wcol0 = j + 1; u.ncols = int(c1 - j - 1);
+        u.C = s.w.p; u.sc = s.w.stride; u.c_wcol0 = j + 1 + skip; u.ncols = int(c1 - j - 1 - skip);
+        if (u.ncols <= 0) return F2GPU_OK;
         u.row_lo = 0; u.row_hi = n; u.a = s.w.p + j * s.w.stride; u.k_bits = 0;
-        u.B = s.w.p; u.sb = s.w.stride; u.b_row0 = 0; u.b_wcol0 = j + 1;
+        u.B = s.w.p; u.sb = s.w.stride; u.b_row0 = 0; u.b_wcol0 = j + 1 + skip;
         u.st = s.st + j;
         u.release = release;
         return check_launch(c, f2::launch_update(u, grid, c->stream), "k_update");
     };
+    const bool colfirst = c->lookahead_col;
     if (!la) {
         for (size_t j = c0; j < c1; ++j) {
             F2_TRY(check_launch(c, f2::launch_panel(s.w.p + j * s.w.stride, n, s.st, int(j),
@@ -686,10 +689,22 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
                             "k_post"));
         if (j + 1 >= c1) break;
         CUDA_TRY(cudaEventRecord(c->ev_post, c->stream));
-        F2_TRY(upd(j, c->scr_flags + j));
+        uint32_t wait_count = uint32_t(grid);
+        if (colfirst) {
+            // the next panel's column alone first (small CTAs, counter), then the
+            // persistent update from column j+2 with no early release
+            const int g1 = f2::update_col_grid(n, c->num_sms);
+            F2_TRY(check_launch(c, f2::launch_update_col(s.w.p + (j + 1) * s.w.stride, s.w.p + j * s.w.stride, n,
+                                                         s.st + j, c->scr_flags + j, g1, c->stream),
+                                "k_update_col"));
+            F2_TRY(upd(j, nullptr, 1));
+            wait_count = uint32_t(g1);
+        } else {
+            F2_TRY(upd(j, c->scr_flags + j));
+        }
         CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_post, 0));
         F2_TRY(check_launch(c, f2::launch_panel(s.w.p + (j + 1) * s.w.stride, n, s.st, int(j + 1),
-                                                c->side, c->scr_flags + j, uint32_t(grid)),
+                                                c->side, c->scr_flags + j, wait_count),
                             "k_panel"));
         CUDA_TRY(cudaEventRecord(c->ev_panel, c->side));
     }
@@ -1098,6 +1113,7 @@ int f2gpu_ctx_create(int device, f2gpu_ctx** out) {
     if (const char* pf = getenv("F2GPU_PROFILE")) c->tl.on = pf[0] == '1';
     if (const char* gr = getenv("F2GPU_GRAPHS")) c->use_graphs = gr[0] != '0';
     if (const char* la = getenv("F2GPU_LOOKAHEAD")) c->lookahead = la[0] != '0';
+    if (const char* lc = getenv("F2GPU_LOOKAHEAD_COL")) c->lookahead_col = lc[0] != '0';
     if (const char* tc = getenv("F2GPU_TC")) c->use_tc = tc[0] != '0';
     if (const char* tcc = getenv("F2GPU_TC_CUT")) c->tc_cutover = size_t(atoll(tcc));
     CUDA_TRY(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));

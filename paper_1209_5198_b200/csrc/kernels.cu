@@ -1531,6 +1531,55 @@ __device__ __forceinline__ void panel_y_body(uint64_t* __restrict__ col, size_t 
     }
 }
 
+// Lookahead column update: the next panel's column only,
+//   next[i] ^= Y_j[i] * B   for i >= R_j + r_j,   B = next[R_j .. R_j + r_j)
+// (panel j's Schur update restricted to word-column j+1).  Many
+// small CTAs, a 1280-entry table per CTA; every CTA increments *done when its
+// rows are in memory, and the next panel kernel spins on the count -- so the
+// panel chain no longer waits for a full column group of the persistent update.
+__global__ void __launch_bounds__(256) k_update_col(uint64_t* __restrict__ next, const uint64_t* __restrict__ ycol,
+                                                    size_t n, const PanelState* __restrict__ st,
+                                                    uint32_t* __restrict__ done) {
+    __shared__ uint64_t bs[64];
+    __shared__ uint64_t tab[kTabEntries];
+    const uint32_t R = st->R, r = st->r;
+    const size_t lo = size_t(R) + r;
+    if (threadIdx.x < 64) bs[threadIdx.x] = (threadIdx.x < r && R + threadIdx.x < n) ? next[R + threadIdx.x] : 0;
+    __syncthreads();
+    if (r != 0 && lo < n) {
+        for (int e = threadIdx.x; e < kTabEntries; e += blockDim.x) {
+            const int t = e < 1024 ? e >> 7 : 8;
+            const int idx = e < 1024 ? e & 127 : e - 1024;
+            uint64_t v = 0;
+#pragma unroll
+            for (int b = 0; b < 8; ++b)
+                if ((idx >> b) & 1) v ^= bs[7 * t + b];
+            tab[e] = v;
+        }
+        __syncthreads();
+        for (size_t i = lo + size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+            const uint64_t y = ycol[i];
+            uint64_t x = 0;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) x ^= tab[128 * t + int((y >> (7 * t)) & 127)];
+            x ^= tab[1024 + int(y >> 56)];
+            next[i] ^= x;
+        }
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(done, 1u);
+}
+
+int update_col_grid(size_t n, int num_sms) {
+    return int(std::max<size_t>(1, std::min<size_t>((n + 255) / 256, size_t(4) * size_t(num_sms))));
+}
+cudaError_t launch_update_col(uint64_t* next, const uint64_t* ycol, size_t n, const PanelState* st, uint32_t* done,
+                              int grid, cudaStream_t s) {
+    k_update_col<<<grid, 256, 0, s>>>(next, ycol, n, st, done);
+    return cudaGetLastError();
+}
+
 __global__ void __launch_bounds__(256) k_panel_y(uint64_t* __restrict__ col, size_t n,
                                                  const PanelState* __restrict__ st) {
     __shared__ uint64_t zt[kTabEntries];

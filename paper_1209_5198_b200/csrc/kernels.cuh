@@ -88,6 +88,10 @@ cudaError_t launch_xor(uint64_t* dst, size_t sd, const uint64_t* a, size_t sa,
                        cudaStream_t s);
 cudaError_t launch_transpose(const uint64_t* a, size_t n, size_t m, size_t sa, uint64_t* out,
                              size_t so, cudaStream_t s);
+// lookahead: panel j's update of word-column j+1 only; increments *done per CTA
+int update_col_grid(size_t n, int num_sms);
+cudaError_t launch_update_col(uint64_t* next, const uint64_t* ycol, size_t n, const PanelState* st, uint32_t* done,
+                              int grid, cudaStream_t s);
 cudaError_t launch_iota(uint32_t* p, size_t n, cudaStream_t s);
 cudaError_t launch_set_diag(uint64_t* w, size_t stride, size_t rows, size_t wcol0, cudaStream_t s);
 cudaError_t launch_gather_rows(uint64_t* dst, size_t sd, const uint64_t* src, size_t ss, const uint32_t* perm,
