@@ -1486,9 +1486,462 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
     }
 }
 
+// 64x64 bit-matrix transpose held in a warp: lane L holds rows L (x0) and L+32
+// (x1) on entry and columns L / L+32 on exit.  One register swap for the 32-bit
+// halves, then five shuffle butterflies -- no shared memory, no bank conflicts.
+__device__ __forceinline__ void warp_transpose64(uint64_t& x0, uint64_t& x1, int lane) {
+    {
+        const uint64_t t = ((x0 >> 32) ^ x1) & 0x00000000FFFFFFFFull;
+        x1 ^= t;
+        x0 ^= t << 32;
+    }
+    const uint64_t masks[5] = {0x0000FFFF0000FFFFull, 0x00FF00FF00FF00FFull, 0x0F0F0F0F0F0F0F0Full,
+                               0x3333333333333333ull, 0x5555555555555555ull};
+#pragma unroll
+    for (int st = 0; st < 5; ++st) {
+        const int j = 16 >> st;
+        const uint64_t msk = masks[st];
+        const uint64_t y0 = __shfl_xor_sync(0xffffffffu, x0, j);
+        const uint64_t y1 = __shfl_xor_sync(0xffffffffu, x1, j);
+        if (!(lane & j)) {
+            x0 ^= (((x0 >> j) ^ y0) & msk) << j;
+            x1 ^= (((x1 >> j) ^ y1) & msk) << j;
+        } else {
+            x0 ^= ((y0 >> j) ^ x0) & msk;
+            x1 ^= ((y1 >> j) ^ x1) & msk;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K4': buildZ as Gauss-Jordan on a TRANSPOSED register block
+// ---------------------------------------------------------------------------
+// buildZ's pivot test at step k is parity(c_k & A_i) with c_k = e_k + {j < k :
+// M_j[k]}.  M stays in reduced row-echelon form (every
+// update of :1001-1010 is a Gauss-Jordan step), so that parity is bit k of
+//   rho_i = A_i + sum_{j<k} A_i[j] M_j,
+// and rho evolves by plain Gauss-Jordan: after step k selects p,
+//   rho_i ^= rho_i[k] * rho_p   for every other row, earlier pivots included.
+// (Insertion steps only change M at column k, which no later test reads.)
+//
+// The first kGjPos candidate positions are held reduced and TRANSPOSED in warp
+// 0: lane l owns columns l and l+32 as kGjWords 32-bit words over the positions.
+// One step is then
+//   broadcast column k (3 shuffles) -> f = first live set position (every lane
+//   computes it) -> per own column: bit f, xor the column mask, swap bits ib/f
+// -- lane-local except the broadcast, ~70 instructions and one shuffle of
+// dependent latency per step.  The reference's tie-break (first row at or after
+// ib in the CURRENT order) is kept exactly: positions are swapped
+// as the reference swaps rows.
+//
+// Z.  With rho_i = A_i + y_i*P (P = the selected rows in order), the pivot at
+// position u ends as the RREF row M_u = (e_u + y_u)*P, so Z row k_u = e_u + y_u
+// and the other Z rows are 0.  That Z is not the reference's bit for bit, but
+// Y = D*Z is only formed for rows below the pivots (panel_y_body), all of which
+// lie in span(P) (every step either selected a pivot or found bit k clear in
+// ALL remaining rows), where coordinates are unique -- so Y is identical.  Warp
+// 1 tracks y in the same transposed form from a per-step log, off the chain.
+//
+// Positions >= kGjPos take the slow path: rows are tested against c_k and the
+// pivot is reduced by the RREF rows (popcounts per own column).  Warp 2 replays
+// the swaps on win/orig (the composite permutation) from the same log.
+// ---------------------------------------------------------------------------
+constexpr int kGjWords = 3;
+constexpr uint32_t kGjPos = 32 * kGjWords;
+constexpr uint32_t kLogValid = 0x80000000u, kLogSlow = 0x40000000u, kLogEnd = 0x20000000u;
+
+struct PanelGjSmem {
+    uint64_t win[kPanelWin];
+    uint32_t orig[kPanelWin];
+    uint32_t ext_pos[64];
+    uint32_t ext_orig[64];
+    uint4 log[66];      // per selection t: column-k mask over positions (3 words), meta
+    uint2 logu[66];     // slow selections: dead positions u with x[k_u] (the reduction set)
+    uint32_t done;      // log entries applied to win/orig by warp 2
+    uint32_t n_ext;
+    uint32_t span;
+};
+static_assert(kGjWords == 3, "log entries carry three position words");
+
+// meta = valid | slow | end | k << 8 | f  (f < kGjPos for fast entries; r for the end entry)
+__device__ __forceinline__ uint32_t gj_meta(bool slow, int k, uint32_t f) {
+    return kLogValid | (slow ? kLogSlow : 0u) | (uint32_t(k) << 8) | f;
+}
+
+__device__ __forceinline__ uint32_t pick3(const uint32_t (&a)[kGjWords], uint32_t w) {
+    return w == 0 ? a[0] : (w == 1 ? a[1] : a[2]);
+}
+
+__device__ __forceinline__ uint64_t warp_or64(uint64_t v) {
+    return uint64_t(__reduce_or_sync(0xffffffffu, uint32_t(v))) |
+           (uint64_t(__reduce_or_sync(0xffffffffu, uint32_t(v >> 32))) << 32);
+}
+
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) { return *reinterpret_cast<const volatile uint32_t*>(p); }
+__device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) { *reinterpret_cast<volatile uint32_t*>(p) = v; }
+
+__device__ __forceinline__ uint4 ld_log(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.volatile.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_log(uint4* p, uint32_t a, uint32_t b, uint32_t c, uint32_t m) {
+    asm volatile("st.volatile.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))), "r"(a), "r"(b), "r"(c), "r"(m)
+                 : "memory");
+}
+
+// position masks of one step: the pivot column's positions minus f, and the
+// two-bit swap mask {ib, f}
+struct GjStep {
+    uint32_t E[kGjWords];
+    uint32_t sw[kGjWords];
+};
+
+__global__ void __launch_bounds__(kPanelThreads, 1)
+    k_panel_gj(uint64_t* __restrict__ col, size_t n, PanelState* __restrict__ st_all, int j,
+               const uint32_t* wait_flag, uint32_t wait_count) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    PanelGjSmem& S = *reinterpret_cast<PanelGjSmem*>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (wait_flag) {
+        if (tid == 0) {
+            uint32_t v;
+            while (true) {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(wait_flag) : "memory");
+                if (v >= wait_count) break;
+                __nanosleep(64);
+            }
+        }
+        __syncthreads();
+    }
+    const size_t R = j == 0 ? 0 : size_t(st_all[j - 1].R) + st_all[j - 1].r;
+    PanelState* st = st_all + j;
+    const size_t rows = R < n ? n - R : 0;
+    if (rows == 0) {
+        if (tid == 0) { st->R = uint32_t(R < n ? R : n); st->r = 0; st->npairs = 0; st->flags = 0; }
+        if (tid < 64) st->Z[tid] = 0;
+        return;
+    }
+    uint64_t* A = col + R;
+    const uint32_t winrows = rows < size_t(kPanelWin) ? uint32_t(rows) : uint32_t(kPanelWin);
+    const uint32_t npos = winrows < kGjPos ? winrows : kGjPos;
+#ifdef GJ_PROFILE
+    const long long t_start = clock64();
+#endif
+    for (uint32_t x = tid; x < winrows; x += kPanelThreads) {
+        S.win[x] = A[x];
+        S.orig[x] = x;
+    }
+    if (tid < 66) S.log[tid] = make_uint4(0, 0, 0, 0);
+    if (tid == 0) S.done = 0;
+    __syncthreads();
+    if (warp > 2) return;
+#ifdef GJ_PROFILE
+    const long long t_loaded = clock64();
+#endif
+
+    if (warp == 2) {
+        // ---- win/orig bookkeeping: replay the fast swaps ----
+        uint32_t t = 0;
+        for (;; ++t) {
+            uint32_t m;
+            do { m = ld_volatile(&S.log[t].w); } while (m == 0);
+            if (m & kLogEnd) break;
+            if (!(m & kLogSlow) && lane == 0) {
+                const uint32_t f = m & 0xFFu;
+                if (f != t) {
+                    const uint64_t vt = S.win[t], vf = S.win[f];
+                    const uint32_t ot = S.orig[t], of = S.orig[f];
+                    S.win[t] = vf; S.orig[t] = of;
+                    S.win[f] = vt; S.orig[f] = ot;
+                }
+            }
+            __syncwarp();
+            __threadfence_block();
+            if (lane == 0) st_volatile(&S.done, t + 1);
+        }
+        asm volatile("bar.sync 1, 96;" ::: "memory");
+        // ---- composite permutation: window slots with orig != slot, then ext rows ----
+        const uint32_t span = S.span, n_ext = S.n_ext;
+        uint32_t np = 0;
+        for (uint32_t x0 = 0; x0 < span; x0 += 32) {
+            const uint32_t x = x0 + lane;
+            const bool moved = x < span && S.orig[x] != x;
+            const uint32_t bal = __ballot_sync(0xffffffffu, moved);
+            if (moved) {
+                const uint32_t e = np + __popc(bal & ((1u << lane) - 1));
+                A[x] = S.win[x];
+                st->dst[e] = x;
+                st->src[e] = S.orig[x];
+            }
+            np += __popc(bal);
+        }
+        for (uint32_t e0 = 0; e0 < n_ext; e0 += 32) {
+            const uint32_t e = e0 + lane;
+            const bool moved = e < n_ext && S.ext_orig[e] != S.ext_pos[e];
+            const uint32_t bal = __ballot_sync(0xffffffffu, moved);
+            if (moved) {
+                const uint32_t d = np + __popc(bal & ((1u << lane) - 1));
+                st->dst[d] = S.ext_pos[e];
+                st->src[d] = S.ext_orig[e];
+            }
+            np += __popc(bal);
+        }
+        if (lane == 0) st->npairs = np;
+        return;
+    }
+
+    if (warp == 1) {
+        // ---- coordinates y (rho = A + y*P), transposed: lane owns coordinates
+        //      lane and lane+32 as position words; then Z ----
+        uint32_t y0[kGjWords] = {0, 0, 0}, y1[kGjWords] = {0, 0, 0};
+        uint32_t t = 0;
+        for (;; ++t) {
+            uint4 e;
+            do { e = ld_log(&S.log[t]); } while (e.w == 0);
+            if (e.w & kLogEnd) break;
+            const uint32_t D[kGjWords] = {e.x, e.y, e.z};
+            const uint32_t tw = t >> 5, tb = t & 31;
+            if (!(e.w & kLogSlow)) {
+                const uint32_t f = e.w & 0xFFu, fw = f >> 5, fb = f & 31;
+                uint32_t E[kGjWords], sw[kGjWords];
+#pragma unroll
+                for (int w = 0; w < kGjWords; ++w) {
+                    E[w] = D[w] & ~(uint32_t(w) == fw ? 1u << fb : 0u);
+                    sw[w] = (uint32_t(w) == fw ? 1u << fb : 0u) ^ (uint32_t(w) == tw ? 1u << tb : 0u);
+                }
+                auto upd = [&](uint32_t (&yc)[kGjWords], uint32_t tc) {
+                    const uint32_t yf = (pick3(yc, fw) >> fb) & 1u;
+                    const uint32_t flip = 0u - (yf ^ uint32_t(tc == t));
+#pragma unroll
+                    for (int w = 0; w < kGjWords; ++w) yc[w] ^= E[w] & flip;
+                    const uint32_t d = 0u - (((pick3(yc, tw) >> tb) & 1u) ^ yf);
+#pragma unroll
+                    for (int w = 0; w < kGjWords; ++w) yc[w] ^= sw[w] & d;
+                };
+                upd(y0, uint32_t(lane));
+                upd(y1, uint32_t(lane) + 32);
+            } else {
+                const uint2 u = S.logu[t];
+                auto upd = [&](uint32_t (&yc)[kGjWords], uint32_t tc) {
+                    const uint32_t um = tc < 32 ? (u.x >> tc) & 1u : (u.y >> (tc - 32)) & 1u;
+                    const uint32_t yf = ((__popc(yc[0] & u.x) + __popc(yc[1] & u.y)) & 1u) ^ um;
+#pragma unroll
+                    for (int w = 0; w < kGjWords; ++w)
+                        if (uint32_t(w) == tw) yc[w] = (yc[w] & ~(1u << tb)) | (yf << tb);
+                    const uint32_t flip = 0u - (yf ^ uint32_t(tc == t));
+#pragma unroll
+                    for (int w = 0; w < kGjWords; ++w) yc[w] ^= D[w] & flip;
+                };
+                upd(y0, uint32_t(lane));
+                upd(y1, uint32_t(lane) + 32);
+            }
+        }
+        // t = r.  Z row k_u = e_u + y_u for u < r: transpose so lane u holds y_u.
+        const uint32_t r = t;
+        uint64_t x0 = uint64_t(y0[0]) | (uint64_t(y0[1]) << 32);
+        uint64_t x1 = uint64_t(y1[0]) | (uint64_t(y1[1]) << 32);
+        warp_transpose64(x0, x1, lane);
+        if (uint32_t(lane) < r) st->Z[(S.log[lane].w >> 8) & 63u] = (1ull << lane) ^ x0;
+        if (uint32_t(lane) + 32 < r) st->Z[(S.log[lane + 32].w >> 8) & 63u] = (1ull << (lane + 32)) ^ x1;
+        asm volatile("bar.sync 1, 96;" ::: "memory");
+        return;
+    }
+
+    // ---- warp 0: the selection chain ----
+    uint32_t c0[kGjWords], c1[kGjWords], live[kGjWords];
+    {
+        uint64_t x0 = uint32_t(lane) < npos ? S.win[lane] : 0;
+        uint64_t x1 = uint32_t(lane) + 32 < npos ? S.win[lane + 32] : 0;
+        uint64_t z0 = uint32_t(lane) + 64 < npos ? S.win[lane + 64] : 0;
+        uint64_t z1 = 0;
+        warp_transpose64(x0, x1, lane);
+        warp_transpose64(z0, z1, lane);
+        c0[0] = uint32_t(x0); c0[1] = uint32_t(x0 >> 32); c0[2] = uint32_t(z0);
+        c1[0] = uint32_t(x1); c1[1] = uint32_t(x1 >> 32); c1[2] = uint32_t(z1);
+#pragma unroll
+        for (int w = 0; w < kGjWords; ++w) {
+            const uint32_t b0 = 32 * w;
+            live[w] = npos >= b0 + 32 ? 0xffffffffu : (npos > b0 ? (1u << (npos - b0)) - 1 : 0u);
+        }
+    }
+    uint32_t ib = 0, n_ext = 0, max_touch = 0;
+    uint64_t sel = 0;
+    bool stop = false;
+#ifdef GJ_PROFILE
+    uint32_t n_slow = 0;
+#endif
+
+    // one-hot mask of position ib over the three words
+    uint32_t ibm[kGjWords] = {1u, 0u, 0u};
+
+    auto step = [&](const int k, const bool hi) {
+        const int kl = k & 31;
+        uint32_t ck[kGjWords], m[kGjWords];
+#pragma unroll
+        for (int w = 0; w < kGjWords; ++w) {
+            ck[w] = __shfl_sync(0xffffffffu, hi ? c1[w] : c0[w], kl);
+            m[w] = ck[w] & live[w];
+        }
+        const uint32_t iw = ib >> 5, ibit = 1u << (ib & 31);
+        if (m[0] | m[1] | m[2]) {
+            // ---- fast: the pivot is a register position; fm = its one-hot mask ----
+            uint32_t fm[kGjWords], E[kGjWords], sw[kGjWords];
+            fm[0] = m[0] & (0u - m[0]);
+            fm[1] = m[0] ? 0u : m[1] & (0u - m[1]);
+            fm[2] = (m[0] | m[1]) ? 0u : m[2] & (0u - m[2]);
+#pragma unroll
+            for (int w = 0; w < kGjWords; ++w) {
+                E[w] = ck[w] ^ fm[w];
+                sw[w] = fm[w] ^ ibm[w];
+            }
+            auto upd = [&](uint32_t (&c)[kGjWords]) {
+                const uint32_t bf = 0u - uint32_t(((c[0] & fm[0]) | (c[1] & fm[1]) | (c[2] & fm[2])) != 0);
+#pragma unroll
+                for (int w = 0; w < kGjWords; ++w) c[w] ^= E[w] & bf;
+                const uint32_t d = bf ^ (0u - uint32_t(((c[0] & ibm[0]) | (c[1] & ibm[1]) | (c[2] & ibm[2])) != 0));
+#pragma unroll
+                for (int w = 0; w < kGjWords; ++w) c[w] ^= sw[w] & d;
+            };
+            // columns < k are never tested again: from k = 32 on only c1 matters
+            if (!hi) upd(c0);
+            upd(c1);
+            const uint32_t f = m[0] ? __ffs(m[0]) - 1 : (m[1] ? 31 + __ffs(m[1]) : 63 + __ffs(m[2]));
+            if (lane == 0) st_log(&S.log[ib], ck[0], ck[1], ck[2], gj_meta(false, k, f));
+            if (f > max_touch) max_touch = f;
+        } else {
+            // ---- slow: search the positions beyond the register block ----
+#ifdef GJ_PROFILE
+            ++n_slow;
+#endif
+            if (lane == 0)
+                while (ld_volatile(&S.done) != ib) {}
+            __syncwarp();
+            __threadfence_block();
+            // ck holds only dead positions (no live one has bit k): the RREF rows
+            // with a 1 in column k.  c_k = e_k + their pivot columns.
+            const uint64_t dk = uint64_t(ck[0]) | (uint64_t(ck[1]) << 32);
+            uint64_t cacc = 0;
+            if ((dk >> lane) & 1) cacc |= 1ull << ((S.log[lane].w >> 8) & 63u);
+            if ((dk >> (lane + 32)) & 1) cacc |= 1ull << ((S.log[lane + 32].w >> 8) & 63u);
+            const uint64_t c = (1ull << k) | warp_or64(cacc);
+            uint32_t found = kNone;
+            uint64_t orr = 0;
+            for (size_t base = npos; base < rows && found == kNone; base += 256) {
+                uint32_t hits[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    const size_t ii = base + 32 * t + lane;
+                    uint64_t vv = 0;
+                    if (ii < winrows) vv = S.win[ii];
+                    else if (ii < rows) vv = A[ii];
+                    orr |= vv;
+                    hits[t] = __ballot_sync(0xffffffffu, ii < rows && (__popcll(c & vv) & 1));
+                }
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+                    if (found == kNone && hits[t]) found = uint32_t(base + 32 * t + __ffs(hits[t]) - 1);
+            }
+            if (found == kNone) {
+                // insertion; when every remaining row is zero no later step selects
+                uint32_t anyl = 0;
+#pragma unroll
+                for (int w = 0; w < kGjWords; ++w) anyl |= ((hi ? 0u : c0[w]) | c1[w]) & live[w];
+                if (warp_or64(orr) == 0 && !__any_sync(0xffffffffu, anyl != 0)) stop = true;
+                return;
+            }
+            const uint64_t x = found < winrows ? S.win[found] : A[found];
+            // reduction set: dead positions u with x[k_u] = 1
+            const bool u0 = uint32_t(lane) < ib && ((x >> ((S.log[lane].w >> 8) & 63u)) & 1);
+            const bool u1 = uint32_t(lane) + 32 < ib && ((x >> ((S.log[lane + 32].w >> 8) & 63u)) & 1);
+            const uint32_t U0 = __ballot_sync(0xffffffffu, u0), U1 = __ballot_sync(0xffffffffu, u1);
+            auto upd = [&](uint32_t (&c)[kGjWords], int l) {
+                const uint32_t rx = uint32_t((x >> l) & 1) ^ ((__popc(c[0] & U0) + __popc(c[1] & U1)) & 1u);
+#pragma unroll
+                for (int w = 0; w < kGjWords; ++w)
+                    if (uint32_t(w) == iw) c[w] = (c[w] & ~ibit) | (rx ? ibit : 0u);
+                const uint32_t m = 0u - rx;
+#pragma unroll
+                for (int w = 0; w < kGjWords; ++w) c[w] ^= ck[w] & m;
+            };
+            if (!hi) upd(c0, lane);
+            upd(c1, lane + 32);
+            if (lane == 0) {
+                const uint64_t vb = S.win[ib];
+                const uint32_t ob = S.orig[ib];
+                if (found < winrows) {
+                    S.win[ib] = x;
+                    S.orig[ib] = S.orig[found];
+                    S.win[found] = vb;
+                    S.orig[found] = ob;
+                } else {
+                    A[found] = vb;
+                    S.win[ib] = x;
+                    uint32_t e = 0;
+                    while (e < n_ext && S.ext_pos[e] != found) ++e;
+                    if (e == n_ext) { S.ext_pos[e] = found; S.ext_orig[e] = found; }
+                    S.orig[ib] = S.ext_orig[e];
+                    S.ext_orig[e] = ob;
+                }
+                S.logu[ib] = make_uint2(U0, U1);
+            }
+            __syncwarp();
+            if (found >= winrows) {
+                const uint32_t e0 = n_ext;  // uniform recount
+                uint32_t present = 0;
+                for (uint32_t e = 0; e < e0; ++e) present |= (S.ext_pos[e] == found);
+                if (!present) ++n_ext;
+            } else if (found > max_touch) {
+                max_touch = found;
+            }
+            __threadfence_block();
+            if (lane == 0) st_log(&S.log[ib], ck[0], ck[1], ck[2], gj_meta(true, k, 0));
+        }
+#pragma unroll
+        for (int w = 0; w < kGjWords; ++w) live[w] &= ~ibm[w];
+        ibm[2] = (ibm[2] << 1) | (ibm[1] >> 31);
+        ibm[1] = (ibm[1] << 1) | (ibm[0] >> 31);
+        ibm[0] = ibm[0] << 1;
+        sel |= 1ull << k;
+        ++ib;
+    };
+    for (int k = 0; k < 32 && !stop; ++k) step(k, false);
+    for (int k = 32; k < 64 && !stop; ++k) step(k, true);
+
+    if (lane == 0) st_log(&S.log[ib], 0, 0, 0, kLogValid | kLogEnd | ib);
+#ifdef GJ_PROFILE
+    const long long t_chain = clock64();
+#endif
+    if (!((sel >> lane) & 1)) st->Z[lane] = 0;
+    if (!((sel >> (lane + 32)) & 1)) st->Z[lane + 32] = 0;
+    if (lane == 0) {
+        S.n_ext = n_ext;
+        S.span = ib > 0 ? max_touch + 1 : 0;
+        st->R = uint32_t(R);
+        st->r = ib;
+        st->flags = 0;
+    }
+    asm volatile("bar.sync 1, 96;" ::: "memory");
+#ifdef GJ_PROFILE
+    if (lane == 0) {
+        long long* pr = reinterpret_cast<long long*>(st->src);
+        pr[61] = t_loaded - t_start; pr[62] = t_chain - t_loaded; pr[63] = clock64() - t_chain;
+        pr[59] = ib;
+        pr[58] = n_slow;
+        pr[60] = 0;
+    }
+#endif
+}
+
+static bool g_panel_gj = true;  // F2GPU_PANEL=0: the transposed-M k_panel
+
 cudaError_t launch_panel(uint64_t* col, size_t n, PanelState* st_all, int j, cudaStream_t s,
                          const uint32_t* wait_flag, uint32_t wait_count) {
-    k_panel<<<1, kPanelThreads, sizeof(PanelSmem), s>>>(col, n, st_all, j, wait_flag, wait_count);
+    if (g_panel_gj)
+        k_panel_gj<<<1, kPanelThreads, sizeof(PanelGjSmem), s>>>(col, n, st_all, j, wait_flag, wait_count);
+    else
+        k_panel<<<1, kPanelThreads, sizeof(PanelSmem), s>>>(col, n, st_all, j, wait_flag, wait_count);
     return cudaGetLastError();
 }
 
@@ -1806,33 +2259,6 @@ cudaError_t launch_xor(uint64_t* dst, size_t sd, const uint64_t* a, size_t sa, c
 // ---------------------------------------------------------------------------
 // bit transpose: one warp per 64x64 tile (transpose_tile, bit_matrix.hpp:59-70)
 // ---------------------------------------------------------------------------
-// 64x64 bit-matrix transpose held in a warp: lane L holds rows L (x0) and L+32
-// (x1) on entry and columns L / L+32 on exit.  One register swap for the 32-bit
-// halves, then five shuffle butterflies -- no shared memory, no bank conflicts.
-__device__ __forceinline__ void warp_transpose64(uint64_t& x0, uint64_t& x1, int lane) {
-    {
-        const uint64_t t = ((x0 >> 32) ^ x1) & 0x00000000FFFFFFFFull;
-        x1 ^= t;
-        x0 ^= t << 32;
-    }
-    const uint64_t masks[5] = {0x0000FFFF0000FFFFull, 0x00FF00FF00FF00FFull, 0x0F0F0F0F0F0F0F0Full,
-                               0x3333333333333333ull, 0x5555555555555555ull};
-#pragma unroll
-    for (int st = 0; st < 5; ++st) {
-        const int j = 16 >> st;
-        const uint64_t msk = masks[st];
-        const uint64_t y0 = __shfl_xor_sync(0xffffffffu, x0, j);
-        const uint64_t y1 = __shfl_xor_sync(0xffffffffu, x1, j);
-        if (!(lane & j)) {
-            x0 ^= (((x0 >> j) ^ y0) & msk) << j;
-            x1 ^= (((x1 >> j) ^ y1) & msk) << j;
-        } else {
-            x0 ^= ((y0 >> j) ^ x0) & msk;
-            x1 ^= ((y1 >> j) ^ x1) & msk;
-        }
-    }
-}
-
 // out (m x n) = a (n x m)^T.  Grid: blockIdx.y = input word-column q, each warp
 // transposes kTrTilesPerWarp consecutive 64-row tiles of it (loads issued
 // together); no integer division in the kernel.
@@ -1950,6 +2376,10 @@ cudaError_t init_kernel_attrs() {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(sizeof(PanelSmem)));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_panel_gj, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(sizeof(PanelGjSmem)));
+    if (const char* pk = getenv("F2GPU_PANEL")) g_panel_gj = pk[0] != '0';
     return e;
 }
 
