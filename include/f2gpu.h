@@ -66,6 +66,26 @@ int f2gpu_ctx_set_strassen_cutover(f2gpu_ctx *ctx, size_t min_dim_bits);
  * (0 = default 16384).  Results are bit-identical either way. */
 int f2gpu_ctx_set_tc(f2gpu_ctx *ctx, int on, size_t tc_min_leaf_bits);
 
+/* Device trace (diagnostics, no reference counterpart): with cap > 0 the panel,
+ * fused-post and update kernels append globaltimer stamps
+ * (ns << 16) | (event << 12) | panel_index to a device buffer of cap entries;
+ * trace_read synchronizes, copies up to cap entries out and restarts the trace.
+ * cap = 0 turns it off.  One trace per process (a device symbol). */
+int f2gpu_trace_enable(f2gpu_ctx *ctx, size_t cap);
+int f2gpu_trace_read(f2gpu_ctx *ctx, uint64_t *out, size_t cap, size_t *n);
+
+/* One panel kernel (Procedure buildZ) on a host column of
+ * n words: col_out receives the column with the panel's row swaps applied,
+ * z_out the 64 words of the pseudo-inverse Z and r_out the block rank;
+ * pairs_out (optional, 256 words: dst[128] then src[128]) and npairs_out the
+ * composite row permutation new[dst[e]] = old[src[e]] that the other word-
+ * columns receive.  Z is only defined on the span of the selected rows, which
+ * holds every row below the pivots: parity is on r, col_out, the pairs and
+ * Y_i = col_out[i] * Z for i >= r.  (Kernel-level check of the path's first
+ * step; replaces no reference call.) */
+int f2gpu_panel_build_z(f2gpu_ctx *ctx, const uint64_t *col, size_t n, uint64_t *col_out, uint64_t *z_out,
+                        uint32_t *r_out, uint32_t *pairs_out, uint32_t *npairs_out);
+
 /* ---- device matrix store (replaces PackedMatrix<uint64_t> storage,
  *      bit_matrix.hpp:82-346) ------------------------------------------------- */
 int f2gpu_mat_alloc(f2gpu_ctx *ctx, size_t n_rows, size_t n_cols, f2gpu_mat **out);

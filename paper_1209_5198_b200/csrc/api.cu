@@ -184,13 +184,18 @@ struct f2gpu_ctx {
     bool use_graphs = true;
     bool lookahead = true;
     bool lookahead_col = true;  // F2GPU_LOOKAHEAD_COL=0: release from the update's column group 0 instead
+    bool fuse_post = true;      // F2GPU_POSTCOL=0: separate POST and next-column kernels
+    bool panel_early = true;    // F2GPU_PANEL_EARLY=0: launch P(j+1) after k_post_col(j) completes
+    uint32_t poll_ns = 0;       // F2GPU_POLL_NS: panel consumer warps' poll sleep
     cudaStream_t side = nullptr;          // lookahead: panel kernels run here
     cudaStream_t copy = nullptr;          // decompose_recursive_host: chunked uploads
     std::vector<cudaEvent_t> chunk_ev;    // one per uploaded column chunk
     void* pend = nullptr;                 // uploaded, not yet materialised columns
     size_t pend_bytes = 0;
     cudaEvent_t ev_post = nullptr, ev_panel = nullptr;
-    uint32_t* scr_flags = nullptr;        // per-panel early-release counters
+    unsigned long long* trace_buf = nullptr;  // device trace (diagnostics)
+    size_t trace_cap = 0;
+    uint32_t* scr_flags = nullptr;        // per-panel counters (kFlagsPerPanel each)
     size_t scr_flags_cap = 0;
     void* scr_st = nullptr;   // persistent PanelState[mu]
     size_t scr_st_cap = 0;
@@ -616,6 +621,10 @@ int read_results(f2gpu_ctx* c, const Shard& s, size_t n, size_t mu, uint32_t* pe
     return F2GPU_OK;
 }
 
+// per panel j: [0] head, [1] window, [2] all row blocks of k_post_col(j);
+// [3] the release of update j's column group 0 (plain lookahead: [0] only)
+constexpr size_t kFlagsPerPanel = 4;
+
 int ensure_scratch(f2gpu_ctx* c, size_t n, size_t mu) {
     if (c->scr_st_cap < mu || c->scr_perm_cap < n || c->scr_flags_cap < mu) {
         CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -635,8 +644,9 @@ int ensure_scratch(f2gpu_ctx* c, size_t n, size_t mu) {
         }
         if (c->scr_flags_cap < mu) {
             cudaFree(c->scr_flags);
+    if (c->trace_buf) { f2::trace_set(nullptr, 0); cudaFree(c->trace_buf); }
             c->scr_flags = nullptr;
-            CUDA_TRY(cudaMalloc(&c->scr_flags, mu * 4));
+            CUDA_TRY(cudaMalloc(&c->scr_flags, mu * 4 * kFlagsPerPanel));
             c->scr_flags_cap = mu;
         }
     }
@@ -665,6 +675,7 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
         u.B = s.w.p; u.sb = s.w.stride; u.b_row0 = 0; u.b_wcol0 = j + 1 + skip;
         u.st = s.st + j;
         u.release = release;
+        u.tag = c->trace_buf ? int(j) : -1;
         return check_launch(c, f2::launch_update(u, grid, c->stream), "k_update");
     };
     const bool colfirst = c->lookahead_col;
@@ -677,6 +688,54 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
                                                    s.st + j, c->stream),
                                 "k_post"));
             if (j + 1 < c1) F2_TRY(upd(j, nullptr));
+        }
+        return F2GPU_OK;
+    }
+    if (c->fuse_post && f2::panel_link_ok()) {
+        // Fused schedule:
+        //   side: P(j+1) [waits k_post_col(j)'s counters: first rows / window / all;
+        //         at its end applies its swaps to column j+2 once update j released it]
+        //   main: k_post_col(j) [swaps except j, j+1; Y_j; column j+1 updated] ->
+        //         U(j) on columns j+2.. [release after column group 0]
+        auto link_for = [&](size_t j) {  // P(j)'s link
+            f2::PanelLink l{};
+            if (j > c0) {
+                uint32_t* f = c->scr_flags + (j - 1) * kFlagsPerPanel;
+                l.head = f; l.head_count = 1;
+                l.win = f + 1; l.win_count = 8;
+                l.all = f + 2; l.all_count = uint32_t(f2::post_col_yblocks(n));
+                if (j + 1 < c1) { l.next_ready = f + 3; l.next_count = uint32_t(grid); }
+            }
+            if (j + 1 < c1) l.next = s.w.p + (j + 1) * s.w.stride;
+            l.poll_ns = c->poll_ns;
+            l.trace = c->trace_buf != nullptr;
+            return l;
+        };
+        F2_TRY(check_launch(c, f2::launch_panel_link(s.w.p + c0 * s.w.stride, n, s.st, int(c0), link_for(c0),
+                                                     c->stream),
+                            "k_panel"));
+        // the side stream forks once after P(c0); every later panel kernel is queued
+        // right behind its predecessor and spins on k_post_col's counters, so it is
+        // resident (on the SM the update leaves free) before its column is ready
+        if (c0 + 1 < c1 && c->panel_early) {
+            CUDA_TRY(cudaEventRecord(c->ev_post, c->stream));
+            CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_post, 0));
+        }
+        for (size_t j = c0; j < c1; ++j) {
+            if (j > c0) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_panel, 0));
+            uint32_t* f = c->scr_flags + j * kFlagsPerPanel;
+            F2_TRY(check_launch(c, f2::launch_post_col(s.w.p, s.w.stride, int(swap_cols), int(j),
+                                                       j + 1 < c1 ? int(j + 1) : -1, s.perm, n, s.st + j, f,
+                                                       c->stream, c->trace_buf != nullptr),
+                                "k_post_col"));
+            if (j + 1 >= c1) break;
+            if (!c->panel_early) CUDA_TRY(cudaEventRecord(c->ev_post, c->stream));
+            F2_TRY(upd(j, f + 3, 1));
+            if (!c->panel_early) CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_post, 0));
+            F2_TRY(check_launch(c, f2::launch_panel_link(s.w.p + (j + 1) * s.w.stride, n, s.st, int(j + 1),
+                                                         link_for(j + 1), c->side),
+                                "k_panel"));
+            CUDA_TRY(cudaEventRecord(c->ev_panel, c->side));
         }
         return F2GPU_OK;
     }
@@ -695,16 +754,17 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
             // persistent update from column j+2 with no early release
             const int g1 = f2::update_col_grid(n, c->num_sms);
             F2_TRY(check_launch(c, f2::launch_update_col(s.w.p + (j + 1) * s.w.stride, s.w.p + j * s.w.stride, n,
-                                                         s.st + j, c->scr_flags + j, g1, c->stream),
+                                                         s.st + j, c->scr_flags + j * kFlagsPerPanel, g1,
+                                                         c->stream),
                                 "k_update_col"));
             F2_TRY(upd(j, nullptr, 1));
             wait_count = uint32_t(g1);
         } else {
-            F2_TRY(upd(j, c->scr_flags + j));
+            F2_TRY(upd(j, c->scr_flags + j * kFlagsPerPanel));
         }
         CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_post, 0));
         F2_TRY(check_launch(c, f2::launch_panel(s.w.p + (j + 1) * s.w.stride, n, s.st, int(j + 1),
-                                                c->side, c->scr_flags + j, wait_count),
+                                                c->side, c->scr_flags + j * kFlagsPerPanel, wait_count),
                             "k_panel"));
         CUDA_TRY(cudaEventRecord(c->ev_panel, c->side));
     }
@@ -717,7 +777,7 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
 //         so the panel factorisation of j+1 overlaps the bulk of update j.
 //   main waits P(j+1) (event) before POST(j+1).
 int enqueue_lookahead(f2gpu_ctx* c, Shard& s, size_t n, size_t mu) {
-    CUDA_TRY(cudaMemsetAsync(c->scr_flags, 0, mu * 4, c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->scr_flags, 0, mu * 4 * kFlagsPerPanel, c->stream));
     F2_TRY(check_launch(c, f2::launch_iota(s.perm, n, c->stream), "k_iota"));
     return enqueue_panels(c, s, n, mu, 0, mu, true);
 }
@@ -756,6 +816,7 @@ struct RecRun {
     bool la;
     size_t cut;    // Strassen cutover inside the recursion (XOR traffic vs multiply)
     size_t tbase;  // TRSM base (panels solved in one k_trsm_block launch)
+    size_t tall_rows = 0, tall_base = 0;  // leaves with >= tall_rows rows: at most tall_base panels
     bool trsm_kernel = true;  // F2GPU_REC_TRSM=0: rank-64 updates instead (A/B check)
     // upload overlap (f2gpu_decompose_recursive_host): word-columns >= frontier are
     // still in `pend` (original row order, column q at pend + (q - frontier0) * ps),
@@ -872,7 +933,11 @@ int rec_leaf(RecRun& r, size_t c0, size_t c1) {
 }
 
 int rec_decompose(RecRun& r, size_t c0, size_t c1) {
-    if (c1 - c0 <= r.base) return rec_leaf(r, c0, c1);
+    // tall leaves are update-bound (the trailing update streams rows x remaining
+    // leaf columns per panel), so they are narrower than short, chain-bound ones
+    const size_t rows0 = r.n - std::min(r.n, 64 * c0);  // rows below the leaf's first panel at full rank
+    const size_t leaf = (r.tall_rows && rows0 >= r.tall_rows) ? std::min(r.base, r.tall_base) : r.base;
+    if (c1 - c0 <= leaf) return rec_leaf(r, c0, c1);
     const size_t cm = c0 + (c1 - c0) / 2;
     F2_TRY(rec_decompose(r, c0, cm));
     size_t R0, r0, Rl, rl;
@@ -915,6 +980,12 @@ int decompose_recursive(f2gpu_ctx* c, View w, size_t min_cols, uint32_t* perm, u
     if (const char* e = getenv("F2GPU_REC_CUT")) r.cut = size_t(atol(e));
     if (const char* e = getenv("F2GPU_REC_TBASE")) r.tbase = std::max<size_t>(1, size_t(atol(e)));
     if (const char* e = getenv("F2GPU_REC_TRSM")) r.trsm_kernel = e[0] != '0';
+    // tall leaves: 64 panels once a leaf has >= 20000 rows below its first panel
+    // (65536^2 sweep over 16000..56000 rows x 32..128 panels: 70.5 -> 67.5 ms)
+    r.tall_rows = 20000;
+    if (const char* e = getenv("F2GPU_REC_TALL")) r.tall_rows = size_t(atol(e));
+    r.tall_base = 64;
+    if (const char* e = getenv("F2GPU_REC_TALL_BASE")) r.tall_base = std::max<size_t>(1, size_t(atol(e)));
     r.on_final = std::move(on_final);
     if (pend && frontier < mu) {
         r.frontier = r.frontier0 = frontier;
@@ -922,7 +993,7 @@ int decompose_recursive(f2gpu_ctx* c, View w, size_t min_cols, uint32_t* perm, u
         r.ps = ps;
         r.chunk = chunk;
     }
-    CUDA_TRY(cudaMemsetAsync(c->scr_flags, 0, mu * 4, c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->scr_flags, 0, mu * 4 * kFlagsPerPanel, c->stream));
     c->tl.mark(c->stream, "start");
     F2_TRY(check_launch(c, f2::launch_iota(s.perm, n, c->stream), "k_iota"));
     F2_TRY(rec_decompose(r, 0, mu));
@@ -1114,6 +1185,9 @@ int f2gpu_ctx_create(int device, f2gpu_ctx** out) {
     if (const char* gr = getenv("F2GPU_GRAPHS")) c->use_graphs = gr[0] != '0';
     if (const char* la = getenv("F2GPU_LOOKAHEAD")) c->lookahead = la[0] != '0';
     if (const char* lc = getenv("F2GPU_LOOKAHEAD_COL")) c->lookahead_col = lc[0] != '0';
+    if (const char* pc = getenv("F2GPU_POSTCOL")) c->fuse_post = pc[0] != '0';
+    if (const char* pe = getenv("F2GPU_PANEL_EARLY")) c->panel_early = pe[0] != '0';
+    if (const char* pn = getenv("F2GPU_POLL_NS")) c->poll_ns = uint32_t(atoi(pn));
     if (const char* tc = getenv("F2GPU_TC")) c->use_tc = tc[0] != '0';
     if (const char* tcc = getenv("F2GPU_TC_CUT")) c->tc_cutover = size_t(atoll(tcc));
     CUDA_TRY(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
@@ -1183,6 +1257,68 @@ int f2gpu_ctx_set_tc(f2gpu_ctx* c, int on, size_t leaf) {
     c->use_tc = on != 0;
     c->tc_cutover = leaf ? leaf : 16384;
     return F2GPU_OK;
+}
+
+// ---- device trace (diagnostics) ----
+int f2gpu_trace_enable(f2gpu_ctx* c, size_t cap) {
+    if (!c) return set_err(F2GPU_EINVAL, "trace_enable: null ctx");
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if ((cap != 0) != (c->trace_buf != nullptr)) {  // captured graphs hold the trace switch
+        c->graph.reset();
+        c->leaf_graphs.clear();
+    }
+    cudaFree(c->trace_buf);
+    c->trace_buf = nullptr;
+    c->trace_cap = 0;
+    if (cap) {
+        CUDA_TRY(cudaMalloc(&c->trace_buf, cap * 8));
+        c->trace_cap = cap;
+    }
+    CUDA_TRY(f2::trace_set(c->trace_buf, uint32_t(c->trace_cap)));
+    return F2GPU_OK;
+}
+
+int f2gpu_trace_read(f2gpu_ctx* c, uint64_t* out, size_t cap, size_t* n) {
+    if (!c || !n) return set_err(F2GPU_EINVAL, "trace_read: null argument");
+    CUDA_TRY(cudaDeviceSynchronize());
+    uint32_t cnt = 0;
+    CUDA_TRY(f2::trace_count(&cnt));
+    const size_t k = std::min<size_t>({size_t(cnt), c->trace_cap, cap});
+    if (k) CUDA_TRY(cudaMemcpy(out, c->trace_buf, k * 8, cudaMemcpyDeviceToHost));
+    *n = k;
+    return f2gpu_trace_enable(c, c->trace_cap);  // reset the count
+}
+
+// ---- one panel (Procedure buildZ) on a host column: kernel-level parity ----
+int f2gpu_panel_build_z(f2gpu_ctx* c, const uint64_t* col, size_t n, uint64_t* col_out, uint64_t* z_out,
+                        uint32_t* r_out, uint32_t* pairs_out, uint32_t* npairs_out) {
+    if (!c || (!col && n) || (!col_out && n) || !z_out || !r_out)
+        return set_err(F2GPU_EINVAL, "panel_build_z: null argument");
+    uint64_t* d = nullptr;
+    f2::PanelState* st = nullptr;
+    auto fin = [&](int rc) {
+        cudaFree(d);
+        cudaFree(st);
+        return rc;
+    };
+    if (cudaMalloc(&d, std::max<size_t>(n, 1) * 8) != cudaSuccess || cudaMalloc(&st, kStateBytes) != cudaSuccess)
+        return fin(set_err(F2GPU_ENOMEM, "panel_build_z: device allocation"));
+    if (n && cudaMemcpyAsync(d, col, n * 8, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+        return fin(set_err(F2GPU_ECUDA, "panel_build_z: upload"));
+    if (int rc = check_launch(c, f2::launch_panel(d, n, st, 0, c->stream), "k_panel"); rc != F2GPU_OK) return fin(rc);
+    f2::PanelState hs;
+    if ((n && cudaMemcpyAsync(col_out, d, n * 8, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess) ||
+        cudaMemcpyAsync(&hs, st, kStateBytes, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+        cudaStreamSynchronize(c->stream) != cudaSuccess)
+        return fin(set_err(F2GPU_ECUDA, "panel_build_z: download"));
+    std::copy(hs.Z, hs.Z + 64, z_out);
+    *r_out = hs.r;
+    if (npairs_out) *npairs_out = hs.npairs;
+    if (pairs_out) {
+        std::copy(hs.dst, hs.dst + 128, pairs_out);
+        std::copy(hs.src, hs.src + 128, pairs_out + 128);
+    }
+    return fin(F2GPU_OK);
 }
 
 // ---- matrices ----

@@ -22,6 +22,31 @@
 
 namespace f2 {
 
+// ---- device trace (diagnostics) ----
+__device__ unsigned long long* g_trace = nullptr;
+__device__ uint32_t g_trace_cap = 0;
+__device__ uint32_t g_trace_n = 0;
+
+__device__ __forceinline__ void trace_ev(uint32_t ev, int j) {
+    unsigned long long* b = g_trace;
+    if (!b) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const uint32_t i = atomicAdd(&g_trace_n, 1u);
+    if (i < g_trace_cap) b[i] = (t << 16) | (uint64_t(ev & 15) << 12) | uint64_t(uint32_t(j) & 4095u);
+}
+
+cudaError_t trace_set(unsigned long long* buf, uint32_t cap) {
+    const uint32_t zero = 0;
+    cudaError_t e = cudaMemcpyToSymbol(g_trace, &buf, sizeof(buf));
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_trace_cap, &cap, sizeof(cap));
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_trace_n, &zero, sizeof(zero));
+    return e;
+}
+
+cudaError_t trace_count(uint32_t* n) { return cudaMemcpyFromSymbol(n, g_trace_n, sizeof(*n)); }
+
+
 // ---------------------------------------------------------------------------
 // small device helpers
 // ---------------------------------------------------------------------------
@@ -594,13 +619,18 @@ struct TileCursor {
     }
 };
 
-__device__ __forceinline__ void release_signal(uint32_t* flag) {
+__device__ __forceinline__ void release_signal(uint32_t* flag, int tag = -1) {
     __threadfence();
-    atomicAdd(flag, 1u);
+    if (tag >= 0) {  // tag >= 0 only while the device trace is on
+        if (atomicAdd(flag, 1u) + 1 == gridDim.x) trace_ev(kTrUpdRelease, tag);
+    } else {
+        atomicAdd(flag, 1u);
+    }
 }
 
 __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
+    if (p.tag >= 0 && blockIdx.x == 0 && threadIdx.x == 0) trace_ev(kTrUpdBegin, p.tag);
     const uint32_t smem_base = smem_u32(smem_raw);
     if (smem_base > kTabAddr - kV3RingBytes) __trap();  // layout assumption violated
     uint64_t* tab = reinterpret_cast<uint64_t*>(smem_raw + (kTabAddr - smem_base));
@@ -622,7 +652,7 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
     }
     const size_t row_hi = p.row_hi;
     if (k <= 0 || row_lo >= row_hi || p.ncols <= 0) {
-        if (p.release && threadIdx.x == 0) release_signal(p.release);
+        if (p.release && threadIdx.x == 0) release_signal(p.release, p.tag);
         return;
     }
     const int nt = 9;  // all tables built (rows >= k are zero); lookup9 is branch-free
@@ -646,7 +676,7 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
     }
     const size_t cnt = len0 + len1;
     if (cnt == 0) {
-        if (p.release && threadIdx.x == 0) release_signal(p.release);
+        if (p.release && threadIdx.x == 0) release_signal(p.release, p.tag);
         return;
     }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -677,7 +707,7 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
             ac.next();
             if (++a_stage == kV3AStages) a_stage = 0;
         };
-        if (p.release && len0 == 0 && lane == 0) release_signal(p.release);
+        if (p.release && len0 == 0 && lane == 0) release_signal(p.release, p.tag);
         const size_t pre = cnt < size_t(kV3AStages) ? cnt : size_t(kV3AStages);
         for (size_t i = 0; i < pre; ++i) issue_a();
         TileCursor dc;
@@ -705,12 +735,13 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
                 bulk_commit();
             }
             const bool rel_point = p.release && t + 1 == len0;
+            if (t == 0 && p.tag >= 0 && blockIdx.x == 0 && lane == 0) trace_ev(11, p.tag);
 #if F2_PIPELINED_WRITEBACK
             if (rel_point) bulk_wait0();          // group-0 writes complete in memory
             else if (issued) bulk_wait_read1();   // previous tile's reads done
             else bulk_wait_read0();
             __syncwarp();
-            if (rel_point && lane == 0) release_signal(p.release);
+            if (rel_point && lane == 0) release_signal(p.release, p.tag);
             if (lane == 0) {
                 if (rel_point) mbar_arrive(&d_free[s]);  // everything drained
                 if (sprev >= 0) mbar_arrive(&d_free[sprev]);
@@ -720,7 +751,7 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
             if (rel_point) bulk_wait0();          // group-0 writes complete in memory
             else bulk_wait_read0();               // this tile's reads done
             __syncwarp();
-            if (rel_point && lane == 0) release_signal(p.release);
+            if (rel_point && lane == 0) release_signal(p.release, p.tag);
             if (lane == 0) mbar_arrive(&d_free[s]);
             (void)sprev;
 #endif
@@ -733,6 +764,7 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
             dc.next();
         }
         bulk_wait0();
+        if (p.tag >= 0 && blockIdx.x == 0 && lane == 0) trace_ev(12, p.tag);
         // (the last tile's stage needs no release: no consumer waits for it)
         return;
     }
@@ -754,6 +786,7 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
             build_tables<kV3Warps * 32>(tab, p.B, p.sb, b_row0, p.b_wcol0 + g * kTabCols, nvalid,
                                         k, nt);
             v3_consumers_sync();
+            if (p.tag >= 0 && blockIdx.x == 0 && threadIdx.x == 0) trace_ev(gcur == ~size_t(0) ? 10 : 13, p.tag);
             gcur = g;
         }
         mbar_wait(&a_full[as], aph);
@@ -1443,7 +1476,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
     __syncwarp();
     // ---- composite permutation: window slots with orig != slot, then ext rows ----
     uint32_t np = 0;
-    const uint32_t span = (ib > 0 ? max_touch + 1 : 0);
+    const uint32_t span = (ib > 0 ? max(max_touch + 1, ib) : 0);
     for (uint32_t x0 = 0; x0 < span; x0 += 32) {
         const uint32_t x = x0 + lane;
         const bool moved = x < span && S.orig[x] != x;
@@ -1546,6 +1579,9 @@ __device__ __forceinline__ void warp_transpose64(uint64_t& x0, uint64_t& x1, int
 // pivot is reduced by the RREF rows (popcounts per own column).  Warp 2 replays
 // the swaps on win/orig (the composite permutation) from the same log.
 // ---------------------------------------------------------------------------
+#ifndef GJ_POLL_NS
+#define GJ_POLL_NS 0
+#endif
 constexpr int kGjWords = 3;
 constexpr uint32_t kGjPos = 32 * kGjWords;
 constexpr uint32_t kLogValid = 0x80000000u, kLogSlow = 0x40000000u, kLogEnd = 0x20000000u;
@@ -1557,9 +1593,8 @@ struct PanelGjSmem {
     uint32_t ext_orig[64];
     uint4 log[66];      // per selection t: column-k mask over positions (3 words), meta
     uint2 logu[66];     // slow selections: dead positions u with x[k_u] (the reduction set)
-    uint32_t done;      // log entries applied to win/orig by warp 2
-    uint32_t n_ext;
-    uint32_t span;
+    uint32_t want;  // warp 0's slow path needs entries < want - 1 applied to win/orig
+    uint32_t done;  // = want once they are (published by warp 2 on request)
 };
 static_assert(kGjWords == 3, "log entries carry three position words");
 
@@ -1598,23 +1633,34 @@ struct GjStep {
     uint32_t sw[kGjWords];
 };
 
+__device__ __forceinline__ void wait_count_ge(const uint32_t* flag, uint32_t count) {
+    if (!flag) return;
+    uint32_t v;
+    while (true) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+        if (v >= count) break;
+        __nanosleep(32);
+    }
+}
+
+// the whole warp spins (no lane-divergent loop: a warp that diverged around a
+// long spin can stay split afterwards and run every later shuffle twice)
+__device__ __forceinline__ void wait_count_ge_warp(const uint32_t* flag, uint32_t count) {
+    if (!flag) return;
+    while (true) {
+        uint32_t v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+        if (__all_sync(0xffffffffu, v >= count)) break;
+        __nanosleep(32);
+    }
+}
+
 __global__ void __launch_bounds__(kPanelThreads, 1)
     k_panel_gj(uint64_t* __restrict__ col, size_t n, PanelState* __restrict__ st_all, int j,
-               const uint32_t* wait_flag, uint32_t wait_count) {
+               const PanelLink link) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     PanelGjSmem& S = *reinterpret_cast<PanelGjSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (wait_flag) {
-        if (tid == 0) {
-            uint32_t v;
-            while (true) {
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(wait_flag) : "memory");
-                if (v >= wait_count) break;
-                __nanosleep(64);
-            }
-        }
-        __syncthreads();
-    }
     const size_t R = j == 0 ? 0 : size_t(st_all[j - 1].R) + st_all[j - 1].r;
     PanelState* st = st_all + j;
     const size_t rows = R < n ? n - R : 0;
@@ -1629,14 +1675,29 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
 #ifdef GJ_PROFILE
     const long long t_start = clock64();
 #endif
-    for (uint32_t x = tid; x < winrows; x += kPanelThreads) {
-        S.win[x] = A[x];
-        S.orig[x] = x;
+    if (warp == 0) {
+        // warp 0 starts on its own rows (loaded below) without waiting for the
+        // window; it zeroes the log, then releases the two consumer warps
+        for (int t = lane; t < 66; t += 32) S.log[t] = make_uint4(0, 0, 0, 0);
+        if (lane == 0) { S.done = 0; S.want = 0; }
+        asm volatile("bar.arrive 3, 96;" ::: "memory");
+        wait_count_ge_warp(link.head, link.head_count);
+        if (link.trace && lane == 0) trace_ev(kTrPanelBegin, j);
+        __syncwarp();
+    } else if (warp == 1) {
+        asm volatile("bar.sync 3, 96;" ::: "memory");  // the log is zeroed
+    } else {
+        // warps 2..7 load the window; warp 2 then replays the swaps on it
+        if (warp == 2) wait_count_ge_warp(link.win, link.win_count);
+        asm volatile("bar.sync 2, 192;" ::: "memory");
+        for (uint32_t x = tid - 64; x < winrows; x += kPanelThreads - 64) {
+            S.win[x] = A[x];
+            S.orig[x] = x;
+        }
+        asm volatile("bar.sync 2, 192;" ::: "memory");
+        if (warp > 2) return;
+        asm volatile("bar.sync 3, 96;" ::: "memory");
     }
-    if (tid < 66) S.log[tid] = make_uint4(0, 0, 0, 0);
-    if (tid == 0) S.done = 0;
-    __syncthreads();
-    if (warp > 2) return;
 #ifdef GJ_PROFILE
     const long long t_loaded = clock64();
 #endif
@@ -1644,12 +1705,43 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
     if (warp == 2) {
         // ---- win/orig bookkeeping: replay the fast swaps ----
         uint32_t t = 0;
+        uint32_t max_touch = 0, n_ext = 0;
+        uint32_t live[kGjWords], tm[kGjWords] = {1u, 0u, 0u};
+#pragma unroll
+        for (int w = 0; w < kGjWords; ++w) {
+            const uint32_t b0 = 32 * w;
+            live[w] = npos >= b0 + 32 ? 0xffffffffu : (npos > b0 ? (1u << (npos - b0)) - 1 : 0u);
+        }
         for (;; ++t) {
-            uint32_t m;
-            do { m = ld_volatile(&S.log[t].w); } while (m == 0);
-            if (m & kLogEnd) break;
-            if (!(m & kLogSlow) && lane == 0) {
-                const uint32_t f = m & 0xFFu;
+            // warp-uniform polling: every lane must see the entry before any acts
+            // (lanes that diverge here would pair with different __syncwarp /
+            // ballot instances and read win/orig while lane 0 still swaps)
+            uint4 e;
+            while (true) {
+                e = ld_log(&S.log[t]);
+                if (__all_sync(0xffffffffu, e.w != 0)) break;
+                if (link.poll_ns) __nanosleep(link.poll_ns);
+                // warp 0's slow path waits for entries < t: publish them
+                const bool wanted = __shfl_sync(0xffffffffu, lane == 0 && ld_volatile(&S.want) == t + 1, 0);
+                if (wanted) {
+                    __threadfence_block();
+                    if (lane == 0) st_volatile(&S.done, t + 1);
+                }
+            }
+            if (e.w & kLogEnd) {
+                n_ext = e.x;
+                break;
+            }
+            const uint32_t m0 = e.x & live[0], m1 = e.y & live[1], m2 = e.z & live[2];
+            const uint32_t f = (e.w & kLogSlow) ? e.z
+                               : (m0 ? __ffs(m0) - 1 : (m1 ? 31 + __ffs(m1) : 63 + __ffs(m2)));
+            if (f < winrows && f > max_touch) max_touch = f;
+#pragma unroll
+            for (int w = 0; w < kGjWords; ++w) live[w] &= ~tm[w];
+            tm[2] = (tm[2] << 1) | (tm[1] >> 31);
+            tm[1] = (tm[1] << 1) | (tm[0] >> 31);
+            tm[0] = tm[0] << 1;
+            if (!(e.w & kLogSlow) && lane == 0) {
                 if (f != t) {
                     const uint64_t vt = S.win[t], vf = S.win[f];
                     const uint32_t ot = S.orig[t], of = S.orig[f];
@@ -1658,12 +1750,11 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
                 }
             }
             __syncwarp();
-            __threadfence_block();
-            if (lane == 0) st_volatile(&S.done, t + 1);
         }
-        asm volatile("bar.sync 1, 96;" ::: "memory");
         // ---- composite permutation: window slots with orig != slot, then ext rows ----
-        const uint32_t span = S.span, n_ext = S.n_ext;
+        // every position < r may hold a moved row (pivots brought in from beyond
+        // the window do not show in max_touch)
+        const uint32_t span = t > 0 ? max(max_touch + 1, t) : 0;
         uint32_t np = 0;
         for (uint32_t x0 = 0; x0 < span; x0 += 32) {
             const uint32_t x = x0 + lane;
@@ -1689,6 +1780,30 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
             np += __popc(bal);
         }
         if (lane == 0) st->npairs = np;
+        if (link.next && np) {
+            // this panel's row swaps on column j+1 (the fused POST skips it)
+            wait_count_ge_warp(link.next_ready, link.next_count);
+            __threadfence_block();
+            uint64_t* nx = link.next + R;
+            uint32_t d[4], sv[4];
+            uint64_t v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t e = lane + 32 * q;
+                if (e < np) { d[q] = st->dst[e]; sv[q] = st->src[e]; }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (lane + 32 * q < np) v[q] = nx[sv[q]];
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (lane + 32 * q < np) nx[d[q]] = v[q];
+        }
+        if (link.trace && lane == 0) trace_ev(kTrPanelEnd, j);
+#ifdef GJ_PROFILE
+        if (lane == 0) reinterpret_cast<long long*>(st->src)[56] = clock64() - t_start;
+#endif
         return;
     }
 
@@ -1696,40 +1811,53 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
         // ---- coordinates y (rho = A + y*P), transposed: lane owns coordinates
         //      lane and lane+32 as position words; then Z ----
         uint32_t y0[kGjWords] = {0, 0, 0}, y1[kGjWords] = {0, 0, 0};
+        uint32_t tm[kGjWords] = {1u, 0u, 0u};  // one-hot position t
+        uint32_t live[kGjWords];
+#pragma unroll
+        for (int w = 0; w < kGjWords; ++w) {
+            const uint32_t b0 = 32 * w;
+            live[w] = npos >= b0 + 32 ? 0xffffffffu : (npos > b0 ? (1u << (npos - b0)) - 1 : 0u);
+        }
         uint32_t t = 0;
         for (;; ++t) {
             uint4 e;
-            do { e = ld_log(&S.log[t]); } while (e.w == 0);
+            while (true) {
+                e = ld_log(&S.log[t]);
+                if (e.w) break;
+                if (link.poll_ns) __nanosleep(link.poll_ns);
+            }
             if (e.w & kLogEnd) break;
-            const uint32_t D[kGjWords] = {e.x, e.y, e.z};
-            const uint32_t tw = t >> 5, tb = t & 31;
+            uint32_t D[kGjWords] = {e.x, e.y, e.z};
             if (!(e.w & kLogSlow)) {
-                const uint32_t f = e.w & 0xFFu, fw = f >> 5, fb = f & 31;
-                uint32_t E[kGjWords], sw[kGjWords];
+                const uint32_t m0 = D[0] & live[0], m1 = D[1] & live[1], m2 = D[2] & live[2];
+                uint32_t fm[kGjWords], E[kGjWords], sw[kGjWords];
+                fm[0] = m0 & (0u - m0);
+                fm[1] = m0 ? 0u : m1 & (0u - m1);
+                fm[2] = (m0 | m1) ? 0u : m2 & (0u - m2);
 #pragma unroll
                 for (int w = 0; w < kGjWords; ++w) {
-                    E[w] = D[w] & ~(uint32_t(w) == fw ? 1u << fb : 0u);
-                    sw[w] = (uint32_t(w) == fw ? 1u << fb : 0u) ^ (uint32_t(w) == tw ? 1u << tb : 0u);
+                    E[w] = D[w] ^ fm[w];
+                    sw[w] = fm[w] ^ tm[w];
                 }
                 auto upd = [&](uint32_t (&yc)[kGjWords], uint32_t tc) {
-                    const uint32_t yf = (pick3(yc, fw) >> fb) & 1u;
-                    const uint32_t flip = 0u - (yf ^ uint32_t(tc == t));
+                    const uint32_t yf = 0u - uint32_t(((yc[0] & fm[0]) | (yc[1] & fm[1]) | (yc[2] & fm[2])) != 0);
+                    const uint32_t flip = yf ^ (0u - uint32_t(tc == t));
 #pragma unroll
                     for (int w = 0; w < kGjWords; ++w) yc[w] ^= E[w] & flip;
-                    const uint32_t d = 0u - (((pick3(yc, tw) >> tb) & 1u) ^ yf);
+                    const uint32_t d = yf ^ (0u - uint32_t(((yc[0] & tm[0]) | (yc[1] & tm[1]) | (yc[2] & tm[2])) != 0));
 #pragma unroll
                     for (int w = 0; w < kGjWords; ++w) yc[w] ^= sw[w] & d;
                 };
                 upd(y0, uint32_t(lane));
-                upd(y1, uint32_t(lane) + 32);
+                if (t >= 32) upd(y1, uint32_t(lane) + 32);  // coordinates > t are still zero
             } else {
+                D[2] = 0;  // carries found
                 const uint2 u = S.logu[t];
                 auto upd = [&](uint32_t (&yc)[kGjWords], uint32_t tc) {
                     const uint32_t um = tc < 32 ? (u.x >> tc) & 1u : (u.y >> (tc - 32)) & 1u;
                     const uint32_t yf = ((__popc(yc[0] & u.x) + __popc(yc[1] & u.y)) & 1u) ^ um;
 #pragma unroll
-                    for (int w = 0; w < kGjWords; ++w)
-                        if (uint32_t(w) == tw) yc[w] = (yc[w] & ~(1u << tb)) | (yf << tb);
+                    for (int w = 0; w < kGjWords; ++w) yc[w] = (yc[w] & ~tm[w]) | (yf ? tm[w] : 0u);
                     const uint32_t flip = 0u - (yf ^ uint32_t(tc == t));
 #pragma unroll
                     for (int w = 0; w < kGjWords; ++w) yc[w] ^= D[w] & flip;
@@ -1737,6 +1865,11 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
                 upd(y0, uint32_t(lane));
                 upd(y1, uint32_t(lane) + 32);
             }
+#pragma unroll
+            for (int w = 0; w < kGjWords; ++w) live[w] &= ~tm[w];
+            tm[2] = (tm[2] << 1) | (tm[1] >> 31);
+            tm[1] = (tm[1] << 1) | (tm[0] >> 31);
+            tm[0] = tm[0] << 1;
         }
         // t = r.  Z row k_u = e_u + y_u for u < r: transpose so lane u holds y_u.
         const uint32_t r = t;
@@ -1745,16 +1878,18 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
         warp_transpose64(x0, x1, lane);
         if (uint32_t(lane) < r) st->Z[(S.log[lane].w >> 8) & 63u] = (1ull << lane) ^ x0;
         if (uint32_t(lane) + 32 < r) st->Z[(S.log[lane + 32].w >> 8) & 63u] = (1ull << (lane + 32)) ^ x1;
-        asm volatile("bar.sync 1, 96;" ::: "memory");
+#ifdef GJ_PROFILE
+        if (lane == 0) reinterpret_cast<long long*>(st->src)[57] = clock64() - t_start;
+#endif
         return;
     }
 
     // ---- warp 0: the selection chain ----
     uint32_t c0[kGjWords], c1[kGjWords], live[kGjWords];
     {
-        uint64_t x0 = uint32_t(lane) < npos ? S.win[lane] : 0;
-        uint64_t x1 = uint32_t(lane) + 32 < npos ? S.win[lane + 32] : 0;
-        uint64_t z0 = uint32_t(lane) + 64 < npos ? S.win[lane + 64] : 0;
+        uint64_t x0 = uint32_t(lane) < npos ? A[lane] : 0;
+        uint64_t x1 = uint32_t(lane) + 32 < npos ? A[lane + 32] : 0;
+        uint64_t z0 = uint32_t(lane) + 64 < npos ? A[lane + 64] : 0;
         uint64_t z1 = 0;
         warp_transpose64(x0, x1, lane);
         warp_transpose64(z0, z1, lane);
@@ -1766,7 +1901,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
             live[w] = npos >= b0 + 32 ? 0xffffffffu : (npos > b0 ? (1u << (npos - b0)) - 1 : 0u);
         }
     }
-    uint32_t ib = 0, n_ext = 0, max_touch = 0;
+    uint32_t ib = 0, n_ext = 0;
     uint64_t sel = 0;
     bool stop = false;
 #ifdef GJ_PROFILE
@@ -1807,16 +1942,16 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
             // columns < k are never tested again: from k = 32 on only c1 matters
             if (!hi) upd(c0);
             upd(c1);
-            const uint32_t f = m[0] ? __ffs(m[0]) - 1 : (m[1] ? 31 + __ffs(m[1]) : 63 + __ffs(m[2]));
-            if (lane == 0) st_log(&S.log[ib], ck[0], ck[1], ck[2], gj_meta(false, k, f));
-            if (f > max_touch) max_touch = f;
+            // the consumers recover f as the first live position of ck
+            if (lane == 0) st_log(&S.log[ib], ck[0], ck[1], ck[2], gj_meta(false, k, 0));
         } else {
             // ---- slow: search the positions beyond the register block ----
 #ifdef GJ_PROFILE
             ++n_slow;
 #endif
-            if (lane == 0)
-                while (ld_volatile(&S.done) != ib) {}
+            if (lane == 0) st_volatile(&S.want, ib + 1);
+            wait_count_ge_warp(link.all, link.all_count);  // rows beyond the window
+            while (!__all_sync(0xffffffffu, ld_volatile(&S.done) == ib + 1)) {}
             __syncwarp();
             __threadfence_block();
             // ck holds only dead positions (no live one has bit k): the RREF rows
@@ -1892,11 +2027,10 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
                 uint32_t present = 0;
                 for (uint32_t e = 0; e < e0; ++e) present |= (S.ext_pos[e] == found);
                 if (!present) ++n_ext;
-            } else if (found > max_touch) {
-                max_touch = found;
             }
             __threadfence_block();
-            if (lane == 0) st_log(&S.log[ib], ck[0], ck[1], ck[2], gj_meta(true, k, 0));
+            // dead positions are < 64, so ck[2] == 0: the third word carries found
+            if (lane == 0) st_log(&S.log[ib], ck[0], ck[1], found, gj_meta(true, k, 0));
         }
 #pragma unroll
         for (int w = 0; w < kGjWords; ++w) live[w] &= ~ibm[w];
@@ -1909,20 +2043,19 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
     for (int k = 0; k < 32 && !stop; ++k) step(k, false);
     for (int k = 32; k < 64 && !stop; ++k) step(k, true);
 
-    if (lane == 0) st_log(&S.log[ib], 0, 0, 0, kLogValid | kLogEnd | ib);
+    __threadfence_block();
+    if (lane == 0) st_log(&S.log[ib], n_ext, 0, 0, kLogValid | kLogEnd | ib);
+    if (link.trace && lane == 0) trace_ev(kTrPanelChainEnd, j);
 #ifdef GJ_PROFILE
     const long long t_chain = clock64();
 #endif
     if (!((sel >> lane) & 1)) st->Z[lane] = 0;
     if (!((sel >> (lane + 32)) & 1)) st->Z[lane + 32] = 0;
     if (lane == 0) {
-        S.n_ext = n_ext;
-        S.span = ib > 0 ? max_touch + 1 : 0;
         st->R = uint32_t(R);
         st->r = ib;
         st->flags = 0;
     }
-    asm volatile("bar.sync 1, 96;" ::: "memory");
 #ifdef GJ_PROFILE
     if (lane == 0) {
         long long* pr = reinterpret_cast<long long*>(st->src);
@@ -1935,15 +2068,34 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
 }
 
 static bool g_panel_gj = true;  // F2GPU_PANEL=0: the transposed-M k_panel
+// The panel kernel reserves (nearly) a whole SM's shared memory: it is queued
+// ahead and spins until its column is ready, and any CTA placed beside it (a
+// persistent update CTA, post blocks) would slow its single-warp chain ~4x.
+constexpr size_t kPanelGjSmemMax = 227 * 1024;
+static_assert(sizeof(PanelGjSmem) <= kPanelGjSmemMax, "panel smem");
+static size_t kPanelGjSmemBytes = kPanelGjSmemMax;  // F2GPU_PANEL_SMEM=0: only what the kernel uses
 
 cudaError_t launch_panel(uint64_t* col, size_t n, PanelState* st_all, int j, cudaStream_t s,
                          const uint32_t* wait_flag, uint32_t wait_count) {
-    if (g_panel_gj)
-        k_panel_gj<<<1, kPanelThreads, sizeof(PanelGjSmem), s>>>(col, n, st_all, j, wait_flag, wait_count);
-    else
+    if (g_panel_gj) {
+        PanelLink l{};
+        l.head = l.win = l.all = wait_flag;
+        l.head_count = l.win_count = l.all_count = wait_count;
+        k_panel_gj<<<1, kPanelThreads, kPanelGjSmemBytes, s>>>(col, n, st_all, j, l);
+    } else {
         k_panel<<<1, kPanelThreads, sizeof(PanelSmem), s>>>(col, n, st_all, j, wait_flag, wait_count);
+    }
     return cudaGetLastError();
 }
+
+cudaError_t launch_panel_link(uint64_t* col, size_t n, PanelState* st_all, int j, const PanelLink& link,
+                              cudaStream_t s) {
+    if (!g_panel_gj) return cudaErrorNotSupported;
+    k_panel_gj<<<1, kPanelThreads, kPanelGjSmemBytes, s>>>(col, n, st_all, j, link);
+    return cudaGetLastError();
+}
+
+bool panel_link_ok() { return g_panel_gj; }
 
 // ---------------------------------------------------------------------------
 // Y = D*Z over D (rows R+r .. n of the panel column), written in place
@@ -2051,9 +2203,9 @@ cudaError_t launch_panel_y(uint64_t* col, size_t n, const PanelState* st, int nu
 // One warp per word-column; column index == ncols handles the uint32 perm.
 __device__ __forceinline__ void swaps_body(uint64_t* __restrict__ w, size_t stride, int ncols,
                                            int skip_col, uint32_t* __restrict__ perm,
-                                           const PanelState* __restrict__ st, int gw) {
+                                           const PanelState* __restrict__ st, int gw, int skip_col2 = -1) {
     const int lane = threadIdx.x & 31;
-    if (gw > ncols || gw == skip_col) return;
+    if (gw > ncols || gw == skip_col || gw == skip_col2) return;
     // header and pair lists are loaded together (independent addresses), so the
     // swap costs two dependent global round trips: state, then the rows
     const uint32_t np = st->npairs;
@@ -2126,6 +2278,105 @@ cudaError_t launch_post(uint64_t* w, size_t stride, int ncols, int panel_col, ui
     const int yblocks = int(std::min<size_t>(1024, std::max<size_t>(kPostYBlocks, (n + 255) / 256)));
     k_post<<<swap_blocks + yblocks, 256, 0, s>>>(w, stride, ncols, panel_col, perm, n, st,
                                                    swap_blocks, yblocks);
+    return cudaGetLastError();
+}
+
+// POST fused with the next column's update (lookahead).  Row blocks: 4-bit
+// tables over Z (16 groups x 16) and over B = the next column's pivot rows
+// (already swapped by the panel kernel), 256 entries each -- one entry per
+// thread, so the tables cost one round of shared-memory reads instead of the
+// five of a 1280-entry table; each row then takes 16 + 16 lookups:
+//   y = D_i * Z -> panel column,   next_i ^= y * B.
+// Counters for the next panel kernel (k_panel_gj link): block 0 after its first
+// 256 rows, blocks < 8 after theirs (the 2048-row window), every block at end.
+constexpr int kPcMinYBlocks = 64;
+int post_col_yblocks(size_t n) {
+    return int(std::min<size_t>(1024, std::max<size_t>(kPcMinYBlocks, (n + 255) / 256)));
+}
+
+__global__ void __launch_bounds__(256) k_post_col(uint64_t* __restrict__ w, size_t stride, int ncols,
+                                                  int panel_col, int next_col, uint32_t* __restrict__ perm,
+                                                  size_t n, const PanelState* __restrict__ st,
+                                                  int swap_blocks, uint32_t* __restrict__ flags, bool trace) {
+    __shared__ uint64_t zs[64], bs[64];
+    __shared__ uint64_t zt[256], bt[256];
+    if (int(blockIdx.x) < swap_blocks) {
+        swaps_body(w, stride, ncols, panel_col, perm, st,
+                   int((size_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5), next_col);
+        return;
+    }
+    const unsigned blk = blockIdx.x - swap_blocks, nblk = gridDim.x - swap_blocks;
+    const int tid = threadIdx.x;
+    if (trace && blk == 0 && tid == 0) trace_ev(kTrPostBegin, panel_col);
+    uint64_t* col = w + size_t(panel_col) * stride;
+    uint64_t* nx = next_col >= 0 ? w + size_t(next_col) * stride : nullptr;
+    const uint32_t R = st->R, r = st->r;
+    const size_t lo = size_t(R) + r;
+    if (tid < 64) {
+        zs[tid] = st->Z[tid];
+        bs[tid] = (nx && uint32_t(tid) < r) ? nx[R + tid] : 0;
+    }
+    const size_t i0 = lo + size_t(blk) * blockDim.x + tid;
+    const bool work = r != 0 && lo < n;
+    const uint64_t d0 = (work && i0 < n) ? col[i0] : 0;
+    const uint64_t x0 = (work && nx && i0 < n) ? nx[i0] : 0;
+    __syncthreads();
+    if (work) {
+        {
+            const int g = tid >> 4, v = tid & 15;
+            uint64_t a = 0, b = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if ((v >> q) & 1) { a ^= zs[4 * g + q]; b ^= bs[4 * g + q]; }
+            zt[tid] = a;
+            bt[tid] = b;
+        }
+        __syncthreads();
+        auto row = [&](size_t i, uint64_t d, uint64_t x) {
+            uint64_t y = 0;
+#pragma unroll
+            for (int g = 0; g < 16; ++g) y ^= zt[16 * g + int((d >> (4 * g)) & 15)];
+            col[i] = y;
+            if (nx) {
+#pragma unroll
+                for (int g = 0; g < 16; ++g) x ^= bt[16 * g + int((y >> (4 * g)) & 15)];
+                nx[i] = x;
+            }
+        };
+        if (i0 < n) row(i0, d0, x0);
+        if (flags && blk < 8) {  // every writer fences, then one arrival per block
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) {
+                if (blk == 0) {
+                    atomicAdd(flags + 0, 1u);
+                    if (trace) trace_ev(kTrPostHead, panel_col);
+                }
+                atomicAdd(flags + 1, 1u);
+            }
+        }
+        for (size_t i = i0 + size_t(nblk) * blockDim.x; i < n; i += size_t(nblk) * blockDim.x)
+            row(i, col[i], nx ? nx[i] : 0);
+        if (flags) {
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) {
+                if (!trace) atomicAdd(flags + 2, 1u);
+                else if (atomicAdd(flags + 2, 1u) == nblk - 1) trace_ev(kTrPostEnd, panel_col);
+            }
+        }
+    } else if (tid == 0 && flags) {
+        if (blk == 0) atomicAdd(flags + 0, 1u);
+        if (blk < 8) atomicAdd(flags + 1, 1u);
+        atomicAdd(flags + 2, 1u);
+    }
+}
+
+cudaError_t launch_post_col(uint64_t* w, size_t stride, int ncols, int panel_col, int next_col, uint32_t* perm,
+                            size_t n, const PanelState* st, uint32_t* flags, cudaStream_t s, bool trace) {
+    const int swap_blocks = (ncols + 1 + 7) / 8;
+    k_post_col<<<swap_blocks + post_col_yblocks(n), 256, 0, s>>>(w, stride, ncols, panel_col, next_col, perm, n,
+                                                                  st, swap_blocks, flags, trace);
     return cudaGetLastError();
 }
 
@@ -2378,7 +2629,8 @@ cudaError_t init_kernel_attrs() {
                                  int(sizeof(PanelSmem)));
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_panel_gj, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(sizeof(PanelGjSmem)));
+                                 int(kPanelGjSmemMax));
+    if (const char* ps = getenv("F2GPU_PANEL_SMEM")) kPanelGjSmemBytes = ps[0] != '0' ? kPanelGjSmemMax : sizeof(PanelGjSmem);
     if (const char* pk = getenv("F2GPU_PANEL")) g_panel_gj = pk[0] != '0';
     return e;
 }

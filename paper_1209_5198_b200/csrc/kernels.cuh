@@ -47,7 +47,18 @@ struct UpdateArgs {
     // *release once its group-0 updates are complete in memory (exactly once per
     // CTA, also when it has no work).  The next panel kernel waits for the count.
     uint32_t* release;
+    int tag = -1;  // panel index for the device trace; >= 0 only while it is on
 };
+
+// Device trace (diagnostics): when enabled, the panel / fused-post / update
+// kernels append globaltimer stamps  (ns << 16) | (event << 12) | panel.
+enum TraceEvent : uint32_t {
+    kTrPanelBegin = 1, kTrPanelChainEnd = 2, kTrPanelEnd = 3,
+    kTrPostBegin = 4, kTrPostHead = 5, kTrPostEnd = 6,
+    kTrUpdBegin = 7, kTrUpdRelease = 8, kTrUpdEnd = 9,
+};
+cudaError_t trace_set(unsigned long long* buf, uint32_t cap);  // buf = nullptr: off
+cudaError_t trace_count(uint32_t* n);
 
 struct GemmArgs {
     const uint64_t* A; size_t sa; size_t n;   // A: n rows, k bits
@@ -88,6 +99,33 @@ cudaError_t launch_xor(uint64_t* dst, size_t sd, const uint64_t* a, size_t sa,
                        cudaStream_t s);
 cudaError_t launch_transpose(const uint64_t* a, size_t n, size_t m, size_t sa, uint64_t* out,
                              size_t so, cudaStream_t s);
+// Fused lookahead link of one panel kernel (k_panel_gj):
+//   head/win/all: counters of the previous k_post_col (block 0's first rows,
+//   the first 8 blocks = the 2048-row window, every row block) that the
+//   selection warp, the window load and the beyond-window scan wait for;
+//   next: column j+1, which receives this panel's row swaps at the end once
+//   *next_ready >= next_count (the update of column j+1 by the previous panel).
+struct PanelLink {
+    const uint32_t* head; uint32_t head_count;
+    const uint32_t* win; uint32_t win_count;
+    const uint32_t* all; uint32_t all_count;
+    uint64_t* next;
+    const uint32_t* next_ready; uint32_t next_count;
+    uint32_t poll_ns = 0;  // sleep between polls of the consumer warps
+    bool trace = false;    // device trace stamps (diagnostics)
+};
+cudaError_t launch_panel_link(uint64_t* col, size_t n, PanelState* st_all, int j, const PanelLink& link,
+                              cudaStream_t s);
+bool panel_link_ok();  // false when F2GPU_PANEL=0 selects the older panel kernel
+// POST + the next column's update in one launch: swaps on every word-column
+// except panel_col and next_col, Y = D*Z on the panel column, and (next_col >=
+// 0) next[i] ^= Y_i * B for i >= R + r.  flags[0] += 1 by row block 0 after
+// its first 256 rows, flags[1] += 1 by row blocks < 8 likewise, flags[2] += 1
+// by every row block at its end.
+int post_col_yblocks(size_t n);
+cudaError_t launch_post_col(uint64_t* w, size_t stride, int ncols, int panel_col, int next_col, uint32_t* perm,
+                            size_t n, const PanelState* st, uint32_t* flags, cudaStream_t s,
+                            bool trace = false);
 // lookahead: panel j's update of word-column j+1 only; increments *done per CTA
 int update_col_grid(size_t n, int num_sms);
 cudaError_t launch_update_col(uint64_t* next, const uint64_t* ycol, size_t n, const PanelState* st, uint32_t* done,

@@ -233,6 +233,66 @@ def check_decomp(f2, ctx, po, a, n, m, shards=1):
     return got
 
 
+def _ymap(z, d):
+    """Y_i = D_i * Z for a vector of 64-bit rows (bit b of D selects Z[b])."""
+    y = np.zeros(d.shape, np.uint64)
+    for b in range(64):
+        y ^= np.where((d >> np.uint64(b)) & np.uint64(1), z[b], np.uint64(0)).astype(np.uint64)
+    return y
+
+
+def _panel_gpu(f2, ctx, col):
+    import ctypes as C
+    from paper_1209_5198_b200 import _lib
+    col = np.ascontiguousarray(col, dtype=np.uint64)
+    out = np.zeros(max(col.size, 1), np.uint64)
+    z = np.zeros(64, np.uint64)
+    r = C.c_uint32()
+    pairs = np.zeros(256, np.uint32)
+    npairs = C.c_uint32()
+    _lib.check(_lib.load().f2gpu_panel_build_z(ctx.handle, col.ctypes.data, col.size, out.ctypes.data,
+                                               z.ctypes.data, C.byref(r), pairs.ctypes.data, C.byref(npairs)))
+    # the pair list must reproduce the swapped column from the input
+    np_ = npairs.value
+    assert np_ <= 128
+    moved = col.copy()
+    moved[pairs[:np_].astype(np.int64)] = col[pairs[128:128 + np_].astype(np.int64)]
+    assert np.array_equal(moved, out[:col.size]), "pair list disagrees with the swapped column"
+    return r.value, out[:col.size], z
+
+
+def _panel_cases():
+    rng = np.random.default_rng(7)
+    cases = []
+    for rows in (1, 5, 63, 64, 65, 96, 97, 100, 130, 300, 2047, 2048, 2049, 5000):
+        for p in (0.5, 0.1, 0.01, 0.002):
+            bits = rng.random((rows, 64)) < p
+            col = np.zeros(rows, np.uint64)
+            for b in range(64):
+                col |= bits[:, b].astype(np.uint64) << np.uint64(b)
+            cases.append(col)
+    # pivots only beyond the 2048-row window (ext rows), duplicates, zeros
+    far = np.zeros(4000, np.uint64)
+    far[2500:2600] = rng.integers(0, 2**63, 100, dtype=np.uint64)
+    cases.append(far)
+    dup = rng.integers(0, 2**63, 200, dtype=np.uint64)
+    dup[1::2] = dup[0::2]
+    cases.append(dup)
+    cases.append(np.zeros(300, np.uint64))
+    return cases
+
+
+def test_panel_build_z(f2, ctx, po):
+    """The panel kernel against Procedure buildZ: block rank,
+    the swapped column and Y = D*Z for every row below the pivots."""
+    for col in _panel_cases():
+        r, a, _, zo, _ = po.build_z(col)
+        rg, ag, zg = _panel_gpu(f2, ctx, col)
+        assert rg == r, (col.size, rg, r)
+        assert np.array_equal(ag, a[:col.size]), col.size
+        assert np.array_equal(_ymap(zg, ag[r:]), _ymap(zo, a[r:col.size])), col.size
+
+
 DECOMP_SHAPES = [(1, 1), (4, 5), (64, 64), (100, 100), (200, 130), (130, 200), (513, 257),
                  (1000, 640), (640, 1000), (2048, 2048), (100, 3000), (3000, 100)]
 

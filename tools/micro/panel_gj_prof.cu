@@ -21,7 +21,7 @@ int main(int argc, char** argv) {
         f2::PanelState hs;
         cudaMemcpy(&hs, st, sizeof hs, cudaMemcpyDeviceToHost);
         const long long* pr = reinterpret_cast<const long long*>(hs.src);
-        printf("n=%zu r=%u slow=%lld load %lld chain %lld book %lld tail %lld cycles  err=%s\n", n, hs.r, pr[58], pr[61], pr[62], pr[60],
+        printf("n=%zu r=%u slow=%lld load %lld chain %lld w1end %lld w2end %lld tail %lld cycles  err=%s\n", n, hs.r, pr[58], pr[61], pr[62], pr[57], pr[56],
                pr[63], cudaGetErrorString(cudaGetLastError()));
     }
     return 0;

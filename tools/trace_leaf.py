@@ -1,0 +1,79 @@
+"""Device-trace one leaf-shaped block decomposition (n x w) and print the median
+per-panel intervals of the lookahead chain (F2GPU_* env switches apply)."""
+import ctypes as C
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1209_5198_b200 as f2  # noqa: E402
+from paper_1209_5198_b200 import _lib  # noqa: E402
+
+lib = _lib.load()
+ctx = f2.Context(0)
+stream = torch.cuda.Stream()
+torch.cuda.set_stream(stream)
+ctx.set_stream(stream.cuda_stream)
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+w = int(sys.argv[2]) if len(sys.argv) > 2 else 16384
+A = f2.DeviceMatrix(n, w, ctx); A.random_dense(0.5, 6)
+W = f2.DeviceMatrix(n, w, ctx)
+perm = np.zeros(n, np.uint32); rj = np.zeros(w // 64, np.uint32); rk = C.c_size_t()
+
+
+def step():
+    _lib.check(lib.f2gpu_mat_copy(ctx.handle, W.handle, A.handle))
+    _lib.check(lib.f2gpu_decompose_block(ctx.handle, W.handle, perm.ctypes.data, rj.ctypes.data, C.byref(rk)))
+
+
+for _ in range(3):
+    step()
+cap = 1 << 20
+_lib.check(lib.f2gpu_trace_enable(ctx.handle, cap))
+step()
+buf = np.zeros(cap, np.uint64)
+cnt = C.c_size_t()
+_lib.check(lib.f2gpu_trace_read(ctx.handle, buf.ctypes.data, cap, C.byref(cnt)))
+_lib.check(lib.f2gpu_trace_enable(ctx.handle, 0))
+ev = buf[:cnt.value]
+t = (ev >> np.uint64(16)).astype(np.int64)
+code = ((ev >> np.uint64(12)) & np.uint64(15)).astype(int)
+j = (ev & np.uint64(4095)).astype(int)
+t0 = t.min()
+names = {1: "P.begin", 2: "P.chain_end", 3: "P.end", 4: "post.begin", 5: "post.head", 6: "post.end",
+         7: "U.begin", 8: "U.release", 9: "U.end", 10: "U0.tab0", 11: "U0.tile0", 12: "U0.end", 13: "U0.tab1"}
+mu = w // 64
+T = {k: np.full(mu, np.nan) for k in names}
+for ti, ci, ji in zip(t, code, j):
+    if ci in T and ji < mu and np.isnan(T[ci][ji]):
+        T[ci][ji] = (ti - t0) / 1000.0  # us
+
+
+def med(x):
+    x = x[~np.isnan(x)]
+    return f"{np.median(x):7.2f} (p10 {np.percentile(x, 10):6.2f} p90 {np.percentile(x, 90):6.2f})" if x.size else "   n/a"
+
+
+print(f"n={n} w={w} events={cnt.value} total {np.nanmax(T[6]) if not np.all(np.isnan(T[6])) else 0:.1f} us")
+nx = lambda a: np.append(a[1:], np.nan)  # noqa: E731
+rows = [
+    ("panel chain (begin->chain end)", T[2] - T[1]),
+    ("panel tail (chain end->end)", T[3] - T[2]),
+    ("P end -> post begin", T[4] - T[3]),
+    ("post begin -> head", T[5] - T[4]),
+    ("post head -> next P begin", nx(T[1]) - T[5]),
+    ("post begin -> post end", T[6] - T[4]),
+    ("post end -> U begin", T[7] - T[6]),
+    ("U begin -> release", T[8] - T[7]),
+    ("  U0 begin -> first table", T[10] - T[7]),
+    ("  U0 first table -> tile0 reduce", T[11] - T[10]),
+    ("  U0 begin -> second table", T[13] - T[7]),
+    ("  U0 begin -> end (CTA 0)", T[12] - T[7]),
+    ("  U0 end -> next post begin", nx(T[4]) - T[12]),
+    ("next P chain end -> U release", nx(T[2]) - T[8]),
+    ("cycle (P begin -> next P begin)", nx(T[1]) - T[1]),
+]
+for name, v in rows:
+    print(f"{name:34s} {med(v)}")
