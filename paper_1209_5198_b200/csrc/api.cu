@@ -211,6 +211,7 @@ struct f2gpu_ctx {
     // fp4 tensor-core leaf (F2GPU_TC=0 disables): products with n, k, m >= 256
     bool use_tc = true;
     size_t tc_cutover = 16384;  // minimum TC Strassen leaf size (F2GPU_TC_CUT)
+    bool use_tc_cut_default = true;  // false once tc_cutover is set explicitly
     void* comm = nullptr;
     int rank = 0, world = 1;
 };
@@ -817,6 +818,8 @@ struct RecRun {
     size_t cut;    // Strassen cutover inside the recursion (XOR traffic vs multiply)
     size_t tbase;  // TRSM base (panels solved in one k_trsm_block launch)
     size_t tall_rows = 0, tall_base = 0;  // leaves with >= tall_rows rows: at most tall_base panels
+    size_t tc_cut = 8192;  // Strassen-Winograd leaf of the TC products (F2GPU_REC_TC_CUT; 65536^2:
+                           // 8192 -> 66.9 ms, 16384 -> 67.3, 4096 -> 69.4, 32768 -> 69.7)
     bool trsm_kernel = true;  // F2GPU_REC_TRSM=0: rank-64 updates instead (A/B check)
     // upload overlap (f2gpu_decompose_recursive_host): word-columns >= frontier are
     // still in `pend` (original row order, column q at pend + (q - frontier0) * ps),
@@ -890,7 +893,7 @@ int rec_trsm(RecRun& r, size_t a, size_t b, size_t Ra, size_t col0, size_t col1)
     F2_TRY(rec_trsm(r, a, m, Ra, col0, col1));
     F2_TRY(best_product(r.c, wview(*r.s, Rm, Rb - Rm, col0, col1 - col0),
                         wview(*r.s, Rm, Rb - Rm, a, m - a), wview(*r.s, Ra, Rm - Ra, col0, col1 - col0),
-                        r.cut, r.c->tc_cutover));
+                        r.cut, r.tc_cut));
     return rec_trsm(r, m, b, Rm, col0, col1);
 }
 
@@ -951,7 +954,7 @@ int rec_decompose(RecRun& r, size_t c0, size_t c1) {
         if (R1 < r.n)
             F2_TRY(best_product(r.c, wview(*r.s, R1, r.n - R1, cm, c1 - cm),
                                 wview(*r.s, R1, r.n - R1, c0, cm - c0),
-                                wview(*r.s, R0, R1 - R0, cm, c1 - cm), r.cut, r.c->tc_cutover));
+                                wview(*r.s, R0, R1 - R0, cm, c1 - cm), r.cut, r.tc_cut));
     } else {
         F2_TRY(rank_updates(r, c0, cm, cm, c1, r.n));
     }
@@ -985,6 +988,8 @@ int decompose_recursive(f2gpu_ctx* c, View w, size_t min_cols, uint32_t* perm, u
     r.tall_rows = 20000;
     if (const char* e = getenv("F2GPU_REC_TALL")) r.tall_rows = size_t(atol(e));
     r.tall_base = 64;
+    if (!r.c->use_tc_cut_default) r.tc_cut = r.c->tc_cutover;  // set explicitly (F2GPU_TC_CUT / ctx_set_tc)
+    if (const char* e = getenv("F2GPU_REC_TC_CUT")) r.tc_cut = size_t(atol(e));
     if (const char* e = getenv("F2GPU_REC_TALL_BASE")) r.tall_base = std::max<size_t>(1, size_t(atol(e)));
     r.on_final = std::move(on_final);
     if (pend && frontier < mu) {
@@ -1189,7 +1194,10 @@ int f2gpu_ctx_create(int device, f2gpu_ctx** out) {
     if (const char* pe = getenv("F2GPU_PANEL_EARLY")) c->panel_early = pe[0] != '0';
     if (const char* pn = getenv("F2GPU_POLL_NS")) c->poll_ns = uint32_t(atoi(pn));
     if (const char* tc = getenv("F2GPU_TC")) c->use_tc = tc[0] != '0';
-    if (const char* tcc = getenv("F2GPU_TC_CUT")) c->tc_cutover = size_t(atoll(tcc));
+    if (const char* tcc = getenv("F2GPU_TC_CUT")) {
+        c->tc_cutover = size_t(atoll(tcc));
+        c->use_tc_cut_default = false;
+    }
     CUDA_TRY(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&c->ev_post, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&c->ev_panel, cudaEventDisableTiming));
@@ -1256,6 +1264,7 @@ int f2gpu_ctx_set_tc(f2gpu_ctx* c, int on, size_t leaf) {
     if (!c) return set_err(F2GPU_EINVAL, "null ctx");
     c->use_tc = on != 0;
     c->tc_cutover = leaf ? leaf : 16384;
+    c->use_tc_cut_default = leaf == 0;
     return F2GPU_OK;
 }
 

@@ -180,6 +180,49 @@ __device__ __forceinline__ void build_tables(uint64_t* __restrict__ tab,
                                              size_t b_row0, size_t bcol0, int ncols_valid,
                                              int k_bits, int nt) {
     const int total = tab_chunks(nt) * kTabCols;
+    if (NTH * 2 >= 640 && nt == 9) {
+        // at most two 32-entry items per thread: issue both items' B loads before
+        // any table work, so the build costs one L2 round trip, not one per item
+        uint64_t rows[2][8];
+        int its[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int it = threadIdx.x + q * NTH;
+            its[q] = it;
+            const int col = it & (kTabCols - 1);
+            const int cg = it >> 4;
+            const int t = cg < 32 ? (cg >> 2) : 8;
+            const int sz = t < 8 ? 7 : 8;
+            const bool cv = it < total && col < ncols_valid;
+            const uint64_t* bp = B + (bcol0 + col) * sb + b_row0 + 7 * t;
+#pragma unroll
+            for (int b = 0; b < 8; ++b)
+                rows[q][b] = (b < sz && cv && 7 * t + b < k_bits) ? __ldg(bp + b) : 0ull;
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int it = its[q];
+            if (it >= total) break;
+            const int col = it & (kTabCols - 1);
+            const int cg = it >> 4;
+            const int t = cg < 32 ? (cg >> 2) : 8;
+            const int chunk = cg < 32 ? (cg & 3) : cg - 32;
+            uint64_t cur = 0;
+#pragma unroll
+            for (int hb = 0; hb < 3; ++hb)
+                if ((chunk >> hb) & 1) cur ^= rows[q][5 + hb];
+            uint64_t* dst = tab + (size_t(128 * t + chunk * 32) * kTabCols + col);
+            uint64_t v[32];
+            v[0] = cur;
+#pragma unroll
+            for (int b = 0; b < 5; ++b)
+#pragma unroll
+                for (int g = 1 << b; g < (2 << b); ++g) v[g] = v[g - (1 << b)] ^ rows[q][b];
+#pragma unroll
+            for (int g = 0; g < 32; ++g) dst[g * kTabCols] = v[g];
+        }
+        return;
+    }
     for (int it = threadIdx.x; it < total; it += NTH) {
         const int col = it & (kTabCols - 1);
         const int cg = it >> 4;
@@ -651,6 +694,7 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
         b_row0 = R;
     }
     const size_t row_hi = p.row_hi;
+    if (p.tag >= 0 && blockIdx.x == 0 && threadIdx.x == 0) trace_ev(14, int(p.tag + 0 * k));
     if (k <= 0 || row_lo >= row_hi || p.ncols <= 0) {
         if (p.release && threadIdx.x == 0) release_signal(p.release, p.tag);
         return;
@@ -692,6 +736,7 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
         fence_async_smem();
     }
     __syncthreads();
+    if (p.tag >= 0 && blockIdx.x == 0 && threadIdx.x == 0) trace_ev(15, p.tag);
 
     if (warp == kV3Warps) {
         // ===== producer warp =====

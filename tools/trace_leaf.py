@@ -28,13 +28,14 @@ def step():
     _lib.check(lib.f2gpu_decompose_block(ctx.handle, W.handle, perm.ctypes.data, rj.ctypes.data, C.byref(rk)))
 
 
-for _ in range(3):
-    step()
 cap = 1 << 20
-_lib.check(lib.f2gpu_trace_enable(ctx.handle, cap))
-step()
+_lib.check(lib.f2gpu_trace_enable(ctx.handle, cap))  # before warm-up: the captured graph carries it
 buf = np.zeros(cap, np.uint64)
 cnt = C.c_size_t()
+for _ in range(3):
+    step()
+_lib.check(lib.f2gpu_trace_read(ctx.handle, buf.ctypes.data, cap, C.byref(cnt)))  # drop warm-up stamps
+step()
 _lib.check(lib.f2gpu_trace_read(ctx.handle, buf.ctypes.data, cap, C.byref(cnt)))
 _lib.check(lib.f2gpu_trace_enable(ctx.handle, 0))
 ev = buf[:cnt.value]
@@ -43,7 +44,7 @@ code = ((ev >> np.uint64(12)) & np.uint64(15)).astype(int)
 j = (ev & np.uint64(4095)).astype(int)
 t0 = t.min()
 names = {1: "P.begin", 2: "P.chain_end", 3: "P.end", 4: "post.begin", 5: "post.head", 6: "post.end",
-         7: "U.begin", 8: "U.release", 9: "U.end", 10: "U0.tab0", 11: "U0.tile0", 12: "U0.end", 13: "U0.tab1"}
+         7: "U.begin", 8: "U.release", 9: "U.end", 10: "U0.tab0", 11: "U0.tile0", 12: "U0.end", 13: "U0.tab1", 14: "U0.state", 15: "U0.barriers"}
 mu = w // 64
 T = {k: np.full(mu, np.nan) for k in names}
 for ti, ci, ji in zip(t, code, j):
@@ -67,7 +68,9 @@ rows = [
     ("post begin -> post end", T[6] - T[4]),
     ("post end -> U begin", T[7] - T[6]),
     ("U begin -> release", T[8] - T[7]),
-    ("  U0 begin -> first table", T[10] - T[7]),
+    ("  U0 begin -> state read", T[14] - T[7]),
+    ("  U0 state -> barriers init", T[15] - T[14]),
+    ("  U0 barriers -> first table", T[10] - T[15]),
     ("  U0 first table -> tile0 reduce", T[11] - T[10]),
     ("  U0 begin -> second table", T[13] - T[7]),
     ("  U0 begin -> end (CTA 0)", T[12] - T[7]),
