@@ -180,49 +180,6 @@ __device__ __forceinline__ void build_tables(uint64_t* __restrict__ tab,
                                              size_t b_row0, size_t bcol0, int ncols_valid,
                                              int k_bits, int nt) {
     const int total = tab_chunks(nt) * kTabCols;
-    if (NTH * 2 >= 640 && nt == 9) {
-        // at most two 32-entry items per thread: issue both items' B loads before
-        // any table work, so the build costs one L2 round trip, not one per item
-        uint64_t rows[2][8];
-        int its[2];
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const int it = threadIdx.x + q * NTH;
-            its[q] = it;
-            const int col = it & (kTabCols - 1);
-            const int cg = it >> 4;
-            const int t = cg < 32 ? (cg >> 2) : 8;
-            const int sz = t < 8 ? 7 : 8;
-            const bool cv = it < total && col < ncols_valid;
-            const uint64_t* bp = B + (bcol0 + col) * sb + b_row0 + 7 * t;
-#pragma unroll
-            for (int b = 0; b < 8; ++b)
-                rows[q][b] = (b < sz && cv && 7 * t + b < k_bits) ? __ldg(bp + b) : 0ull;
-        }
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const int it = its[q];
-            if (it >= total) break;
-            const int col = it & (kTabCols - 1);
-            const int cg = it >> 4;
-            const int t = cg < 32 ? (cg >> 2) : 8;
-            const int chunk = cg < 32 ? (cg & 3) : cg - 32;
-            uint64_t cur = 0;
-#pragma unroll
-            for (int hb = 0; hb < 3; ++hb)
-                if ((chunk >> hb) & 1) cur ^= rows[q][5 + hb];
-            uint64_t* dst = tab + (size_t(128 * t + chunk * 32) * kTabCols + col);
-            uint64_t v[32];
-            v[0] = cur;
-#pragma unroll
-            for (int b = 0; b < 5; ++b)
-#pragma unroll
-                for (int g = 1 << b; g < (2 << b); ++g) v[g] = v[g - (1 << b)] ^ rows[q][b];
-#pragma unroll
-            for (int g = 0; g < 32; ++g) dst[g * kTabCols] = v[g];
-        }
-        return;
-    }
     for (int it = threadIdx.x; it < total; it += NTH) {
         const int col = it & (kTabCols - 1);
         const int cg = it >> 4;
@@ -246,6 +203,63 @@ __device__ __forceinline__ void build_tables(uint64_t* __restrict__ tab,
         for (int b = 0; b < 5; ++b)
 #pragma unroll
             for (int g = 1 << b; g < (2 << b); ++g) v[g] = v[g - (1 << b)] ^ rows[b];
+#pragma unroll
+        for (int g = 0; g < 32; ++g) dst[g * kTabCols] = v[g];
+    }
+}
+
+// build_tables for a CTA of NTH >= 320 threads (at most two 32-entry items each)
+// with B staged through shared memory first: the 16 columns x 64 rows are loaded
+// coalesced into the start of the table region, each thread copies its rows to
+// registers, and only then is the table written over the staging area.  Direct
+// per-item __ldg touched 16 cache lines per warp load: 7.0k vs 3.5k cycles per
+// group (tools/micro/tab_build.cu).  sync() must be a barrier of the NTH threads.
+constexpr int kStagePitch = 66;  // words per staged column (conflict-free row reads)
+template <int NTH, typename Sync>
+__device__ __forceinline__ void build_tables_staged(uint64_t* __restrict__ tab, const uint64_t* __restrict__ B,
+                                                    size_t sb, size_t b_row0, size_t bcol0, int ncols_valid,
+                                                    int k_bits, Sync sync) {
+    static_assert(NTH * 2 >= 640, "two items per thread");
+    constexpr int total = 640;  // tab_chunks(9) * kTabCols
+    uint64_t* stage = tab;
+    for (int i = threadIdx.x; i < kTabCols * 64; i += NTH) {
+        const int col = i >> 6, r = i & 63;
+        stage[col * kStagePitch + r] =
+            (col < ncols_valid && r < k_bits) ? __ldg(B + (bcol0 + col) * sb + b_row0 + r) : 0ull;
+    }
+    sync();
+    uint64_t rows[2][8];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const int it = threadIdx.x + q * NTH;
+        const int col = it & (kTabCols - 1);
+        const int cg = it >> 4;
+        const int t = cg < 32 ? (cg >> 2) : 8;
+        const int sz = t < 8 ? 7 : 8;
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+            rows[q][b] = (it < total && b < sz) ? stage[col * kStagePitch + 7 * t + b] : 0ull;
+    }
+    sync();
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const int it = threadIdx.x + q * NTH;
+        if (it >= total) break;
+        const int col = it & (kTabCols - 1);
+        const int cg = it >> 4;
+        const int t = cg < 32 ? (cg >> 2) : 8;
+        const int chunk = cg < 32 ? (cg & 3) : cg - 32;
+        uint64_t cur = 0;
+#pragma unroll
+        for (int hb = 0; hb < 3; ++hb)
+            if ((chunk >> hb) & 1) cur ^= rows[q][5 + hb];
+        uint64_t* dst = tab + (size_t(128 * t + chunk * 32) * kTabCols + col);
+        uint64_t v[32];
+        v[0] = cur;
+#pragma unroll
+        for (int b = 0; b < 5; ++b)
+#pragma unroll
+            for (int g = 1 << b; g < (2 << b); ++g) v[g] = v[g - (1 << b)] ^ rows[q][b];
 #pragma unroll
         for (int g = 0; g < 32; ++g) dst[g * kTabCols] = v[g];
     }
@@ -828,8 +842,8 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
         if (g != gcur) {
             v3_consumers_sync();
             const int nvalid = min(kTabCols, int(size_t(p.ncols) - g * kTabCols));
-            build_tables<kV3Warps * 32>(tab, p.B, p.sb, b_row0, p.b_wcol0 + g * kTabCols, nvalid,
-                                        k, nt);
+            build_tables_staged<kV3Warps * 32>(tab, p.B, p.sb, b_row0, p.b_wcol0 + g * kTabCols, nvalid, k,
+                                               [] { v3_consumers_sync(); });
             v3_consumers_sync();
             if (p.tag >= 0 && blockIdx.x == 0 && threadIdx.x == 0) trace_ev(gcur == ~size_t(0) ? 10 : 13, p.tag);
             gcur = g;
