@@ -818,6 +818,10 @@ struct RecRun {
     size_t cut;    // Strassen cutover inside the recursion (XOR traffic vs multiply)
     size_t tbase;  // TRSM base (panels solved in one k_trsm_block launch)
     size_t tall_rows = 0, tall_base = 0;  // leaves with >= tall_rows rows: at most tall_base panels
+    // F2GPU_REC_TIMES=1: CUDA events around every leaf / TRSM / product on the main
+    // stream, summed per phase and printed (diagnostics; the side stream is untouched)
+    struct Phase { std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev; };
+    std::map<std::string, Phase>* phases = nullptr;
     size_t tc_cut = 8192;  // Strassen-Winograd leaf of the TC products (F2GPU_REC_TC_CUT; 65536^2:
                            // 8192 -> 66.9 ms, 16384 -> 67.3, 4096 -> 69.4, 32768 -> 69.7)
     bool trsm_kernel = true;  // F2GPU_REC_TRSM=0: rank-64 updates instead (A/B check)
@@ -880,20 +884,26 @@ View wview(const Shard& s, size_t r0, size_t nr, size_t wc0, size_t nwc) {
 
 // full-rank block TRSM: panels [a, b) own pivot rows [Ra, Ra + 64(b-a)); solve in
 // place on word-cols [col0, col1) of those rows.
+template <typename F>
+int timed(RecRun& r, const char* what, F&& f);
+
 int rec_trsm(RecRun& r, size_t a, size_t b, size_t Ra, size_t col0, size_t col1) {
     const size_t Rb = Ra + 64 * (b - a);
     if (b - a <= r.tbase) {
         if (b - a <= 16 && r.trsm_kernel)
-            return check_launch(r.c, f2::launch_trsm_block(r.s->w.p, r.s->w.stride, int(a), int(b - a), Ra, col0,
-                                                           int(col1 - col0), r.c->stream),
-                                "k_trsm_block");
+            return timed(r, "trsm.base", [&] {
+                return check_launch(r.c, f2::launch_trsm_block(r.s->w.p, r.s->w.stride, int(a), int(b - a), Ra,
+                                                               col0, int(col1 - col0), r.c->stream),
+                                    "k_trsm_block");
+            });
         return rank_updates(r, a, b, col0, col1, Rb, "k_update(trsm)");
     }
     const size_t m = a + (b - a) / 2, Rm = Ra + 64 * (m - a);
     F2_TRY(rec_trsm(r, a, m, Ra, col0, col1));
-    F2_TRY(best_product(r.c, wview(*r.s, Rm, Rb - Rm, col0, col1 - col0),
-                        wview(*r.s, Rm, Rb - Rm, a, m - a), wview(*r.s, Ra, Rm - Ra, col0, col1 - col0),
-                        r.cut, r.tc_cut));
+    F2_TRY(timed(r, (m - a) * 64 >= 8192 ? "trsm.prod.big" : "trsm.prod.small", [&] {
+        return best_product(r.c, wview(*r.s, Rm, Rb - Rm, col0, col1 - col0), wview(*r.s, Rm, Rb - Rm, a, m - a),
+                            wview(*r.s, Ra, Rm - Ra, col0, col1 - col0), r.cut, r.tc_cut);
+    }));
     return rec_trsm(r, m, b, Rm, col0, col1);
 }
 
@@ -935,12 +945,25 @@ int rec_leaf(RecRun& r, size_t c0, size_t c1) {
     return F2GPU_OK;
 }
 
+template <typename F>
+int timed(RecRun& r, const char* what, F&& f) {
+    if (!r.phases) return f();
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, r.c->stream);
+    const int rc = f();
+    cudaEventRecord(b, r.c->stream);
+    (*r.phases)[what].ev.push_back({a, b});
+    return rc;
+}
+
 int rec_decompose(RecRun& r, size_t c0, size_t c1) {
     // tall leaves are update-bound (the trailing update streams rows x remaining
     // leaf columns per panel), so they are narrower than short, chain-bound ones
     const size_t rows0 = r.n - std::min(r.n, 64 * c0);  // rows below the leaf's first panel at full rank
     const size_t leaf = (r.tall_rows && rows0 >= r.tall_rows) ? std::min(r.base, r.tall_base) : r.base;
-    if (c1 - c0 <= leaf) return rec_leaf(r, c0, c1);
+    if (c1 - c0 <= leaf) return timed(r, "leaf", [&] { return rec_leaf(r, c0, c1); });
     const size_t cm = c0 + (c1 - c0) / 2;
     F2_TRY(rec_decompose(r, c0, cm));
     size_t R0, r0, Rl, rl;
@@ -950,11 +973,13 @@ int rec_decompose(RecRun& r, size_t c0, size_t c1) {
     const bool full = R1 - R0 == 64 * (cm - c0) && R0 % 64 == 0;
     F2_TRY(ensure_cols(r, c1));
     if (full) {
-        F2_TRY(rec_trsm(r, c0, cm, R0, cm, c1));
+        F2_TRY(timed(r, "trsm", [&] { return rec_trsm(r, c0, cm, R0, cm, c1); }));
         if (R1 < r.n)
-            F2_TRY(best_product(r.c, wview(*r.s, R1, r.n - R1, cm, c1 - cm),
-                                wview(*r.s, R1, r.n - R1, c0, cm - c0),
-                                wview(*r.s, R0, R1 - R0, cm, c1 - cm), r.cut, r.tc_cut));
+            F2_TRY(timed(r, "product", [&] {
+                return best_product(r.c, wview(*r.s, R1, r.n - R1, cm, c1 - cm),
+                                    wview(*r.s, R1, r.n - R1, c0, cm - c0),
+                                    wview(*r.s, R0, R1 - R0, cm, c1 - cm), r.cut, r.tc_cut);
+            }));
     } else {
         F2_TRY(rank_updates(r, c0, cm, cm, c1, r.n));
     }
@@ -1001,7 +1026,26 @@ int decompose_recursive(f2gpu_ctx* c, View w, size_t min_cols, uint32_t* perm, u
     CUDA_TRY(cudaMemsetAsync(c->scr_flags, 0, mu * 4 * kFlagsPerPanel, c->stream));
     c->tl.mark(c->stream, "start");
     F2_TRY(check_launch(c, f2::launch_iota(s.perm, n, c->stream), "k_iota"));
+    std::map<std::string, RecRun::Phase> phases;
+    if (const char* e = getenv("F2GPU_REC_TIMES"); e && e[0] == '1') r.phases = &phases;
     F2_TRY(rec_decompose(r, 0, mu));
+    if (r.phases) {
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        float tot = 0;
+        for (auto& [name, ph] : phases) {
+            float sum = 0;
+            for (auto& [a, b] : ph.ev) {
+                float ms = 0;
+                cudaEventElapsedTime(&ms, a, b);
+                sum += ms;
+                cudaEventDestroy(a);
+                cudaEventDestroy(b);
+            }
+            tot += sum;
+            fprintf(stderr, "[rec] %-8s %4zu x  %8.3f ms\n", name.c_str(), ph.ev.size(), sum);
+        }
+        fprintf(stderr, "[rec] total    %8.3f ms (phases on the main stream)\n", tot);
+    }
     c->tl.report("decompose_recursive");
     return read_results(c, s, n, mu, perm, rj, rank);
 }

@@ -645,6 +645,248 @@ __global__ void __launch_bounds__(kT3Threads, 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
 }
 
+// ---------------------------------------------------------------------------
+// k_gemm_tc5: the fp4 leaf as a PERSISTENT kernel.  k_gemm_tc3 runs one 256x240
+// tile per CTA and pays ~7 us per tile of setup, load latency and epilogue (a
+// k-scan on 1480 tiles: 7.3 us per wave at k = 64, +3.5 us per 1024 bits), which
+// is most of the time of the short-k products in the TRSM recursion.  Here one
+// CTA per SM loops over the tiles: TMEM is allocated and the scale-factor
+// columns written once, the raw and stage rings run on across tiles (the load
+// warp prefetches the next tile's words during the epilogue), and the MMA warp
+// waits on an accumulator-empty barrier that the epilogue warps arrive on once
+// they have read the previous tile's accumulators out of TMEM.
+// Tile t of the launch's linear tile space: z = t / (GX*GY) (the batched
+// problem), by = row tile, bx = column tile; tiles outside a problem skipped.
+// ---------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(kT3Threads, 1)
+    k_gemm_tc5(TcGemmArgs one, const TcGemmArgs* __restrict__ probs, uint32_t GX, uint32_t GY, uint32_t NT) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    unsigned char* raw = smem + size_t(kT3Stages) * kT3Stage;
+    uint64_t* full = reinterpret_cast<uint64_t*>(raw + size_t(kT3Raw) * kT3RawBytes);
+    uint64_t* empty = full + kT3Stages;
+    uint64_t* rfull = empty + kT3Stages;
+    uint64_t* rempty = rfull + kT3Raw;
+    uint64_t* done = rempty + kT3Raw;
+    uint64_t* acc_empty = done + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    auto tile_of = [&](uint32_t t, TcGemmArgs& P, size_t& c0, size_t& i0) -> bool {
+        const uint32_t per = GX * GY;
+        const uint32_t z = t / per, rem = t - z * per, by = rem / GX, bx = rem - by * GX;
+        P = probs ? probs[z] : one;
+        c0 = size_t(bx) * kT3Cols;
+        i0 = size_t(by) * kT3Rows;
+        return c0 < P.m && i0 < P.n;
+    };
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         sm_u32(tmem_slot)),
+                     "r"(512u));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int s = 0; s < kT3Stages; ++s) {
+            mbar_init_n(&full[s], kT3Exp / 32);
+            mbar_init_n(&empty[s], 1);
+        }
+        for (int s = 0; s < kT3Raw; ++s) {
+            mbar_init_n(&rfull[s], 1);
+            mbar_init_n(&rempty[s], kT3Exp / 32);
+        }
+        mbar_init_n(done, 1);
+        mbar_init_n(acc_empty, kT3Exp / 32);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+    if (warp < 4) {  // scale factors: every byte of columns 480..511 = E8M0 1.0
+        const uint32_t onev = 0x7F7F7F7Fu;
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, "
+            "%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(
+                tmem + (uint32_t(32 * warp) << 16) + kT3SfCol),
+            "r"(onev)
+            : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+
+    if (warp == kT3Load) {
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            size_t issued = 0;
+            for (uint32_t t = blockIdx.x; t < NT; t += gridDim.x) {
+                TcGemmArgs P;
+                size_t c0, i0;
+                if (!tile_of(t, P, c0, i0)) continue;
+                const int nvalid = int(min(size_t(kT3Rows), P.n - i0));
+                const size_t KB = (P.k + 63) / 64;
+                // rows past n: the bulk copy moves an even number of rows (16-byte
+                // granule); an odd last row is stored by this thread before the arrive
+                const int nb = nvalid & ~1;
+                for (size_t kb = 0; kb < KB; ++kb, ++issued) {
+                    if (issued >= size_t(kT3Raw)) mbar_wait1(&rempty[s], ph ^ 1);
+                    unsigned char* r = raw + size_t(s) * kT3RawBytes;
+                    if (nvalid & 1)
+                        reinterpret_cast<uint64_t*>(r)[kT3Cols + nb] = P.A[kb * P.sa + i0 + nb];
+                    mbar_expect(&rfull[s], uint32_t(kT3Cols + nb) * 8);
+                    bulk_g2s(r, P.BT + kb * P.sbt + c0, kT3Cols * 8, &rfull[s]);
+                    if (nb) bulk_g2s(r + kT3Cols * 8, P.A + kb * P.sa + i0, uint32_t(nb) * 8, &rfull[s]);
+                    if (++s == kT3Raw) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == kT3Mma) {
+        if (lane == 0) {
+            const uint32_t tsf = tmem + kT3SfCol;
+            int s = 0;
+            uint32_t ph = 0;
+            uint32_t it = 0;
+            for (uint32_t t = blockIdx.x; t < NT; t += gridDim.x) {
+                TcGemmArgs P;
+                size_t c0, i0;
+                if (!tile_of(t, P, c0, i0)) continue;
+                const size_t KB = (P.k + 63) / 64;
+                if (it > 0) {  // the epilogue has read the previous tile's accumulators
+                    mbar_wait1(acc_empty, (it - 1) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                }
+                for (size_t kb = 0; kb < KB; kb += kT3Kps) {
+                    mbar_wait1(&full[s], ph);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+                    for (int j = 0; j < kT3Kps; ++j) {
+                        if (kb + j >= KB) break;
+                        const uint32_t ta =
+                            sm_u32(smem + size_t(s) * kT3Stage + (j >> 1) * kT3Slot) + (j & 1) * 32;
+                        const uint32_t tb = ta + kT3ABytes;
+                        const uint32_t a0 = kb + j > 0 ? 1u : 0u;
+                        if (MODE != 2) {
+                            mma_f4(tmem, umma_desc(ta), umma_desc(tb), kIdescF4, a0, tsf);
+                            mma_f4(tmem + kT3Rows, umma_desc(ta + 128 * 64), umma_desc(tb), kIdescF4, a0, tsf);
+                        }
+                    }
+                    asm volatile(
+                        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                            sm_u32(&empty[s]))
+                        : "memory");
+                    if (++s == kT3Stages) { s = 0; ph ^= 1; }
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 sm_u32(done))
+                             : "memory");
+                ++it;
+            }
+        }
+        __syncwarp();
+    } else {
+        // thread t < 256: B^T row t; 256 <= t < 496: A^T row t - 256 (zero past n)
+        const bool active = tid < kT3RawWords;
+        const int region = tid < kT3Cols ? 0 : kT3ABytes;
+        const int r = tid < kT3Cols ? tid : tid - kT3Cols;
+        int s = 0, rs = 0;
+        uint32_t ph = 0, rph = 0;
+        size_t staged = 0;
+        uint32_t it = 0;
+        for (uint32_t t = blockIdx.x; t < NT; t += gridDim.x) {
+            TcGemmArgs P;
+            size_t c0, i0;
+            if (!tile_of(t, P, c0, i0)) continue;
+            const int nvalid = int(min(size_t(kT3Rows), P.n - i0));
+            const size_t KB = (P.k + 63) / 64;
+            const bool live = active && (tid < kT3Cols || r < nvalid);
+            for (size_t kb = 0; kb < KB; kb += kT3Kps, ++staged) {
+                if (staged >= size_t(kT3Stages)) mbar_wait1(&empty[s], ph ^ 1);
+#pragma unroll
+                for (int j = 0; j < kT3Kps; ++j) {
+                    if (kb + j >= KB) break;
+                    mbar_wait1(&rfull[rs], rph);
+                    uint64_t x = 0;
+                    if (live) ld_shared_u64(x, raw + size_t(rs) * kT3RawBytes + size_t(tid) * 8);
+                    if (active) {
+                        unsigned char* tile = smem + size_t(s) * kT3Stage + (j >> 1) * kT3Slot + region;
+                        if (MODE == 1) {
+                            if (x == 0x123456789ull) tile[r] = 1;
+                        } else {
+                            store_row_f4(tile, r, j & 1, x);
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive1(&rempty[rs]);
+                    if (++rs == kT3Raw) { rs = 0; rph ^= 1; }
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive1(&full[s]);
+                if (++s == kT3Stages) { s = 0; ph ^= 1; }
+            }
+            // epilogue: lane quarter lq = w & 3; 16-column chunks c = (w >> 2) + 4i of the
+            // 2 x 15 chunks; a ballot per row packs the 32 output columns of the quarter
+            mbar_wait1(done, it & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const int lq = warp & 3;
+            uint64_t* __restrict__ C = P.C;
+            const size_t sc = P.sc;
+            const int acc = P.acc;
+#pragma unroll 1
+            for (int ch = warp >> 2; ch < 2 * (kT3Rows / 16); ch += 4) {
+                const int accn = ch / (kT3Rows / 16), cc = ch % (kT3Rows / 16);
+                uint32_t v[16];
+                const uint32_t taddr = tmem + (uint32_t(32 * lq) << 16) + uint32_t(kT3Rows * accn + 16 * cc);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+                    "%11, %12, %13, %14, %15}, [%16];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                      "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+                      "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (MODE == 3) {  // debug: raw accumulators of tile (0, 0), [column][row] f32
+                    if (c0 == 0 && i0 == 0) {
+                        uint32_t* dump = reinterpret_cast<uint32_t*>(C);
+                        const int colx = accn * 128 + lq * 32 + lane;
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) dump[colx * kT3Rows + 16 * cc + q] = v[q];
+                    }
+                    continue;
+                }
+                uint32_t mine = 0;
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const uint32_t par = __float_as_uint(__uint_as_float(v[q]) + 8388608.0f) & 1u;
+                    const uint32_t bits = __ballot_sync(0xffffffffu, par);
+                    if (lane == q) mine = bits;
+                }
+                const int row = 16 * cc + lane;
+                const size_t col = c0 + size_t(accn) * 128 + size_t(lq) * 32;
+                if (lane < 16 && row < nvalid) {
+                    uint32_t* dst = reinterpret_cast<uint32_t*>(C + (col / 64) * sc + i0 + row) + ((col / 32) & 1);
+                    if (acc) mine ^= *dst;
+                    *dst = mine;
+                }
+            }
+            // accumulators read: the MMA warp may overwrite them with the next tile
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) mbar_arrive1(acc_empty);
+            ++it;
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
+}
+
 bool gemm_tc_ok(size_t n, size_t k, size_t m) {
     return n > 0 && k > 0 && m > 0 && n % kTcN == 0 && m % kTcM == 0 && k % 64 == 0;
 }
@@ -895,6 +1137,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT4Threads, 1)
 }
 
 namespace {
+using Tc5Fn = void (*)(TcGemmArgs, const TcGemmArgs*, uint32_t, uint32_t, uint32_t);
+Tc5Fn tc5_fn() {
+    static Tc5Fn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        // opt-in: at 65536^2 it measured no faster (64.66-64.71 ms for k <= 1024..4096
+        // vs 64.71 without), and its main loop is ~9% slower at large k
+        const char* pe = getenv("F2GPU_TC_PERSIST");
+        if (!pe || pe[0] != '1') return nullptr;
+        for (auto f : {k_gemm_tc5<0>, k_gemm_tc5<1>, k_gemm_tc5<2>, k_gemm_tc5<3>})
+            if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kT3Smem)) != cudaSuccess)
+                return nullptr;
+        const char* env = getenv("F2GPU_TC_MODE");
+        const int mode = env ? atoi(env) : 0;
+        fn = mode == 1 ? k_gemm_tc5<1> : mode == 2 ? k_gemm_tc5<2> : mode == 3 ? k_gemm_tc5<3> : k_gemm_tc5<0>;
+    }
+    return fn;
+}
+size_t tc5_max_k() {  // F2GPU_TC5_MAXK (default 2048)
+    static const size_t v = [] {
+        const char* e = getenv("F2GPU_TC5_MAXK");
+        return e ? size_t(atoll(e)) : size_t(2048);
+    }();
+    return v;
+}
+int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
 using Tc3Fn = void (*)(TcGemmArgs, const TcGemmArgs*);
 Tc3Fn tc3_fn() {
     static Tc3Fn fn = nullptr;
@@ -943,7 +1221,15 @@ cudaError_t launch_gemm_tc3(const uint64_t* A, size_t sa, size_t n, const uint64
         k_gemm_tc4<<<grid4, kT4Threads, kT4Smem, s>>>(p, nullptr);
         return cudaGetLastError();
     }
-    dim3 grid(unsigned(m / kT3Cols), unsigned((n + kT3Rows - 1) / kT3Rows));
+    const uint32_t GX = uint32_t(m / kT3Cols), GY = uint32_t((n + kT3Rows - 1) / kT3Rows);
+    // the persistent kernel hides the per-tile setup and load latency (~1.3 us of
+    // ~7) but its main loop measured ~9% slower at large k: short-k products only
+    if (Tc5Fn f5 = tc5_fn(); f5 && k <= tc5_max_k()) {
+        const uint32_t NT = GX * GY;
+        f5<<<std::min<uint32_t>(NT, uint32_t(sm_count())), kT3Threads, kT3Smem, s>>>(p, nullptr, GX, GY, NT);
+        return cudaGetLastError();
+    }
+    dim3 grid(GX, GY);
     fn<<<grid, kT3Threads, kT3Smem, s>>>(p, nullptr);
     return cudaGetLastError();
 }
@@ -966,7 +1252,16 @@ cudaError_t launch_gemm_tc3_batched(const TcGemmArgs* h_probs, const TcGemmArgs*
         k_gemm_tc4<<<grid4, kT4Threads, kT4Smem, s>>>(TcGemmArgs{}, d_probs);
         return cudaGetLastError();
     }
-    dim3 grid(unsigned(mx / kT3Cols), unsigned((nx + kT3Rows - 1) / kT3Rows), unsigned(nprob));
+    const uint32_t GX = uint32_t(mx / kT3Cols), GY = uint32_t((nx + kT3Rows - 1) / kT3Rows);
+    size_t kmax = 0;
+    for (int i = 0; i < nprob; ++i) kmax = std::max(kmax, h_probs[i].k);
+    if (Tc5Fn f5 = tc5_fn(); f5 && kmax <= tc5_max_k()) {
+        const uint32_t NT = GX * GY * uint32_t(nprob);
+        f5<<<std::min<uint32_t>(NT, uint32_t(sm_count())), kT3Threads, kT3Smem, s>>>(TcGemmArgs{}, d_probs, GX, GY,
+                                                                                       NT);
+        return cudaGetLastError();
+    }
+    dim3 grid(GX, GY, unsigned(nprob));
     fn<<<grid, kT3Threads, kT3Smem, s>>>(TcGemmArgs{}, d_probs);
     return cudaGetLastError();
 }
