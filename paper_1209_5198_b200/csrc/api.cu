@@ -187,7 +187,12 @@ struct f2gpu_ctx {
     bool fuse_post = true;      // F2GPU_POSTCOL=0: separate POST and next-column kernels
     bool panel_early = true;    // F2GPU_PANEL_EARLY=0: launch P(j+1) after k_post_col(j) completes
     uint32_t poll_ns = 0;       // F2GPU_POLL_NS: panel consumer warps' poll sleep
+    bool u_first_col = true;    // F2GPU_U_FIRSTCOL=0: release after column group 0 instead
+    bool panel_head = false;    // F2GPU_PANEL_HEAD=1: the panel kernel does the first rows itself (measured slower)
+    bool post_spin = true;      // F2GPU_POST_SPIN=0: k_post_col(j) waits for P(j) by event, not by counter
+    cudaEvent_t ev_panel2 = nullptr;
     cudaStream_t side = nullptr;          // lookahead: panel kernels run here
+    cudaStream_t side2 = nullptr;         // fused schedule: alternate panels (the next one is resident early)
     cudaStream_t copy = nullptr;          // decompose_recursive_host: chunked uploads
     std::vector<cudaEvent_t> chunk_ev;    // one per uploaded column chunk
     void* pend = nullptr;                 // uploaded, not yet materialised columns
@@ -623,8 +628,9 @@ int read_results(f2gpu_ctx* c, const Shard& s, size_t n, size_t mu, uint32_t* pe
 }
 
 // per panel j: [0] head, [1] window, [2] all row blocks of k_post_col(j);
-// [3] the release of update j's column group 0 (plain lookahead: [0] only)
-constexpr size_t kFlagsPerPanel = 4;
+// [3] the release of update j's first column (group); [4] panel kernel j done
+// (plain lookahead: [0] only)
+constexpr size_t kFlagsPerPanel = 8;
 
 int ensure_scratch(f2gpu_ctx* c, size_t n, size_t mu) {
     if (c->scr_st_cap < mu || c->scr_perm_cap < n || c->scr_flags_cap < mu) {
@@ -667,7 +673,10 @@ int ensure_scratch(f2gpu_ctx* c, size_t n, size_t mu) {
 int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_t c1, bool la,
                    size_t swap_cols = size_t(-1)) {
     if (swap_cols > mu) swap_cols = mu;
-    const int grid = la ? c->num_sms - 1 : c->num_sms;
+    const bool fused = la && c->fuse_post && f2::panel_link_ok();
+    // fused schedule: two panel kernels can be resident (the running one and the
+    // next one waiting for its head), each on its own SM
+    const int grid = !la ? c->num_sms : (fused && c->num_sms > 2 ? c->num_sms - 2 : c->num_sms - 1);
     auto upd = [&](size_t j, uint32_t* release, size_t skip = 0) {
         f2::UpdateArgs u{};
         u.C = s.w.p; u.sc = s.w.stride; u.c_wcol0 = j + 1 + skip; u.ncols = int(c1 - j - 1 - skip);
@@ -676,6 +685,7 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
         u.B = s.w.p; u.sb = s.w.stride; u.b_row0 = 0; u.b_wcol0 = j + 1 + skip;
         u.st = s.st + j;
         u.release = release;
+        u.first_col = release != nullptr && c->u_first_col;
         u.tag = c->trace_buf ? int(j) : -1;
         return check_launch(c, f2::launch_update(u, grid, c->stream), "k_update");
     };
@@ -692,24 +702,31 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
         }
         return F2GPU_OK;
     }
-    if (c->fuse_post && f2::panel_link_ok()) {
+    if (fused) {
         // Fused schedule:
         //   side: P(j+1) [waits k_post_col(j)'s counters: first rows / window / all;
         //         at its end applies its swaps to column j+2 once update j released it]
         //   main: k_post_col(j) [swaps except j, j+1; Y_j; column j+1 updated] ->
         //         U(j) on columns j+2.. [release after column group 0]
+        // k_post_col(j) queued ahead on the main stream waits on P(j)'s done counter
+        // (needs P(j+1) queued early on the alternating side streams)
+        const bool spin = c->post_spin && c->panel_early;
         auto link_for = [&](size_t j) {  // P(j)'s link
             f2::PanelLink l{};
             if (j > c0) {
                 uint32_t* f = c->scr_flags + (j - 1) * kFlagsPerPanel;
-                l.head = f; l.head_count = 1;
-                l.win = f + 1; l.win_count = 8;
+                l.head = f; l.head_count = 1;  // P(j-1)'s head chunk (or k_post_col's block 0)
+                l.win = f + 1; l.win_count = c->panel_head ? 8 - f2::kPanelHeadRows / 256 : 8;
                 l.all = f + 2; l.all_count = uint32_t(f2::post_col_yblocks(n));
                 if (j + 1 < c1) { l.next_ready = f + 3; l.next_count = uint32_t(grid); }
             }
-            if (j + 1 < c1) l.next = s.w.p + (j + 1) * s.w.stride;
+            if (j + 1 < c1) {
+                l.next = s.w.p + (j + 1) * s.w.stride;
+                if (c->panel_head) l.head_out = c->scr_flags + j * kFlagsPerPanel;  // this panel's head counter
+            }
             l.poll_ns = c->poll_ns;
             l.trace = c->trace_buf != nullptr;
+            if (spin) l.done_out = c->scr_flags + j * kFlagsPerPanel + 4;
             return l;
         };
         F2_TRY(check_launch(c, f2::launch_panel_link(s.w.p + c0 * s.w.stride, n, s.st, int(c0), link_for(c0),
@@ -718,25 +735,38 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
         // the side stream forks once after P(c0); every later panel kernel is queued
         // right behind its predecessor and spins on k_post_col's counters, so it is
         // resident (on the SM the update leaves free) before its column is ready
+        cudaStream_t sides[2] = {c->side, c->side2};
         if (c0 + 1 < c1 && c->panel_early) {
             CUDA_TRY(cudaEventRecord(c->ev_post, c->stream));
             CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_post, 0));
+            CUDA_TRY(cudaStreamWaitEvent(c->side2, c->ev_post, 0));
         }
         for (size_t j = c0; j < c1; ++j) {
-            if (j > c0) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_panel, 0));
+            if (j > c0 && !spin) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_panel, 0));
             uint32_t* f = c->scr_flags + j * kFlagsPerPanel;
             F2_TRY(check_launch(c, f2::launch_post_col(s.w.p, s.w.stride, int(swap_cols), int(j),
                                                        j + 1 < c1 ? int(j + 1) : -1, s.perm, n, s.st + j, f,
-                                                       c->stream, c->trace_buf != nullptr),
+                                                       c->stream, c->trace_buf != nullptr,
+                                                       j + 1 < c1 && c->panel_head ? f2::kPanelHeadRows : 0,
+                                                       j > c0 && spin ? f + 4 : nullptr),
                                 "k_post_col"));
             if (j + 1 >= c1) break;
             if (!c->panel_early) CUDA_TRY(cudaEventRecord(c->ev_post, c->stream));
             F2_TRY(upd(j, f + 3, 1));
-            if (!c->panel_early) CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_post, 0));
+            // P(j+1) alternates between the two side streams: queued behind P(j-1),
+            // it is resident while P(j) runs and starts on P(j)'s head counter
+            cudaStream_t ps = c->panel_early ? sides[(j - c0) & 1] : c->side;
+            if (!c->panel_early) CUDA_TRY(cudaStreamWaitEvent(ps, c->ev_post, 0));
             F2_TRY(check_launch(c, f2::launch_panel_link(s.w.p + (j + 1) * s.w.stride, n, s.st, int(j + 1),
-                                                         link_for(j + 1), c->side),
+                                                         link_for(j + 1), ps),
                                 "k_panel"));
+            CUDA_TRY(cudaEventRecord(c->ev_panel, ps));
+        }
+        if (spin && c0 + 1 < c1) {  // join both side streams (the posts only waited on counters)
             CUDA_TRY(cudaEventRecord(c->ev_panel, c->side));
+            CUDA_TRY(cudaEventRecord(c->ev_panel2, c->side2));
+            CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_panel, 0));
+            CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_panel2, 0));
         }
         return F2GPU_OK;
     }
@@ -1237,13 +1267,18 @@ int f2gpu_ctx_create(int device, f2gpu_ctx** out) {
     if (const char* pc = getenv("F2GPU_POSTCOL")) c->fuse_post = pc[0] != '0';
     if (const char* pe = getenv("F2GPU_PANEL_EARLY")) c->panel_early = pe[0] != '0';
     if (const char* pn = getenv("F2GPU_POLL_NS")) c->poll_ns = uint32_t(atoi(pn));
+    if (const char* uf = getenv("F2GPU_U_FIRSTCOL")) c->u_first_col = uf[0] != '0';
+    if (const char* ph = getenv("F2GPU_PANEL_HEAD")) c->panel_head = ph[0] != '0';
+    if (const char* ps = getenv("F2GPU_POST_SPIN")) c->post_spin = ps[0] != '0';
     if (const char* tc = getenv("F2GPU_TC")) c->use_tc = tc[0] != '0';
     if (const char* tcc = getenv("F2GPU_TC_CUT")) {
         c->tc_cutover = size_t(atoll(tcc));
         c->use_tc_cut_default = false;
     }
     CUDA_TRY(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->side2, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&c->ev_post, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_panel2, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&c->ev_panel, cudaEventDisableTiming));
     CUDA_TRY(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
     c->stream = c->own_stream;
@@ -1273,10 +1308,12 @@ int f2gpu_ctx_destroy(f2gpu_ctx* c) {
     cudaFree(c->scr_perm);
     cudaFree(c->scr_flags);
     if (c->side) { cudaStreamSynchronize(c->side); cudaStreamDestroy(c->side); }
+    if (c->side2) { cudaStreamSynchronize(c->side2); cudaStreamDestroy(c->side2); }
     if (c->copy) { cudaStreamSynchronize(c->copy); cudaStreamDestroy(c->copy); }
     for (cudaEvent_t e : c->chunk_ev) cudaEventDestroy(e);
     cudaFree(c->pend);
     if (c->ev_post) cudaEventDestroy(c->ev_post);
+    if (c->ev_panel2) cudaEventDestroy(c->ev_panel2);
     if (c->ev_panel) cudaEventDestroy(c->ev_panel);
     cudaFree(c->d_jump);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);

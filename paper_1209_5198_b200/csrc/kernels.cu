@@ -713,6 +713,41 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
         if (p.release && threadIdx.x == 0) release_signal(p.release, p.tag);
         return;
     }
+    if (p.release && p.first_col) {
+        // the first column alone: one 256-entry 4-bit table over its 64 B rows,
+        // rows split evenly over the CTAs, plain loads/stores -- the release the
+        // next panel kernel waits for comes ~1-2 us after launch instead of after
+        // a whole 16-column group (table build + tile pipeline + bulk drain)
+        uint64_t* t4 = tab;
+        const uint64_t* Bc = p.B + p.b_wcol0 * p.sb + b_row0;
+        if (threadIdx.x < 256) {
+            const int g = threadIdx.x >> 4, v = threadIdx.x & 15;
+            uint64_t x = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (((v >> q) & 1) && 4 * g + q < k) x ^= __ldg(Bc + 4 * g + q);
+            t4[threadIdx.x] = x;
+        }
+        __syncthreads();
+        uint64_t* Cc = p.C + p.c_wcol0 * p.sc;
+        const size_t G = gridDim.x, nrows = row_hi - row_lo, per = (nrows + G - 1) / G;
+        const size_t r0 = row_lo + size_t(blockIdx.x) * per, r1 = min(row_hi, r0 + per);
+        for (size_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+            const uint64_t a = p.a[i];
+            uint64_t x = Cc[i];
+#pragma unroll
+            for (int g = 0; g < 16; ++g) x ^= t4[16 * g + int((a >> (4 * g)) & 15)];
+            Cc[i] = x;
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) release_signal(p.release, p.tag);
+        __syncthreads();  // t4 lives where the group tables go
+        p.release = nullptr;
+        ++p.c_wcol0;
+        ++p.b_wcol0;
+        if (--p.ncols <= 0) return;
+    }
     const int nt = 9;  // all tables built (rows >= k are zero); lookup9 is branch-free
     const size_t base = row_lo & ~size_t(kV3Rows - 1);
     const size_t T = (row_hi - base + kV3Rows - 1) / kV3Rows;  // tiles per column group
@@ -1652,6 +1687,13 @@ struct PanelGjSmem {
     uint32_t ext_orig[64];
     uint4 log[66];      // per selection t: column-k mask over positions (3 words), meta
     uint2 logu[66];     // slow selections: dead positions u with x[k_u] (the reduction set)
+    uint32_t pd[128];   // composite pair list (dst, src), also kept here for the next-column swaps
+    uint32_t ps[128];
+    uint32_t fin;       // warps 0-2 finished (done_out)
+    uint64_t z[64];     // Z rows (head chunk)
+    uint64_t bs[64];    // next column's pivot rows after the swaps (head chunk)
+    uint64_t zt[256];   // 4-bit tables over Z and B (head chunk)
+    uint64_t bt[256];
     uint32_t want;  // warp 0's slow path needs entries < want - 1 applied to win/orig
     uint32_t done;  // = want once they are (published by warp 2 on request)
 };
@@ -1720,12 +1762,22 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     PanelGjSmem& S = *reinterpret_cast<PanelGjSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // every warp waits for the previous panel's head chunk (or the fused post's
+    // head) before reading its state: the kernel may be queued on another stream
+    // and resident while the previous panel kernel still runs
+    wait_count_ge_warp(link.head, link.head_count);
     const size_t R = j == 0 ? 0 : size_t(st_all[j - 1].R) + st_all[j - 1].r;
     PanelState* st = st_all + j;
     const size_t rows = R < n ? n - R : 0;
     if (rows == 0) {
         if (tid == 0) { st->R = uint32_t(R < n ? R : n); st->r = 0; st->npairs = 0; st->flags = 0; }
         if (tid < 64) st->Z[tid] = 0;
+        if (link.head_out || link.done_out) {  // counters other kernels wait on
+            __threadfence();
+            __syncthreads();
+            if (tid == 0 && link.head_out) atomicAdd(link.head_out, 1u);
+            if (tid == 0 && link.done_out) atomicAdd(link.done_out, 1u);
+        }
         return;
     }
     uint64_t* A = col + R;
@@ -1738,9 +1790,8 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
         // warp 0 starts on its own rows (loaded below) without waiting for the
         // window; it zeroes the log, then releases the two consumer warps
         for (int t = lane; t < 66; t += 32) S.log[t] = make_uint4(0, 0, 0, 0);
-        if (lane == 0) { S.done = 0; S.want = 0; }
+        if (lane == 0) { S.done = 0; S.want = 0; S.fin = 0; }
         asm volatile("bar.arrive 3, 96;" ::: "memory");
-        wait_count_ge_warp(link.head, link.head_count);
         if (link.trace && lane == 0) trace_ev(kTrPanelBegin, j);
         __syncwarp();
     } else if (warp == 1) {
@@ -1760,6 +1811,56 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
 #ifdef GJ_PROFILE
     const long long t_loaded = clock64();
 #endif
+
+    // Head chunk (warps 0-2 after their own work, link.head_out set): Y = D*Z for
+    // the first kPanelHeadRows rows below the pivots (D from the swapped window)
+    // and next[i] ^= Y_i * B, B = the next column's pivot rows (swapped by warp 2
+    // just before), then the head counter the next panel kernel waits on.  This
+    // takes the fused post's launch and first chunk off the panel chain.
+    auto head_chunk = [&](uint32_t r) {
+        const int t3 = tid;  // 0..95
+        asm volatile("bar.sync 4, 96;" ::: "memory");
+        const size_t lo = R + r;
+        const uint32_t H = (r != 0 && lo < n) ? uint32_t(min(size_t(kPanelHeadRows), n - lo)) : 0u;
+        if (H) {
+            if (t3 < 64) S.bs[t3] = uint32_t(t3) < r ? link.next[R + t3] : 0ull;
+            asm volatile("bar.sync 4, 96;" ::: "memory");
+            for (int e = t3; e < 256; e += 96) {
+                const int g = e >> 4, v = e & 15;
+                uint64_t za = 0, zb = 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if ((v >> q) & 1) { za ^= S.z[4 * g + q]; zb ^= S.bs[4 * g + q]; }
+                S.zt[e] = za;
+                S.bt[e] = zb;
+            }
+            asm volatile("bar.sync 4, 96;" ::: "memory");
+            for (uint32_t p = r + t3; p < r + H; p += 96) {
+                const uint64_t d = S.win[p];
+                uint64_t y = 0;
+#pragma unroll
+                for (int g = 0; g < 16; ++g) y ^= S.zt[16 * g + int((d >> (4 * g)) & 15)];
+                uint64_t x = link.next[R + p];
+#pragma unroll
+                for (int g = 0; g < 16; ++g) x ^= S.bt[16 * g + int((y >> (4 * g)) & 15)];
+                A[p] = y;
+                link.next[R + p] = x;
+            }
+        }
+        __threadfence();
+        asm volatile("bar.sync 4, 96;" ::: "memory");
+        if (t3 == 0) atomicAdd(link.head_out, 1u);
+    };
+    // each of warps 0-2 calls this once, after its last global write
+    auto finish = [&]() {
+        if (!link.done_out) return;
+        __threadfence();
+        __syncwarp();
+        if (lane == 0 && atomicAdd(&S.fin, 1u) == 2u) {
+            __threadfence();
+            atomicAdd(link.done_out, 1u);
+        }
+    };
 
     if (warp == 2) {
         // ---- win/orig bookkeeping: replay the fast swaps ----
@@ -1822,8 +1923,8 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
             if (moved) {
                 const uint32_t e = np + __popc(bal & ((1u << lane) - 1));
                 A[x] = S.win[x];
-                st->dst[e] = x;
-                st->src[e] = S.orig[x];
+                st->dst[e] = S.pd[e] = x;
+                st->src[e] = S.ps[e] = S.orig[x];
             }
             np += __popc(bal);
         }
@@ -1833,15 +1934,18 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
             const uint32_t bal = __ballot_sync(0xffffffffu, moved);
             if (moved) {
                 const uint32_t d = np + __popc(bal & ((1u << lane) - 1));
-                st->dst[d] = S.ext_pos[e];
-                st->src[d] = S.ext_orig[e];
+                st->dst[d] = S.pd[d] = S.ext_pos[e];
+                st->src[d] = S.ps[d] = S.ext_orig[e];
             }
             np += __popc(bal);
         }
+        __syncwarp();
         if (lane == 0) st->npairs = np;
+        // column j+1 is final for the earlier panels once the previous update has
+        // released it: needed by the swaps below AND by the head chunk's reads
+        if (link.next) wait_count_ge_warp(link.next_ready, link.next_count);
         if (link.next && np) {
             // this panel's row swaps on column j+1 (the fused POST skips it)
-            wait_count_ge_warp(link.next_ready, link.next_count);
             __threadfence_block();
             uint64_t* nx = link.next + R;
             uint32_t d[4], sv[4];
@@ -1849,7 +1953,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const uint32_t e = lane + 32 * q;
-                if (e < np) { d[q] = st->dst[e]; sv[q] = st->src[e]; }
+                if (e < np) { d[q] = S.pd[e]; sv[q] = S.ps[e]; }
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q)
@@ -1863,6 +1967,11 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
 #ifdef GJ_PROFILE
         if (lane == 0) reinterpret_cast<long long*>(st->src)[56] = clock64() - t_start;
 #endif
+        if (link.head_out) {
+            __threadfence_block();
+            head_chunk(t);
+        }
+        finish();
         return;
     }
 
@@ -1935,11 +2044,19 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
         uint64_t x0 = uint64_t(y0[0]) | (uint64_t(y0[1]) << 32);
         uint64_t x1 = uint64_t(y1[0]) | (uint64_t(y1[1]) << 32);
         warp_transpose64(x0, x1, lane);
-        if (uint32_t(lane) < r) st->Z[(S.log[lane].w >> 8) & 63u] = (1ull << lane) ^ x0;
-        if (uint32_t(lane) + 32 < r) st->Z[(S.log[lane + 32].w >> 8) & 63u] = (1ull << (lane + 32)) ^ x1;
+        if (uint32_t(lane) < r) {
+            const uint32_t kz = (S.log[lane].w >> 8) & 63u;
+            st->Z[kz] = S.z[kz] = (1ull << lane) ^ x0;
+        }
+        if (uint32_t(lane) + 32 < r) {
+            const uint32_t kz = (S.log[lane + 32].w >> 8) & 63u;
+            st->Z[kz] = S.z[kz] = (1ull << (lane + 32)) ^ x1;
+        }
 #ifdef GJ_PROFILE
         if (lane == 0) reinterpret_cast<long long*>(st->src)[57] = clock64() - t_start;
 #endif
+        if (link.head_out) head_chunk(r);
+        finish();
         return;
     }
 
@@ -2108,8 +2225,8 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
 #ifdef GJ_PROFILE
     const long long t_chain = clock64();
 #endif
-    if (!((sel >> lane) & 1)) st->Z[lane] = 0;
-    if (!((sel >> (lane + 32)) & 1)) st->Z[lane + 32] = 0;
+    if (!((sel >> lane) & 1)) st->Z[lane] = S.z[lane] = 0;
+    if (!((sel >> (lane + 32)) & 1)) st->Z[lane + 32] = S.z[lane + 32] = 0;
     if (lane == 0) {
         st->R = uint32_t(R);
         st->r = ib;
@@ -2124,6 +2241,8 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
         pr[60] = 0;
     }
 #endif
+    if (link.head_out) head_chunk(ib);
+    finish();
 }
 
 static bool g_panel_gj = true;  // F2GPU_PANEL=0: the transposed-M k_panel
@@ -2356,9 +2475,21 @@ int post_col_yblocks(size_t n) {
 __global__ void __launch_bounds__(256) k_post_col(uint64_t* __restrict__ w, size_t stride, int ncols,
                                                   int panel_col, int next_col, uint32_t* __restrict__ perm,
                                                   size_t n, const PanelState* __restrict__ st,
-                                                  int swap_blocks, uint32_t* __restrict__ flags, bool trace) {
+                                                  int swap_blocks, uint32_t* __restrict__ flags, bool trace,
+                                                  int skip, const uint32_t* wait_panel) {
     __shared__ uint64_t zs[64], bs[64];
     __shared__ uint64_t zt[256], bt[256];
+    if (wait_panel) {  // queued ahead: the panel kernel's writes are complete
+        if (threadIdx.x < 32) {
+            while (true) {
+                uint32_t v;
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(wait_panel) : "memory");
+                if (__all_sync(0xffffffffu, v != 0)) break;
+                __nanosleep(128);
+            }
+        }
+        __syncthreads();
+    }
     if (int(blockIdx.x) < swap_blocks) {
         swaps_body(w, stride, ncols, panel_col, perm, st,
                    int((size_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5), next_col);
@@ -2375,8 +2506,11 @@ __global__ void __launch_bounds__(256) k_post_col(uint64_t* __restrict__ w, size
         zs[tid] = st->Z[tid];
         bs[tid] = (nx && uint32_t(tid) < r) ? nx[R + tid] : 0;
     }
-    const size_t i0 = lo + size_t(blk) * blockDim.x + tid;
-    const bool work = r != 0 && lo < n;
+    // rows [lo, lo + skip) were done by the panel kernel (its head chunk), which
+    // also signals flags[0]; the window counter then covers blocks < 8 - skip/256
+    const size_t i0 = lo + size_t(skip) + size_t(blk) * blockDim.x + tid;
+    const unsigned nwin = 8u - unsigned(skip) / 256u;
+    const bool work = r != 0 && lo + size_t(skip) < n;
     const uint64_t d0 = (work && i0 < n) ? col[i0] : 0;
     const uint64_t x0 = (work && nx && i0 < n) ? nx[i0] : 0;
     __syncthreads();
@@ -2403,11 +2537,11 @@ __global__ void __launch_bounds__(256) k_post_col(uint64_t* __restrict__ w, size
             }
         };
         if (i0 < n) row(i0, d0, x0);
-        if (flags && blk < 8) {  // every writer fences, then one arrival per block
+        if (flags && blk < nwin) {  // every writer fences, then one arrival per block
             __threadfence();
             __syncthreads();
             if (tid == 0) {
-                if (blk == 0) {
+                if (blk == 0 && skip == 0) {
                     atomicAdd(flags + 0, 1u);
                     if (trace) trace_ev(kTrPostHead, panel_col);
                 }
@@ -2425,17 +2559,18 @@ __global__ void __launch_bounds__(256) k_post_col(uint64_t* __restrict__ w, size
             }
         }
     } else if (tid == 0 && flags) {
-        if (blk == 0) atomicAdd(flags + 0, 1u);
-        if (blk < 8) atomicAdd(flags + 1, 1u);
+        if (blk == 0 && skip == 0) atomicAdd(flags + 0, 1u);
+        if (blk < nwin) atomicAdd(flags + 1, 1u);
         atomicAdd(flags + 2, 1u);
     }
 }
 
 cudaError_t launch_post_col(uint64_t* w, size_t stride, int ncols, int panel_col, int next_col, uint32_t* perm,
-                            size_t n, const PanelState* st, uint32_t* flags, cudaStream_t s, bool trace) {
+                            size_t n, const PanelState* st, uint32_t* flags, cudaStream_t s, bool trace,
+                            int skip, const uint32_t* wait_panel) {
     const int swap_blocks = (ncols + 1 + 7) / 8;
     k_post_col<<<swap_blocks + post_col_yblocks(n), 256, 0, s>>>(w, stride, ncols, panel_col, next_col, perm, n,
-                                                                  st, swap_blocks, flags, trace);
+                                                                  st, swap_blocks, flags, trace, skip, wait_panel);
     return cudaGetLastError();
 }
 

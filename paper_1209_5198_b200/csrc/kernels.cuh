@@ -47,6 +47,10 @@ struct UpdateArgs {
     // *release once its group-0 updates are complete in memory (exactly once per
     // CTA, also when it has no work).  The next panel kernel waits for the count.
     uint32_t* release;
+    // with release: the first column (the one the next panel kernel waits for)
+    // alone first, split by rows over every CTA with a 4-bit table, then the
+    // release, then the remaining columns in 16-column groups
+    bool first_col = false;
     int tag = -1;  // panel index for the device trace; >= 0 only while it is on
 };
 
@@ -113,7 +117,17 @@ struct PanelLink {
     const uint32_t* next_ready; uint32_t next_count;
     uint32_t poll_ns = 0;  // sleep between polls of the consumer warps
     bool trace = false;    // device trace stamps (diagnostics)
+    // head_out != nullptr (needs next): the panel kernel itself writes Y and the
+    // next column's update for the first kPanelHeadRows rows below its pivots,
+    // then increments *head_out (the next panel kernel's head counter); the
+    // fused post skips those rows
+    uint32_t* head_out = nullptr;
+    // done_out: incremented once every write of this panel kernel (state, pair
+    // list, swapped window, next-column swaps) is in memory; a fused post queued
+    // ahead of time waits on it instead of a cross-stream event
+    uint32_t* done_out = nullptr;
 };
+constexpr int kPanelHeadRows = 256;
 cudaError_t launch_panel_link(uint64_t* col, size_t n, PanelState* st_all, int j, const PanelLink& link,
                               cudaStream_t s);
 bool panel_link_ok();  // false when F2GPU_PANEL=0 selects the older panel kernel
@@ -125,7 +139,7 @@ bool panel_link_ok();  // false when F2GPU_PANEL=0 selects the older panel kerne
 int post_col_yblocks(size_t n);
 cudaError_t launch_post_col(uint64_t* w, size_t stride, int ncols, int panel_col, int next_col, uint32_t* perm,
                             size_t n, const PanelState* st, uint32_t* flags, cudaStream_t s,
-                            bool trace = false);
+                            bool trace = false, int skip = 0, const uint32_t* wait_panel = nullptr);
 // lookahead: panel j's update of word-column j+1 only; increments *done per CTA
 int update_col_grid(size_t n, int num_sms);
 cudaError_t launch_update_col(uint64_t* next, const uint64_t* ycol, size_t n, const PanelState* st, uint32_t* done,
