@@ -454,10 +454,17 @@ constexpr uint32_t kIdescF4 = idesc_f4(128, kT3Rows);
 
 __device__ __forceinline__ void ld_shared_u64(uint64_t& v, const void* p) { v = *reinterpret_cast<const uint64_t*>(p); }
 
+#ifdef TC3_PROFILE
+__device__ long long g_tc3_prof[8];
+#endif
 template <int MODE>
 __global__ void __launch_bounds__(kT3Threads, 1)
     k_gemm_tc3(TcGemmArgs one, const TcGemmArgs* __restrict__ probs) {
     // one problem per launch, or a batch (blockIdx.z = problem; Strassen leaves)
+#ifdef TC3_PROFILE
+    const bool prof = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+    if (prof && threadIdx.x == 0) g_tc3_prof[0] = clock64();
+#endif
     const TcGemmArgs P = probs ? probs[blockIdx.z] : one;
     if (size_t(blockIdx.x) * kT3Cols >= P.m || size_t(blockIdx.y) * kT3Rows >= P.n) return;
     const uint64_t* __restrict__ A = P.A;
@@ -514,6 +521,9 @@ __global__ void __launch_bounds__(kT3Threads, 1)
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
+#ifdef TC3_PROFILE
+    if (prof && threadIdx.x == 0) g_tc3_prof[1] = clock64();
+#endif
 
     if (warp == kT3Load) {
         if (lane == 0) {
@@ -542,6 +552,9 @@ __global__ void __launch_bounds__(kT3Threads, 1)
             for (size_t kb = 0; kb < KB; kb += kT3Kps) {
                 mbar_wait1(&full[s], ph);
                 asm volatile("tcgen05.fence::after_thread_sync;");
+#ifdef TC3_PROFILE
+                if (prof && kb == 0) g_tc3_prof[2] = clock64();
+#endif
 #pragma unroll
                 for (int j = 0; j < kT3Kps; ++j) {
                     if (kb + j >= KB) break;
@@ -561,6 +574,9 @@ __global__ void __launch_bounds__(kT3Threads, 1)
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                              sm_u32(done))
                          : "memory");
+#ifdef TC3_PROFILE
+            if (prof) g_tc3_prof[3] = clock64();
+#endif
         }
         __syncwarp();
     } else {
@@ -600,6 +616,9 @@ __global__ void __launch_bounds__(kT3Threads, 1)
         // 2 x 15 chunks; a ballot per row packs the 32 output columns of the quarter
         mbar_wait1(done, 0);
         asm volatile("tcgen05.fence::after_thread_sync;");
+#ifdef TC3_PROFILE
+        if (prof && threadIdx.x == 0) g_tc3_prof[4] = clock64();
+#endif
         const int lq = warp & 3;
 #pragma unroll 1
         for (int ch = warp >> 2; ch < 2 * (kT3Rows / 16); ch += 4) {
@@ -639,10 +658,16 @@ __global__ void __launch_bounds__(kT3Threads, 1)
             }
         }
     }
+#ifdef TC3_PROFILE
+    if (prof && threadIdx.x == 0) g_tc3_prof[5] = clock64();
+#endif
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
+#ifdef TC3_PROFILE
+    if (prof && threadIdx.x == 0) g_tc3_prof[6] = clock64();
+#endif
 }
 
 // ---------------------------------------------------------------------------
