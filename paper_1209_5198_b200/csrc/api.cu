@@ -1036,13 +1036,16 @@ int decompose_recursive(f2gpu_ctx* c, View w, size_t min_cols, uint32_t* perm, u
     RecRun r{c, &s, n, mu, std::max<size_t>(1, (min_cols ? min_cols : 256 * 64) / 64),
              lookahead_ok(c, s, n), 16384, 16};
     if (const char* e = getenv("F2GPU_REC_CUT")) r.cut = size_t(atol(e));
+    if (const char* e = getenv("F2GPU_REC_BASE")) r.base = std::max<size_t>(1, size_t(atol(e)));
     if (const char* e = getenv("F2GPU_REC_TBASE")) r.tbase = std::max<size_t>(1, size_t(atol(e)));
     if (const char* e = getenv("F2GPU_REC_TRSM")) r.trsm_kernel = e[0] != '0';
-    // tall leaves: 64 panels once a leaf has >= 20000 rows below its first panel
-    // (65536^2 sweep over 16000..56000 rows x 32..128 panels: 70.5 -> 67.5 ms)
+    // tall leaves: 128 panels once a leaf has >= 20000 rows below its first panel
+    // (65536^2 sweeps over 12000..56000 rows x 32..128 panels; first 70.5 -> 67.5 ms
+    // with 64 panels, re-swept after the panel-chain work: 128 panels 64.3 ms,
+    // 64: 64.6, 32: 66.3)
     r.tall_rows = 20000;
     if (const char* e = getenv("F2GPU_REC_TALL")) r.tall_rows = size_t(atol(e));
-    r.tall_base = 64;
+    r.tall_base = 128;
     if (!r.c->use_tc_cut_default) r.tc_cut = r.c->tc_cutover;  // set explicitly (F2GPU_TC_CUT / ctx_set_tc)
     if (const char* e = getenv("F2GPU_REC_TC_CUT")) r.tc_cut = size_t(atol(e));
     if (const char* e = getenv("F2GPU_REC_TALL_BASE")) r.tall_base = std::max<size_t>(1, size_t(atol(e)));
