@@ -2596,18 +2596,27 @@ __global__ void __launch_bounds__(kTrsmThreads) k_trsm_block(uint64_t* __restric
     const int tid = threadIdx.x;
     uint64_t* col = W + (col0 + blockIdx.x) * stride + Ra;
     const int rows = 64 * P;
-    for (int i = tid; i < rows; i += kTrsmThreads) cs[i] = col[i];
-    __syncthreads();
-    for (int t = 0; t < P; ++t) {
-        // all multiplier words this thread needs for panel t, loaded together
+    // multiplier words of panel t for this thread's rows; panel t+1's are loaded
+    // while panel t is applied (one L2 round trip per panel otherwise)
+    auto load_y = [&](int t, uint64_t (&y)[kTrsmRowsPerThread]) {
         const uint64_t* Y = W + size_t(a + t) * stride + Ra;
         const int r0 = 64 * (t + 1) + tid;
-        uint64_t y[kTrsmRowsPerThread];
 #pragma unroll
         for (int i = 0; i < kTrsmRowsPerThread; ++i) {
             const int r = r0 + kTrsmThreads * i;
             y[i] = r < rows ? Y[r] : 0;
         }
+    };
+    uint64_t ynext[kTrsmRowsPerThread];
+    load_y(0, ynext);
+    for (int i = tid; i < rows; i += kTrsmThreads) cs[i] = col[i];
+    __syncthreads();
+    for (int t = 0; t < P; ++t) {
+        const int r0 = 64 * (t + 1) + tid;
+        uint64_t y[kTrsmRowsPerThread];
+#pragma unroll
+        for (int i = 0; i < kTrsmRowsPerThread; ++i) y[i] = ynext[i];
+        if (t + 1 < P) load_y(t + 1, ynext);
         // 4-bit table of panel t's final pivot words (2 entries per thread)
         const uint64_t* B = cs + 64 * t;
 #pragma unroll

@@ -912,6 +912,274 @@ __global__ void __launch_bounds__(kT3Threads, 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
 }
 
+// ---------------------------------------------------------------------------
+// k_gemm_tc6: persistent fp4 leaf with DOUBLE-BUFFERED accumulators, for short-k
+// products.  A 256x240 tile needs all 480 TMEM columns, so the next tile's MMAs
+// wait for the epilogue (~6.7k cycles of TMEM reads + ballots per tile, ~40% of a
+// k = 1024 tile, tools/micro/tc3_prof.cu).  Here a tile is 128 output columns
+// (M = 128, one MMA per k-block) x 240 rows: two accumulators fit (columns 0 and
+// 240), four dedicated epilogue warps (one per TMEM lane quarter) drain tile t
+// while the MMA warp fills the other buffer with tile t+1.  Per MAC it moves
+// ~22% more shared memory than k_gemm_tc3 (the 240 B-side rows are expanded per
+// 128 columns instead of per 256), so it is used only for short k.
+// Warps 0-11 expand (thread t < 128: B^T row t; 128 <= t < 368: A row t - 128),
+// 12-19 epilogue (two warps per TMEM lane quarter, alternate 16-column chunks,
+// two TMEM loads in flight), 20 MMA, 21 load.
+// ---------------------------------------------------------------------------
+constexpr int kT6Cols = 128;                 // output columns per tile (M)
+constexpr int kT6Rows = kT3Rows;             // output rows per tile (N = 240)
+constexpr int kT6Exp = 384;                  // expansion threads (warps 0-11)
+constexpr int kT6Epi = 12;                   // first epilogue warp (12-19: two per TMEM lane quarter)
+constexpr int kT6EpiWarps = 8;
+constexpr int kT6Mma = 20;
+constexpr int kT6Load = 21;
+constexpr int kT6Threads = 22 * 32;
+constexpr int kT6ABytes = kT6Cols * 64;      // B^T side of a slot: 2 k-blocks x 32 B per row
+constexpr int kT6BBytes = kT6Rows * 64;      // A side
+constexpr int kT6Slot = kT6ABytes + kT6BBytes;
+constexpr int kT6Stage = kT3Slots * kT6Slot;  // 4 k-blocks per stage
+constexpr int kT6Stages = 3;
+constexpr int kT6RawWords = kT6Cols + kT6Rows;
+constexpr int kT6RawBytes = kT6RawWords * 8;
+constexpr int kT6Raw = 8;
+constexpr size_t kT6Smem = size_t(kT6Stages) * kT6Stage + size_t(kT6Raw) * kT6RawBytes + 256;
+static_assert(kT6ABytes % 512 == 0 && kT6BBytes % 512 == 0, "SWIZZLE_64B atoms");
+
+template <int MODE>
+__global__ void __launch_bounds__(kT6Threads, 1)
+    k_gemm_tc6(TcGemmArgs one, const TcGemmArgs* __restrict__ probs, uint32_t GX, uint32_t GY, uint32_t NT) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    unsigned char* raw = smem + size_t(kT6Stages) * kT6Stage;
+    uint64_t* full = reinterpret_cast<uint64_t*>(raw + size_t(kT6Raw) * kT6RawBytes);
+    uint64_t* empty = full + kT6Stages;
+    uint64_t* rfull = empty + kT6Stages;
+    uint64_t* rempty = rfull + kT6Raw;
+    uint64_t* acc_full = rempty + kT6Raw;   // [2]
+    uint64_t* acc_empty = acc_full + 2;     // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    auto tile_of = [&](uint32_t t, TcGemmArgs& P, size_t& c0, size_t& i0) -> bool {
+        const uint32_t per = GX * GY;
+        const uint32_t z = t / per, rem = t - z * per, by = rem / GX, bx = rem - by * GX;
+        P = probs ? probs[z] : one;
+        c0 = size_t(bx) * kT6Cols;
+        i0 = size_t(by) * kT6Rows;
+        return c0 < P.m && i0 < P.n;
+    };
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         sm_u32(tmem_slot)),
+                     "r"(512u));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int s = 0; s < kT6Stages; ++s) {
+            mbar_init_n(&full[s], kT6Exp / 32);
+            mbar_init_n(&empty[s], 1);
+        }
+        for (int s = 0; s < kT6Raw; ++s) {
+            mbar_init_n(&rfull[s], 1);
+            mbar_init_n(&rempty[s], kT6Exp / 32);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init_n(&acc_full[b], 1);
+            mbar_init_n(&acc_empty[b], kT6EpiWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = *tmem_slot;
+    if (warp < 4) {  // scale factors: every byte of columns 480..511 = E8M0 1.0
+        const uint32_t onev = 0x7F7F7F7Fu;
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, "
+            "%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(
+                tmem + (uint32_t(32 * warp) << 16) + kT3SfCol),
+            "r"(onev)
+            : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+
+    if (warp == kT6Load) {
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            size_t issued = 0;
+            for (uint32_t t = blockIdx.x; t < NT; t += gridDim.x) {
+                TcGemmArgs P;
+                size_t c0, i0;
+                if (!tile_of(t, P, c0, i0)) continue;
+                const int nvalid = int(min(size_t(kT6Rows), P.n - i0));
+                const size_t KB = (P.k + 63) / 64;
+                const int nb = nvalid & ~1;
+                for (size_t kb = 0; kb < KB; ++kb, ++issued) {
+                    if (issued >= size_t(kT6Raw)) mbar_wait1(&rempty[s], ph ^ 1);
+                    unsigned char* r = raw + size_t(s) * kT6RawBytes;
+                    if (nvalid & 1)
+                        reinterpret_cast<uint64_t*>(r)[kT6Cols + nb] = P.A[kb * P.sa + i0 + nb];
+                    mbar_expect(&rfull[s], uint32_t(kT6Cols + nb) * 8);
+                    bulk_g2s(r, P.BT + kb * P.sbt + c0, kT6Cols * 8, &rfull[s]);
+                    if (nb) bulk_g2s(r + kT6Cols * 8, P.A + kb * P.sa + i0, uint32_t(nb) * 8, &rfull[s]);
+                    if (++s == kT6Raw) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == kT6Mma) {
+        if (lane == 0) {
+            const uint32_t tsf = tmem + kT3SfCol;
+            int s = 0;
+            uint32_t ph = 0;
+            uint32_t it = 0;
+            for (uint32_t t = blockIdx.x; t < NT; t += gridDim.x) {
+                TcGemmArgs P;
+                size_t c0, i0;
+                if (!tile_of(t, P, c0, i0)) continue;
+                const size_t KB = (P.k + 63) / 64;
+                const uint32_t b = it & 1;
+                if (it >= 2) {  // the epilogue has drained this buffer's previous tile
+                    mbar_wait1(&acc_empty[b], ((it >> 1) - 1) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                }
+                const uint32_t tacc = tmem + b * uint32_t(kT6Rows);
+                for (size_t kb = 0; kb < KB; kb += kT3Kps) {
+                    mbar_wait1(&full[s], ph);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+                    for (int j = 0; j < kT3Kps; ++j) {
+                        if (kb + j >= KB) break;
+                        const uint32_t ta =
+                            sm_u32(smem + size_t(s) * kT6Stage + (j >> 1) * kT6Slot) + (j & 1) * 32;
+                        const uint32_t tb = ta + kT6ABytes;
+                        const uint32_t a0 = kb + j > 0 ? 1u : 0u;
+                        if (MODE != 2) mma_f4(tacc, umma_desc(ta), umma_desc(tb), kIdescF4, a0, tsf);
+                    }
+                    asm volatile(
+                        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                            sm_u32(&empty[s]))
+                        : "memory");
+                    if (++s == kT6Stages) { s = 0; ph ^= 1; }
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 sm_u32(&acc_full[b]))
+                             : "memory");
+                ++it;
+            }
+        }
+        __syncwarp();
+    } else if (warp >= kT6Epi) {
+        // epilogue: this warp's TMEM lane quarter lq = 32 output columns; of the 15
+        // chunks of 16 accumulator columns (240 output rows) it takes every other
+        // one, two loads in flight; a ballot per row
+        const int lq = warp & 3, half = (warp - kT6Epi) >> 2;
+        uint32_t it = 0;
+        for (uint32_t t = blockIdx.x; t < NT; t += gridDim.x) {
+            TcGemmArgs P;
+            size_t c0, i0;
+            if (!tile_of(t, P, c0, i0)) continue;
+            const int nvalid = int(min(size_t(kT6Rows), P.n - i0));
+            const uint32_t b = it & 1;
+            mbar_wait1(&acc_full[b], (it >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            uint64_t* __restrict__ C = P.C;
+            const size_t sc = P.sc;
+            const int acc = P.acc;
+            const size_t col = c0 + size_t(lq) * 32;
+            const uint32_t tq = tmem + (uint32_t(32 * lq) << 16) + b * uint32_t(kT6Rows);
+            auto emit = [&](const uint32_t (&v)[16], int cc) {
+                uint32_t mine = 0;
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const uint32_t par = __float_as_uint(__uint_as_float(v[q]) + 8388608.0f) & 1u;
+                    const uint32_t bits = __ballot_sync(0xffffffffu, par);
+                    if (lane == q) mine = bits;
+                }
+                const int row = 16 * cc + lane;
+                if (lane < 16 && row < nvalid) {
+                    uint32_t* dst = reinterpret_cast<uint32_t*>(C + (col / 64) * sc + i0 + row) + ((col / 32) & 1);
+                    if (acc) mine ^= *dst;
+                    *dst = mine;
+                }
+            };
+#pragma unroll 1
+            for (int cc = half; cc < kT6Rows / 16; cc += 4) {  // chunks cc and cc + 2
+                const bool two = cc + 2 < kT6Rows / 16;
+                uint32_t v[16], w[16];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+                    "%11, %12, %13, %14, %15}, [%16];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                      "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+                      "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                    : "r"(tq + uint32_t(16 * cc)));
+                if (two)
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+                        "%11, %12, %13, %14, %15}, [%16];"
+                        : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+                          "=r"(w[7]), "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]),
+                          "=r"(w[13]), "=r"(w[14]), "=r"(w[15])
+                        : "r"(tq + uint32_t(16 * (cc + 2))));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (MODE == 3) continue;
+                emit(v, cc);
+                if (two) emit(w, cc + 2);
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) mbar_arrive1(&acc_empty[b]);
+            ++it;
+        }
+    } else {
+        const bool active = tid < kT6RawWords;
+        const int region = tid < kT6Cols ? 0 : kT6ABytes;
+        const int r = tid < kT6Cols ? tid : tid - kT6Cols;
+        int s = 0, rs = 0;
+        uint32_t ph = 0, rph = 0;
+        size_t staged = 0;
+        for (uint32_t t = blockIdx.x; t < NT; t += gridDim.x) {
+            TcGemmArgs P;
+            size_t c0, i0;
+            if (!tile_of(t, P, c0, i0)) continue;
+            const int nvalid = int(min(size_t(kT6Rows), P.n - i0));
+            const size_t KB = (P.k + 63) / 64;
+            const bool live = active && (tid < kT6Cols || r < nvalid);
+            for (size_t kb = 0; kb < KB; kb += kT3Kps, ++staged) {
+                if (staged >= size_t(kT6Stages)) mbar_wait1(&empty[s], ph ^ 1);
+#pragma unroll
+                for (int j = 0; j < kT3Kps; ++j) {
+                    if (kb + j >= KB) break;
+                    mbar_wait1(&rfull[rs], rph);
+                    uint64_t x = 0;
+                    if (live) ld_shared_u64(x, raw + size_t(rs) * kT6RawBytes + size_t(tid) * 8);
+                    if (active) {
+                        unsigned char* tile = smem + size_t(s) * kT6Stage + (j >> 1) * kT6Slot + region;
+                        store_row_f4(tile, r, j & 1, x);
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive1(&rempty[rs]);
+                    if (++rs == kT6Raw) { rs = 0; rph ^= 1; }
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive1(&full[s]);
+                if (++s == kT6Stages) { s = 0; ph ^= 1; }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
+}
+
 bool gemm_tc_ok(size_t n, size_t k, size_t m) {
     return n > 0 && k > 0 && m > 0 && n % kTcN == 0 && m % kTcM == 0 && k % 64 == 0;
 }
@@ -1181,6 +1449,33 @@ Tc5Fn tc5_fn() {
     }
     return fn;
 }
+using Tc6Fn = void (*)(TcGemmArgs, const TcGemmArgs*, uint32_t, uint32_t, uint32_t);
+// F2GPU_TC6_MAXK: short-k products on the double-buffered leaf (default 0 = off).
+// Measured: its epilogue overlaps (3.4 us per 128-column tile at k = 64 vs 5.3 us
+// per 256-column-equivalent for k_gemm_tc3), but its main loop is ~2x slower per
+// MAC, so at k = 1024 it only ties and at k >= 2048 it loses; the decomposition
+// showed no gain (64.08 vs 64.13 ms at k <= 1024).
+size_t tc6_max_k() {
+    static const size_t v = [] {
+        const char* e = getenv("F2GPU_TC6_MAXK");
+        return e ? size_t(atoll(e)) : size_t(0);
+    }();
+    return v;
+}
+Tc6Fn tc6_fn() {
+    static Tc6Fn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        if (tc6_max_k() == 0) return nullptr;
+        for (auto f : {k_gemm_tc6<0>, k_gemm_tc6<2>})
+            if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kT6Smem)) != cudaSuccess)
+                return nullptr;
+        const char* env = getenv("F2GPU_TC_MODE");
+        fn = (env && atoi(env) == 2) ? k_gemm_tc6<2> : k_gemm_tc6<0>;
+    }
+    return fn;
+}
 size_t tc5_max_k() {  // F2GPU_TC5_MAXK (default 2048)
     static const size_t v = [] {
         const char* e = getenv("F2GPU_TC5_MAXK");
@@ -1246,6 +1541,11 @@ cudaError_t launch_gemm_tc3(const uint64_t* A, size_t sa, size_t n, const uint64
         k_gemm_tc4<<<grid4, kT4Threads, kT4Smem, s>>>(p, nullptr);
         return cudaGetLastError();
     }
+    if (Tc6Fn f6 = tc6_fn(); f6 && k <= tc6_max_k()) {
+        const uint32_t GX6 = uint32_t(m / kT6Cols), GY6 = uint32_t((n + kT6Rows - 1) / kT6Rows), NT = GX6 * GY6;
+        f6<<<std::min<uint32_t>(NT, uint32_t(sm_count())), kT6Threads, kT6Smem, s>>>(p, nullptr, GX6, GY6, NT);
+        return cudaGetLastError();
+    }
     const uint32_t GX = uint32_t(m / kT3Cols), GY = uint32_t((n + kT3Rows - 1) / kT3Rows);
     // the persistent kernel hides the per-tile setup and load latency (~1.3 us of
     // ~7) but its main loop measured ~9% slower at large k: short-k products only
@@ -1280,6 +1580,13 @@ cudaError_t launch_gemm_tc3_batched(const TcGemmArgs* h_probs, const TcGemmArgs*
     const uint32_t GX = uint32_t(mx / kT3Cols), GY = uint32_t((nx + kT3Rows - 1) / kT3Rows);
     size_t kmax = 0;
     for (int i = 0; i < nprob; ++i) kmax = std::max(kmax, h_probs[i].k);
+    if (Tc6Fn f6 = tc6_fn(); f6 && kmax <= tc6_max_k()) {
+        const uint32_t GX6 = uint32_t(mx / kT6Cols), GY6 = uint32_t((nx + kT6Rows - 1) / kT6Rows);
+        const uint32_t NT = GX6 * GY6 * uint32_t(nprob);
+        f6<<<std::min<uint32_t>(NT, uint32_t(sm_count())), kT6Threads, kT6Smem, s>>>(TcGemmArgs{}, d_probs, GX6,
+                                                                                       GY6, NT);
+        return cudaGetLastError();
+    }
     if (Tc5Fn f5 = tc5_fn(); f5 && kmax <= tc5_max_k()) {
         const uint32_t NT = GX * GY * uint32_t(nprob);
         f5<<<std::min<uint32_t>(NT, uint32_t(sm_count())), kT3Threads, kT3Smem, s>>>(TcGemmArgs{}, d_probs, GX, GY,

@@ -534,6 +534,29 @@ def test_gemm_tc_persistent_kernel(f2, po):
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
+def test_gemm_tc_double_buffered_kernel(f2, po):
+    """The double-buffered short-k fp4 leaf k_gemm_tc6 (opt-in via F2GPU_TC6_MAXK) in a
+    fresh process, on every product and on the batched Strassen-Winograd leaves."""
+    import os
+    import subprocess
+    import sys
+    code = ("import numpy as np, paper_1209_5198_b200 as f2; from oracle import pyoracle as po; "
+            "ctx=f2.Context(0); lib=f2._lib.load()\n"
+            "for (n,k,m) in [(7,100,512),(2048,4096,1536),(3000,5000,1024),(481,64,512),(4800,1024,9728),(240,64,256)]:\n"
+            "    a=po.random_dense(n,k,0.5,n+k); b=po.random_dense(k,m,0.5,k+m)\n"
+            "    A=f2.DeviceMatrix.from_host(f2.BitMatrix(n,k,a),ctx); B=f2.DeviceMatrix.from_host(f2.BitMatrix(k,m,b),ctx)\n"
+            "    Cm=f2.DeviceMatrix(n,m,ctx); f2._lib.check(lib.f2gpu_gemm_tc(ctx.handle,A.handle,B.handle,Cm.handle,0))\n"
+            "    assert np.array_equal(Cm.download().words[:, :n], po.m4rm_mult(a,n,k,b,m)[:, :n]), (n,k,m)\n"
+            "n=1024; a=po.random_dense(n,n,0.5,5); b=po.random_dense(n,n,0.5,6); ctx.set_tc(True, 256)\n"
+            "got=f2.strassen_mult(f2.BitMatrix(n,n,a), f2.BitMatrix(n,n,b), ctx=ctx)\n"
+            "assert np.array_equal(got.words[:, :n], po.m4rm_mult(a,n,n,b,n)[:, :n])\n"
+            "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, F2GPU_TC6_MAXK="100000", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
 @pytest.mark.parametrize("G", [2, 3, 8])
 def test_strassen_mult_dist_shards(f2, ctx, po, G):
     """The column-sharded multiply at world 1 (broadcast = no-op), G shards emulated
