@@ -848,6 +848,8 @@ struct RecRun {
     size_t cut;    // Strassen cutover inside the recursion (XOR traffic vs multiply)
     size_t tbase;  // TRSM base (panels solved in one k_trsm_block launch)
     size_t tall_rows = 0, tall_base = 0;  // leaves with >= tall_rows rows: at most tall_base panels
+    size_t final_base = 32;               // right-spine leaves when downloads overlap (F2GPU_REC_FINAL;
+                                          // e2e at 65536^2: 32: 68.1-68.5 ms, 64: 68.6, off: 69.8)
     // F2GPU_REC_TIMES=1: CUDA events around every leaf / TRSM / product on the main
     // stream, summed per phase and printed (diagnostics; the side stream is untouched)
     struct Phase { std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev; };
@@ -992,7 +994,10 @@ int rec_decompose(RecRun& r, size_t c0, size_t c1) {
     // tall leaves are update-bound (the trailing update streams rows x remaining
     // leaf columns per panel), so they are narrower than short, chain-bound ones
     const size_t rows0 = r.n - std::min(r.n, 64 * c0);  // rows below the leaf's first panel at full rank
-    const size_t leaf = (r.tall_rows && rows0 >= r.tall_rows) ? std::min(r.base, r.tall_base) : r.base;
+    size_t leaf = (r.tall_rows && rows0 >= r.tall_rows) ? std::min(r.base, r.tall_base) : r.base;
+    // with a download hook (the host entry), leaves on the right spine are narrow so
+    // the final row blocks go back to the host while the last panels are factored
+    if (r.on_final && c1 == r.mu && r.final_base) leaf = std::min(leaf, r.final_base);
     if (c1 - c0 <= leaf) return timed(r, "leaf", [&] { return rec_leaf(r, c0, c1); });
     const size_t cm = c0 + (c1 - c0) / 2;
     F2_TRY(rec_decompose(r, c0, cm));
@@ -1048,6 +1053,7 @@ int decompose_recursive(f2gpu_ctx* c, View w, size_t min_cols, uint32_t* perm, u
     r.tall_base = 128;
     if (!r.c->use_tc_cut_default) r.tc_cut = r.c->tc_cutover;  // set explicitly (F2GPU_TC_CUT / ctx_set_tc)
     if (const char* e = getenv("F2GPU_REC_TC_CUT")) r.tc_cut = size_t(atol(e));
+    if (const char* e = getenv("F2GPU_REC_FINAL")) r.final_base = size_t(atol(e));
     if (const char* e = getenv("F2GPU_REC_TALL_BASE")) r.tall_base = std::max<size_t>(1, size_t(atol(e)));
     r.on_final = std::move(on_final);
     if (pend && frontier < mu) {
@@ -1876,7 +1882,15 @@ int f2gpu_decompose_recursive_host(f2gpu_ctx* c, const uint64_t* a, size_t n, si
     // stream on the copy stream, chunk by chunk, into `pend` in the host's row
     // order, and the recursion materialises each chunk under the row permutation
     // of the panels factored so far when it first needs it (ensure_cols).
-    const size_t cw = std::max<size_t>(1, (min_cols ? min_cols : 256 * 64) / 64);
+    // first chunk = the recursion's first leaf (tall leaves are narrower)
+    size_t cw = std::max<size_t>(1, (min_cols ? min_cols : 256 * 64) / 64);
+    {
+        size_t tall = 20000, tall_base = 128;
+        if (const char* e = getenv("F2GPU_REC_TALL")) tall = size_t(atol(e));
+        if (const char* e = getenv("F2GPU_REC_TALL_BASE")) tall_base = std::max<size_t>(1, size_t(atol(e)));
+        if (const char* e = getenv("F2GPU_REC_BASE")) cw = std::max<size_t>(1, size_t(atol(e)));
+        if (tall && n >= tall) cw = std::min(cw, tall_base);
+    }
     if (n == 0 || mu <= cw || !a || getenv("F2GPU_NO_UPLOAD_OVERLAP")) {
         F2_TRY(f2gpu_mat_upload(c, W, a, stride));
         F2_TRY(f2gpu_decompose_recursive(c, W, min_cols, perm, rj, rank));
