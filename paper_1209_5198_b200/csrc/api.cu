@@ -190,6 +190,7 @@ struct f2gpu_ctx {
     bool u_first_col = true;    // F2GPU_U_FIRSTCOL=0: release after column group 0 instead
     bool panel_head = false;    // F2GPU_PANEL_HEAD=1: the panel kernel does the first rows itself (measured slower)
     bool post_spin = true;      // F2GPU_POST_SPIN=0: k_post_col(j) waits for P(j) by event, not by counter
+    bool panel_hand = true;     // F2GPU_PANEL_HAND=0: P(j+1) starts on k_post_col(j)'s head, not P(j)'s hand-off
     cudaEvent_t ev_panel2 = nullptr;
     cudaStream_t side = nullptr;          // lookahead: panel kernels run here
     cudaStream_t side2 = nullptr;         // fused schedule: alternate panels (the next one is resident early)
@@ -202,6 +203,7 @@ struct f2gpu_ctx {
     size_t trace_cap = 0;
     uint32_t* scr_flags = nullptr;        // per-panel counters (kFlagsPerPanel each)
     size_t scr_flags_cap = 0;
+    uint64_t* scr_hand = nullptr;         // per-panel hand-off blocks (f2::kHandWords each)
     void* scr_st = nullptr;   // persistent PanelState[mu]
     size_t scr_st_cap = 0;
     uint32_t* scr_perm = nullptr;
@@ -650,7 +652,11 @@ int ensure_scratch(f2gpu_ctx* c, size_t n, size_t mu) {
             c->scr_perm_cap = n;
         }
         if (c->scr_flags_cap < mu) {
+            cudaFree(c->scr_hand);
+            c->scr_hand = nullptr;
+            CUDA_TRY(cudaMalloc(&c->scr_hand, mu * 8 * f2::kHandWords));
             cudaFree(c->scr_flags);
+    cudaFree(c->scr_hand);
     if (c->trace_buf) { f2::trace_set(nullptr, 0); cudaFree(c->trace_buf); }
             c->scr_flags = nullptr;
             CUDA_TRY(cudaMalloc(&c->scr_flags, mu * 4 * kFlagsPerPanel));
@@ -711,11 +717,19 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
         // k_post_col(j) queued ahead on the main stream waits on P(j)'s done counter
         // (needs P(j+1) queued early on the alternating side streams)
         const bool spin = c->post_spin && c->panel_early;
+        // hand-off: P(j+1) starts on P(j)'s done counter with P(j)'s hand-off block
+        // (not on k_post_col(j)'s first rows); needs P(j+1) queued early
+        const bool hand = c->panel_hand && c->panel_early && !c->panel_head;
         auto link_for = [&](size_t j) {  // P(j)'s link
             f2::PanelLink l{};
             if (j > c0) {
                 uint32_t* f = c->scr_flags + (j - 1) * kFlagsPerPanel;
                 l.head = f; l.head_count = 1;  // P(j-1)'s head chunk (or k_post_col's block 0)
+                if (hand) {
+                    l.head = f + 4;  // P(j-1) done
+                    l.hand_in = c->scr_hand + (j - 1) * f2::kHandWords;
+                    l.prev = s.st + (j - 1);
+                }
                 l.win = f + 1; l.win_count = c->panel_head ? 8 - f2::kPanelHeadRows / 256 : 8;
                 l.all = f + 2; l.all_count = uint32_t(f2::post_col_yblocks(n));
                 if (j + 1 < c1) { l.next_ready = f + 3; l.next_count = uint32_t(grid); }
@@ -726,7 +740,8 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
             }
             l.poll_ns = c->poll_ns;
             l.trace = c->trace_buf != nullptr;
-            if (spin) l.done_out = c->scr_flags + j * kFlagsPerPanel + 4;
+            if (spin || hand) l.done_out = c->scr_flags + j * kFlagsPerPanel + 4;
+            if (hand && j + 1 < c1) l.hand_out = c->scr_hand + j * f2::kHandWords;
             return l;
         };
         F2_TRY(check_launch(c, f2::launch_panel_link(s.w.p + c0 * s.w.stride, n, s.st, int(c0), link_for(c0),
@@ -1279,6 +1294,7 @@ int f2gpu_ctx_create(int device, f2gpu_ctx** out) {
     if (const char* uf = getenv("F2GPU_U_FIRSTCOL")) c->u_first_col = uf[0] != '0';
     if (const char* ph = getenv("F2GPU_PANEL_HEAD")) c->panel_head = ph[0] != '0';
     if (const char* ps = getenv("F2GPU_POST_SPIN")) c->post_spin = ps[0] != '0';
+    if (const char* ph2 = getenv("F2GPU_PANEL_HAND")) c->panel_hand = ph2[0] != '0';
     if (const char* tc = getenv("F2GPU_TC")) c->use_tc = tc[0] != '0';
     if (const char* tcc = getenv("F2GPU_TC_CUT")) {
         c->tc_cutover = size_t(atoll(tcc));

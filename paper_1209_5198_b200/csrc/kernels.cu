@@ -1687,6 +1687,8 @@ struct PanelGjSmem {
     uint32_t ext_orig[64];
     uint4 log[66];      // per selection t: column-k mask over positions (3 words), meta
     uint2 logu[66];     // slow selections: dead positions u with x[k_u] (the reduction set)
+    uint64_t rows0[kGjPos];  // hand-in: this panel's first kGjPos rows after the previous panel's update
+    uint64_t dh[kGjPos];     // hand-in: the previous panel's D rows
     uint32_t pd[128];   // composite pair list (dst, src), also kept here for the next-column swaps
     uint32_t ps[128];
     uint32_t fin;       // warps 0-2 finished (done_out)
@@ -1781,6 +1783,40 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
         return;
     }
     uint64_t* A = col + R;
+    if (link.hand_in && warp < 3) {
+        // the previous panel's update of this panel's first kGjPos rows, from its
+        // hand-off block: Y = D*Z, rows ^= Y*B (4-bit tables), warps 0-2
+        const int t3 = tid;
+        for (int i2 = t3; i2 < kHandWords; i2 += 96) {
+            const uint64_t v = link.hand_in[i2];
+            if (i2 < 64) S.bs[i2] = v;
+            else if (i2 < 64 + int(kGjPos)) S.rows0[i2 - 64] = v;
+            else S.dh[i2 - 64 - kGjPos] = v;
+        }
+        if (t3 < 64) S.z[t3] = link.prev->Z[t3];
+        asm volatile("bar.sync 5, 96;" ::: "memory");
+        for (int e = t3; e < 256; e += 96) {
+            const int g = e >> 4, v = e & 15;
+            uint64_t za = 0, zb = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if ((v >> q) & 1) { za ^= S.z[4 * g + q]; zb ^= S.bs[4 * g + q]; }
+            S.zt[e] = za;
+            S.bt[e] = zb;
+        }
+        asm volatile("bar.sync 5, 96;" ::: "memory");
+        if (t3 < int(kGjPos)) {
+            const uint64_t d = S.dh[t3];
+            uint64_t y = 0;
+#pragma unroll
+            for (int g = 0; g < 16; ++g) y ^= S.zt[16 * g + int((d >> (4 * g)) & 15)];
+            uint64_t x = S.rows0[t3];
+#pragma unroll
+            for (int g = 0; g < 16; ++g) x ^= S.bt[16 * g + int((y >> (4 * g)) & 15)];
+            S.rows0[t3] = x;
+        }
+        asm volatile("bar.sync 5, 96;" ::: "memory");
+    }
     const uint32_t winrows = rows < size_t(kPanelWin) ? uint32_t(rows) : uint32_t(kPanelWin);
     const uint32_t npos = winrows < kGjPos ? winrows : kGjPos;
 #ifdef GJ_PROFILE
@@ -1967,6 +2003,28 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
 #ifdef GJ_PROFILE
         if (lane == 0) reinterpret_cast<long long*>(st->src)[56] = clock64() - t_start;
 #endif
+        if (link.hand_out) {
+            // hand-off for the next panel kernel: the next column's pivot rows and its
+            // next kGjPos rows (swapped, before this panel's update) and this
+            // column's kGjPos rows below the pivots
+            __syncwarp();
+            __threadfence_block();
+            const uint32_t r = t;
+            const uint64_t* nx = link.next + R;
+            for (int i2 = lane; i2 < kHandWords; i2 += 32) {
+                uint64_t v = 0;
+                if (i2 < 64) {
+                    if (uint32_t(i2) < r) v = nx[i2];
+                } else if (i2 < 64 + int(kGjPos)) {
+                    const size_t p = size_t(r) + (i2 - 64);
+                    if (p < rows) v = nx[p];
+                } else {
+                    const size_t p = size_t(r) + (i2 - 64 - kGjPos);
+                    if (p < rows) v = S.win[p];
+                }
+                link.hand_out[i2] = v;
+            }
+        }
         if (link.head_out) {
             __threadfence_block();
             head_chunk(t);
@@ -2063,9 +2121,10 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
     // ---- warp 0: the selection chain ----
     uint32_t c0[kGjWords], c1[kGjWords], live[kGjWords];
     {
-        uint64_t x0 = uint32_t(lane) < npos ? A[lane] : 0;
-        uint64_t x1 = uint32_t(lane) + 32 < npos ? A[lane + 32] : 0;
-        uint64_t z0 = uint32_t(lane) + 64 < npos ? A[lane + 64] : 0;
+        const uint64_t* src0 = link.hand_in ? S.rows0 : A;
+        uint64_t x0 = uint32_t(lane) < npos ? src0[lane] : 0;
+        uint64_t x1 = uint32_t(lane) + 32 < npos ? src0[lane + 32] : 0;
+        uint64_t z0 = uint32_t(lane) + 64 < npos ? src0[lane + 64] : 0;
         uint64_t z1 = 0;
         warp_transpose64(x0, x1, lane);
         warp_transpose64(z0, z1, lane);

@@ -126,7 +126,18 @@ struct PanelLink {
     // list, swapped window, next-column swaps) is in memory; a fused post queued
     // ahead of time waits on it instead of a cross-stream event
     uint32_t* done_out = nullptr;
+    // hand-off (fused schedule): hand_out != nullptr -> at its end this panel kernel
+    // writes kHandWords words: the next column's pivot rows (64), the next column's
+    // next kGjPos rows, and its own column's kGjPos rows below the pivots (D), all
+    // swapped, before incrementing done_out.  hand_in != nullptr -> this kernel
+    // starts on the previous panel's done counter (link.head) and applies the
+    // previous panel's update to its first kGjPos rows itself (Y = D*Z, x ^= Y*B)
+    // instead of waiting for the fused post's first rows.
+    uint64_t* hand_out = nullptr;
+    const uint64_t* hand_in = nullptr;
+    const PanelState* prev = nullptr;  // the previous panel's state (Z, r) for hand_in
 };
+constexpr int kHandWords = 256;
 constexpr int kPanelHeadRows = 256;
 cudaError_t launch_panel_link(uint64_t* col, size_t n, PanelState* st_all, int j, const PanelLink& link,
                               cudaStream_t s);

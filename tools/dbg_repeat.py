@@ -18,7 +18,11 @@ for rep in range(reps):
         for p in (0.5, 0.1, 0.01):
             a = po.random_dense(n, m, p, n * 31 + m)
             w, perm, rj, rank = po.decompose_block(a, n, m)
-            got = f2.decompose_block(f2.BitMatrix(n, m, a), ctx=ctx)
+            try:
+                got = f2.decompose_block(f2.BitMatrix(n, m, a), ctx=ctx)
+            except Exception as e:  # noqa: BLE001
+                print("ERROR rep", rep, n, m, p, e, flush=True)
+                raise
             ok = (got.rank == rank and np.array_equal(got.block_ranks, rj) and np.array_equal(got.P.perm, perm)
                   and np.array_equal(got.overlay.words[:, :n], w[:, :n]))
             if not ok:
