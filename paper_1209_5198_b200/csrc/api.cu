@@ -190,7 +190,10 @@ struct f2gpu_ctx {
     bool u_first_col = true;    // F2GPU_U_FIRSTCOL=0: release after column group 0 instead
     bool panel_head = false;    // F2GPU_PANEL_HEAD=1: the panel kernel does the first rows itself (measured slower)
     bool post_spin = true;      // F2GPU_POST_SPIN=0: k_post_col(j) waits for P(j) by event, not by counter
-    bool panel_hand = true;     // F2GPU_PANEL_HAND=0: P(j+1) starts on k_post_col(j)'s head, not P(j)'s hand-off
+    // F2GPU_PANEL_HAND=1: P(j+1) starts on P(j)'s done counter with P(j)'s hand-off block.
+    // Off: measured no faster at 65536^2 (64.12 vs 64.17 ms); kept opt-in
+    // (tests/test_gpu_parity.py::test_panel_hand_off)
+    bool panel_hand = false;
     cudaEvent_t ev_panel2 = nullptr;
     cudaStream_t side = nullptr;          // lookahead: panel kernels run here
     cudaStream_t side2 = nullptr;         // fused schedule: alternate panels (the next one is resident early)
@@ -656,8 +659,6 @@ int ensure_scratch(f2gpu_ctx* c, size_t n, size_t mu) {
             c->scr_hand = nullptr;
             CUDA_TRY(cudaMalloc(&c->scr_hand, mu * 8 * f2::kHandWords));
             cudaFree(c->scr_flags);
-    cudaFree(c->scr_hand);
-    if (c->trace_buf) { f2::trace_set(nullptr, 0); cudaFree(c->trace_buf); }
             c->scr_flags = nullptr;
             CUDA_TRY(cudaMalloc(&c->scr_flags, mu * 4 * kFlagsPerPanel));
             c->scr_flags_cap = mu;
@@ -1328,13 +1329,15 @@ int f2gpu_ctx_destroy(f2gpu_ctx* c) {
     if (c->own_stream) cudaStreamSynchronize(c->own_stream);
     c->graph.reset();
     c->leaf_graphs.clear();
+    if (c->side) { cudaStreamSynchronize(c->side); cudaStreamDestroy(c->side); }
+    if (c->side2) { cudaStreamSynchronize(c->side2); cudaStreamDestroy(c->side2); }
+    if (c->copy) { cudaStreamSynchronize(c->copy); cudaStreamDestroy(c->copy); }
     if (c->stage) { f2gpu_mat_free(c->stage); c->stage = nullptr; }
     cudaFree(c->scr_st);
     cudaFree(c->scr_perm);
     cudaFree(c->scr_flags);
-    if (c->side) { cudaStreamSynchronize(c->side); cudaStreamDestroy(c->side); }
-    if (c->side2) { cudaStreamSynchronize(c->side2); cudaStreamDestroy(c->side2); }
-    if (c->copy) { cudaStreamSynchronize(c->copy); cudaStreamDestroy(c->copy); }
+    cudaFree(c->scr_hand);
+    if (c->trace_buf) { f2::trace_set(nullptr, 0); cudaFree(c->trace_buf); }
     for (cudaEvent_t e : c->chunk_ev) cudaEventDestroy(e);
     cudaFree(c->pend);
     if (c->ev_post) cudaEventDestroy(c->ev_post);

@@ -557,6 +557,49 @@ def test_gemm_tc_double_buffered_kernel(f2, po):
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
+def _fresh_process(code, **env_extra):
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PYTHONPATH=root, **env_extra)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_scratch_growth_one_context():
+    """Growing shapes in ONE fresh context: every growth reallocates the panel
+    scratch (states, perm, counters, hand-off words) and drops the captured graphs;
+    the first decomposition after each growth must still match the oracle."""
+    _fresh_process(
+        "import numpy as np, paper_1209_5198_b200 as f2; from oracle import pyoracle as po\n"
+        "ctx=f2.Context(0)\n"
+        "for n in (300, 1024, 1024, 2048, 4096):\n"
+        "  for fn in (f2.decompose_block, f2.decompose_recursive):\n"
+        "    a=po.random_dense(n,n,0.5,n); w,perm,rj,rank=po.decompose_block(a,n,n)\n"
+        "    got=fn(f2.BitMatrix(n,n,a), ctx=ctx)\n"
+        "    assert got.rank==rank and np.array_equal(got.P.perm, perm), (n, fn)\n"
+        "    assert np.array_equal(got.overlay.words[:, :n], w[:, :n]), (n, fn)\n"
+        "print('ok')\n")
+
+
+def test_panel_hand_off():
+    """The opt-in panel hand-off (F2GPU_PANEL_HAND=1: P(j+1) starts on P(j)'s done
+    counter and applies panel j to its own first rows) on ragged and rank-deficient
+    shapes, block and recursive."""
+    _fresh_process(
+        "import numpy as np, paper_1209_5198_b200 as f2; from oracle import pyoracle as po\n"
+        "ctx=f2.Context(0)\n"
+        "for (n,m,d,seed) in [(300,257,0.5,1),(1000,257,0.5,2),(513,257,0.5,3),(2000,700,0.5,4),"
+        "(700,2000,0.5,5),(3000,3000,0.02,6),(4096,4096,0.5,7)]:\n"
+        "  a=po.random_dense(n,m,d,seed); w,perm,rj,rank=po.decompose_block(a,n,m)\n"
+        "  for fn in (f2.decompose_block, f2.decompose_recursive):\n"
+        "    got=fn(f2.BitMatrix(n,m,a), ctx=ctx)\n"
+        "    assert got.rank==rank and np.array_equal(got.P.perm, perm), (n, m, fn)\n"
+        "    assert np.array_equal(got.overlay.words[:, :n], w[:, :n]), (n, m, fn)\n"
+        "print('ok')\n", F2GPU_PANEL_HAND="1")
+
+
 @pytest.mark.parametrize("G", [2, 3, 8])
 def test_strassen_mult_dist_shards(f2, ctx, po, G):
     """The column-sharded multiply at world 1 (broadcast = no-op), G shards emulated
