@@ -864,6 +864,10 @@ struct RecRun {
     size_t cut;    // Strassen cutover inside the recursion (XOR traffic vs multiply)
     size_t tbase;  // TRSM base (panels solved in one k_trsm_block launch)
     size_t tall_rows = 0, tall_base = 0;  // leaves with >= tall_rows rows: at most tall_base panels
+    // TRSM products with k <= this go to M4RM: at k = 1024 it beats the fp4 leaf's
+    // per-tile fixed cost (n = k = 1024, m = 8192 / 32768 / 57344: 23 / 54 / 72 us vs
+    // 26 / 60 / 95 us; ties at k = 2048, loses at 4096 -- tools/trsm_prod_scan.py)
+    size_t trsm_m4rm_k = 1024;            // F2GPU_TRSM_M4RM_K
     size_t final_base = 32;               // right-spine leaves when downloads overlap (F2GPU_REC_FINAL;
                                           // e2e at 65536^2: 32: 68.1-68.5 ms, 64: 68.6, off: 69.8)
     // F2GPU_REC_TIMES=1: CUDA events around every leaf / TRSM / product on the main
@@ -949,8 +953,10 @@ int rec_trsm(RecRun& r, size_t a, size_t b, size_t Ra, size_t col0, size_t col1)
     const size_t m = a + (b - a) / 2, Rm = Ra + 64 * (m - a);
     F2_TRY(rec_trsm(r, a, m, Ra, col0, col1));
     F2_TRY(timed(r, (m - a) * 64 >= 8192 ? "trsm.prod.big" : "trsm.prod.small", [&] {
-        return best_product(r.c, wview(*r.s, Rm, Rb - Rm, col0, col1 - col0), wview(*r.s, Rm, Rb - Rm, a, m - a),
-                            wview(*r.s, Ra, Rm - Ra, col0, col1 - col0), r.cut, r.tc_cut);
+        const View C = wview(*r.s, Rm, Rb - Rm, col0, col1 - col0), A = wview(*r.s, Rm, Rb - Rm, a, m - a),
+                   B = wview(*r.s, Ra, Rm - Ra, col0, col1 - col0);
+        if ((m - a) * 64 <= r.trsm_m4rm_k) return strassen_acc(r.c, C, A, B, r.cut);
+        return best_product(r.c, C, A, B, r.cut, r.tc_cut);
     }));
     return rec_trsm(r, m, b, Rm, col0, col1);
 }
@@ -1070,6 +1076,7 @@ int decompose_recursive(f2gpu_ctx* c, View w, size_t min_cols, uint32_t* perm, u
     if (!r.c->use_tc_cut_default) r.tc_cut = r.c->tc_cutover;  // set explicitly (F2GPU_TC_CUT / ctx_set_tc)
     if (const char* e = getenv("F2GPU_REC_TC_CUT")) r.tc_cut = size_t(atol(e));
     if (const char* e = getenv("F2GPU_REC_FINAL")) r.final_base = size_t(atol(e));
+    if (const char* e = getenv("F2GPU_TRSM_M4RM_K")) r.trsm_m4rm_k = size_t(atol(e));
     if (const char* e = getenv("F2GPU_REC_TALL_BASE")) r.tall_base = std::max<size_t>(1, size_t(atol(e)));
     r.on_final = std::move(on_final);
     if (pend && frontier < mu) {
