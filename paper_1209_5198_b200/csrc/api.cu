@@ -190,6 +190,7 @@ struct f2gpu_ctx {
     bool u_first_col = true;    // F2GPU_U_FIRSTCOL=0: release after column group 0 instead
     bool panel_head = false;    // F2GPU_PANEL_HEAD=1: the panel kernel does the first rows itself (measured slower)
     bool post_spin = true;      // F2GPU_POST_SPIN=0: k_post_col(j) waits for P(j) by event, not by counter
+    bool pdl = true;            // F2GPU_PDL=0: the update after k_post_col is a plain stream-ordered launch
     // F2GPU_PANEL_HAND=1: P(j+1) starts on P(j)'s done counter with P(j)'s hand-off block.
     // Off: measured no faster at 65536^2 (64.12 vs 64.17 ms); kept opt-in
     // (tests/test_gpu_parity.py::test_panel_hand_off)
@@ -684,7 +685,7 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
     // fused schedule: two panel kernels can be resident (the running one and the
     // next one waiting for its head), each on its own SM
     const int grid = !la ? c->num_sms : (fused && c->num_sms > 2 ? c->num_sms - 2 : c->num_sms - 1);
-    auto upd = [&](size_t j, uint32_t* release, size_t skip = 0) {
+    auto upd = [&](size_t j, uint32_t* release, size_t skip = 0, bool pdl = false) {
         f2::UpdateArgs u{};
         u.C = s.w.p; u.sc = s.w.stride; u.c_wcol0 = j + 1 + skip; u.ncols = int(c1 - j - 1 - skip);
         if (u.ncols <= 0) return F2GPU_OK;
@@ -694,6 +695,7 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
         u.release = release;
         u.first_col = release != nullptr && c->u_first_col;
         u.tag = c->trace_buf ? int(j) : -1;
+        u.pdl = pdl;
         return check_launch(c, f2::launch_update(u, grid, c->stream), "k_update");
     };
     const bool colfirst = c->lookahead_col;
@@ -768,7 +770,7 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
                                 "k_post_col"));
             if (j + 1 >= c1) break;
             if (!c->panel_early) CUDA_TRY(cudaEventRecord(c->ev_post, c->stream));
-            F2_TRY(upd(j, f + 3, 1));
+            F2_TRY(upd(j, f + 3, 1, spin && c->pdl));
             // P(j+1) alternates between the two side streams: queued behind P(j-1),
             // it is resident while P(j) runs and starts on P(j)'s head counter
             cudaStream_t ps = c->panel_early ? sides[(j - c0) & 1] : c->side;
@@ -1302,6 +1304,7 @@ int f2gpu_ctx_create(int device, f2gpu_ctx** out) {
     if (const char* uf = getenv("F2GPU_U_FIRSTCOL")) c->u_first_col = uf[0] != '0';
     if (const char* ph = getenv("F2GPU_PANEL_HEAD")) c->panel_head = ph[0] != '0';
     if (const char* ps = getenv("F2GPU_POST_SPIN")) c->post_spin = ps[0] != '0';
+    if (const char* pd = getenv("F2GPU_PDL")) c->pdl = pd[0] != '0';
     if (const char* ph2 = getenv("F2GPU_PANEL_HAND")) c->panel_hand = ph2[0] != '0';
     if (const char* tc = getenv("F2GPU_TC")) c->use_tc = tc[0] != '0';
     if (const char* tcc = getenv("F2GPU_TC_CUT")) {

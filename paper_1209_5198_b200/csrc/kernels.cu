@@ -687,6 +687,9 @@ __device__ __forceinline__ void release_signal(uint32_t* flag, int tag = -1) {
 
 __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // programmatic dependent launch: no-op unless launched with p.pdl; every read
+    // of the panel state, A, B or C comes after it
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (p.tag >= 0 && blockIdx.x == 0 && threadIdx.x == 0) trace_ev(kTrUpdBegin, p.tag);
     const uint32_t smem_base = smem_u32(smem_raw);
     if (smem_base > kTabAddr - kV3RingBytes) __trap();  // layout assumption violated
@@ -933,6 +936,19 @@ cudaError_t launch_update(const UpdateArgs& a, int num_sms, cudaStream_t s) {
     if (a.ncols <= 0) return cudaSuccess;
     if (a.release && !update_v3_ok(a)) return cudaErrorInvalidValue;
     if (update_v3_ok(a)) {
+        if (a.pdl) {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(num_sms);
+            cfg.blockDim = dim3(kV3Threads);
+            cfg.dynamicSmemBytes = kV3Smem;
+            cfg.stream = s;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            return cudaLaunchKernelEx(&cfg, k_update_v3, a);
+        }
         k_update_v3<<<num_sms, kV3Threads, kV3Smem, s>>>(a);
         return cudaGetLastError();
     }
@@ -2538,6 +2554,9 @@ __global__ void __launch_bounds__(256) k_post_col(uint64_t* __restrict__ w, size
                                                   int skip, const uint32_t* wait_panel) {
     __shared__ uint64_t zs[64], bs[64];
     __shared__ uint64_t zt[256], bt[256];
+    // the update that follows (UpdateArgs::pdl) may start placing its CTAs now; it
+    // waits for this grid's completion before touching data
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (wait_panel) {  // queued ahead: the panel kernel's writes are complete
         if (threadIdx.x < 32) {
             while (true) {

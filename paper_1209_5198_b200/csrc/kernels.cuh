@@ -52,6 +52,10 @@ struct UpdateArgs {
     // release, then the remaining columns in 16-column groups
     bool first_col = false;
     int tag = -1;  // panel index for the device trace; >= 0 only while it is on
+    // launched as a programmatic dependent of the preceding kernel (k_post_col):
+    // the CTAs start as its blocks retire and wait (griddepcontrol.wait) before
+    // reading any data
+    bool pdl = false;
 };
 
 // Device trace (diagnostics): when enabled, the panel / fused-post / update

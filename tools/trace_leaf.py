@@ -43,8 +43,8 @@ t = (ev >> np.uint64(16)).astype(np.int64)
 code = ((ev >> np.uint64(12)) & np.uint64(15)).astype(int)
 j = (ev & np.uint64(4095)).astype(int)
 t0 = t.min()
-names = {1: "P.begin", 2: "P.chain_end", 3: "P.end", 4: "post.begin", 5: "post.head", 6: "post.end",
-         7: "U.begin", 8: "U.release", 9: "U.end", 10: "U0.tab0", 11: "U0.tile0", 12: "U0.end", 13: "U0.tab1", 14: "U0.state", 15: "U0.barriers"}
+names = {0: "P.w1end", 1: "P.begin", 2: "P.chain_end", 3: "P.end", 4: "post.begin", 5: "post.head", 6: "post.end",
+         7: "U.begin", 8: "U.release", 9: "U.end", 10: "U0.tab0", 11: "U0.tile0", 12: "U0.end", 13: "P.done", 14: "U0.state", 15: "U0.barriers"}
 mu = w // 64
 T = {k: np.full(mu, np.nan) for k in names}
 for ti, ci, ji in zip(t, code, j):
@@ -63,6 +63,10 @@ rows = [
     ("panel chain (begin->chain end)", T[2] - T[1]),
     ("panel tail (chain end->end)", T[3] - T[2]),
     ("P end -> post begin", T[4] - T[3]),
+    ("  P end -> P done (all warps)", T[13] - T[3]),
+    ("  P done -> post begin", T[4] - T[13]),
+    ("  P chain end -> warp 1 end", T[0] - T[2]),
+    ("  P end (warp 2) -> warp 1 end", T[0] - T[3]),
     ("post begin -> head", T[5] - T[4]),
     ("post head -> next P begin", nx(T[1]) - T[5]),
     ("post begin -> post end", T[6] - T[4]),
@@ -72,7 +76,6 @@ rows = [
     ("  U0 state -> barriers init", T[15] - T[14]),
     ("  U0 barriers -> first table", T[10] - T[15]),
     ("  U0 first table -> tile0 reduce", T[11] - T[10]),
-    ("  U0 begin -> second table", T[13] - T[7]),
     ("  U0 begin -> end (CTA 0)", T[12] - T[7]),
     ("  U0 end -> next post begin", nx(T[4]) - T[12]),
     ("next P chain end -> U release", nx(T[2]) - T[8]),
