@@ -188,6 +188,8 @@ struct f2gpu_ctx {
     bool panel_early = true;    // F2GPU_PANEL_EARLY=0: launch P(j+1) after k_post_col(j) completes
     uint32_t poll_ns = 0;       // F2GPU_POLL_NS: panel consumer warps' poll sleep
     bool u_first_col = true;    // F2GPU_U_FIRSTCOL=0: release after column group 0 instead
+    int u_fc_ctas = 16;         // F2GPU_U_FC_CTAS: CTAs doing that first column (0: all)
+    int u_fc_weight = 3;        // F2GPU_U_FC_W: their bulk share in quarters
     bool panel_head = false;    // F2GPU_PANEL_HEAD=1: the panel kernel does the first rows itself (measured slower)
     bool post_spin = true;      // F2GPU_POST_SPIN=0: k_post_col(j) waits for P(j) by event, not by counter
     bool pdl = true;            // F2GPU_PDL=0: the update after k_post_col is a plain stream-ordered launch
@@ -694,6 +696,8 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
         u.st = s.st + j;
         u.release = release;
         u.first_col = release != nullptr && c->u_first_col;
+        u.fc_ctas = c->u_fc_ctas;
+        u.fc_weight = c->u_fc_weight;
         u.tag = c->trace_buf ? int(j) : -1;
         u.pdl = pdl;
         return check_launch(c, f2::launch_update(u, grid, c->stream), "k_update");
@@ -1302,6 +1306,8 @@ int f2gpu_ctx_create(int device, f2gpu_ctx** out) {
     if (const char* pe = getenv("F2GPU_PANEL_EARLY")) c->panel_early = pe[0] != '0';
     if (const char* pn = getenv("F2GPU_POLL_NS")) c->poll_ns = uint32_t(atoi(pn));
     if (const char* uf = getenv("F2GPU_U_FIRSTCOL")) c->u_first_col = uf[0] != '0';
+    if (const char* e = getenv("F2GPU_U_FC_CTAS")) c->u_fc_ctas = atoi(e);
+    if (const char* e = getenv("F2GPU_U_FC_W")) c->u_fc_weight = std::max(1, std::min(4, atoi(e)));
     if (const char* ph = getenv("F2GPU_PANEL_HEAD")) c->panel_head = ph[0] != '0';
     if (const char* ps = getenv("F2GPU_POST_SPIN")) c->post_spin = ps[0] != '0';
     if (const char* pd = getenv("F2GPU_PDL")) c->pdl = pd[0] != '0';

@@ -716,11 +716,25 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
         if (p.release && threadIdx.x == 0) release_signal(p.release, p.tag);
         return;
     }
-    if (p.release && p.first_col) {
+    // first-column CTAs: [G - F, G) (F = 0: none, the split is uniform)
+    const size_t G_all = gridDim.x;
+    size_t fc_n = 0;
+    if (p.release && p.first_col)
+        fc_n = p.fc_ctas > 0 ? min(G_all, size_t(p.fc_ctas)) : G_all;
+    const bool fc_mine = fc_n != 0 && blockIdx.x >= G_all - fc_n;
+    if (fc_n != 0 && !fc_mine) {
+        // never writes the first column: its arrival is vacuous
+        if (threadIdx.x == 0) release_signal(p.release, p.tag);
+        p.release = nullptr;
+        ++p.c_wcol0;
+        ++p.b_wcol0;
+        if (--p.ncols <= 0) return;
+    }
+    if (fc_mine) {
         // the first column alone: one 256-entry 4-bit table over its 64 B rows,
-        // rows split evenly over the CTAs, plain loads/stores -- the release the
-        // next panel kernel waits for comes ~1-2 us after launch instead of after
-        // a whole 16-column group (table build + tile pipeline + bulk drain)
+        // rows split evenly over the first-column CTAs, plain loads/stores -- the
+        // release the next panel kernel waits for comes ~2-3 us after launch instead
+        // of after a whole 16-column group (table build + tile pipeline + bulk drain)
         uint64_t* t4 = tab;
         const uint64_t* Bc = p.B + p.b_wcol0 * p.sb + b_row0;
         if (threadIdx.x < 256) {
@@ -733,14 +747,24 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
         }
         __syncthreads();
         uint64_t* Cc = p.C + p.c_wcol0 * p.sc;
-        const size_t G = gridDim.x, nrows = row_hi - row_lo, per = (nrows + G - 1) / G;
-        const size_t r0 = row_lo + size_t(blockIdx.x) * per, r1 = min(row_hi, r0 + per);
-        for (size_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-            const uint64_t a = p.a[i];
-            uint64_t x = Cc[i];
+        const size_t nrows = row_hi - row_lo, per = (nrows + fc_n - 1) / fc_n;
+        const size_t r0 = row_lo + size_t(blockIdx.x - (G_all - fc_n)) * per, r1 = min(row_hi, r0 + per);
+        // 4 rows per thread in flight (a first-column CTA has ~4096 rows at 65536)
+        for (size_t i0 = r0 + threadIdx.x; i0 < r1; i0 += 4 * size_t(blockDim.x)) {
+            uint64_t a[4], x[4];
 #pragma unroll
-            for (int g = 0; g < 16; ++g) x ^= t4[16 * g + int((a >> (4 * g)) & 15)];
-            Cc[i] = x;
+            for (int u = 0; u < 4; ++u) {
+                const size_t i = i0 + size_t(u) * blockDim.x;
+                a[u] = i < r1 ? p.a[i] : 0;
+                x[u] = i < r1 ? Cc[i] : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const size_t i = i0 + size_t(u) * blockDim.x;
+#pragma unroll
+                for (int g = 0; g < 16; ++g) x[u] ^= t4[16 * g + int((a[u] >> (4 * g)) & 15)];
+                if (i < r1) Cc[i] = x[u];
+            }
         }
         __threadfence();
         __syncthreads();
@@ -763,6 +787,15 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
         const size_t TB = T * (ncg - 1);
         s1 = T + TB * b / G;
         len1 = T + TB * (b + 1) / G - s1;
+    } else if (fc_n != 0 && fc_n < G && p.fc_weight < 4) {
+        // weighted split: the first-column CTAs take fc_weight/4 of a share
+        const size_t TU = T * ncg, d = size_t(4 - p.fc_weight), gf = G - fc_n;
+        const size_t Wt = 4 * G - d * fc_n;
+        auto W = [&](size_t x) { return 4 * x - d * (x > gf ? x - gf : 0); };
+        s0 = TU * W(b) / Wt;
+        len0 = TU * W(b + 1) / Wt - s0;
+        s1 = s0 + len0;
+        len1 = 0;
     } else {
         const size_t TU = T * ncg;
         s0 = TU * b / G;

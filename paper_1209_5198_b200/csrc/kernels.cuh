@@ -51,6 +51,11 @@ struct UpdateArgs {
     // alone first, split by rows over every CTA with a 4-bit table, then the
     // release, then the remaining columns in 16-column groups
     bool first_col = false;
+    // first_col: only the last fc_ctas CTAs do the first column (the others signal
+    // the release at once and start their tiles); their share of the bulk tiles is
+    // fc_weight / 4 of a full one.  0: every CTA does a slice of it
+    int fc_ctas = 0;
+    int fc_weight = 3;
     int tag = -1;  // panel index for the device trace; >= 0 only while it is on
     // launched as a programmatic dependent of the preceding kernel (k_post_col):
     // the CTAs start as its blocks retire and wait (griddepcontrol.wait) before
