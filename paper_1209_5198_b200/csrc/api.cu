@@ -874,6 +874,7 @@ struct RecRun {
     // per-tile fixed cost (n = k = 1024, m = 8192 / 32768 / 57344: 23 / 54 / 72 us vs
     // 26 / 60 / 95 us; ties at k = 2048, loses at 4096 -- tools/trsm_prod_scan.py)
     size_t trsm_m4rm_k = 1024;            // F2GPU_TRSM_M4RM_K
+    size_t first_base = 0;                // left-spine leaves when uploads overlap (= the upload chunk)
     size_t final_base = 32;               // right-spine leaves when downloads overlap (F2GPU_REC_FINAL;
                                           // e2e at 65536^2: 32: 68.1-68.5 ms, 64: 68.6, off: 69.8)
     // F2GPU_REC_TIMES=1: CUDA events around every leaf / TRSM / product on the main
@@ -1026,6 +1027,9 @@ int rec_decompose(RecRun& r, size_t c0, size_t c1) {
     // with a download hook (the host entry), leaves on the right spine are narrow so
     // the final row blocks go back to the host while the last panels are factored
     if (r.on_final && c1 == r.mu && r.final_base) leaf = std::min(leaf, r.final_base);
+    // and on the left spine the first leaf is one upload chunk, so the factorisation
+    // starts after that chunk's copy instead of a whole tall leaf's
+    if (r.on_final && c0 == 0 && r.first_base) leaf = std::min(leaf, r.first_base);
     if (c1 - c0 <= leaf) return timed(r, "leaf", [&] { return rec_leaf(r, c0, c1); });
     const size_t cm = c0 + (c1 - c0) / 2;
     F2_TRY(rec_decompose(r, c0, cm));
@@ -1090,6 +1094,7 @@ int decompose_recursive(f2gpu_ctx* c, View w, size_t min_cols, uint32_t* perm, u
         r.pend = pend;
         r.ps = ps;
         r.chunk = chunk;
+        if (r.on_final) r.first_base = chunk;
     }
     CUDA_TRY(cudaMemsetAsync(c->scr_flags, 0, mu * 4 * kFlagsPerPanel, c->stream));
     c->tl.mark(c->stream, "start");
@@ -1925,6 +1930,11 @@ int f2gpu_decompose_recursive_host(f2gpu_ctx* c, const uint64_t* a, size_t n, si
         if (const char* e = getenv("F2GPU_REC_TALL_BASE")) tall_base = std::max<size_t>(1, size_t(atol(e)));
         if (const char* e = getenv("F2GPU_REC_BASE")) cw = std::max<size_t>(1, size_t(atol(e)));
         if (tall && n >= tall) cw = std::min(cw, tall_base);
+        // first leaf = upload chunk width (F2GPU_REC_FIRST; 65536^2 e2e: 128: 67.83 ms,
+        // 64: 67.36, 32: 67.40-67.45, 16: 67.62 at the same 63.2 ms device time)
+        size_t first = 64;
+        if (const char* e = getenv("F2GPU_REC_FIRST")) first = std::max<size_t>(1, size_t(atol(e)));
+        cw = std::min(cw, first);
     }
     if (n == 0 || mu <= cw || !a || getenv("F2GPU_NO_UPLOAD_OVERLAP")) {
         F2_TRY(f2gpu_mat_upload(c, W, a, stride));

@@ -147,6 +147,28 @@ def test_cfg4_decompose_recursive_65536(f2, ctx, po):
     check_against(po, g, None, A.download(), perm, rj, int(rk.value), n, n, freivalds=False)
 
 
+def test_cfg4_decompose_recursive_host_65536(f2, ctx, po):
+    """The host entry (chunked upload under the running permutation, narrow first
+    and last leaves, row blocks downloaded as they become final) at full size."""
+    from paper_1209_5198_b200 import _lib
+
+    g = digests()["cfg4"]
+    n = g["n"]
+    lib = _lib.load()
+    A = f2.DeviceMatrix(n, n, ctx)
+    A.random_dense(0.5, g["seed"])
+    a = np.ascontiguousarray(A.download().words)
+    del A
+    wout = np.zeros_like(a)
+    perm = np.zeros(n, np.uint32)
+    rj = np.zeros(n // 64, np.uint32)
+    rk = C.c_size_t()
+    _lib.check(lib.f2gpu_decompose_recursive_host(ctx.handle, a.ctypes.data, n, n, a.shape[1], 0,
+                                                  wout.ctypes.data, perm.ctypes.data, rj.ctypes.data,
+                                                  C.byref(rk)))
+    check_against(po, g, None, f2.BitMatrix(n, n, wout), perm, rj, int(rk.value), n, n, freivalds=False)
+
+
 def _run_recursive(f2, ctx, A, n, m):
     from paper_1209_5198_b200 import _lib
     lib = _lib.load()
