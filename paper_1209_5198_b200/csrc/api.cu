@@ -188,7 +188,8 @@ struct f2gpu_ctx {
     bool panel_early = true;    // F2GPU_PANEL_EARLY=0: launch P(j+1) after k_post_col(j) completes
     uint32_t poll_ns = 0;       // F2GPU_POLL_NS: panel consumer warps' poll sleep
     bool u_first_col = true;    // F2GPU_U_FIRSTCOL=0: release after column group 0 instead
-    int u_fc_ctas = 16;         // F2GPU_U_FC_CTAS: CTAs doing that first column (0: all)
+    int u_fc_ctas = 24;         // F2GPU_U_FC_CTAS: CTAs doing that first column (0: all; 65536^2:
+                                // 16: 63.18, 20: 63.21, 24: 63.00, 28: 63.30, 32: 63.28 ms)
     int u_fc_weight = 3;        // F2GPU_U_FC_W: their bulk share in quarters
     bool panel_head = false;    // F2GPU_PANEL_HEAD=1: the panel kernel does the first rows itself (measured slower)
     bool post_spin = true;      // F2GPU_POST_SPIN=0: k_post_col(j) waits for P(j) by event, not by counter
