@@ -1042,6 +1042,9 @@ int rec_decompose(RecRun& r, size_t c0, size_t c1) {
     F2_TRY(ensure_cols(r, c1));
     if (full) {
         F2_TRY(timed(r, "trsm", [&] { return rec_trsm(r, c0, cm, R0, cm, c1); }));
+        // rows [0, R1) are final once the TRSM is done (the product writes rows >= R1
+        // only), so their download overlaps the product too
+        if (c1 == r.mu && r.on_final) F2_TRY(r.on_final(R1));
         if (R1 < r.n)
             F2_TRY(timed(r, "product", [&] {
                 return best_product(r.c, wview(*r.s, R1, r.n - R1, cm, c1 - cm),
@@ -1050,8 +1053,8 @@ int rec_decompose(RecRun& r, size_t c0, size_t c1) {
             }));
     } else {
         F2_TRY(rank_updates(r, c0, cm, cm, c1, r.n));
+        if (c1 == r.mu && r.on_final) F2_TRY(r.on_final(R1));
     }
-    if (c1 == r.mu && r.on_final) F2_TRY(r.on_final(R1));
     return rec_decompose(r, cm, c1);
 }
 
