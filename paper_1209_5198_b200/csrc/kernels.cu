@@ -916,7 +916,7 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
             build_tables_staged<kV3Warps * 32>(tab, p.B, p.sb, b_row0, p.b_wcol0 + g * kTabCols, nvalid, k,
                                                [] { v3_consumers_sync(); });
             v3_consumers_sync();
-            if (p.tag >= 0 && blockIdx.x == 0 && threadIdx.x == 0) trace_ev(gcur == ~size_t(0) ? 10 : 13, p.tag);
+            if (p.tag >= 0 && gcur == ~size_t(0) && blockIdx.x == 0 && threadIdx.x == 0) trace_ev(10, p.tag);
             gcur = g;
         }
         mbar_wait(&a_full[as], aph);
@@ -1936,15 +1936,24 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
         asm volatile("bar.sync 4, 96;" ::: "memory");
         if (t3 == 0) atomicAdd(link.head_out, 1u);
     };
-    // each of warps 0-2 calls this once, after its last global write
+    // each of warps 0-2 calls this once, after its last global write.  Warp 2 ends
+    // last (the pair list and the next column's swaps): it waits for the other two
+    // (long done), so one device fence orders its own stores -- and, cumulatively,
+    // theirs -- before the done counter (one fence on the chain instead of two)
     auto finish = [&]() {
         if (!link.done_out) return;
-        __threadfence();
         __syncwarp();
-        if (lane == 0 && atomicAdd(&S.fin, 1u) == 2u) {
+        if (lane != 0) return;
+        if (warp != 2) {
             __threadfence();
-            atomicAdd(link.done_out, 1u);
+            atomicAdd(&S.fin, 1u);
+            return;
         }
+        while (atomicAdd(&S.fin, 0u) < 2u) {
+        }
+        __threadfence();
+        atomicAdd(link.done_out, 1u);
+        if (link.trace) trace_ev(13, j);
     };
 
     if (warp == 2) {
