@@ -615,15 +615,33 @@ __global__ void __launch_bounds__(kT3Threads, 1)
             if (++s == kT3Stages) { s = 0; ph ^= 1; }
         }
         // epilogue: lane quarter lq = w & 3; 16-column chunks c = (w >> 2) + 4i of the
-        // 2 x 15 chunks; a ballot per row packs the 32 output columns of the quarter
+        // 2 x 15 chunks; a ballot per row packs the 32 output columns of the quarter.
+        // C ^= A*B: this tile's C words are loaded before the accumulator is ready
+        // (the CTA owns them), so the read-modify-write is off the chunk chain
+        constexpr int kChunks = 2 * (kT3Rows / 16), kPerWarp = (kChunks + 3) / 4;
+        const int lq = warp & 3;
+        uint32_t* dsts[kPerWarp];
+        uint32_t pre[kPerWarp];
+#pragma unroll
+        for (int it = 0; it < kPerWarp; ++it) {
+            const int ch = (warp >> 2) + 4 * it;
+            const int accn = ch / (kT3Rows / 16), cc = ch % (kT3Rows / 16);
+            const int row = 16 * cc + lane;
+            const size_t col = c0 + size_t(accn) * 128 + size_t(lq) * 32;
+            const bool mine_row = ch < kChunks && lane < 16 && row < nvalid;
+            dsts[it] = mine_row ? reinterpret_cast<uint32_t*>(C + (col / 64) * sc + i0 + row) + ((col / 32) & 1)
+                                : nullptr;
+            pre[it] = (acc && mine_row) ? *dsts[it] : 0u;
+        }
         mbar_wait1(done, 0);
         asm volatile("tcgen05.fence::after_thread_sync;");
 #ifdef TC3_PROFILE
         if (prof && threadIdx.x == 0) g_tc3_prof[4] = clock64();
 #endif
-        const int lq = warp & 3;
-#pragma unroll 1
-        for (int ch = warp >> 2; ch < 2 * (kT3Rows / 16); ch += 4) {
+#pragma unroll
+        for (int it = 0; it < kPerWarp; ++it) {
+            const int ch = (warp >> 2) + 4 * it;
+            if (ch >= kChunks) break;
             const int accn = ch / (kT3Rows / 16), cc = ch % (kT3Rows / 16);
             uint32_t v[16];
             const uint32_t taddr = tmem + (uint32_t(32 * lq) << 16) + uint32_t(kT3Rows * accn + 16 * cc);
@@ -651,13 +669,7 @@ __global__ void __launch_bounds__(kT3Threads, 1)
                 const uint32_t bits = __ballot_sync(0xffffffffu, par);
                 if (lane == q) mine = bits;
             }
-            const int row = 16 * cc + lane;
-            const size_t col = c0 + size_t(accn) * 128 + size_t(lq) * 32;
-            if (lane < 16 && row < nvalid) {
-                uint32_t* dst = reinterpret_cast<uint32_t*>(C + (col / 64) * sc + i0 + row) + ((col / 32) & 1);
-                if (acc) mine ^= *dst;
-                *dst = mine;
-            }
+            if (dsts[it]) *dsts[it] = mine ^ pre[it];
         }
     }
 #ifdef TC3_PROFILE
