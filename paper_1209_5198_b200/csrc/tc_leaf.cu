@@ -869,15 +869,29 @@ __global__ void __launch_bounds__(kT3Threads, 1)
                 if (++s == kT3Stages) { s = 0; ph ^= 1; }
             }
             // epilogue: lane quarter lq = w & 3; 16-column chunks c = (w >> 2) + 4i of the
-            // 2 x 15 chunks; a ballot per row packs the 32 output columns of the quarter
-            mbar_wait1(done, it & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;");
+            // 2 x 15 chunks; a ballot per row packs the 32 output columns of the quarter.
+            // C ^= A*B: the tile's C words are loaded before the accumulator is ready
             const int lq = warp & 3;
             uint64_t* __restrict__ C = P.C;
             const size_t sc = P.sc;
             const int acc = P.acc;
-#pragma unroll 1
-            for (int ch = warp >> 2; ch < 2 * (kT3Rows / 16); ch += 4) {
+            constexpr int kChunks = 2 * (kT3Rows / 16), kPerWarp = (kChunks + 3) / 4;
+            uint32_t pre[kPerWarp];
+#pragma unroll
+            for (int q = 0; q < kPerWarp; ++q) {
+                const int ch = (warp >> 2) + 4 * q;
+                const int row = 16 * (ch % (kT3Rows / 16)) + lane;
+                const size_t col = c0 + size_t(ch / (kT3Rows / 16)) * 128 + size_t(lq) * 32;
+                pre[q] = (acc && ch < kChunks && lane < 16 && row < nvalid)
+                             ? *(reinterpret_cast<const uint32_t*>(C + (col / 64) * sc + i0 + row) + ((col / 32) & 1))
+                             : 0u;
+            }
+            mbar_wait1(done, it & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+            for (int q = 0; q < kPerWarp; ++q) {
+                const int ch = (warp >> 2) + 4 * q;
+                if (ch >= kChunks) break;
                 const int accn = ch / (kT3Rows / 16), cc = ch % (kT3Rows / 16);
                 uint32_t v[16];
                 const uint32_t taddr = tmem + (uint32_t(32 * lq) << 16) + uint32_t(kT3Rows * accn + 16 * cc);
@@ -909,8 +923,7 @@ __global__ void __launch_bounds__(kT3Threads, 1)
                 const size_t col = c0 + size_t(accn) * 128 + size_t(lq) * 32;
                 if (lane < 16 && row < nvalid) {
                     uint32_t* dst = reinterpret_cast<uint32_t*>(C + (col / 64) * sc + i0 + row) + ((col / 32) & 1);
-                    if (acc) mine ^= *dst;
-                    *dst = mine;
+                    *dst = mine ^ pre[q];
                 }
             }
             // accumulators read: the MMA warp may overwrite them with the next tile
