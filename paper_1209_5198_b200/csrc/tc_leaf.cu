@@ -914,10 +914,10 @@ __global__ void __launch_bounds__(kT3Threads, 1)
                 }
                 uint32_t mine = 0;
 #pragma unroll
-                for (int q = 0; q < 16; ++q) {
-                    const uint32_t par = __float_as_uint(__uint_as_float(v[q]) + 8388608.0f) & 1u;
+                for (int t = 0; t < 16; ++t) {
+                    const uint32_t par = __float_as_uint(__uint_as_float(v[t]) + 8388608.0f) & 1u;
                     const uint32_t bits = __ballot_sync(0xffffffffu, par);
-                    if (lane == q) mine = bits;
+                    if (lane == t) mine = bits;
                 }
                 const int row = 16 * cc + lane;
                 const size_t col = c0 + size_t(accn) * 128 + size_t(lq) * 32;
