@@ -1416,7 +1416,7 @@ __device__ __forceinline__ uint64_t pext64(uint64_t x, uint64_t sel) {
 __global__ void __launch_bounds__(kPanelThreads, 1)
     k_panel(uint64_t* __restrict__ col, size_t n, PanelState* __restrict__ st_all, int j,
             const uint32_t* wait_flag, uint32_t wait_count) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
     PanelSmem& S = *reinterpret_cast<PanelSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31;
     if (wait_flag) {
@@ -1810,7 +1810,7 @@ __device__ __forceinline__ void wait_count_ge_warp(const uint32_t* flag, uint32_
 __global__ void __launch_bounds__(kPanelThreads, 1)
     k_panel_gj(uint64_t* __restrict__ col, size_t n, PanelState* __restrict__ st_all, int j,
                const PanelLink link) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
     PanelGjSmem& S = *reinterpret_cast<PanelGjSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // every warp waits for the previous panel's head chunk (or the fused post's
