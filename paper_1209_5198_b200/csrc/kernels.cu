@@ -847,7 +847,9 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
         // Pipelined write-back: tile t's reductions are committed, and the stage of
         // tile t-1 is released once ITS reductions have read shared memory
         // (wait_group.read 1), so the producer never blocks on the tile it just issued.
+#if F2_PIPELINED_WRITEBACK
         int sprev = -1;
+#endif
         for (size_t t = 0; t < cnt; ++t) {
             const size_t r0 = base + dc.tt * kV3Rows;
             const int nvalid = min(kTabCols, int(size_t(p.ncols) - dc.g * kTabCols));
@@ -883,7 +885,6 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
             __syncwarp();
             if (rel_point && lane == 0) release_signal(p.release, p.tag);
             if (lane == 0) mbar_arrive(&d_free[s]);
-            (void)sprev;
 #endif
             if (t + kV3AStages < cnt) {
                 mbar_wait(&a_empty[ae], aph);
