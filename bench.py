@@ -5,7 +5,8 @@ Default workload (BASELINE.json configs[3], the metric's headline): full
 decomposition P*A = L*U of a 65536 x 65536 dense F2 matrix, bits Bernoulli(0.5)
 from PackedMatrix::random_dense(seed 6) — synthetic input generated bit-exactly
 on the device.  One step = copy A -> W (the API never modifies its input,
-SPEC.md:379) + decompose_block(W).  Metric: Gbitop/s = n^3 / t (BASELINE.md).
+SPEC.md:379) + decompose_recursive(W) (--variant block: decompose_block(W);
+both give the identical overlay, perm and r_j).  Metric: Gbitop/s = n^3 / t.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -13,11 +14,15 @@ N > 1 (torchrun): column blocks round-robin over the ranks, one NCCL broadcast
 per panel (strong scaling: the job is one 65536^2 decomposition).
 
 The JSON line carries: value (device-resident, CUDA events, max over ranks),
+parity (the LAST timed step's W, perm and r_j -- a CUDA-graph replay --
+digested and compared with tests/golden/digests.json; exit 1 on mismatch),
 e2e (through the C-ABI host entry point: H2D of A from pinned memory, the
-decomposition, D2H of W/perm/r_j), roofline (the dominant kernel: the fused
-M4RM Schur update, measured live as the north-star unit
-C(65536x65536) ^= A(65536x64) * B(64x65536)), cpu_baseline (the reference
-CPU path on this host: bounded sample, extrapolated), clocks, gpu_launches.
+decomposition, D2H of W/perm/r_j), roofline (the fused M4RM Schur update,
+measured live as the north-star unit C(65536x65536) ^= A(65536x64) *
+B(64x65536)), roofline_tensor (the fp4 product leaf), gemm (BASELINE
+configs[1], 16384^2 products, with the reference's m4rm_mult timed beside it),
+cpu_baseline (one FULL reference CPU decomposition of the same input on this
+host's cores), clocks, gpu_launches.
 """
 from __future__ import annotations
 
@@ -111,67 +116,146 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the reference's own M4RM (oracle/_ref, compiled from the
-# reference headers) under the restated buildZ; bounded sample of panels.
+# Parity of the benchmarked run: the order-independent digests of
+# tests/golden/digests.json (computed once with oracle/_ref by
+# tests/golden/make_golden.py), restated here in numpy so the bench does not
+# load the oracle outside its CPU legs.
 # ---------------------------------------------------------------------------
-def panel_work(n: int, mu: int, P: int) -> float:
-    """Remaining trailing area summed over the first P panels of a full-rank
-    n x 64mu decomposition (rows below the pivots x word-columns right of the
-    panel) — the Schur update work that dominates the CPU time."""
-    w = 0.0
-    for j in range(min(P, mu)):
-        w += max(n - 64 * (j + 1), 0) * (mu - j - 1) + (n - 64 * j)
-    return w
+M64 = (1 << 64) - 1
 
 
-def cpu_baseline(n: int, m: int, p: float, seed: int, panels: int, reps: int = 1) -> dict:
-    from oracle import pyoracle as po
+def _mix64_int(z: int) -> int:
+    z &= M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+    return z ^ (z >> 31)
 
-    threads = os.cpu_count() or 1
-    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
-    po.build(ref=False)
-    a = po.random_dense(n, m, p, seed)  # parallel jump-ahead twin of random_dense (pinned by tests)
+
+def _mix64(z: np.ndarray) -> np.ndarray:
+    z = z ^ (z >> np.uint64(30))
+    z = z * np.uint64(0xBF58476D1CE4E5B9)
+    z = z ^ (z >> np.uint64(27))
+    z = z * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def digest_words(w: np.ndarray, n: int, m: int) -> int:
+    """f2o_digest (oracle/f2oracle.c): mix64 sum over every word of the matrix,
+    salted by row index and word-column; w is (mu, stride) uint64."""
     mu = (m + 63) // 64
-    use_ref = po.ref_available()
-    best = float("inf")
-    for _ in range(reps):
-        if use_ref:
+    s = _mix64_int((n * 0x9E3779B97F4A7C15) ^ m)
+    with np.errstate(over="ignore"):
+        salt_i = np.arange(n, dtype=np.uint64) * np.uint64(0xD6E8FEB86659FD93)
+        for q in range(mu):
+            salt = np.uint64(_mix64_int(q + 0x1234567))
+            s = (s + int(_mix64(w[q, :n] ^ salt_i ^ salt).sum(dtype=np.uint64))) & M64
+    return s
+
+
+def digest_u32(v: np.ndarray) -> int:
+    v = np.ascontiguousarray(v, dtype=np.uint32)
+    with np.errstate(over="ignore"):
+        x = (v.astype(np.uint64) << np.uint64(32)) ^ np.arange(v.size, dtype=np.uint64)
+        return (_mix64_int(v.size) + int(_mix64(x).sum(dtype=np.uint64))) & M64
+
+
+def golden(key: str) -> dict | None:
+    p = ROOT / "tests" / "golden" / "digests.json"
+    try:
+        return json.loads(p.read_text()).get(key)
+    except Exception:
+        return None
+
+
+def decomp_parity(cfg: dict, w: np.ndarray | None, perm: np.ndarray, rj: np.ndarray, rank: int) -> dict:
+    key, g = None, None
+    for k in ("cfg4", "cfg1"):
+        e = golden(k)
+        if e and (e["n"], e["m"], e["seed"], e["p"]) == (cfg["n"], cfg["m"], cfg["seed"], cfg["p"]):
+            key, g = k, e
+    if not g:
+        return {"status": "unchecked", "why": "no committed digest for this configuration"}
+    bad = []
+    if rank != g["rank"]:
+        bad.append(f"rank {rank} != {g['rank']}")
+    if digest_u32(rj) != g["rj_digest"]:
+        bad.append("r_j digest")
+    if digest_u32(perm) != g["perm_digest"]:
+        bad.append("perm digest")
+    if w is not None and digest_words(w, cfg["n"], cfg["m"]) != g["w_digest"]:
+        bad.append("W digest")
+    return {"status": "ok" if not bad else "MISMATCH: " + ", ".join(bad),
+            "checked": "rank, r_j, perm" + (", W" if w is not None else "") +
+                       f" of the last timed step vs tests/golden/digests.json {key} (oracle/_ref)"}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference's own M4RM (oracle/_ref, compiled from the
+# reference headers) under the restated buildZ -- FULL decompositions.
+# ---------------------------------------------------------------------------
+class RefCpu:
+    """The reference CPU decomposition of one input on this host's cores:
+    oracle/_ref (reference m4rm.hpp build_tables/mult_acc + the restated buildZ,
+    OpenMP over word-columns), or the oracle/f2oracle.c port when _ref is absent."""
+
+    def __init__(self, n: int, m: int, p: float, seed: int):
+        from oracle import pyoracle as po
+
+        self.threads = os.cpu_count() or 1
+        os.environ.setdefault("OMP_NUM_THREADS", str(self.threads))
+        po.build(ref=False)
+        self.po, self.n, self.m, self.seed = po, n, m, seed
+        self.mu = (m + 63) // 64
+        t0 = time.perf_counter()
+        self.a = po.random_dense(n, m, p, seed)  # parallel jump-ahead twin of random_dense (pinned by tests)
+        self.t_gen = time.perf_counter() - t0
+        self.use_ref = po.ref_available()
+        self.kind = "reference" if self.use_ref else "port"
+        self.last = None
+
+    def decompose(self, keep: bool = False) -> float:
+        """One full decomposition; returns its wall time (generation and copies excluded)."""
+        po, n, m, mu = self.po, self.n, self.m, self.mu
+        perm = np.zeros(n, np.uint32)
+        rj = np.zeros(mu, np.uint32)
+        if self.use_ref:
             r = po.ref()
-            h = r.ref_matrix_new(a, n, m, a.shape[1])
-            perm = np.zeros(n, np.uint32)
-            rj = np.zeros(mu, np.uint32)
+            h = r.ref_matrix_new(self.a, n, m, self.a.shape[1])
             t0 = time.perf_counter()
-            r.ref_decompose_block(h, perm, rj, 8, panels)
+            rank = r.ref_decompose_block(h, perm, rj, 8, mu)
             dt = time.perf_counter() - t0
+            w = None
+            if keep:
+                w = po.zeros(n, m)
+                r.ref_matrix_read(h, w, w.shape[1])
             r.ref_matrix_free(h)
         else:
-            w = a.copy()
-            perm = np.zeros(n, np.uint32)
-            rj = np.zeros(mu, np.uint32)
+            w = self.a.copy()
             t0 = time.perf_counter()
-            po.lib().f2o_decompose_block(w, n, m, w.shape[1], perm, rj, 8, panels)
+            rank = po.lib().f2o_decompose_block(w, n, m, w.shape[1], perm, rj, 8, mu)
             dt = time.perf_counter() - t0
-        best = min(best, dt)
-    frac = panel_work(n, mu, panels) / panel_work(n, mu, mu)
-    t_full = best / frac
-    return {
-        "value": round(n * n * min(n, m) / t_full / 1e9, 2),
-        "unit": UNIT,
-        "cores": threads,
-        "kind": "reference" if use_ref else "port",
-        "sample": (f"first {panels} of {mu} panels of the same {n}x{m} seed-{seed} decomposition "
-                   f"({'reference m4rm.hpp build_tables/mult_acc compiled from the reference headers + restated buildZ' if use_ref else 'oracle/f2oracle.c port'}), "
-                   f"OpenMP {threads} threads, {best:.2f} s measured = {frac:.3f} of the Schur work; "
-                   f"full-run time extrapolated {t_full:.1f} s"),
-        "t_sample_s": round(best, 3),
-        "t_full_est_s": round(t_full, 2),
-    }
+        if keep:
+            self.last = (w, perm, rj, int(rank))
+        return dt
+
+    def sample(self, runs: int) -> str:
+        what = ("reference m4rm.hpp build_tables/mult_acc compiled from the reference headers + restated buildZ"
+                if self.use_ref else "oracle/f2oracle.c port")
+        return (f"{runs} full {self.n}x{self.m} seed-{self.seed} decomposition(s), all {self.mu} panels "
+                f"({what}), OpenMP {self.threads} threads, no extrapolation")
 
 
-def gemm_cpu_baseline(n: int) -> dict:
+def cpu_baseline(n: int, m: int, p: float, seed: int) -> dict:
+    rc = RefCpu(n, m, p, seed)
+    dt = rc.decompose()
+    return {"value": round(n * n * min(n, m) / dt / 1e9, 2), "unit": UNIT, "cores": rc.threads,
+            "kind": rc.kind, "sample": rc.sample(1) + f": {dt:.2f} s", "t_s": round(dt, 3)}
+
+
+def gemm_cpu_baseline(n: int, reps: int = 3) -> dict:
     """The reference's own m4rm_mult (m4rm.hpp:177-196, compiled from the reference
     headers into oracle/_ref, OpenMP over output word-columns) on the full n^3
-    product with the same seeds, on all host cores."""
+    product with the same seeds, on all host cores: one warm-up + `reps` timed runs."""
     from oracle import pyoracle as po
 
     threads = os.cpu_count() or 1
@@ -181,11 +265,18 @@ def gemm_cpu_baseline(n: int) -> dict:
         return {"unavailable": "oracle/_ref not built"}
     a = po.random_dense(n, n, 0.5, 2)
     b = po.random_dense(n, n, 0.5, 3)
-    t0 = time.perf_counter()
-    po.ref_m4rm_mult(a, n, n, b, n, tc=0)  # c = 0: the reference's cost-model table size
-    dt = time.perf_counter() - t0
-    return {"value": round(n ** 3 / dt / 1e9, 1), "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": f"full {n}^3 reference m4rm_mult (table size from tuning, c=0), one run, {dt:.2f} s"}
+    c = po.ref_m4rm_mult(a, n, n, b, n, tc=0)  # c = 0: the reference's cost-model table size
+    g = golden("cfg2")
+    ok = None if not g else po.digest(c, n, n) == g["c_digest"]
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        po.ref_m4rm_mult(a, n, n, b, n, tc=0)
+        ts.append(time.perf_counter() - t0)
+    dt = sum(ts) / len(ts)
+    return {"value": round(n ** 3 / dt / 1e9, 1), "unit": UNIT, "ms": round(dt * 1e3, 1), "cores": threads,
+            "kind": "reference", "parity": "ok" if ok else ("unchecked" if ok is None else "MISMATCH"),
+            "sample": f"full {n}^3 reference m4rm_mult (table size from tuning, c=0), mean of {reps} runs"}
 
 
 # ---------------------------------------------------------------------------
@@ -197,45 +288,60 @@ def dist_env():
 
 
 def run_reference(args, cfg) -> None:
+    """The reference arm: W + K FULL CPU decompositions of the bench input (the
+    reference's compiled M4RM + the restated buildZ, all host threads); value =
+    n^3 / (mean time of the K timed runs).  Rank 0 only under torchrun."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    vals = []
-    base = None
-    for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(cfg["n"], cfg["m"], cfg["p"], cfg["seed"], args.ref_panels)
-        if i >= args.warmup:
-            vals.append(cb["value"])
-            base = cb
-    v = float(np.median(vals))
-    t_step = cfg["n"] ** 2 * min(cfg["n"], cfg["m"]) / (v * 1e9)
+    rc = RefCpu(cfg["n"], cfg["m"], cfg["p"], cfg["seed"])
+    for i in range(args.warmup):
+        rc.decompose(keep=(i == 0))
+    t0 = time.perf_counter()
+    ts = [rc.decompose() for _ in range(args.steps)]
+    region = time.perf_counter() - t0
+    t_step = sum(ts) / len(ts)
+    v = round(cfg["n"] ** 2 * min(cfg["n"], cfg["m"]) / t_step / 1e9, 2)
+    parity = {"status": "unchecked"}
+    if rc.last is not None:
+        w, perm, rj, rk = rc.last
+        parity = decomp_parity(cfg, w, perm, rj, rk)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 1),
+        "timed_region_s": round(region, 2),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (random_dense seed %d, p=%g)" % (cfg["seed"], cfg["p"]),
         "config": cfg_json(cfg, args.gpus, args.variant),
-        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "parity": parity,
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": rc.threads, "kind": rc.kind,
+                         "sample": rc.sample(args.steps) + f" per step ({args.warmup} warm-up runs untimed)"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_gemm:
+        line["gemm"] = {"metric": "M4RM GEMM Gbitop/s (n^3/t), 16384^2 (BASELINE configs[1])",
+                        "reference_m4rm_mult": gemm_cpu_baseline(16384)}
     print(json.dumps(line), flush=True)
 
 
 VARIANTS = {
     "block": "decompose_block (lookahead 1, CUDA-graph replay)",
-    "recursive": "decompose_recursive (256-panel block leaves with lookahead; TRSM + products on the fp4 "
-                 "tensor-core leaf, Strassen-Winograd over 16384 leaves)",
+    "recursive": "decompose_recursive (block leaves of <= 256 panels with lookahead, replayed from CUDA graphs; "
+                 "TRSM + A' = D ^ L21 X products on the fp4 tensor-core leaf, Strassen-Winograd over 8192 leaves)",
 }
 
 
 def cfg_json(cfg, gpus, variant="block"):
-    return {"workload": f"decompose {cfg['n']}x{cfg['m']} dense F2, Bernoulli({cfg['p']}), "
-                        f"seed {cfg['seed']} (BASELINE configs[3])",
-            "n": cfg["n"], "m": cfg["m"], "density": cfg["p"], "seed": cfg["seed"],
+    n, m = cfg["n"], cfg["m"]
+    which = {65536: "BASELINE configs[3]", 4096: "BASELINE configs[0] size"}.get(n, "non-BASELINE size")
+    mib = n * ((m + 63) // 64) * 8 / 2 ** 20
+    return {"workload": f"decompose {n}x{m} dense F2, Bernoulli({cfg['p']}), seed {cfg['seed']} ({which})",
+            "n": n, "m": m, "density": cfg["p"], "seed": cfg["seed"],
             "word_bits": 64, "tables": "9 groups (7x8+8 bits), 16 word-cols/CTA",
             "parallelism": f"column-round-robin x{gpus}" if gpus > 1 else "single GPU",
             "variant": VARIANTS[variant] if gpus == 1 else VARIANTS["block"],
-            "l2": "inputs (512 MiB) larger than L2 (126 MB); no flush needed"}
+            "l2": (f"inputs ({mib:.0f} MiB) larger than L2 (126 MB); no flush needed" if mib > 126
+                   else f"inputs ({mib:.0f} MiB) fit in L2: warm-cache timing")}
 
 
 def main() -> None:
@@ -245,15 +351,15 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=65536, help="matrix size (default: BASELINE cfg4)")
-    ap.add_argument("--ref-panels", type=int, default=32, help="CPU sample size in panels")
+    ap.add_argument("--seed", type=int, default=6, help="input seed (cfg4: 6; cfg1 4096^2: 1)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--gemm", action="store_true", help="also time the cfg2 16384^2 GEMM")
+    ap.add_argument("--no-gemm", action="store_true", help="skip the cfg2 16384^2 products")
     ap.add_argument("--variant", default="recursive", choices=["block", "recursive"],
                     help="decompose_recursive (default, fastest) or decompose_block; bit-identical factors")
     ap.add_argument("--min-cols", type=int, default=0, help="recursive leaf width in bits (0 = default)")
     args = ap.parse_args()
-    cfg = {"n": args.n, "m": args.n, "p": 0.5, "seed": 6}
+    cfg = {"n": args.n, "m": args.n, "p": 0.5, "seed": args.seed}
 
     if args.impl == "reference":
         run_reference(args, cfg)
@@ -335,6 +441,14 @@ def main() -> None:
     value = n * n * min(n, m) / (ms_step * 1e-3) / 1e9
     rank_found = int(rk.value)
 
+    # ---- parity of the benchmarked (graph-replayed) run ----
+    w_host = None
+    if world == 1:
+        w_host = np.zeros((mu, (n + 7) // 8 * 8), np.uint64)
+        _lib.check(lib.f2gpu_mat_download(ctx.handle, W.handle, C.c_void_p(w_host.ctypes.data), w_host.shape[1]))
+    parity = decomp_parity(cfg, w_host, perm, rj, rank_found) if rank == 0 else None
+    del w_host
+
     # ---- roofline: the dominant kernel, measured live (north-star unit) ----
     roof = roof_tc = None
     if rank == 0:
@@ -347,17 +461,17 @@ def main() -> None:
     if not args.no_e2e:
         e2e = measure_e2e(f2, lib, _lib, ctx, torch, A, n, m, mu, world, rank, dist,
                           steps=min(args.steps, 3), variant=args.variant, min_cols=args.min_cols,
-                          warmup=args.warmup)
+                          warmup=args.warmup, cfg=cfg)
 
     gemm = None
-    if args.gemm and world == 1:
-        gemm = measure_gemm(f2, lib, _lib, ctx, stream, torch)
-    elif args.gemm:
+    if not args.no_gemm and world == 1:
+        gemm = measure_gemm(f2, lib, _lib, ctx, stream, torch, cpu=not args.no_cpu)
+    elif not args.no_gemm:
         gemm = measure_gemm_dist(f2, lib, _lib, ctx, stream, torch, rank, world, dist)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(n, m, cfg["p"], cfg["seed"], args.ref_panels)
+        cpu = cpu_baseline(n, m, cfg["p"], cfg["seed"])
         cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
     if rank == 0:
@@ -367,16 +481,21 @@ def main() -> None:
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
             "data": f"synthetic (random_dense seed {cfg['seed']}, p={cfg['p']}, generated on device)",
             "config": cfg_json(cfg, world, args.variant),
-            "rank": rank_found,
+            "rank": rank_found, "parity": parity,
             "e2e": e2e, "roofline": roof, "roofline_tensor": roof_tc, "cpu_baseline": cpu, "clocks": ck,
             "gpu_launches": launches,
         }
         if gemm:
             line["gemm"] = gemm
         print(json.dumps(line), flush=True)
+    bad = (parity and parity["status"] not in ("ok", "unchecked")) or (
+        gemm and any(str(v.get("parity", "ok")) not in ("ok", "unchecked") for v in gemm.values() if isinstance(v, dict)))
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+    if bad:
+        print("bench: PARITY MISMATCH in the benchmarked results", file=sys.stderr, flush=True)
+        sys.exit(1)
 
 
 def measure_update_roofline(f2, lib, _lib, ctx, stream, torch, n: int) -> dict:
@@ -468,7 +587,7 @@ def measure_tensor_roofline(f2, lib, _lib, ctx, stream, torch, n: int = 16384) -
 
 
 def measure_e2e(f2, lib, _lib, ctx, torch, A, n, m, mu, world, rank, dist, steps: int,
-                variant: str = "block", min_cols: int = 0, warmup: int = 3) -> dict:
+                variant: str = "block", min_cols: int = 0, warmup: int = 3, cfg: dict | None = None) -> dict:
     """Same metric through the public C-ABI host entry point with host buffers:
     H2D of A (pinned) + decomposition + D2H of W, perm, r_j inside the region."""
     host_stride = (n + 7) // 8 * 8
@@ -519,7 +638,10 @@ def measure_e2e(f2, lib, _lib, ctx, torch, A, n, m, mu, world, rank, dist, steps
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt = float(t.item())
     hbytes = lw * host_stride * 8
-    return {"value": round(n * n * min(n, m) / dt / 1e9, 1), "unit": UNIT,
+    parity = None
+    if world == 1 and cfg is not None:  # the host output of the last timed call
+        parity = decomp_parity(cfg, hW, perm, rj, int(rk.value))["status"]
+    return {"value": round(n * n * min(n, m) / dt / 1e9, 1), "unit": UNIT, "parity": parity,
             "h2d_bytes_per_step": hbytes * world,
             "d2h_bytes_per_step": hbytes * world + 4 * n + 4 * mu,
             "ms_per_step": round(dt * 1e3, 2),
@@ -564,12 +686,16 @@ def measure_gemm_dist(f2, lib, _lib, ctx, stream, torch, rank, world, dist, n: i
             "ms": round(ms, 3), "Gbitop_s": round(n ** 3 / (ms * 1e-3) / 1e9, 1)}
 
 
-def measure_gemm(f2, lib, _lib, ctx, stream, torch) -> dict:
-    """BASELINE configs[1]: C = A*B, A, B 16384^2 (seeds 2, 3), M4RM and Strassen-Winograd."""
+def measure_gemm(f2, lib, _lib, ctx, stream, torch, cpu: bool = True) -> dict:
+    """BASELINE configs[1]: C = A*B, A, B 16384^2 (seeds 2, 3): the M4RM kernel,
+    Strassen-Winograd over M4RM leaves, the fp4 tensor-core leaf alone, and the
+    default strassen_mult; each output is digested against tests/golden/digests.json
+    cfg2 (oracle/_ref).  The reference's own m4rm_mult is timed beside them."""
     n = 16384
     Am, Bm, Cm = (f2.DeviceMatrix(n, n, ctx) for _ in range(3))
     Am.random_dense(0.5, 2)
     Bm.random_dense(0.5, 3)
+    g = golden("cfg2")
     out = {}
     def smult(tc, cut):
         def run():
@@ -594,10 +720,19 @@ def measure_gemm(f2, lib, _lib, ctx, stream, torch) -> dict:
         e1.record(stream)
         torch.cuda.synchronize()
         t = e0.elapsed_time(e1) / 5 * 1e-3
-        out[name] = {"ms": round(t * 1e3, 3), "Gbitop_s": round(n ** 3 / t / 1e9, 1)}
+        par = "unchecked"
+        if g:
+            c = np.zeros((n // 64, n), np.uint64)
+            _lib.check(lib.f2gpu_mat_download(ctx.handle, Cm.handle, C.c_void_p(c.ctypes.data), n))
+            par = "ok" if digest_words(c, n, n) == g["c_digest"] else "MISMATCH"
+        out[name] = {"ms": round(t * 1e3, 3), "Gbitop_s": round(n ** 3 / t / 1e9, 1), "parity": par}
     ctx.set_tc(True)
-    out["cpu_baseline"] = gemm_cpu_baseline(n)
-    return {"metric": "M4RM GEMM Gbitop/s (n^3/t), 16384^2 (BASELINE configs[1])", **out}
+    Am.free(); Bm.free(); Cm.free()
+    res = {"metric": "M4RM GEMM Gbitop/s (n^3/t), 16384^2 (BASELINE configs[1])",
+           "value": out["strassen_mult_default"]["Gbitop_s"], "unit": UNIT, **out}
+    if cpu:
+        res["reference_m4rm_mult"] = gemm_cpu_baseline(n)
+    return res
 
 
 if __name__ == "__main__":

@@ -13,7 +13,9 @@
  * mu = ceil(n_cols/64) word-columns; word (i, q) is at base[q*col_stride + i];
  * bit k of word (i,q) is entry (i, 64q+k) (LSB = leftmost column); padding bits
  * are zero.  Host buffers carry their own col_stride (the reference uses
- * ceil(n/8)*8, bit_matrix.hpp:330-333); device matrices use a 32-row stride.
+ * ceil(n/8)*8, bit_matrix.hpp:330-333); device matrices use a stride of rows
+ * rounded up to 128 words (1 KiB column segments for the bulk-copy kernels;
+ * f2gpu_mat_shape reports it).
  *
  * Errors: every function returns an int status.  The codes mirror the
  * reference's exceptions: F2GPU_EINVAL <-> std::invalid_argument (shape
@@ -23,6 +25,12 @@
  * Threading: a context owns one CUDA device + stream; it is not shared between
  * host threads (the reference contract is single-threaded per call).
  * Distinct contexts may be used concurrently.
+ *
+ * Device use: the decompositions' lookahead schedule runs kernels on three
+ * streams that wait on each other through device counters, so they must be
+ * co-resident: run them with the GPU to themselves (no concurrent kernels from
+ * other streams or MPS clients).  Every such wait is bounded (20 s); a wait that
+ * expires traps and the call returns F2GPU_ECUDA instead of hanging.
  */
 #ifndef F2GPU_H
 #define F2GPU_H
@@ -50,7 +58,12 @@ const char *f2gpu_version(void);
 /* ---- context -------------------------------------------------------------- */
 int f2gpu_ctx_create(int device, f2gpu_ctx **out);
 int f2gpu_ctx_destroy(f2gpu_ctx *ctx);
-/* Run subsequent work on an external stream (e.g. torch's); NULL = own stream. */
+/* Run subsequent work on an external CUDA stream (e.g. torch's current stream);
+ * F2GPU_OWN_STREAM returns to the context's own stream.  Handle 0 is the legacy
+ * default stream (torch's default stream), not "own": work is ordered with it,
+ * and CUDA-graph replay is off while it (or cudaStreamPerThread) is selected,
+ * because stream capture is illegal there. */
+#define F2GPU_OWN_STREAM ((void *)(~(uintptr_t)0))
 int f2gpu_ctx_set_stream(f2gpu_ctx *ctx, void *cuda_stream);
 int f2gpu_ctx_sync(f2gpu_ctx *ctx);
 /* Kernel launches issued through this context since creation (evidence for
@@ -89,6 +102,7 @@ int f2gpu_panel_build_z(f2gpu_ctx *ctx, const uint64_t *col, size_t n, uint64_t 
 /* ---- device matrix store (replaces PackedMatrix<uint64_t> storage,
  *      bit_matrix.hpp:82-346) ------------------------------------------------- */
 int f2gpu_mat_alloc(f2gpu_ctx *ctx, size_t n_rows, size_t n_cols, f2gpu_mat **out);
+/* a matrix must be freed before the context it was allocated on is destroyed */
 int f2gpu_mat_free(f2gpu_mat *m);
 int f2gpu_mat_shape(const f2gpu_mat *m, size_t *n_rows, size_t *n_cols, size_t *col_stride);
 /* raw device pointer to word (0,0) (for interop, e.g. torch.from_blob) */
@@ -128,6 +142,20 @@ int f2gpu_m4rm_mult_acc(f2gpu_ctx *ctx, const f2gpu_mat *a, const f2gpu_mat *b, 
 int f2gpu_mult_acc(f2gpu_ctx *ctx, f2gpu_mat *c, size_t c_row0, size_t c_wcol0,
                    size_t n_wcols, const uint64_t *d_a_words, size_t n_rows, size_t k_bits,
                    const f2gpu_mat *b, size_t b_row0, size_t b_wcol0);
+/* The same on HOST matrices in the reference layout (what f2la::gpu::mult_acc
+ * over f2la::gpu::build_tables calls): C (c_rows x c_cols, c_stride) rows
+ * [c_row0, c_row0+n_rows) x word-cols [c_wcol0, c_wcol0+n_wcols) ^= a_words[i] *
+ * B[b_row0, b_row0+k_bits) x word-cols [b_wcol0, b_wcol0+n_wcols), B being
+ * b_rows x b_cols with b_stride.  Replaces build_tables(B, row0, k, wcol0, n,
+ * splits) (m4rm.hpp:93-113) + mult_acc(C, c_row0, c_wcol0, a_words, tables)
+ * (m4rm.hpp:140-172); the result does not depend on the splits, bits
+ * of a_words at or above k_bits are ignored.  Errors: k_bits > 64 ->
+ * F2GPU_EINVAL (m4rm.hpp:97-98); block outside B / destination outside C ->
+ * F2GPU_ERANGE (m4rm.hpp:99-100, 144-145).  C is updated when the call returns. */
+int f2gpu_mult_acc_host(f2gpu_ctx *ctx, uint64_t *c, size_t c_rows, size_t c_cols, size_t c_stride,
+                        size_t c_row0, size_t c_wcol0, const uint64_t *a_words, size_t n_rows,
+                        const uint64_t *b, size_t b_rows, size_t b_cols, size_t b_stride, size_t b_row0,
+                        size_t k_bits, size_t b_wcol0, size_t n_wcols);
 /* The evaluated alternative leaf (north_star): C = A*B (acc=0) or C ^= A*B on the
  * tensor cores.  Default: tcgen05.mma kind::mxf4 (bits as E2M1 1.0/0.0, unit
  * E8M0 scales, exact f32 sums, parity), any n and k, m % 256 == 0.  With
@@ -158,7 +186,8 @@ int f2gpu_decompose_block(f2gpu_ctx *ctx, f2gpu_mat *w, uint32_t *perm, uint32_t
  * factor the left half, update the right half with a block TRSM + one
  * Strassen-Winograd GEMM (A' = D ^ L21 L11^-1 C), recurse.  Exact arithmetic and
  * 64-aligned splits make the result bit-identical to decompose_block.
- * min_cols = 0 -> 128 panels (8192 columns) per leaf. */
+ * min_cols = 0 -> leaves of at most 256 panels (16384 columns), 128 panels once
+ * a leaf has >= 20000 rows below its first panel. */
 int f2gpu_decompose_recursive(f2gpu_ctx *ctx, f2gpu_mat *w, size_t min_cols, uint32_t *perm,
                               uint32_t *rj, size_t *rank);
 /* Same algorithm, column blocks distributed round-robin over `shards` logical

@@ -3,6 +3,9 @@
 // f2gpu.h.  Header-only; include AFTER the reference's "f2la/bit_matrix.hpp".
 //
 //   reference (header-only CPU)                       this shim (B200)
+//   f2la::make_splits(k, c)        m4rm.hpp:39-48     f2la::gpu::make_splits(k, c)
+//   f2la::build_tables(...) x4     m4rm.hpp:93-135    f2la::gpu::build_tables(...) x4
+//   f2la::mult_acc(C, r0, q0, a, t) m4rm.hpp:140-172  f2la::gpu::mult_acc(C, r0, q0, a, t)
 //   f2la::m4rm_mult(A, B, c)       m4rm.hpp:177-196   f2la::gpu::m4rm_mult(A, B, c)
 //   strassen_mult(A, B, thr, c)    SPEC.md:192-200    f2la::gpu::strassen_mult(A, B, thr, c)
 //   decompose_block(A)->LUFactors  SPEC.md:319-327    f2la::gpu::decompose_block(A)
@@ -13,14 +16,21 @@
 // Matrices are passed in the reference layout (PackedMatrix<uint64_t>:
 // col_block(q) + col_stride(), bit_matrix.hpp:74-81).  Errors are rethrown as
 // the reference's exception types (std::invalid_argument / std::out_of_range).
+// Only Word = std::uint64_t (BitMatrix) runs on the device.
+//
+// include/f2la_gpu_dropin.hpp goes one step further: included in place of
+// "f2la/m4rm.hpp", it makes the reference's own unqualified call sites
+// (f2la::build_tables / f2la::mult_acc / f2la::m4rm_mult ...) resolve here.
 #ifndef F2LA_GPU_HPP
 #define F2LA_GPU_HPP
 
 #include <cstddef>
 #include <cstdint>
 #include <optional>
+#include <span>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "f2gpu.h"
@@ -45,6 +55,114 @@ inline f2gpu_ctx* context() {
     };
     thread_local Holder h;
     return h.c;
+}
+
+/// make_splits (m4rm.hpp:39-48): floor(k/c) groups of c plus the remainder.
+inline std::vector<std::uint32_t> make_splits(std::size_t k_bits, std::size_t c) {
+    if (c == 0) throw std::invalid_argument("make_splits: c must be positive");
+    std::vector<std::uint32_t> splits;
+    for (std::size_t done = 0; done < k_bits;) {
+        const std::size_t l = std::min(c, k_bits - done);
+        splits.push_back(static_cast<std::uint32_t>(l));
+        done += l;
+    }
+    return splits;
+}
+
+/// M4rmTables (m4rm.hpp:21-35) for the device: the tables themselves are built in
+/// shared memory inside the fused mult_acc kernel, so this records the B block
+/// they cover (plus the reference's group metadata: shifts / sizes / masks /
+/// offsets, computed as make_table_shell does, m4rm.hpp:52-70).  `entries` is not
+/// materialised.  The B matrix must outlive the tables (the reference copies it).
+template <class Word>
+struct M4rmTables {
+    static_assert(std::is_same_v<Word, std::uint64_t>, "f2la::gpu: only 64-bit words run on the device");
+    std::size_t k_bits = 0;
+    std::size_t width_words = 0;
+    std::vector<std::uint32_t> shifts, sizes;
+    std::vector<Word> masks;
+    std::vector<std::size_t> offsets;
+    // the B block: rows [row0, row0 + k_bits) x word-columns [wcol0, wcol0 + width_words)
+    const Word* b_base = nullptr;
+    std::size_t b_rows = 0, b_cols = 0, b_stride = 0, row0 = 0, wcol0 = 0;
+    std::vector<Word> own_rows;  // the bare-word overload keeps its rows here
+    std::size_t table_count() const noexcept { return sizes.size(); }
+};
+
+namespace detail {
+template <class Word>
+void table_shell(M4rmTables<Word>& t, std::size_t k_bits, std::size_t width, std::span<const std::uint32_t> splits) {
+    t.k_bits = k_bits;
+    t.width_words = width;
+    std::size_t bit = 0, rows = 0;
+    for (const std::uint32_t l : splits) {
+        t.shifts.push_back(static_cast<std::uint32_t>(bit));
+        t.sizes.push_back(l);
+        t.masks.push_back(l >= 64 ? ~Word(0) : ((Word(1) << l) - 1));
+        t.offsets.push_back(rows);
+        bit += l;
+        rows += l >= 64 ? 0 : (std::size_t(1) << l);
+    }
+    if (bit != k_bits) throw std::invalid_argument("build_tables: splits do not sum to k");
+}
+}  // namespace detail
+
+/// build_tables(B, row0, k, wcol0, n, splits) (m4rm.hpp:93-113).
+template <class Word>
+M4rmTables<Word> build_tables(const PackedMatrix<Word>& b_mat, std::size_t row0, std::size_t k_bits,
+                              std::size_t wcol0, std::size_t n_wcols, std::span<const std::uint32_t> splits) {
+    if (k_bits > PackedMatrix<Word>::word_bits) throw std::invalid_argument("build_tables: block taller than a word");
+    if (row0 + k_bits > b_mat.rows() || wcol0 + n_wcols > b_mat.word_cols())
+        throw std::out_of_range("build_tables: block outside B");
+    M4rmTables<Word> t;
+    detail::table_shell(t, k_bits, n_wcols, splits);
+    t.b_base = b_mat.word_cols() ? b_mat.col_block(0) : nullptr;
+    t.b_rows = b_mat.rows();
+    t.b_cols = b_mat.cols();
+    t.b_stride = b_mat.col_stride();
+    t.row0 = row0;
+    t.wcol0 = wcol0;
+    return t;
+}
+/// Whole-matrix convenience (m4rm.hpp:117-121): B has at most 64 rows.
+template <class Word>
+M4rmTables<Word> build_tables(const PackedMatrix<Word>& b_mat, std::span<const std::uint32_t> splits) {
+    return gpu::build_tables(b_mat, 0, b_mat.rows(), 0, b_mat.word_cols(), splits);
+}
+/// m4rm.hpp:122-126.
+template <class Word>
+M4rmTables<Word> build_tables(const PackedMatrix<Word>& b_mat, std::size_t c) {
+    const auto splits = gpu::make_splits(b_mat.rows(), c);
+    return gpu::build_tables(b_mat, std::span<const std::uint32_t>(splits));
+}
+/// Bare words (m4rm.hpp:128-135; compute_Y's Y = D*Z): row r of B is rows[r].
+template <class Word>
+M4rmTables<Word> build_tables(std::span<const Word> rows, std::size_t c) {
+    if (rows.size() > 64) throw std::invalid_argument("build_tables: block taller than a word");
+    const auto splits = gpu::make_splits(rows.size(), c);
+    M4rmTables<Word> t;
+    detail::table_shell(t, rows.size(), 1, std::span<const std::uint32_t>(splits));
+    t.own_rows.assign(rows.begin(), rows.end());
+    t.b_rows = rows.size();
+    t.b_cols = 64;
+    t.b_stride = rows.size();
+    return t;
+}
+
+/// mult_acc(C, c_row0, c_wcol0, a_words, tables) (m4rm.hpp:140-172): C rows
+/// [c_row0 + i] x word-columns [c_wcol0, c_wcol0 + width) ^= a_words[i] * B.
+template <class Word>
+void mult_acc(PackedMatrix<Word>& c_mat, std::size_t c_row0, std::size_t c_wcol0, std::span<const Word> a_words,
+              const M4rmTables<Word>& tables) {
+    const std::size_t w = tables.width_words;
+    if (c_row0 + a_words.size() > c_mat.rows() || c_wcol0 + w > c_mat.word_cols())
+        throw std::out_of_range("mult_acc: destination outside C");
+    if (a_words.empty() || w == 0 || tables.k_bits == 0) return;
+    const Word* b = tables.own_rows.empty() ? tables.b_base : tables.own_rows.data();
+    check(f2gpu_mult_acc_host(context(), c_mat.col_block(0), c_mat.rows(), c_mat.cols(), c_mat.col_stride(), c_row0,
+                              c_wcol0, a_words.data(), a_words.size(), b, tables.b_rows, tables.b_cols,
+                              tables.b_stride, tables.row0, tables.k_bits, tables.wcol0, w),
+          "mult_acc");
 }
 
 /// C = A*B over F2 (m4rm.hpp:177-196).  `c` is accepted for signature parity.

@@ -18,6 +18,7 @@ Reference surface mirrored here (names and argument meaning kept):
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -221,6 +222,8 @@ class Context:
         _lib.check(lib.f2gpu_ctx_create(int(device), C.byref(h)), "ctx_create")
         self._h = h
         self.device = device
+        self._mats = weakref.WeakSet()  # live matrices: freed before the context is destroyed
+        self.stream = None  # None: the context's own stream
         self.rank, self.world = 0, 1
 
     @property
@@ -228,7 +231,12 @@ class Context:
         return self._h
 
     def set_stream(self, cuda_stream: int | None) -> None:
-        _lib.check(_lib.load().f2gpu_ctx_set_stream(self._h, C.c_void_p(cuda_stream or 0)))
+        """Run on an external CUDA stream handle (e.g. ``torch.cuda.current_stream().cuda_stream``;
+        0 is the legacy default stream, i.e. torch's default stream); None returns to the
+        context's own stream."""
+        h = _lib.OWN_STREAM if cuda_stream is None else int(cuda_stream)
+        _lib.check(_lib.load().f2gpu_ctx_set_stream(self._h, C.c_void_p(h)))
+        self.stream = cuda_stream
 
     def sync(self) -> None:
         _lib.check(_lib.load().f2gpu_ctx_sync(self._h), "sync")
@@ -255,7 +263,11 @@ class Context:
         return buf.raw
 
     def close(self) -> None:
+        """Destroy the context; matrices still alive on it are freed first (a device
+        matrix must not outlive its context, include/f2gpu.h)."""
         if getattr(self, "_h", None):
+            for m in list(getattr(self, "_mats", ())):
+                m.free()
             _lib.load().f2gpu_ctx_destroy(self._h)
             self._h = None
 
@@ -277,7 +289,7 @@ def default_context() -> Context:
 
 
 class DeviceMatrix:
-    """Device-resident packed matrix (32-row stride), owned by the library."""
+    """Device-resident packed matrix (stride: rows rounded up to 128 words), owned by the library."""
 
     def __init__(self, n_rows: int, n_cols: int, ctx: Context | None = None):
         self.ctx = ctx or default_context()
@@ -286,6 +298,7 @@ class DeviceMatrix:
         _lib.check(lib.f2gpu_mat_alloc(self.ctx.handle, int(n_rows), int(n_cols), C.byref(h)),
                    "mat_alloc")
         self._h = h
+        self.ctx._mats.add(self)
         self.n, self.m = int(n_rows), int(n_cols)
         r, c, s = C.c_size_t(), C.c_size_t(), C.c_size_t()
         lib.f2gpu_mat_shape(h, C.byref(r), C.byref(c), C.byref(s))
@@ -300,6 +313,7 @@ class DeviceMatrix:
         """Wrap a matrix handle the library allocated (e.g. f2gpu_null_space's basis)."""
         d = cls.__new__(cls)
         d.ctx, d._h = ctx, h
+        ctx._mats.add(d)
         r, c, st = C.c_size_t(), C.c_size_t(), C.c_size_t()
         _lib.load().f2gpu_mat_shape(h, C.byref(r), C.byref(c), C.byref(st))
         d.n, d.m, d.stride = int(r.value), int(c.value), int(st.value)
@@ -427,7 +441,19 @@ def mult_acc(c_mat: DeviceMatrix, c_row0: int, c_wcol0: int, a_words, tables: M4
     CUDA tensor of dtype int64/uint64."""
     ctx = c_mat.ctx
     lib = _lib.load()
-    if hasattr(a_words, "data_ptr"):
+    if hasattr(a_words, "data_ptr"):  # a torch tensor: validated, then ordered after its producer
+        import torch
+
+        if not a_words.is_cuda or a_words.device.index != ctx.device:
+            raise ValueError(f"mult_acc: a_words must be a CUDA tensor on device {ctx.device}")
+        if a_words.element_size() != 8 or a_words.is_floating_point() or a_words.is_complex():
+            raise ValueError("mult_acc: a_words must be a 64-bit integer tensor")
+        if not a_words.is_contiguous() or a_words.dim() != 1:
+            raise ValueError("mult_acc: a_words must be a contiguous 1-D tensor")
+        producer = torch.cuda.current_stream(a_words.device)
+        if ctx.stream is None or int(ctx.stream) != producer.cuda_stream:
+            # the library runs on another stream: finish the torch work that writes a_words
+            producer.synchronize()
         ptr, n_rows, keep = a_words.data_ptr(), a_words.numel(), None
     else:
         host = np.ascontiguousarray(a_words, dtype=np.uint64)
@@ -476,7 +502,8 @@ def decompose_recursive(a, min_cols: int = 0, ctx: Context | None = None) -> LUF
     half recursively, right half brought up to date by a block TRSM and one
     Strassen-Winograd GEMM (A' = D + L21 L11^-1 C), then recursion.  Exact
     arithmetic with 64-aligned splits: the factors equal decompose_block's
-    bit-for-bit.  min_cols = 0 picks the device default (8192 columns per leaf)."""
+    bit-for-bit.  min_cols = 0 picks the device default (leaves of at most 256 panels =
+    16384 columns; 128 panels once a leaf has >= 20000 rows below it)."""
     ctx = ctx or (a.ctx if isinstance(a, DeviceMatrix) else default_context())
     host = a.download() if isinstance(a, DeviceMatrix) else a
     n, m = host.rows(), host.cols()

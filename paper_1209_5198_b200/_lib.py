@@ -15,6 +15,7 @@ from pathlib import Path
 LIB_PATH = Path(__file__).resolve().parent / "libf2gpu.so"
 
 OK, EINVAL, ERANGE, ECUDA, ENCCL, ENOMEM = range(6)
+OWN_STREAM = (1 << 64) - 1  # F2GPU_OWN_STREAM (include/f2gpu.h)
 
 
 class F2GpuError(RuntimeError):
@@ -29,7 +30,7 @@ SYMBOLS = [
     "f2gpu_mat_alloc", "f2gpu_mat_free", "f2gpu_mat_shape", "f2gpu_mat_device_ptr",
     "f2gpu_mat_zero", "f2gpu_mat_upload", "f2gpu_mat_download", "f2gpu_mat_random_dense",
     "f2gpu_mat_copy", "f2gpu_mat_select_wcols", "f2gpu_mat_xor", "f2gpu_mat_transpose",
-    "f2gpu_m4rm_mult", "f2gpu_m4rm_mult_acc", "f2gpu_mult_acc", "f2gpu_strassen_mult",
+    "f2gpu_m4rm_mult", "f2gpu_m4rm_mult_acc", "f2gpu_mult_acc", "f2gpu_mult_acc_host", "f2gpu_strassen_mult",
     "f2gpu_gemm_tc",
     "f2gpu_update_tc", "f2gpu_panel_build_z", "f2gpu_trace_enable", "f2gpu_trace_read",
     "f2gpu_decompose_block", "f2gpu_decompose_recursive", "f2gpu_decompose_block_sharded",
@@ -71,6 +72,7 @@ _SIG = {
     "f2gpu_m4rm_mult": ([vp, vp, vp, vp, C.c_uint], C.c_int),
     "f2gpu_m4rm_mult_acc": ([vp, vp, vp, vp], C.c_int),
     "f2gpu_mult_acc": ([vp, vp, sz, sz, sz, vp, sz, sz, vp, sz, sz], C.c_int),
+    "f2gpu_mult_acc_host": ([vp, vp, sz, sz, sz, sz, sz, vp, sz, vp, sz, sz, sz, sz, sz, sz, sz], C.c_int),
     "f2gpu_strassen_mult": ([vp, vp, vp, vp, sz], C.c_int),
     "f2gpu_gemm_tc": ([vp, vp, vp, vp, C.c_int], C.c_int),
     "f2gpu_update_tc": ([vp, vp, sz, sz, sz, sz, vp, sz, sz, vp], C.c_int),

@@ -182,6 +182,7 @@ struct f2gpu_ctx {
     GraphCache graph;
     LeafGraphs leaf_graphs;
     bool use_graphs = true;
+    bool graphs_stream_ok = true;  // false on the legacy / per-thread default stream (no capture)
     bool lookahead = true;
     bool lookahead_col = true;  // F2GPU_LOOKAHEAD_COL=0: release from the update's column group 0 instead
     bool fuse_post = true;      // F2GPU_POSTCOL=0: separate POST and next-column kernels
@@ -976,7 +977,7 @@ int rec_leaf(RecRun& r, size_t c0, size_t c1) {
     Shard& s = *r.s;
     F2_TRY(ensure_cols(r, c1));
     const size_t sw = std::min(r.frontier, r.mu);
-    if (!c->use_graphs || c->tl.on) return enqueue_panels(c, s, r.n, r.mu, c0, c1, r.la, sw);
+    if (!c->use_graphs || !c->graphs_stream_ok || c->tl.on) return enqueue_panels(c, s, r.n, r.mu, c0, c1, r.la, sw);
     const std::array<uintptr_t, 8> key{uintptr_t(s.w.p), s.w.stride, r.n, r.mu, c0, c1,
                                        uintptr_t(s.st) ^ (r.la ? 1u : 0u), sw};
     LeafGraph& g = c->leaf_graphs.m[key];
@@ -1139,7 +1140,7 @@ int decompose_single(f2gpu_ctx* c, View w, uint32_t* perm, uint32_t* rj, size_t*
     Shard s;
     s.w = w; s.lw = mu; s.st = static_cast<f2::PanelState*>(c->scr_st); s.perm = c->scr_perm;
     GraphCache& g = c->graph;
-    const bool graphs = c->use_graphs && !c->tl.on;
+    const bool graphs = c->use_graphs && c->graphs_stream_ok && !c->tl.on;
     if (graphs && g.match(w.p, w.stride, n, mu, s.st) && g.exec) {
         CUDA_TRY(cudaGraphLaunch(g.exec, c->stream));
         c->launches += g.nodes;
@@ -1376,7 +1377,13 @@ int f2gpu_ctx_destroy(f2gpu_ctx* c) {
 
 int f2gpu_ctx_set_stream(f2gpu_ctx* c, void* s) {
     if (!c) return set_err(F2GPU_EINVAL, "null ctx");
-    c->stream = s ? static_cast<cudaStream_t>(s) : c->own_stream;
+    // F2GPU_OWN_STREAM selects the context's own stream; any other value is a CUDA
+    // stream handle, including 0 / cudaStreamLegacy / cudaStreamPerThread (torch's
+    // default stream is handle 0).  Stream capture is illegal on those, so the
+    // CUDA-graph replay is off while one of them is selected.
+    c->stream = s == F2GPU_OWN_STREAM ? c->own_stream : static_cast<cudaStream_t>(s);
+    c->graphs_stream_ok = !(c->stream == nullptr || c->stream == cudaStreamLegacy ||
+                            c->stream == cudaStreamPerThread);
     return F2GPU_OK;
 }
 
@@ -1586,6 +1593,13 @@ int f2gpu_mat_transpose(f2gpu_ctx* c, const f2gpu_mat* a, f2gpu_mat* out) {
 }
 
 // ---- products ----
+namespace {
+struct MatGuard {
+    f2gpu_mat* m = nullptr;
+    ~MatGuard() { f2gpu_mat_free(m); }
+};
+}  // namespace
+
 int f2gpu_m4rm_mult_acc(f2gpu_ctx* c, const f2gpu_mat* a, const f2gpu_mat* b, f2gpu_mat* cm) {
     if (!c || !a || !b || !cm) return set_err(F2GPU_EINVAL, "null argument");
     if (a->cols != b->rows) return set_err(F2GPU_EINVAL, "m4rm_mult: shape mismatch");  // m4rm.hpp:181
@@ -1689,6 +1703,44 @@ int f2gpu_mult_acc(f2gpu_ctx* c, f2gpu_mat* cm, size_t c_row0, size_t c_wcol0, s
     u.B = b->d; u.sb = b->stride; u.b_row0 = b_row0; u.b_wcol0 = b_wcol0;
     u.st = nullptr;
     return check_launch(c, f2::launch_update(u, c->num_sms, c->stream), "k_update");
+}
+
+// mult_acc over build_tables on HOST matrices in the reference layout: the
+// destination block, the driving words and the B block are staged on the device,
+// the fused table-build + XOR kernel runs, the destination block comes back.
+// Validation and error codes follow m4rm.hpp:97-100 (build_tables) and :144-145
+// (mult_acc).  Bits of a driving word at or above k_bits are ignored, as the
+// reference's table lookups never read them.
+int f2gpu_mult_acc_host(f2gpu_ctx* c, uint64_t* ch, size_t c_rows, size_t c_cols, size_t c_stride, size_t c_row0,
+                        size_t c_wcol0, const uint64_t* a_words, size_t n_rows, const uint64_t* bh, size_t b_rows,
+                        size_t b_cols, size_t b_stride, size_t b_row0, size_t k_bits, size_t b_wcol0,
+                        size_t n_wcols) {
+    if (!c) return set_err(F2GPU_EINVAL, "null ctx");
+    if (k_bits > 64) return set_err(F2GPU_EINVAL, "build_tables: block taller than a word");  // m4rm.hpp:97-98
+    if (b_row0 + k_bits > b_rows || b_wcol0 + n_wcols > ceil64(b_cols))
+        return set_err(F2GPU_ERANGE, "build_tables: block outside B");  // m4rm.hpp:99-100
+    if (c_row0 + n_rows > c_rows || c_wcol0 + n_wcols > ceil64(c_cols))
+        return set_err(F2GPU_ERANGE, "mult_acc: destination outside C");  // m4rm.hpp:144-145
+    if (n_rows == 0 || n_wcols == 0 || k_bits == 0) return F2GPU_OK;
+    if (!ch || !a_words || !bh) return set_err(F2GPU_EINVAL, "mult_acc_host: null buffer");
+    if (c_stride < c_rows || b_stride < b_rows) return set_err(F2GPU_EINVAL, "mult_acc_host: stride < rows");
+    MatGuard Cd, Bd, Ad;
+    F2_TRY(f2gpu_mat_alloc(c, n_rows, n_wcols * 64, &Cd.m));
+    F2_TRY(f2gpu_mat_alloc(c, k_bits, n_wcols * 64, &Bd.m));
+    F2_TRY(f2gpu_mat_alloc(c, n_rows, 64, &Ad.m));
+    std::vector<uint64_t> a(a_words, a_words + n_rows);
+    if (k_bits < 64)
+        for (auto& x : a) x &= (uint64_t(1) << k_bits) - 1;
+    CUDA_TRY(cudaMemcpy2DAsync(Cd.m->d, Cd.m->stride * 8, ch + c_wcol0 * c_stride + c_row0, c_stride * 8, n_rows * 8,
+                               n_wcols, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaMemcpy2DAsync(Bd.m->d, Bd.m->stride * 8, bh + b_wcol0 * b_stride + b_row0, b_stride * 8, k_bits * 8,
+                               n_wcols, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(Ad.m->d, a.data(), n_rows * 8, cudaMemcpyHostToDevice, c->stream));
+    F2_TRY(f2gpu_mult_acc(c, Cd.m, 0, 0, n_wcols, Ad.m->d, n_rows, k_bits, Bd.m, 0, 0));
+    CUDA_TRY(cudaMemcpy2DAsync(ch + c_wcol0 * c_stride + c_row0, c_stride * 8, Cd.m->d, Cd.m->stride * 8, n_rows * 8,
+                               n_wcols, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));  // `a` is a local; the caller's C is final on return
+    return F2GPU_OK;
 }
 
 int f2gpu_strassen_mult(f2gpu_ctx* c, const f2gpu_mat* a, const f2gpu_mat* b, f2gpu_mat* cm,
@@ -1856,12 +1908,6 @@ int f2gpu_solve(f2gpu_ctx* c, const f2gpu_mat* a, const uint64_t* rhs, uint64_t*
 }
 
 // ---- host-buffer entry points ----
-namespace {
-struct MatGuard {
-    f2gpu_mat* m = nullptr;
-    ~MatGuard() { f2gpu_mat_free(m); }
-};
-}  // namespace
 
 int f2gpu_m4rm_mult_host(f2gpu_ctx* c, const uint64_t* a, size_t n, size_t k, size_t sa,
                          const uint64_t* b, size_t m, size_t sb, uint64_t* out, size_t sc,

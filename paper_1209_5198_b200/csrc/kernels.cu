@@ -27,6 +27,28 @@ __device__ unsigned long long* g_trace = nullptr;
 __device__ uint32_t g_trace_cap = 0;
 __device__ uint32_t g_trace_n = 0;
 
+// Cross-kernel waits (lookahead counters, release flags) are bounded: the fused
+// schedule relies on its kernels being co-resident, which the CUDA model does not
+// guarantee when other work holds the SMs (another stream, an MPS client).  A
+// wait that exceeds kSpinLimitNs traps, so the call fails with a CUDA error
+// instead of hanging the device.  Legitimate waits last microseconds.
+constexpr uint64_t kSpinLimitNs = 20ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+struct SpinGuard {
+    uint64_t t0 = 0;
+    uint32_t polls = 0;
+    __device__ __forceinline__ void tick() {
+        if ((++polls & 1023u) != 0) return;
+        const uint64_t now = gtimer();
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > kSpinLimitNs) __trap();
+    }
+};
+
 __device__ __forceinline__ void trace_ev(uint32_t ev, int j) {
     unsigned long long* b = g_trace;
     if (!b) return;
@@ -1424,10 +1446,12 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
         // lookahead: the previous panel's update releases this column early
         if (tid == 0) {
             uint32_t v;
+            SpinGuard g;
             while (true) {
                 asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(wait_flag) : "memory");
                 if (v >= wait_count) break;
                 __nanosleep(64);
+                g.tick();
             }
         }
         __syncthreads();
@@ -1789,10 +1813,12 @@ struct GjStep {
 __device__ __forceinline__ void wait_count_ge(const uint32_t* flag, uint32_t count) {
     if (!flag) return;
     uint32_t v;
+    SpinGuard g;
     while (true) {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
         if (v >= count) break;
         __nanosleep(32);
+        g.tick();
     }
 }
 
@@ -1800,11 +1826,13 @@ __device__ __forceinline__ void wait_count_ge(const uint32_t* flag, uint32_t cou
 // long spin can stay split afterwards and run every later shuffle twice)
 __device__ __forceinline__ void wait_count_ge_warp(const uint32_t* flag, uint32_t count) {
     if (!flag) return;
+    SpinGuard g;
     while (true) {
         uint32_t v;
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
         if (__all_sync(0xffffffffu, v >= count)) break;
         __nanosleep(32);
+        g.tick();
     }
 }
 
@@ -2602,11 +2630,13 @@ __global__ void __launch_bounds__(256) k_post_col(uint64_t* __restrict__ w, size
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (wait_panel) {  // queued ahead: the panel kernel's writes are complete
         if (threadIdx.x < 32) {
+            SpinGuard g;
             while (true) {
                 uint32_t v;
                 asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(wait_panel) : "memory");
                 if (__all_sync(0xffffffffu, v != 0)) break;
                 __nanosleep(128);
+                g.tick();
             }
         }
         __syncthreads();

@@ -1,7 +1,7 @@
 // kernels.cuh — sm_100a kernels of the GF(2) block decomposition hot path.
 //
 // Layout (reference bit_matrix.hpp:74-81): word (i,q) at p[q*stride + i],
-// bit k = entry (i, 64q+k).  Device strides are multiples of 32 words so every
+// bit k = entry (i, 64q+k).  Device strides are multiples of 128 words (api.cu dev_stride), so every
 // 16-row unit is 128-byte aligned (LDG/STG.256 friendly).
 #pragma once
 #include <cstddef>

@@ -98,14 +98,16 @@ def test_host_api_validation_without_gpu():
     assert f2.BitMatrix.identity(70).padding_is_zero()
 
 
-def test_cpp_shim_compiles_against_reference():
-    """include/f2la_gpu.hpp (the drop-in C++ shim) compiles against the reference
-    headers and links against libf2gpu.so."""
+@pytest.mark.parametrize("name", ["shim_example", "dropin_example"])
+def test_cpp_shim_compiles_against_reference(name):
+    """include/f2la_gpu.hpp (the C++ shim) and include/f2la_gpu_dropin.hpp (the
+    opt-in drop-in for the reference's own f2la:: call sites) compile against the
+    reference headers and link against libf2gpu.so."""
     ref = Path("/root/reference/proj/include")
     if not ref.is_dir():
         pytest.skip("reference headers not present")
-    src = ROOT / "tests" / "cpp" / "shim_example.cpp"
-    out = ROOT / "tests" / "cpp" / "shim_example.bin"  # travels to the GPU box (git-ignored)
+    src = ROOT / "tests" / "cpp" / f"{name}.cpp"
+    out = ROOT / "tests" / "cpp" / f"{name}.bin"  # travels to the GPU box (git-ignored)
     from paper_1209_5198_b200 import _lib
 
     _lib.load()
