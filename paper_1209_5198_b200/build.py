@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libf2gpu.so"
-SOURCES = [CSRC / "kernels.cu", CSRC / "tc_leaf.cu", CSRC / "tc_update.cu", CSRC / "api.cu"]
+SOURCES = [CSRC / "kernels.cu", CSRC / "tc_leaf.cu", CSRC / "tc_pair.cu", CSRC / "tc_update.cu", CSRC / "api.cu"]
 HEADERS = [CSRC / "kernels.cuh", CSRC / "tc_common.cuh", ROOT / "include" / "f2gpu.h"]
 
 NVCC_FLAGS = [

@@ -199,6 +199,12 @@ struct TcGemmArgs {
 cudaError_t launch_gemm_tc3_batched(const TcGemmArgs* h_probs, const TcGemmArgs* d_probs, int nprob,
                                     cudaStream_t s);
 bool gemm_tc3_ok(size_t n, size_t k, size_t m);
+// k_gemm_tc7 (tc_pair.cu): the same product on CTA pairs, persistent, M-side operand
+// in TMEM; m % 256 == 0.  F2GPU_TC7=0 disables it (A/B checks).
+bool gemm_tc7_enabled();
+cudaError_t launch_gemm_tc7(const TcGemmArgs& p, cudaStream_t s);
+cudaError_t launch_gemm_tc7_batched(const TcGemmArgs* h_probs, const TcGemmArgs* d_probs, int nprob,
+                                    cudaStream_t s);
 cudaError_t launch_gemm_tc3(const uint64_t* A, size_t sa, size_t n, const uint64_t* BT, size_t sbt,
                             uint64_t* C, size_t sc, size_t k, size_t m, bool acc, cudaStream_t s);
 

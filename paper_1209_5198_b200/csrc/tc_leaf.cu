@@ -1563,6 +1563,7 @@ cudaError_t launch_gemm_tc3(const uint64_t* A, size_t sa, size_t n, const uint64
     if (!fn) return cudaErrorInvalidValue;
     const TcGemmArgs p{A, sa, n, BT, sbt, C, sc, k, m, acc ? 1 : 0};
     if (!tc3_args_ok(p)) return cudaErrorInvalidValue;
+    if (gemm_tc7_enabled()) return launch_gemm_tc7(p, s);
     if (tc4_use(m)) {
         dim3 grid4(unsigned(2 * (m / kT4Cols)), unsigned((n + kT4Rows - 1) / kT4Rows));
         k_gemm_tc4<<<grid4, kT4Threads, kT4Smem, s>>>(p, nullptr);
@@ -1597,6 +1598,7 @@ cudaError_t launch_gemm_tc3_batched(const TcGemmArgs* h_probs, const TcGemmArgs*
         mx = std::max(mx, h_probs[i].m);
         nx = std::max(nx, h_probs[i].n);
     }
+    if (gemm_tc7_enabled()) return launch_gemm_tc7_batched(h_probs, d_probs, nprob, s);
     bool all4 = true;
     for (int i = 0; i < nprob; ++i) all4 = all4 && tc4_use(h_probs[i].m);
     if (all4) {
