@@ -152,6 +152,18 @@ def digest_words(w: np.ndarray, n: int, m: int) -> int:
     return s
 
 
+def digest_cols(w: np.ndarray, n: int, cols: list[int]) -> int:
+    """The digest's sum over the listed global word-columns only (w[l] = column
+    cols[l]); the full digest is the base term plus the partial sums of every rank."""
+    s = 0
+    with np.errstate(over="ignore"):
+        salt_i = np.arange(n, dtype=np.uint64) * np.uint64(0xD6E8FEB86659FD93)
+        for l, q in enumerate(cols):
+            salt = np.uint64(_mix64_int(q + 0x1234567))
+            s = (s + int(_mix64(w[l, :n] ^ salt_i ^ salt).sum(dtype=np.uint64))) & M64
+    return s
+
+
 def digest_u32(v: np.ndarray) -> int:
     v = np.ascontiguousarray(v, dtype=np.uint32)
     with np.errstate(over="ignore"):
@@ -167,7 +179,8 @@ def golden(key: str) -> dict | None:
         return None
 
 
-def decomp_parity(cfg: dict, w: np.ndarray | None, perm: np.ndarray, rj: np.ndarray, rank: int) -> dict:
+def decomp_parity(cfg: dict, w: np.ndarray | None, perm: np.ndarray, rj: np.ndarray, rank: int,
+                  w_digest: int | None = None) -> dict:
     key, g = None, None
     for k in ("cfg4", "cfg1"):
         e = golden(k)
@@ -182,10 +195,12 @@ def decomp_parity(cfg: dict, w: np.ndarray | None, perm: np.ndarray, rj: np.ndar
         bad.append("r_j digest")
     if digest_u32(perm) != g["perm_digest"]:
         bad.append("perm digest")
-    if w is not None and digest_words(w, cfg["n"], cfg["m"]) != g["w_digest"]:
+    if w is not None and w_digest is None:
+        w_digest = digest_words(w, cfg["n"], cfg["m"])
+    if w_digest is not None and w_digest != g["w_digest"]:
         bad.append("W digest")
     return {"status": "ok" if not bad else "MISMATCH: " + ", ".join(bad),
-            "checked": "rank, r_j, perm" + (", W" if w is not None else "") +
+            "checked": "rank, r_j, perm" + (", W" if w_digest is not None else "") +
                        f" of the last timed step vs tests/golden/digests.json {key} (oracle/_ref)"}
 
 
@@ -280,6 +295,21 @@ def gemm_cpu_baseline(n: int, reps: int = 3) -> dict:
 
 
 # ---------------------------------------------------------------------------
+class StdoutToStderr:
+    """File-descriptor level: NCCL prints its version banner on stdout when a
+    communicator is created; rank 0's stdout must carry only the JSON line."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -339,7 +369,8 @@ def cfg_json(cfg, gpus, variant="block"):
             "n": n, "m": m, "density": cfg["p"], "seed": cfg["seed"],
             "word_bits": 64, "tables": "9 groups (7x8+8 bits), 16 word-cols/CTA",
             "parallelism": f"column-round-robin x{gpus}" if gpus > 1 else "single GPU",
-            "variant": VARIANTS[variant] if gpus == 1 else VARIANTS["block"],
+            "variant": VARIANTS[variant] + (f"; word-columns round-robin over {gpus} GPUs (f2gpu_decompose_{variant}_dist)"
+                                            if gpus > 1 else ""),
             "l2": (f"inputs ({mib:.0f} MiB) larger than L2 (126 MB); no flush needed" if mib > 126
                    else f"inputs ({mib:.0f} MiB) fit in L2: warm-cache timing")}
 
@@ -355,6 +386,8 @@ def main() -> None:
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-gemm", action="store_true", help="skip the cfg2 16384^2 products")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="one GPU through the distributed (NCCL) drivers with a 1-rank communicator")
     ap.add_argument("--variant", default="recursive", choices=["block", "recursive"],
                     help="decompose_recursive (default, fastest) or decompose_block; bit-identical factors")
     ap.add_argument("--min-cols", type=int, default=0, help="recursive leaf width in bits (0 = default)")
@@ -381,10 +414,18 @@ def main() -> None:
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
-    if world > 1:
-        obj = [f2.Context.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        ctx.init_comm(rank, world, obj[0])
+    # the distributed drivers (f2gpu_decompose_*_dist over NCCL): N > 1, or on one
+    # GPU with --force-dist (a 1-rank communicator: checks this code path)
+    dpath = world > 1 or args.force_dist
+    with StdoutToStderr():
+        if world > 1:
+            obj = [f2.Context.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            ctx.init_comm(rank, world, obj[0])
+            dist.barrier()
+        elif args.force_dist:
+            os.environ["F2GPU_FORCE_NCCL"] = "1"
+            ctx.init_comm(0, 1, f2.Context.nccl_unique_id())
 
     n, m = cfg["n"], cfg["m"]
     mu = (m + 63) // 64
@@ -403,7 +444,10 @@ def main() -> None:
 
     def step():
         _lib.check(lib.f2gpu_mat_copy(ctx.handle, W.handle, A.handle))
-        if world > 1:
+        if dpath and args.variant == "recursive":
+            _lib.check(lib.f2gpu_decompose_recursive_dist(ctx.handle, W.handle, m, args.min_cols, perm.ctypes.data,
+                                                          rj.ctypes.data, C.byref(rk)))
+        elif dpath:
             _lib.check(lib.f2gpu_decompose_block_dist(ctx.handle, W.handle, m, perm.ctypes.data,
                                                       rj.ctypes.data, C.byref(rk)))
         elif args.variant == "recursive":
@@ -442,24 +486,31 @@ def main() -> None:
     rank_found = int(rk.value)
 
     # ---- parity of the benchmarked (graph-replayed) run ----
-    w_host = None
-    if world == 1:
-        w_host = np.zeros((mu, (n + 7) // 8 * 8), np.uint64)
+    # every rank digests its own word-columns; the partial sums add up (mod 2^64)
+    lcols = list(range(rank, mu, world))
+    w_host = np.zeros((max(1, len(lcols)), (n + 7) // 8 * 8), np.uint64)
+    if lcols:
         _lib.check(lib.f2gpu_mat_download(ctx.handle, W.handle, C.c_void_p(w_host.ctypes.data), w_host.shape[1]))
-    parity = decomp_parity(cfg, w_host, perm, rj, rank_found) if rank == 0 else None
+    part = digest_cols(w_host, n, lcols)
+    if dist:
+        t = torch.tensor([part - (1 << 64) if part >= (1 << 63) else part], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t)
+        part = int(t.item()) & M64
+    w_dig = (_mix64_int((n * 0x9E3779B97F4A7C15) ^ m) + part) & M64
+    parity = decomp_parity(cfg, None, perm, rj, rank_found, w_digest=w_dig) if rank == 0 else None
     del w_host
 
     # ---- roofline: the dominant kernel, measured live (north-star unit) ----
     roof = roof_tc = None
     if rank == 0:
         roof = measure_update_roofline(f2, lib, _lib, ctx, stream, torch, n)
-        if args.variant == "recursive" and world == 1:
+        if args.variant == "recursive":
             roof_tc = measure_tensor_roofline(f2, lib, _lib, ctx, stream, torch)
 
     # ---- e2e through the C-ABI host entry point (pinned host buffers) ----
     e2e = None
     if not args.no_e2e:
-        e2e = measure_e2e(f2, lib, _lib, ctx, torch, A, n, m, mu, world, rank, dist,
+        e2e = measure_e2e(f2, lib, _lib, ctx, torch, A, n, m, mu, world, rank, dist, dpath,
                           steps=min(args.steps, 3), variant=args.variant, min_cols=args.min_cols,
                           warmup=args.warmup, cfg=cfg)
 
@@ -586,7 +637,7 @@ def measure_tensor_roofline(f2, lib, _lib, ctx, stream, torch, n: int = 16384) -
             "peak_source": src}
 
 
-def measure_e2e(f2, lib, _lib, ctx, torch, A, n, m, mu, world, rank, dist, steps: int,
+def measure_e2e(f2, lib, _lib, ctx, torch, A, n, m, mu, world, rank, dist, dpath, steps: int,
                 variant: str = "block", min_cols: int = 0, warmup: int = 3, cfg: dict | None = None) -> dict:
     """Same metric through the public C-ABI host entry point with host buffers:
     H2D of A (pinned) + decomposition + D2H of W, perm, r_j inside the region."""
@@ -603,11 +654,15 @@ def measure_e2e(f2, lib, _lib, ctx, torch, A, n, m, mu, world, rank, dist, steps
     rk = C.c_size_t()
 
     def one():
-        if world > 1:
+        if dpath:
             Wd = f2.DeviceMatrix(n, lw * 64, ctx)
             Wd.upload_words(hA, host_stride)
-            _lib.check(lib.f2gpu_decompose_block_dist(ctx.handle, Wd.handle, m, perm.ctypes.data,
-                                                      rj.ctypes.data, C.byref(rk)))
+            if variant == "recursive":
+                _lib.check(lib.f2gpu_decompose_recursive_dist(ctx.handle, Wd.handle, m, min_cols, perm.ctypes.data,
+                                                              rj.ctypes.data, C.byref(rk)))
+            else:
+                _lib.check(lib.f2gpu_decompose_block_dist(ctx.handle, Wd.handle, m, perm.ctypes.data,
+                                                          rj.ctypes.data, C.byref(rk)))
             _lib.check(lib.f2gpu_mat_download(ctx.handle, Wd.handle, C.c_void_p(hW.ctypes.data),
                                               host_stride))
             Wd.free()
@@ -639,14 +694,14 @@ def measure_e2e(f2, lib, _lib, ctx, torch, A, n, m, mu, world, rank, dist, steps
         dt = float(t.item())
     hbytes = lw * host_stride * 8
     parity = None
-    if world == 1 and cfg is not None:  # the host output of the last timed call
+    if world == 1 and not dpath and cfg is not None:  # the host output of the last timed call
         parity = decomp_parity(cfg, hW, perm, rj, int(rk.value))["status"]
     return {"value": round(n * n * min(n, m) / dt / 1e9, 1), "unit": UNIT, "parity": parity,
             "h2d_bytes_per_step": hbytes * world,
             "d2h_bytes_per_step": hbytes * world + 4 * n + 4 * mu,
             "ms_per_step": round(dt * 1e3, 2),
-            "api": (f"f2gpu_decompose_{variant}_host" if world == 1
-                    else "f2gpu_decompose_block_dist + host upload/download")}
+            "api": (f"f2gpu_decompose_{variant}_host" if not dpath
+                    else f"f2gpu_decompose_{variant}_dist + host upload/download")}
 
 
 def measure_gemm_dist(f2, lib, _lib, ctx, stream, torch, rank, world, dist, n: int = 16384) -> dict:

@@ -240,6 +240,44 @@ int f2gpu_decompose_block_dist(f2gpu_ctx *ctx, f2gpu_mat *w_local, size_t n_cols
                                uint32_t *perm, uint32_t *rj, size_t *rank);
 /* number of local word-columns rank `rank` owns out of mu */
 size_t f2gpu_local_wcols(size_t mu, int rank, int world);
+/* decompose_recursive over word-column shards: the same
+ * factors as f2gpu_decompose_recursive.  Per leaf panel the owner factors and
+ * replicates {state, column rows [R_lb, n)} (R_lb = the leaf's first R); per
+ * split the left columns (rows [R0, n)) are replicated once and every rank
+ * solves X = L11^-1 C and forms A' = D ^ L21 X on its OWN right-half columns.
+ * _dist: one rank per GPU over NCCL (w_local as for f2gpu_decompose_block_dist;
+ * world 1 without a communicator = f2gpu_decompose_recursive).  _sharded: the
+ * same schedule over `shards` logical shards on this device (testing). */
+int f2gpu_decompose_recursive_dist(f2gpu_ctx *ctx, f2gpu_mat *w_local, size_t n_cols_global, size_t min_cols,
+                                   uint32_t *perm, uint32_t *rj, size_t *rank);
+int f2gpu_decompose_recursive_sharded(f2gpu_ctx *ctx, f2gpu_mat *w, int shards, size_t min_cols, uint32_t *perm,
+                                      uint32_t *rj, size_t *rank);
+/* The recursion's schedule alone (host code, no device work): calls `ops` in the
+ * order the distributed drivers execute them, for rank-agnostic callbacks
+ * (each callback acts for the calling rank).  Used by the CPU protocol test
+ * (tests/test_dist_gloo.py) to run the library's own plan over gloo.
+ *   panel(j, owner, row_lo):  owner factors panel j; state j and the panel
+ *                             column rows [row_lo, n) become replicated
+ *   apply(j, owner, lo, hi):  non-owners apply panel j's row swaps to all their
+ *                             columns; every rank updates its columns in [lo, hi)
+ *   state(j, *R, *r):         replicated R_j, r_j
+ *   gather(c0, cm, row_lo):   replicate columns [c0, cm), rows [row_lo, n)
+ *   solve(c0, cm, R0, lo, hi): X = L11^-1 C on own columns in [lo, hi)
+ *   product(c0, cm, R0, R1, lo, hi): rows [R1, n) of own columns ^= L21 X
+ *   rank_update(c0, cm, lo, hi): panels [c0, cm) as rank-r_j updates (not full rank)
+ * A non-zero callback return aborts the schedule with that code. */
+typedef struct f2gpu_dist_ops {
+    void *user;
+    int (*panel)(void *user, size_t j, int owner, size_t row_lo);
+    int (*apply)(void *user, size_t j, int owner, size_t col_lo, size_t col_hi);
+    int (*state)(void *user, size_t j, size_t *R, size_t *r);
+    int (*gather)(void *user, size_t c0, size_t cm, size_t row_lo);
+    int (*solve)(void *user, size_t c0, size_t cm, size_t R0, size_t col_lo, size_t col_hi);
+    int (*product)(void *user, size_t c0, size_t cm, size_t R0, size_t R1, size_t col_lo, size_t col_hi);
+    int (*rank_update)(void *user, size_t c0, size_t cm, size_t col_lo, size_t col_hi);
+} f2gpu_dist_ops;
+int f2gpu_dist_schedule(size_t n_rows, size_t mu, int world, size_t leaf_panels, size_t tall_rows,
+                        size_t tall_leaf_panels, const f2gpu_dist_ops *ops);
 /* NCCL broadcast of a whole device matrix from `root` (no-op at world 1). */
 int f2gpu_mat_broadcast(f2gpu_ctx *ctx, f2gpu_mat *m, int root);
 /* Multiply sharded by column blocks (BASELINE configs[1] on G GPUs):

@@ -39,6 +39,7 @@ SYMBOLS = [
     "f2gpu_decompose_recursive_host", "f2gpu_null_space", "f2gpu_solve",
     "f2gpu_rank_host",
     "f2gpu_nccl_unique_id", "f2gpu_ctx_init_comm", "f2gpu_decompose_block_dist",
+    "f2gpu_decompose_recursive_dist", "f2gpu_decompose_recursive_sharded", "f2gpu_dist_schedule",
     "f2gpu_local_wcols", "f2gpu_mat_broadcast", "f2gpu_strassen_mult_dist",
 ]
 
@@ -94,9 +95,29 @@ _SIG = {
     "f2gpu_ctx_init_comm": ([vp, C.c_int, C.c_int, vp], C.c_int),
     "f2gpu_decompose_block_dist": ([vp, vp, sz, vp, vp, C.POINTER(sz)], C.c_int),
     "f2gpu_local_wcols": ([sz, C.c_int, C.c_int], sz),
+    "f2gpu_decompose_recursive_dist": ([vp, vp, sz, sz, vp, vp, C.POINTER(sz)], C.c_int),
+    "f2gpu_decompose_recursive_sharded": ([vp, vp, C.c_int, sz, vp, vp, C.POINTER(sz)], C.c_int),
     "f2gpu_mat_broadcast": ([vp, vp, C.c_int], C.c_int),
     "f2gpu_strassen_mult_dist": ([vp, vp, vp, vp, sz], C.c_int),
 }
+
+# f2gpu_dist_ops (include/f2gpu.h): the distributed recursion's callbacks
+PANEL_FN = C.CFUNCTYPE(C.c_int, vp, sz, C.c_int, sz)
+APPLY_FN = C.CFUNCTYPE(C.c_int, vp, sz, C.c_int, sz, sz)
+STATE_FN = C.CFUNCTYPE(C.c_int, vp, sz, C.POINTER(sz), C.POINTER(sz))
+GATHER_FN = C.CFUNCTYPE(C.c_int, vp, sz, sz, sz)
+SOLVE_FN = C.CFUNCTYPE(C.c_int, vp, sz, sz, sz, sz, sz)
+PRODUCT_FN = C.CFUNCTYPE(C.c_int, vp, sz, sz, sz, sz, sz, sz)
+RANKUPD_FN = C.CFUNCTYPE(C.c_int, vp, sz, sz, sz, sz)
+
+
+class DistOps(C.Structure):
+    _fields_ = [("user", vp), ("panel", PANEL_FN), ("apply", APPLY_FN), ("state", STATE_FN),
+                ("gather", GATHER_FN), ("solve", SOLVE_FN), ("product", PRODUCT_FN),
+                ("rank_update", RANKUPD_FN)]
+
+
+_SIG["f2gpu_dist_schedule"] = ([sz, sz, C.c_int, sz, sz, sz, C.POINTER(DistOps)], C.c_int)
 
 _lib = None
 

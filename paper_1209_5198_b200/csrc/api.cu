@@ -61,6 +61,8 @@ struct NcclApi {
     void* commInitRankSym = nullptr;
     int (*broadcast)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
     int (*commDestroy)(void*) = nullptr;
+    int (*groupStart)() = nullptr;
+    int (*groupEnd)() = nullptr;
     const char* (*getErrorString)(int) = nullptr;
     bool ok = false;
     std::string why;
@@ -85,8 +87,11 @@ NcclApi& nccl() {
         api.broadcast = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(
             api.h, "ncclBroadcast");
         api.commDestroy = (int (*)(void*))dlsym(api.h, "ncclCommDestroy");
+        api.groupStart = (int (*)())dlsym(api.h, "ncclGroupStart");
+        api.groupEnd = (int (*)())dlsym(api.h, "ncclGroupEnd");
         api.getErrorString = (const char* (*)(int))dlsym(api.h, "ncclGetErrorString");
-        api.ok = api.getUniqueId && api.commInitRankSym && api.broadcast && api.commDestroy;
+        api.ok = api.getUniqueId && api.commInitRankSym && api.broadcast && api.commDestroy && api.groupStart &&
+                 api.groupEnd;
         if (!api.ok) api.why = "libnccl.so.2 lacks required symbols";
     }
     return api;
@@ -590,6 +595,7 @@ struct Shard {
     f2::PanelState* st = nullptr;  // mu states (device)
     uint32_t* perm = nullptr;    // device perm (replicated)
     uint64_t* bcast = nullptr;   // [PanelState | n words] broadcast landing buffer
+    uint64_t* land = nullptr;    // recursive variant: landing column (stride rows; rows >= row_lo filled)
 };
 
 constexpr size_t kStateBytes = sizeof(f2::PanelState);
@@ -1180,7 +1186,18 @@ struct Exchange {
     virtual ~Exchange() = default;
     virtual int bcast(f2gpu_ctx* c, std::vector<Shard>& sh, int owner_local, int owner_global,
                       size_t n) = 0;
+    // decompose_recursive: replicate panel j's state and its column rows [row_lo, n)
+    // from the owner (local column lj) into every other shard's st[j] / land
+    virtual int panel(f2gpu_ctx* c, std::vector<Shard>& sh, int owner_local, int owner_global, size_t j,
+                      size_t lj, size_t row_lo, size_t n) = 0;
+    // replicate global word-columns [c0, cm), rows [row_lo, n), into Lg (column
+    // q - c0 of Lg holds global column q); shards hold columns round-robin
+    virtual int gather(f2gpu_ctx* c, std::vector<Shard>& sh, int base, int G, size_t c0, size_t cm, size_t row_lo,
+                       size_t n, View Lg) = 0;
 };
+
+// word-columns with global index < q owned by shard g of G (round-robin)
+size_t lidx(int g, int G, size_t q) { return q <= size_t(g) ? 0 : (q - size_t(g) - 1) / size_t(G) + 1; }
 
 struct LocalExchange : Exchange {
     int bcast(f2gpu_ctx* c, std::vector<Shard>& sh, int owner, int, size_t n) override {
@@ -1192,17 +1209,106 @@ struct LocalExchange : Exchange {
         }
         return F2GPU_OK;
     }
+    int panel(f2gpu_ctx* c, std::vector<Shard>& sh, int owner, int, size_t j, size_t lj, size_t row_lo,
+              size_t n) override {
+        const Shard& o = sh[owner];
+        for (size_t g = 0; g < sh.size(); ++g) {
+            if (int(g) == owner) continue;
+            CUDA_TRY(cudaMemcpyAsync(sh[g].st + j, o.st + j, kStateBytes, cudaMemcpyDeviceToDevice, c->stream));
+            if (row_lo < n)
+                CUDA_TRY(cudaMemcpyAsync(sh[g].land + row_lo, o.w.p + lj * o.w.stride + row_lo, (n - row_lo) * 8,
+                                         cudaMemcpyDeviceToDevice, c->stream));
+        }
+        return F2GPU_OK;
+    }
+    int gather(f2gpu_ctx* c, std::vector<Shard>& sh, int base, int G, size_t c0, size_t cm, size_t row_lo,
+               size_t n, View Lg) override {
+        if (row_lo >= n) return F2GPU_OK;
+        for (size_t i = 0; i < sh.size(); ++i) {
+            const int g = base + int(i);
+            const size_t l0 = lidx(g, G, c0), l1 = lidx(g, G, cm);
+            if (l0 >= l1) continue;
+            const size_t q0 = size_t(g) + l0 * size_t(G) - c0;  // Lg column of local column l0
+            CUDA_TRY(cudaMemcpy2DAsync(Lg.p + q0 * Lg.stride + row_lo, size_t(G) * Lg.stride * 8,
+                                       sh[i].w.p + l0 * sh[i].w.stride + row_lo, sh[i].w.stride * 8,
+                                       (n - row_lo) * 8, l1 - l0, cudaMemcpyDeviceToDevice, c->stream));
+        }
+        return F2GPU_OK;
+    }
 };
 
+int nccl_rc(int rc, const char* what) {
+    if (rc == 0) return F2GPU_OK;
+    NcclApi& api = nccl();
+    return set_err(F2GPU_ENCCL, std::string(what) + ": " + (api.getErrorString ? api.getErrorString(rc) : "?"));
+}
+
 struct NcclExchange : Exchange {
+    std::deque<DevBuf> scratch;  // gather staging (grown on demand)
+    void* stage = nullptr;
+    size_t stage_bytes = 0;
     int bcast(f2gpu_ctx* c, std::vector<Shard>& sh, int, int owner_global, size_t n) override {
         NcclApi& api = nccl();
         const size_t bytes = kBcastHdr + n * 8;
-        int rc = api.broadcast(sh[0].bcast, sh[0].bcast, bytes, kNcclUint8, owner_global, c->comm,
-                               c->stream);
-        if (rc != 0)
-            return set_err(F2GPU_ENCCL, std::string("ncclBroadcast: ") +
-                                            (api.getErrorString ? api.getErrorString(rc) : "?"));
+        return nccl_rc(api.broadcast(sh[0].bcast, sh[0].bcast, bytes, kNcclUint8, owner_global, c->comm, c->stream),
+                       "ncclBroadcast");
+    }
+    // one grouped launch: the state (root: its st[j]) and the column rows
+    // [row_lo, n) (root: straight from its W) -- (n - row_lo) * 8 + 1.5 KiB bytes
+    int panel(f2gpu_ctx* c, std::vector<Shard>& sh, int owner_local, int owner_global, size_t j, size_t lj,
+              size_t row_lo, size_t n) override {
+        NcclApi& api = nccl();
+        Shard& s = sh[0];
+        const bool root = owner_local == 0;
+        F2_TRY(nccl_rc(api.groupStart(), "ncclGroupStart"));
+        int rc = api.broadcast(s.st + j, s.st + j, kStateBytes, kNcclUint8, owner_global, c->comm, c->stream);
+        if (rc == 0 && row_lo < n)
+            rc = api.broadcast(root ? static_cast<const void*>(s.w.p + lj * s.w.stride + row_lo)
+                                    : static_cast<const void*>(s.land + row_lo),
+                               s.land + row_lo, (n - row_lo) * 8, kNcclUint8, owner_global, c->comm, c->stream);
+        const int re = api.groupEnd();
+        F2_TRY(nccl_rc(rc, "ncclBroadcast(panel)"));
+        return nccl_rc(re, "ncclGroupEnd");
+    }
+    // every rank broadcasts its packed block of the left columns (G broadcasts in
+    // one group), then scatters the blocks into Lg
+    int gather(f2gpu_ctx* c, std::vector<Shard>& sh, int base, int G, size_t c0, size_t cm, size_t row_lo,
+               size_t n, View Lg) override {
+        if (row_lo >= n) return F2GPU_OK;
+        NcclApi& api = nccl();
+        const size_t rows = n - row_lo;
+        std::vector<size_t> off(size_t(G) + 1, 0);
+        for (int g = 0; g < G; ++g) off[g + 1] = off[g] + (lidx(g, G, cm) - lidx(g, G, c0)) * rows;
+        if (off[G] == 0) return F2GPU_OK;
+        if (stage_bytes < off[G] * 8) {
+            scratch.clear();
+            scratch.emplace_back(c);
+            F2_TRY(scratch.back().alloc(off[G] * 8));
+            stage = scratch.back().p;
+            stage_bytes = off[G] * 8;
+        }
+        uint64_t* st = static_cast<uint64_t*>(stage);
+        const Shard& me = sh[0];
+        const size_t l0 = lidx(base, G, c0), l1 = lidx(base, G, cm);
+        if (l1 > l0)
+            CUDA_TRY(cudaMemcpy2DAsync(st + off[base], rows * 8, me.w.p + l0 * me.w.stride + row_lo, me.w.stride * 8,
+                                       rows * 8, l1 - l0, cudaMemcpyDeviceToDevice, c->stream));
+        F2_TRY(nccl_rc(api.groupStart(), "ncclGroupStart"));
+        int rc = 0;
+        for (int g = 0; g < G && rc == 0; ++g)
+            if (off[g + 1] > off[g])
+                rc = api.broadcast(st + off[g], st + off[g], (off[g + 1] - off[g]) * 8, kNcclUint8, g, c->comm,
+                                   c->stream);
+        const int re = api.groupEnd();
+        F2_TRY(nccl_rc(rc, "ncclBroadcast(gather)"));
+        F2_TRY(nccl_rc(re, "ncclGroupEnd"));
+        for (int g = 0; g < G; ++g) {
+            const size_t a = lidx(g, G, c0), b = lidx(g, G, cm);
+            if (a >= b) continue;
+            const size_t q0 = size_t(g) + a * size_t(G) - c0;
+            CUDA_TRY(cudaMemcpy2DAsync(Lg.p + q0 * Lg.stride + row_lo, size_t(G) * Lg.stride * 8, st + off[g],
+                                       rows * 8, rows * 8, b - a, cudaMemcpyDeviceToDevice, c->stream));
+        }
         return F2GPU_OK;
     }
 };
@@ -1269,7 +1375,222 @@ int alloc_shard_aux(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, std::deque<DevB
     F2_TRY(keep.back().alloc(kBcastHdr + s.w.stride * 8));
     s.bcast = keep.back().as<uint64_t>();
     CUDA_TRY(cudaMemsetAsync(s.bcast, 0, kBcastHdr + s.w.stride * 8, c->stream));
+    keep.emplace_back(c);
+    F2_TRY(keep.back().alloc(s.w.stride * 8));
+    s.land = keep.back().as<uint64_t>();
+    CUDA_TRY(cudaMemsetAsync(s.land, 0, s.w.stride * 8, c->stream));
     return F2GPU_OK;
+}
+
+// ---- decompose_recursive over column shards ----
+// The recursion's control flow is host-only and separate from the work it
+// orders, so the GPU drivers below and the CPU protocol test
+// (tests/test_dist_gloo.py through f2gpu_dist_schedule) run the SAME schedule:
+//   leaf [c0, c1): per panel j, its owner (j mod G) factors it and the state +
+//     column rows [R_lb, n) are replicated (R_lb <= R_j: the leaf's first R,
+//     known on the host); every rank applies the row swaps and the Schur update
+//     to its own columns in (j, c1);
+//   split at cm: left half recursively; R0 / R1 read back; the left columns
+//     rows [R0, n) replicated once (one gather per split); full rank -> every
+//     rank solves X = L11^-1 C on its own right-half columns and forms
+//     A' = D ^ L21 X on them (one product sharded by output word-columns, no
+//     further exchange); otherwise the left panels are applied as rank-r_j
+//     updates; then the right half.
+int dist_schedule(size_t n, size_t mu, int world, size_t base, size_t tall_rows, size_t tall_base,
+                  const f2gpu_dist_ops* o) {
+    std::function<int(size_t, size_t, size_t)> rec = [&](size_t c0, size_t c1, size_t rlb) -> int {
+        const size_t rows0 = n - std::min(n, 64 * c0);
+        const size_t leaf = (tall_rows && rows0 >= tall_rows) ? std::min(base, tall_base) : base;
+        if (c1 - c0 <= leaf) {
+            for (size_t j = c0; j < c1; ++j) {
+                const int owner = int(j % size_t(world));
+                F2_TRY(o->panel(o->user, j, owner, rlb));
+                F2_TRY(o->apply(o->user, j, owner, j + 1, c1));
+            }
+            return F2GPU_OK;
+        }
+        const size_t cm = c0 + (c1 - c0) / 2;
+        F2_TRY(rec(c0, cm, rlb));
+        size_t R0 = 0, r0 = 0, Rl = 0, rl = 0;
+        F2_TRY(o->state(o->user, c0, &R0, &r0));
+        F2_TRY(o->state(o->user, cm - 1, &Rl, &rl));
+        const size_t R1 = Rl + rl;
+        const bool full = R1 - R0 == 64 * (cm - c0) && R0 % 64 == 0;
+        F2_TRY(o->gather(o->user, c0, cm, R0));
+        if (full) {
+            F2_TRY(o->solve(o->user, c0, cm, R0, cm, c1));
+            if (R1 < n) F2_TRY(o->product(o->user, c0, cm, R0, R1, cm, c1));
+        } else {
+            F2_TRY(o->rank_update(o->user, c0, cm, cm, c1));
+        }
+        return rec(cm, c1, R1);
+    };
+    if (n == 0 || mu == 0) return F2GPU_OK;
+    return rec(0, mu, 0);
+}
+
+// The GPU side of the schedule: shards sh (global index base + i of G), Lg = the
+// replicated left columns of the current split (full n rows, one per process).
+struct DistGpu {
+    f2gpu_ctx* c = nullptr;
+    std::vector<Shard>* sh = nullptr;
+    int base = 0, G = 1;
+    size_t n = 0, mu = 0;
+    Exchange* ex = nullptr;
+    View Lg{};
+    std::deque<DevBuf> lg_keep;
+    size_t lg_cols = 0;
+    size_t tbase = 16, trsm_m4rm_k = 1024, cut = 16384, tc_cut = 8192;
+
+    static DistGpu& of(void* u) { return *static_cast<DistGpu*>(u); }
+    int local(int owner) const { return owner - base; }  // may be outside [0, sh.size())
+
+    static int panel(void* u, size_t j, int owner, size_t row_lo) {
+        DistGpu& d = of(u);
+        const int ol = d.local(owner);
+        const size_t lj = j / size_t(d.G);
+        if (ol >= 0 && ol < int(d.sh->size())) {
+            Shard& o = (*d.sh)[size_t(ol)];
+            F2_TRY(check_launch(d.c, f2::launch_panel(o.w.p + lj * o.w.stride, d.n, o.st, int(j), d.c->stream),
+                                "k_panel"));
+            F2_TRY(check_launch(d.c, f2::launch_post(o.w.p, o.w.stride, int(o.lw), int(lj), o.perm, d.n, o.st + j,
+                                                     d.c->stream),
+                                "k_post"));
+        }
+        return d.ex->panel(d.c, *d.sh, ol, owner, j, lj, row_lo, d.n);
+    }
+    static int apply(void* u, size_t j, int owner, size_t col_lo, size_t col_hi) {
+        DistGpu& d = of(u);
+        for (size_t i = 0; i < d.sh->size(); ++i) {
+            Shard& s = (*d.sh)[i];
+            const int gg = d.base + int(i);
+            if (gg != owner)
+                F2_TRY(check_launch(d.c, f2::launch_swaps(s.w.p, s.w.stride, int(s.lw), -1, s.perm, s.st + j,
+                                                          d.c->stream),
+                                    "k_swaps"));
+            const size_t l0 = lidx(gg, d.G, col_lo), l1 = lidx(gg, d.G, col_hi);
+            if (l0 >= l1) continue;
+            f2::UpdateArgs a{};
+            a.C = s.w.p; a.sc = s.w.stride; a.c_wcol0 = l0; a.ncols = int(l1 - l0);
+            a.row_lo = 0; a.row_hi = d.n;
+            a.a = gg == owner ? s.w.p + (j / size_t(d.G)) * s.w.stride : s.land;
+            a.B = s.w.p; a.sb = s.w.stride; a.b_wcol0 = l0;
+            a.st = s.st + j;
+            F2_TRY(check_launch(d.c, f2::launch_update(a, d.c->num_sms, d.c->stream), "k_update"));
+        }
+        return F2GPU_OK;
+    }
+    static int state(void* u, size_t j, size_t* R, size_t* r) {
+        DistGpu& d = of(u);
+        f2::PanelState h;
+        CUDA_TRY(cudaStreamSynchronize(d.c->stream));
+        CUDA_TRY(cudaMemcpy(&h, (*d.sh)[0].st + j, 16, cudaMemcpyDeviceToHost));
+        *R = h.R;
+        *r = h.r;
+        return F2GPU_OK;
+    }
+    static int gather(void* u, size_t c0, size_t cm, size_t row_lo) {
+        DistGpu& d = of(u);
+        const size_t cols = cm - c0, gs = dev_stride(d.n);
+        if (cols > d.lg_cols) {
+            d.lg_keep.clear();
+            d.lg_keep.emplace_back(d.c);
+            F2_TRY(d.lg_keep.back().alloc(gs * cols * 8));
+            d.lg_cols = cols;
+        }
+        d.Lg = View{d.lg_keep.back().as<uint64_t>(), d.n, cols * 64, gs, gs};
+        return d.ex->gather(d.c, *d.sh, d.base, d.G, c0, cm, row_lo, d.n, d.Lg);
+    }
+    // X = L11^-1 C on shard s's word-columns [l0, l1), panels [a, b) of the split
+    // starting at c0 (L from Lg), rows [Ra, Ra + 64 (b - a))
+    int trsm(Shard& s, size_t l0, size_t l1, size_t c0, size_t a, size_t b, size_t Ra) {
+        const size_t nc = l1 - l0;
+        if (b - a <= tbase)
+            return check_launch(c, f2::launch_trsm_block_l(Lg.p + (a - c0) * Lg.stride + Ra, Lg.stride,
+                                                           s.w.p + l0 * s.w.stride + Ra, s.w.stride, int(b - a),
+                                                           int(nc), c->stream),
+                                "k_trsm_block");
+        const size_t m = a + (b - a) / 2, Rm = Ra + 64 * (m - a), Rb = Ra + 64 * (b - a);
+        F2_TRY(trsm(s, l0, l1, c0, a, m, Ra));
+        const View C = wview(s, Rm, Rb - Rm, l0, nc), A = Lg.sub(Rm, Rb - Rm, a - c0, m - a),
+                   B = wview(s, Ra, Rm - Ra, l0, nc);
+        if ((m - a) * 64 <= trsm_m4rm_k) F2_TRY(strassen_acc(c, C, A, B, cut));
+        else F2_TRY(best_product(c, C, A, B, cut, tc_cut));
+        return trsm(s, l0, l1, c0, m, b, Rm);
+    }
+    static int solve(void* u, size_t c0, size_t cm, size_t R0, size_t col_lo, size_t col_hi) {
+        DistGpu& d = of(u);
+        for (size_t i = 0; i < d.sh->size(); ++i) {
+            const int gg = d.base + int(i);
+            const size_t l0 = lidx(gg, d.G, col_lo), l1 = lidx(gg, d.G, col_hi);
+            if (l0 < l1) F2_TRY(d.trsm((*d.sh)[i], l0, l1, c0, c0, cm, R0));
+        }
+        return F2GPU_OK;
+    }
+    static int product(void* u, size_t c0, size_t cm, size_t R0, size_t R1, size_t col_lo, size_t col_hi) {
+        DistGpu& d = of(u);
+        for (size_t i = 0; i < d.sh->size(); ++i) {
+            Shard& s = (*d.sh)[i];
+            const int gg = d.base + int(i);
+            const size_t l0 = lidx(gg, d.G, col_lo), l1 = lidx(gg, d.G, col_hi);
+            if (l0 >= l1) continue;
+            F2_TRY(best_product(d.c, wview(s, R1, d.n - R1, l0, l1 - l0), d.Lg.sub(R1, d.n - R1, 0, cm - c0),
+                                wview(s, R0, R1 - R0, l0, l1 - l0), d.cut, d.tc_cut));
+        }
+        return F2GPU_OK;
+    }
+    static int rank_update(void* u, size_t c0, size_t cm, size_t col_lo, size_t col_hi) {
+        DistGpu& d = of(u);
+        for (size_t i = 0; i < d.sh->size(); ++i) {
+            Shard& s = (*d.sh)[i];
+            const int gg = d.base + int(i);
+            const size_t l0 = lidx(gg, d.G, col_lo), l1 = lidx(gg, d.G, col_hi);
+            if (l0 >= l1) continue;
+            for (size_t j = c0; j < cm; ++j) {
+                f2::UpdateArgs a{};
+                a.C = s.w.p; a.sc = s.w.stride; a.c_wcol0 = l0; a.ncols = int(l1 - l0);
+                a.row_lo = 0; a.row_hi = d.n; a.a = d.Lg.p + (j - c0) * d.Lg.stride;
+                a.B = s.w.p; a.sb = s.w.stride; a.b_wcol0 = l0;
+                a.st = s.st + j;
+                F2_TRY(check_launch(d.c, f2::launch_update(a, d.c->num_sms, d.c->stream), "k_update"));
+            }
+        }
+        return F2GPU_OK;
+    }
+    f2gpu_dist_ops ops() {
+        f2gpu_dist_ops o{};
+        o.user = this;
+        o.panel = &DistGpu::panel;
+        o.apply = &DistGpu::apply;
+        o.state = &DistGpu::state;
+        o.gather = &DistGpu::gather;
+        o.solve = &DistGpu::solve;
+        o.product = &DistGpu::product;
+        o.rank_update = &DistGpu::rank_update;
+        return o;
+    }
+};
+
+// leaf geometry shared with the single-GPU recursion (decompose_recursive)
+void rec_leaf_params(size_t min_cols, size_t* base, size_t* tall_rows, size_t* tall_base) {
+    *base = std::max<size_t>(1, (min_cols ? min_cols : 256 * 64) / 64);
+    *tall_rows = 20000;
+    *tall_base = 128;
+    if (const char* e = getenv("F2GPU_REC_BASE")) *base = std::max<size_t>(1, size_t(atol(e)));
+    if (const char* e = getenv("F2GPU_REC_TALL")) *tall_rows = size_t(atol(e));
+    if (const char* e = getenv("F2GPU_REC_TALL_BASE")) *tall_base = std::max<size_t>(1, size_t(atol(e)));
+}
+
+int run_dist_recursive(f2gpu_ctx* c, std::vector<Shard>& sh, int base, int G, size_t n, size_t mu, size_t min_cols,
+                       Exchange& ex) {
+    for (auto& s : sh) F2_TRY(check_launch(c, f2::launch_iota(s.perm, n, c->stream), "k_iota"));
+    DistGpu d;
+    d.c = c; d.sh = &sh; d.base = base; d.G = G; d.n = n; d.mu = mu; d.ex = &ex;
+    if (!c->use_tc_cut_default) d.tc_cut = c->tc_cutover;
+    size_t lb = 0, tr = 0, tb = 0;
+    rec_leaf_params(min_cols, &lb, &tr, &tb);
+    const f2gpu_dist_ops o = d.ops();
+    return dist_schedule(n, mu, G, lb, tr, tb, &o);
 }
 
 }  // namespace
@@ -2126,6 +2447,72 @@ int f2gpu_decompose_block_dist(f2gpu_ctx* c, f2gpu_mat* w_local, size_t m_global
     F2_TRY(alloc_shard_aux(c, sh[0], n, mu, keep));
     NcclExchange ex;
     F2_TRY(decompose_sharded(c, sh, c->rank, c->world, n, mu, ex));
+    return read_results(c, sh[0], n, mu, perm, rj, rank);
+}
+
+// ---- distributed decompose_recursive ----
+int f2gpu_dist_schedule(size_t n_rows, size_t mu, int world, size_t leaf_panels, size_t tall_rows,
+                        size_t tall_leaf_panels, const f2gpu_dist_ops* ops) {
+    if (!ops || !ops->panel || !ops->apply || !ops->state || !ops->gather || !ops->solve || !ops->product ||
+        !ops->rank_update)
+        return set_err(F2GPU_EINVAL, "dist_schedule: null callback");
+    if (world < 1) return set_err(F2GPU_EINVAL, "dist_schedule: world must be >= 1");
+    return dist_schedule(n_rows, mu, world, std::max<size_t>(1, leaf_panels), tall_rows,
+                         std::max<size_t>(1, tall_leaf_panels), ops);
+}
+
+int f2gpu_decompose_recursive_sharded(f2gpu_ctx* c, f2gpu_mat* w, int G, size_t min_cols, uint32_t* perm,
+                                      uint32_t* rj, size_t* rank) {
+    if (!c || !w) return set_err(F2GPU_EINVAL, "null argument");
+    if (G < 1) return set_err(F2GPU_EINVAL, "shards must be >= 1");
+    if (w->rows > 0xFFFFFFF0ull) return set_err(F2GPU_ERANGE, "decompose: too many rows for uint32 perm");
+    const size_t n = w->rows, mu = ceil64(w->cols);
+    if (n == 0 || mu == 0) return decompose_single(c, view_of(w), perm, rj, rank);
+    std::deque<DevBuf> keep;
+    std::vector<Shard> sh(G);
+    for (int g = 0; g < G; ++g) {
+        sh[g].lw = f2gpu_local_wcols(mu, g, G);
+        keep.emplace_back(c);
+        F2_TRY(keep.back().alloc(std::max<size_t>(1, sh[g].lw) * w->stride * 8));
+        sh[g].w = View{keep.back().as<uint64_t>(), n, sh[g].lw * 64, w->stride, w->stride};
+        if (sh[g].lw)
+            CUDA_TRY(cudaMemcpy2DAsync(sh[g].w.p, w->stride * 8, w->d + size_t(g) * w->stride,
+                                       size_t(G) * w->stride * 8, w->stride * 8, sh[g].lw, cudaMemcpyDeviceToDevice,
+                                       c->stream));
+        F2_TRY(alloc_shard_aux(c, sh[g], n, mu, keep));
+    }
+    LocalExchange ex;
+    F2_TRY(run_dist_recursive(c, sh, 0, G, n, mu, min_cols, ex));
+    for (int g = 0; g < G; ++g)
+        if (sh[g].lw)
+            CUDA_TRY(cudaMemcpy2DAsync(w->d + size_t(g) * w->stride, size_t(G) * w->stride * 8, sh[g].w.p,
+                                       w->stride * 8, w->stride * 8, sh[g].lw, cudaMemcpyDeviceToDevice, c->stream));
+    return read_results(c, sh[0], n, mu, perm, rj, rank);
+}
+
+int f2gpu_decompose_recursive_dist(f2gpu_ctx* c, f2gpu_mat* w_local, size_t m_global, size_t min_cols,
+                                   uint32_t* perm, uint32_t* rj, size_t* rank) {
+    if (!c || !w_local) return set_err(F2GPU_EINVAL, "null argument");
+    if (w_local->rows > 0xFFFFFFF0ull) return set_err(F2GPU_ERANGE, "decompose: too many rows for uint32 perm");
+    const size_t n = w_local->rows, mu = ceil64(m_global);
+    const size_t lw = f2gpu_local_wcols(mu, c->rank, c->world);
+    if (ceil64(w_local->cols) != lw)
+        return set_err(F2GPU_EINVAL, "decompose_dist: local matrix has the wrong number of word-columns");
+    if (c->world == 1 && !c->comm) return decompose_recursive(c, view_of(w_local), min_cols, perm, rj, rank);
+    if (!c->comm) return set_err(F2GPU_ENCCL, "decompose_dist: communicator not initialised");
+    if (n == 0 || mu == 0) {
+        if (rank) *rank = 0;
+        if (rj) std::fill(rj, rj + mu, 0u);
+        if (perm) for (size_t i = 0; i < n; ++i) perm[i] = uint32_t(i);
+        return F2GPU_OK;
+    }
+    std::deque<DevBuf> keep;
+    std::vector<Shard> sh(1);
+    sh[0].w = View{w_local->d, n, lw * 64, w_local->stride, w_local->stride};
+    sh[0].lw = lw;
+    F2_TRY(alloc_shard_aux(c, sh[0], n, mu, keep));
+    NcclExchange ex;
+    F2_TRY(run_dist_recursive(c, sh, c->rank, c->world, n, mu, min_cols, ex));
     return read_results(c, sh[0], n, mu, perm, rj, rank);
 }
 

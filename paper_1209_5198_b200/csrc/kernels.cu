@@ -2740,17 +2740,20 @@ cudaError_t launch_post_col(uint64_t* w, size_t stride, int ncols, int panel_col
 constexpr int kTrsmThreads = 128;  // one CTA per word-column
 constexpr int kTrsmMaxP = 16;
 constexpr int kTrsmRowsPerThread = 64 * kTrsmMaxP / kTrsmThreads;
-__global__ void __launch_bounds__(kTrsmThreads) k_trsm_block(uint64_t* __restrict__ W, size_t stride, int a,
-                                                             int P, size_t Ra, size_t col0) {
+// L: panel a's column at row Ra (panel a + t at L + t * ls); C: the first of the
+// ncols word-columns at row Ra (column q at C + q * sc).  L and C may live in
+// different matrices (the distributed recursion keeps L in a gathered copy).
+__global__ void __launch_bounds__(kTrsmThreads) k_trsm_block(const uint64_t* __restrict__ L, size_t ls,
+                                                             uint64_t* __restrict__ C, size_t sc, int P) {
     __shared__ uint64_t cs[64 * kTrsmMaxP];
     __shared__ uint64_t tb[256];
     const int tid = threadIdx.x;
-    uint64_t* col = W + (col0 + blockIdx.x) * stride + Ra;
+    uint64_t* col = C + size_t(blockIdx.x) * sc;
     const int rows = 64 * P;
     // multiplier words of panel t for this thread's rows; panel t+1's are loaded
     // while panel t is applied (one L2 round trip per panel otherwise)
     auto load_y = [&](int t, uint64_t (&y)[kTrsmRowsPerThread]) {
-        const uint64_t* Y = W + size_t(a + t) * stride + Ra;
+        const uint64_t* Y = L + size_t(t) * ls;
         const int r0 = 64 * (t + 1) + tid;
 #pragma unroll
         for (int i = 0; i < kTrsmRowsPerThread; ++i) {
@@ -2797,8 +2800,13 @@ __global__ void __launch_bounds__(kTrsmThreads) k_trsm_block(uint64_t* __restric
 
 cudaError_t launch_trsm_block(uint64_t* W, size_t stride, int a, int P, size_t Ra, size_t col0, int ncols,
                               cudaStream_t s) {
+    return launch_trsm_block_l(W + size_t(a) * stride + Ra, stride, W + col0 * stride + Ra, stride, P, ncols, s);
+}
+
+cudaError_t launch_trsm_block_l(const uint64_t* L, size_t ls, uint64_t* C, size_t sc, int P, int ncols,
+                                cudaStream_t s) {
     if (P < 1 || P > kTrsmMaxP || ncols < 1) return cudaErrorInvalidValue;
-    k_trsm_block<<<ncols, kTrsmThreads, 0, s>>>(W, stride, a, P, Ra, col0);
+    k_trsm_block<<<ncols, kTrsmThreads, 0, s>>>(L, ls, C, sc, P);
     return cudaGetLastError();
 }
 

@@ -231,6 +231,10 @@ cudaError_t launch_update_tc(const TcUpdateArgs& a, int grid, cudaStream_t s);
 // rows Ra .. Ra+64P, in place on word-columns [col0, col0+ncols)
 cudaError_t launch_trsm_block(uint64_t* W, size_t stride, int a, int P, size_t Ra, size_t col0, int ncols,
                               cudaStream_t s);
+// the same with L and C in separate matrices: L = panel a's column at row Ra
+// (panel a+t at L + t*ls), C = the first target word-column at row Ra
+cudaError_t launch_trsm_block_l(const uint64_t* L, size_t ls, uint64_t* C, size_t sc, int P, int ncols,
+                                cudaStream_t s);
 
 // per-device one-time setup (dynamic shared memory opt-in)
 cudaError_t init_kernel_attrs();

@@ -185,3 +185,196 @@ def test_sharded_multiply_protocol(po, n, k, m):
             assert np.array_equal(c_local[l, :n], want[qcol, :n]), qcol
             seen.add(qcol)
     assert seen == set(range(po.wcols(m)))
+
+
+# ---------------------------------------------------------------------------
+# decompose_recursive over column shards: the library's OWN schedule
+# (f2gpu_dist_schedule, the host code the GPU drivers run) executed on two
+# gloo ranks with numpy/oracle callbacks for the device work.
+# ---------------------------------------------------------------------------
+def rec_worker(rank, world, port, n, m, kind, leaf, out_q):
+    import ctypes as C
+    import traceback
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import pyoracle as po
+    from paper_1209_5198_b200 import _lib
+
+    lib = _lib.load()
+    ol = po.lib()
+    u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+    ol.f2o_m4rm_update.argtypes = [u64p, C.c_size_t, C.c_size_t, u64p, C.c_size_t, C.c_size_t, u64p,
+                                   C.c_size_t, C.c_size_t, C.c_size_t, C.c_uint]
+    a = make_input(po, n, m, kind)
+    mu = (m + 63) // 64
+    mine = list(range(rank, mu, world))
+    S = a.shape[1]
+    W = a[mine].copy() if mine else np.zeros((0, S), np.uint64)
+    perm = np.arange(n, dtype=np.uint32)
+    Rj = np.zeros(mu + 1, np.int64)          # R_j (replicated); R_{j+1} = R_j + r_j
+    rj = np.zeros(mu, np.int64)
+    pairs_of = {}
+    land = np.zeros(S, np.uint64)
+    Lg = {}
+
+    def local_of(q):
+        return q // world if q % world == rank else None
+
+    def own_cols(lo, hi):
+        return [(l, q) for l, q in enumerate(mine) if lo <= q < hi]
+
+    def permute(col, R, pairs):
+        old = col[R:n].copy()
+        for d_, s_ in pairs:
+            col[R + d_] = old[s_]
+
+    def update(l, a_col, R, r):
+        """W[l] rows [R+r, n) ^= a_col rows (low r bits) * W[l] rows [R, R+r)."""
+        if r == 0 or R + r >= n:
+            return
+        aw = np.ascontiguousarray(a_col[R + r:n])
+        colv = np.ascontiguousarray(W[l:l + 1])
+        ol.f2o_m4rm_update(colv, S, R + r, aw, n - R - r, r, colv, S, R, 1, 8)
+        W[l] = colv[0]
+
+    def guard(fn):
+        def inner(*args):
+            try:
+                fn(*args)
+                return 0
+            except Exception:
+                traceback.print_exc()
+                return 3
+        return inner
+
+    @guard
+    def panel(_, j, owner, row_lo):
+        R = int(Rj[j])
+        hdr = torch.zeros(2 + 256, dtype=torch.int64)
+        col = torch.zeros(n - row_lo, dtype=torch.int64)
+        if rank == owner:
+            lj = local_of(j)
+            pnl = W[lj, R:n].copy()
+            r, A, P, Z, sb = po.build_z(pnl) if n - R > 0 else (0, pnl, None, np.zeros(64, np.uint64), [])
+            pairs = composite_pairs(sb, r)
+            D = A[r:]
+            Y = np.zeros_like(D)
+            for t in range(64):
+                sel = ((D >> np.uint64(t)) & np.uint64(1)).astype(bool)
+                Y[sel] ^= Z[t]
+            A[r:] = Y
+            W[lj, R:n] = A
+            for l in range(W.shape[0]):      # the post: swaps on the owner's other columns
+                if l != lj:
+                    permute(W[l], R, pairs)
+            permute(perm, R, pairs)
+            hdr[0], hdr[1] = r, len(pairs)
+            for e, (d_, s_) in enumerate(pairs):
+                hdr[2 + e], hdr[2 + 128 + e] = d_, s_
+            col[:] = torch.from_numpy(W[lj, row_lo:n].view(np.int64).copy())
+        dist.broadcast(hdr, src=owner)
+        dist.broadcast(col, src=owner)
+        r, npairs = int(hdr[0]), int(hdr[1])
+        rj[j] = r
+        Rj[j + 1] = R + r
+        pairs_of[j] = [(int(hdr[2 + e]), int(hdr[2 + 128 + e])) for e in range(npairs)]
+        land[:] = 0
+        land[row_lo:n] = col.numpy().view(np.uint64)
+
+    @guard
+    def apply(_, j, owner, lo, hi):
+        R, r = int(Rj[j]), int(rj[j])
+        if rank != owner:
+            for l in range(W.shape[0]):
+                permute(W[l], R, pairs_of[j])
+            permute(perm, R, pairs_of[j])
+        a_col = W[local_of(j)].copy() if rank == owner else land.copy()
+        for l, _q in own_cols(lo, hi):
+            update(l, a_col, R, r)
+
+    @guard
+    def state(_, j, Rp, rp):
+        Rp[0], rp[0] = int(Rj[j]), int(rj[j])
+
+    @guard
+    def gather(_, c0, cm, row_lo):
+        Lg.clear()
+        for q in range(c0, cm):
+            t = torch.zeros(n - row_lo, dtype=torch.int64)
+            if q % world == rank:
+                t[:] = torch.from_numpy(W[local_of(q), row_lo:n].view(np.int64).copy())
+            dist.broadcast(t, src=q % world)
+            full = np.zeros(S, np.uint64)
+            full[row_lo:n] = t.numpy().view(np.uint64)
+            Lg[q] = full
+
+    @guard
+    def solve(_, c0, cm, R0, lo, hi):
+        R1 = R0 + 64 * (cm - c0)
+        for l, _q in own_cols(lo, hi):
+            for t in range(c0, cm):        # forward substitution inside the pivot block
+                Rt = R0 + 64 * (t - c0)
+                rows = np.ascontiguousarray(Lg[t][Rt + 64:R1])
+                if rows.size:
+                    colv = np.ascontiguousarray(W[l:l + 1])
+                    ol.f2o_m4rm_update(colv, S, Rt + 64, rows, R1 - Rt - 64, 64, colv, S, Rt, 1, 8)
+                    W[l] = colv[0]
+
+    @guard
+    def product(_, c0, cm, R0, R1, lo, hi):
+        for l, _q in own_cols(lo, hi):
+            for t in range(c0, cm):        # A' = D ^ L21 X, one 64-column block of L21 at a time
+                Rt = R0 + 64 * (t - c0)
+                rows = np.ascontiguousarray(Lg[t][R1:n])
+                colv = np.ascontiguousarray(W[l:l + 1])
+                ol.f2o_m4rm_update(colv, S, R1, rows, n - R1, 64, colv, S, Rt, 1, 8)
+                W[l] = colv[0]
+
+    @guard
+    def rank_update(_, c0, cm, lo, hi):
+        for j in range(c0, cm):
+            for l, _q in own_cols(lo, hi):
+                update(l, Lg[j], int(Rj[j]), int(rj[j]))
+
+    ops = _lib.DistOps(None, _lib.PANEL_FN(panel), _lib.APPLY_FN(apply), _lib.STATE_FN(state),
+                       _lib.GATHER_FN(gather), _lib.SOLVE_FN(solve), _lib.PRODUCT_FN(product),
+                       _lib.RANKUPD_FN(rank_update))
+    rc = lib.f2gpu_dist_schedule(n, mu, world, leaf, 0, leaf, C.byref(ops))
+    out_q.put((rank, rc, mine, W, perm, rj.astype(np.uint32)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def make_input(po, n, m, kind):
+    if kind == "xy":  # rank-deficient: the splits take the rank-r_j path
+        k = 70
+        return po.m4rm_mult(po.random_dense(n, k, 0.5, 31), n, k, po.random_dense(k, m, 0.5, 32), m)
+    return po.random_dense(n, m, 0.5 if kind == "dense" else 0.05, 33)
+
+
+@pytest.mark.parametrize("n,m,kind,leaf", [(700, 640, "dense", 2), (400, 1000, "dense", 1), (900, 512, "xy", 2),
+                                           (300, 577, "sparse", 3)])
+def test_recursive_schedule_matches_oracle(po, n, m, kind, leaf):
+    """The distributed recursion (leaves, splits with gather + solve + product, and
+    the rank-deficient fallback) driven by libf2gpu's f2gpu_dist_schedule on two
+    gloo ranks gives the single-process oracle's W, perm and r_j bit-for-bit."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=rec_worker, args=(r, world, port, n, m, kind, leaf, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    w, perm, rj, rank = po.decompose_block(make_input(po, n, m, kind), n, m)
+    for r_, rc, mine, W, prm, rjj in res:
+        assert rc == 0
+        assert np.array_equal(prm, perm), r_
+        assert np.array_equal(rjj, rj), r_
+        for l, qcol in enumerate(mine):
+            assert np.array_equal(W[l, :n], w[qcol, :n]), (r_, qcol)
