@@ -19,8 +19,14 @@ LIB = PKG / "libf2gpu.so"
 SOURCES = [CSRC / "kernels.cu", CSRC / "tc_leaf.cu", CSRC / "tc_pair.cu", CSRC / "tc_update.cu", CSRC / "api.cu"]
 HEADERS = [CSRC / "kernels.cuh", CSRC / "tc_common.cuh", ROOT / "include" / "f2gpu.h"]
 
+# F2GPU_BUILD_EXPERIMENTAL=1 also compiles the evaluated-and-rejected variants
+# (int8 leaves, single-CTA pair / persistent / double-buffered fp4 leaves, the
+# tensor-core update); the default library carries only the kernels in use.
+EXPERIMENTAL = os.environ.get("F2GPU_BUILD_EXPERIMENTAL", "0") == "1"
+
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
+    f"-DF2GPU_EXPERIMENTAL={1 if EXPERIMENTAL else 0}",
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
     "-diag-suppress", "177",

@@ -22,7 +22,7 @@
 #include "../../include/f2gpu.h"
 #include "kernels.cuh"
 
-#define F2GPU_VERSION "0.1.0"
+#define F2GPU_VERSION "0.2.0"
 
 namespace {
 
@@ -1601,7 +1601,13 @@ int run_dist_recursive(f2gpu_ctx* c, std::vector<Shard>& sh, int base, int G, si
 extern "C" {
 
 const char* f2gpu_last_error(void) { return g_err.c_str(); }
-const char* f2gpu_version(void) { return F2GPU_VERSION " sm_100a"; }
+const char* f2gpu_version(void) {
+#if F2GPU_EXPERIMENTAL
+    return F2GPU_VERSION " sm_100a +experimental";
+#else
+    return F2GPU_VERSION " sm_100a";
+#endif
+}
 
 int f2gpu_ctx_create(int device, f2gpu_ctx** out) {
     if (!out) return set_err(F2GPU_EINVAL, "ctx_create: null out");
@@ -1943,10 +1949,14 @@ int f2gpu_gemm_tc(f2gpu_ctx* c, const f2gpu_mat* a, const f2gpu_mat* b, f2gpu_ma
     if (!c || !a || !b || !cm) return set_err(F2GPU_EINVAL, "null argument");
     if (a->cols != b->rows || cm->rows != a->rows || cm->cols != b->cols)
         return set_err(F2GPU_EINVAL, "gemm_tc: shape mismatch");
+#if F2GPU_EXPERIMENTAL
     static const int kind = [] {
         const char* e = getenv("F2GPU_TC_KIND");  // evaluation switch: "i8" selects the int8 leaf
         return (e && e[0] == 'i') ? 8 : 4;
     }();
+#else
+    constexpr int kind = 4;
+#endif
     if (kind == 4 && f2::gemm_tc3_ok(a->rows, a->cols, b->cols)) {
         const size_t sbt = (b->cols + 127) / 128 * 128;
         DevBuf bt(c);
@@ -1959,6 +1969,10 @@ int f2gpu_gemm_tc(f2gpu_ctx* c, const f2gpu_mat* a, const f2gpu_mat* b, f2gpu_ma
                                                    cm->stride, a->cols, b->cols, acc != 0, c->stream),
                             "k_gemm_tc3");
     }
+#if !F2GPU_EXPERIMENTAL
+    return set_err(F2GPU_EINVAL, "gemm_tc: the fp4 leaf needs m % 256 == 0 (the int8 leaf is built only with "
+                                 "F2GPU_EXPERIMENTAL=1)");
+#else
     if (!f2::gemm_tc_ok(a->rows, a->cols, b->cols))
         return set_err(F2GPU_EINVAL, kind == 4 ? "gemm_tc: needs m % 256 == 0"
                                                : "gemm_tc: needs n % 256 == 0, m % 128 == 0, k % 64 == 0");
@@ -1978,6 +1992,7 @@ int f2gpu_gemm_tc(f2gpu_ctx* c, const f2gpu_mat* a, const f2gpu_mat* b, f2gpu_ma
     return check_launch(c, f2::launch_gemm_tc(a->d, a->stride, b->d, b->stride, cm->d, cm->stride,
                                               a->rows, a->cols, b->cols, acc != 0, c->stream),
                         "k_gemm_tc");
+#endif
 }
 
 int f2gpu_update_tc(f2gpu_ctx* c, f2gpu_mat* cm, size_t row_lo, size_t row_hi, size_t c_wcol0,
@@ -1991,6 +2006,10 @@ int f2gpu_update_tc(f2gpu_ctx* c, f2gpu_mat* cm, size_t row_lo, size_t row_hi, s
     if (bt->rows < n_wcols * 64 || bt->cols < kwords * 64)
         return set_err(F2GPU_EINVAL, "update_tc: BT must be (n_wcols*64) x (kwords*64)");
     if (n_wcols == 0 || row_lo == row_hi) return F2GPU_OK;
+#if !F2GPU_EXPERIMENTAL
+    return set_err(F2GPU_EINVAL, "update_tc: the tensor-core update is built only with F2GPU_EXPERIMENTAL=1 "
+                                 "(evaluated, not used: DESIGN.md)");
+#else
     // B^T with the row padding the kernel's 192-row bulk loads read
     const size_t sbt = (f2::update_tc_bt_rows(int(n_wcols)) + 127) / 128 * 128;
     DevBuf pad(c);
@@ -2004,6 +2023,7 @@ int f2gpu_update_tc(f2gpu_ctx* c, f2gpu_mat* cm, size_t row_lo, size_t row_hi, s
     u.bt = pad.as<uint64_t>(); u.sbt = sbt;
     if (!f2::update_tc_ok(u)) return set_err(F2GPU_EINVAL, "update_tc: operands not aligned");
     return check_launch(c, f2::launch_update_tc(u, c->num_sms, c->stream), "k_update_tc");
+#endif
 }
 
 int f2gpu_mult_acc(f2gpu_ctx* c, f2gpu_mat* cm, size_t c_row0, size_t c_wcol0, size_t n_wcols,

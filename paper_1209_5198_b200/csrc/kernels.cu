@@ -452,26 +452,8 @@ __global__ void __launch_bounds__(kUpdThreads, 1) k_update(UpdateArgs p) {
 }
 
 // ---------------------------------------------------------------------------
-// K2 v2: fused table build + XOR update with C staged by bulk-async copies
+// bulk-copy helpers of the v3 update
 // ---------------------------------------------------------------------------
-// ncu on k_update (v1) showed the L1TEX data pipe at 91% of peak with half of
-// its wavefronts spent on LSU global traffic (one wavefront per 32-byte
-// sector).  v2 moves C through shared memory with cp.async.bulk (the TMA
-// engine, not the LSU): a producer warp streams 128-row x 16-column tiles of C
-// (16 x 1 KiB column segments, padded to 1040 B so 128-bit shared loads of the
-// consumers are bank-conflict free) plus the 128 driving words into a 3-stage
-// mbarrier ring, and writes finished tiles back with bulk stores.  16 consumer
-// warps keep the v1 lookup pattern (lane = (row half, column), one 128-byte
-// table row per half-warp lookup).  Requires 128-row aligned strides and a
-// 16-byte aligned driving column (device matrices and the decomposition).
-constexpr int kV2Warps = 16;
-constexpr int kV2Threads = (kV2Warps + 1) * 32;
-constexpr int kV2Rows = 128;
-constexpr int kV2Stages = 3;
-constexpr int kV2ColPitch = kV2Rows * 8 + 16;                      // 1040 B
-constexpr int kV2CBytes = kTabCols * kV2ColPitch;                  // 16640 B
-constexpr int kV2StageBytes = kV2CBytes + kV2Rows * 8;             // + driving words
-constexpr size_t kV2Smem = kTabBytes + size_t(kV2Stages) * kV2StageBytes + 64;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -518,131 +500,6 @@ __device__ __forceinline__ void bulk_wait_read1() {
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void consumers_sync() {
-    asm volatile("bar.sync 1, %0;" ::"n"(kV2Warps * 32) : "memory");
-}
-
-__global__ void __launch_bounds__(kV2Threads, 1) k_update_v2(UpdateArgs p) {
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    uint64_t* tab = reinterpret_cast<uint64_t*>(smem_raw);
-    unsigned char* stage0 = smem_raw + kTabBytes;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(stage0 + size_t(kV2Stages) * kV2StageBytes);
-    uint64_t* full = bars;               // [kV2Stages]
-    uint64_t* done = bars + kV2Stages;   // [kV2Stages]
-
-    size_t row_lo = p.row_lo, b_row0 = p.b_row0;
-    int k = p.k_bits;
-    if (p.st) {
-        const uint32_t R = p.st->R, r = p.st->r;
-        row_lo = size_t(R) + r;
-        k = int(r);
-        b_row0 = R;
-    }
-    const size_t row_hi = p.row_hi;
-    if (k <= 0 || row_lo >= row_hi || p.ncols <= 0) return;
-    const int nt = k > 56 ? 9 : (k + 6) / 7;
-    const size_t base = row_lo & ~size_t(kV2Rows - 1);
-    const size_t T = (row_hi - base + kV2Rows - 1) / kV2Rows;  // tiles per column group
-    const size_t ncg = (size_t(p.ncols) + kTabCols - 1) / kTabCols;
-    const size_t TU = T * ncg;
-    const size_t u0 = TU * blockIdx.x / gridDim.x;
-    const size_t u1 = TU * (blockIdx.x + 1) / gridDim.x;
-    if (u0 >= u1) return;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kV2Stages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&done[s], kV2Warps);
-        }
-        fence_async_smem();
-    }
-    __syncthreads();
-
-    if (warp == kV2Warps) {
-        // ===== producer warp: bulk loads into the ring, bulk stores out of it =====
-        for (size_t u = u0; u < u1 + kV2Stages; ++u) {
-            const size_t it = u - u0;
-            const int s = int(it % kV2Stages);
-            unsigned char* sb = stage0 + size_t(s) * kV2StageBytes;
-            if (it >= size_t(kV2Stages)) {
-                // write back tile it - kV2Stages from stage s
-                const size_t uo = u - kV2Stages;
-                mbar_wait(&done[s], uint32_t(((it / kV2Stages) - 1) & 1));
-                const size_t g = uo / T, t = uo % T;
-                const int nvalid = min(kTabCols, int(size_t(p.ncols) - g * kTabCols));
-                const size_t r0 = base + t * kV2Rows;
-                if (lane < nvalid) {
-                    bulk_s2g(p.C + (p.c_wcol0 + g * kTabCols + lane) * p.sc + r0,
-                             sb + lane * kV2ColPitch, kV2Rows * 8);
-                    bulk_commit();
-                    bulk_wait_read0();
-                }
-                __syncwarp();
-            }
-            if (u >= u1) continue;
-            const size_t g = u / T, t = u % T;
-            const int nvalid = min(kTabCols, int(size_t(p.ncols) - g * kTabCols));
-            const size_t r0 = base + t * kV2Rows;
-            if (lane == 0) mbar_expect_tx(&full[s], uint32_t((nvalid + 1) * kV2Rows * 8));
-            __syncwarp();
-            if (lane < nvalid)
-                bulk_g2s(sb + lane * kV2ColPitch,
-                         p.C + (p.c_wcol0 + g * kTabCols + lane) * p.sc + r0, kV2Rows * 8,
-                         &full[s]);
-            if (lane == kTabCols)
-                bulk_g2s(sb + kV2CBytes, p.a + r0, kV2Rows * 8, &full[s]);
-        }
-        bulk_wait0();
-        return;
-    }
-
-    // ===== 16 consumer warps =====
-    const int h = lane >> 4, col = lane & 15;
-    const uint64_t* tl = tab + col;
-    const int rl = 8 * warp + 4 * h;  // this lane's 4 rows within the tile
-    size_t gcur = ~size_t(0);
-    for (size_t u = u0; u < u1; ++u) {
-        const size_t it = u - u0;
-        const int s = int(it % kV2Stages);
-        const size_t g = u / T, t = u % T;
-        if (g != gcur) {
-            consumers_sync();
-            const int nvalid = min(kTabCols, int(size_t(p.ncols) - g * kTabCols));
-            build_tables<kV2Warps * 32>(tab, p.B, p.sb, b_row0, p.b_wcol0 + g * kTabCols, nvalid,
-                                        k, nt);
-            consumers_sync();
-            gcur = g;
-        }
-        unsigned char* sb = stage0 + size_t(s) * kV2StageBytes;
-        mbar_wait(&full[s], uint32_t((it / kV2Stages) & 1));
-        uint64_t* cw = reinterpret_cast<uint64_t*>(sb + col * kV2ColPitch) + rl;
-        const uint64_t* aw = reinterpret_cast<const uint64_t*>(sb + kV2CBytes) + rl;
-        const ulonglong2 c01 = *reinterpret_cast<const ulonglong2*>(cw);
-        const ulonglong2 c23 = *reinterpret_cast<const ulonglong2*>(cw + 2);
-        const ulonglong2 a01 = *reinterpret_cast<const ulonglong2*>(aw);
-        const ulonglong2 a23 = *reinterpret_cast<const ulonglong2*>(aw + 2);
-        const size_t row = base + t * kV2Rows + rl;
-        uint64_t x[4] = {a01.x, a01.y, a23.x, a23.y};
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-            if (row + q < row_lo || row + q >= row_hi) x[q] = 0;
-        ulonglong2 o01, o23;
-        o01.x = c01.x ^ lookup(tl, x[0], nt);
-        o01.y = c01.y ^ lookup(tl, x[1], nt);
-        o23.x = c23.x ^ lookup(tl, x[2], nt);
-        o23.y = c23.y ^ lookup(tl, x[3], nt);
-        *reinterpret_cast<ulonglong2*>(cw) = o01;
-        *reinterpret_cast<ulonglong2*>(cw + 2) = o23;
-        fence_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&done[s]);
-    }
-}
-
-bool update_v2_ok(const UpdateArgs& a) {
-    return (a.sc % kV2Rows) == 0 && (reinterpret_cast<uintptr_t>(a.C) % 16) == 0 &&
-           (reinterpret_cast<uintptr_t>(a.a) % 16) == 0 && a.row_hi <= a.sc;
 }
 
 // ---------------------------------------------------------------------------
@@ -2971,9 +2828,6 @@ cudaError_t launch_mask_cols(uint64_t* w, size_t stride, size_t n, size_t m, cud
 cudaError_t init_kernel_attrs() {
     cudaError_t e = cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(kTabBytes));
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_update_v2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(kV2Smem));
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_update_v3, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(kV3Smem));

@@ -25,6 +25,7 @@
 
 namespace f2 {
 
+#if F2GPU_EXPERIMENTAL  // evaluated and rejected variants: built only with F2GPU_EXPERIMENTAL=1 (build.py)
 namespace {
 
 constexpr int kTcThreads = 256;  // 8 warps: expansion; thread 0 issues MMAs; warps 0-3 epilogue
@@ -423,6 +424,7 @@ __global__ void __launch_bounds__(kT2Threads, 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
 }
 
+#endif
 // ---- v3: block-scaled FP4 (kind::mxf4) on the same warp-specialised pipeline ----
 // A bit becomes the E2M1 nibble 0x2 (= 1.0) or 0x0, two elements per byte, so a
 // 64-bit k-block is one 32-byte K=64 row slice: half the expansion stores and
@@ -684,6 +686,7 @@ __global__ void __launch_bounds__(kT3Threads, 1)
 #endif
 }
 
+#if F2GPU_EXPERIMENTAL  // evaluated and rejected variants: built only with F2GPU_EXPERIMENTAL=1 (build.py)
 // ---------------------------------------------------------------------------
 // k_gemm_tc5: the fp4 leaf as a PERSISTENT kernel.  k_gemm_tc3 runs one 256x240
 // tile per CTA and pays ~7 us per tile of setup, load latency and epilogue (a
@@ -1239,8 +1242,10 @@ cudaError_t launch_gemm_tc2(const uint64_t* A, size_t sa, const uint64_t* BT, si
     return cudaGetLastError();
 }
 
+#endif
 bool gemm_tc3_ok(size_t n, size_t k, size_t m) { return n > 0 && k > 0 && m > 0 && m % kT3Cols == 0; }
 
+#if F2GPU_EXPERIMENTAL  // evaluated and rejected variants: built only with F2GPU_EXPERIMENTAL=1 (build.py)
 // ---- v4: the fp4 leaf on CTA pairs (cta_group::2) ----
 // A cluster of 2 CTAs computes a 512-column x 240-row tile with M = 256 MMAs
 // issued by the leader: for each of the two accumulators the M = 256 output
@@ -1456,7 +1461,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kT4Threads, 1)
         asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
 }
 
+#endif
 namespace {
+#if F2GPU_EXPERIMENTAL  // evaluated and rejected variants: built only with F2GPU_EXPERIMENTAL=1 (build.py)
 using Tc5Fn = void (*)(TcGemmArgs, const TcGemmArgs*, uint32_t, uint32_t, uint32_t);
 Tc5Fn tc5_fn() {
     static Tc5Fn fn = nullptr;
@@ -1510,6 +1517,8 @@ size_t tc5_max_k() {  // F2GPU_TC5_MAXK (default 2048)
     }();
     return v;
 }
+#endif
+#if F2GPU_EXPERIMENTAL
 int sm_count() {
     static int n = 0;
     if (!n) {
@@ -1520,6 +1529,7 @@ int sm_count() {
     }
     return n;
 }
+#endif
 using Tc3Fn = void (*)(TcGemmArgs, const TcGemmArgs*);
 Tc3Fn tc3_fn() {
     static Tc3Fn fn = nullptr;
@@ -1533,6 +1543,7 @@ Tc3Fn tc3_fn() {
     }
     return fn;
 }
+#if F2GPU_EXPERIMENTAL  // evaluated and rejected variants: built only with F2GPU_EXPERIMENTAL=1 (build.py)
 // the pair kernel is opt-in (F2GPU_TC_PAIR=1) for products whose width is a
 // multiple of 512.  Measured at 16384^3: 1.85 ms vs 1.86 ms for the single-CTA
 // kernel -- it takes the shared-memory pipe from ~95% to ~64% busy, but the raw-
@@ -1549,6 +1560,7 @@ bool tc4_use(size_t m) {
     }();
     return on && m % kT4Cols == 0;
 }
+#endif
 bool tc3_args_ok(const TcGemmArgs& p) {
     return gemm_tc3_ok(p.n, p.k, p.m) && p.sbt % 2 == 0 && p.sa % 2 == 0 &&
            reinterpret_cast<uintptr_t>(p.A) % 16 == 0 && reinterpret_cast<uintptr_t>(p.BT) % 16 == 0;
@@ -1564,6 +1576,7 @@ cudaError_t launch_gemm_tc3(const uint64_t* A, size_t sa, size_t n, const uint64
     const TcGemmArgs p{A, sa, n, BT, sbt, C, sc, k, m, acc ? 1 : 0};
     if (!tc3_args_ok(p)) return cudaErrorInvalidValue;
     if (gemm_tc7_enabled()) return launch_gemm_tc7(p, s);
+#if F2GPU_EXPERIMENTAL
     if (tc4_use(m)) {
         dim3 grid4(unsigned(2 * (m / kT4Cols)), unsigned((n + kT4Rows - 1) / kT4Rows));
         k_gemm_tc4<<<grid4, kT4Threads, kT4Smem, s>>>(p, nullptr);
@@ -1582,6 +1595,9 @@ cudaError_t launch_gemm_tc3(const uint64_t* A, size_t sa, size_t n, const uint64
         f5<<<std::min<uint32_t>(NT, uint32_t(sm_count())), kT3Threads, kT3Smem, s>>>(p, nullptr, GX, GY, NT);
         return cudaGetLastError();
     }
+#else
+    const uint32_t GX = uint32_t(m / kT3Cols), GY = uint32_t((n + kT3Rows - 1) / kT3Rows);
+#endif
     dim3 grid(GX, GY);
     fn<<<grid, kT3Threads, kT3Smem, s>>>(p, nullptr);
     return cudaGetLastError();
@@ -1599,6 +1615,8 @@ cudaError_t launch_gemm_tc3_batched(const TcGemmArgs* h_probs, const TcGemmArgs*
         nx = std::max(nx, h_probs[i].n);
     }
     if (gemm_tc7_enabled()) return launch_gemm_tc7_batched(h_probs, d_probs, nprob, s);
+    const uint32_t GX = uint32_t(mx / kT3Cols), GY = uint32_t((nx + kT3Rows - 1) / kT3Rows);
+#if F2GPU_EXPERIMENTAL
     bool all4 = true;
     for (int i = 0; i < nprob; ++i) all4 = all4 && tc4_use(h_probs[i].m);
     if (all4) {
@@ -1606,7 +1624,6 @@ cudaError_t launch_gemm_tc3_batched(const TcGemmArgs* h_probs, const TcGemmArgs*
         k_gemm_tc4<<<grid4, kT4Threads, kT4Smem, s>>>(TcGemmArgs{}, d_probs);
         return cudaGetLastError();
     }
-    const uint32_t GX = uint32_t(mx / kT3Cols), GY = uint32_t((nx + kT3Rows - 1) / kT3Rows);
     size_t kmax = 0;
     for (int i = 0; i < nprob; ++i) kmax = std::max(kmax, h_probs[i].k);
     if (Tc6Fn f6 = tc6_fn(); f6 && kmax <= tc6_max_k()) {
@@ -1622,11 +1639,13 @@ cudaError_t launch_gemm_tc3_batched(const TcGemmArgs* h_probs, const TcGemmArgs*
                                                                                        NT);
         return cudaGetLastError();
     }
+#endif
     dim3 grid(GX, GY, unsigned(nprob));
     fn<<<grid, kT3Threads, kT3Smem, s>>>(TcGemmArgs{}, d_probs);
     return cudaGetLastError();
 }
 
+#if F2GPU_EXPERIMENTAL  // evaluated and rejected variants: built only with F2GPU_EXPERIMENTAL=1 (build.py)
 cudaError_t launch_gemm_tc(const uint64_t* A, size_t sa, const uint64_t* B, size_t sb, uint64_t* C,
                            size_t sc, size_t n, size_t k, size_t m, bool acc, cudaStream_t s) {
     static bool attr = false;
@@ -1641,5 +1660,7 @@ cudaError_t launch_gemm_tc(const uint64_t* A, size_t sa, const uint64_t* B, size
     k_gemm_tc<<<grid, kTcThreads, kTcSmem, s>>>(A, sa, B, sb, C, sc, n, k, m, acc ? 1 : 0);
     return cudaGetLastError();
 }
+
+#endif
 
 }  // namespace f2

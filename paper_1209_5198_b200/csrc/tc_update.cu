@@ -52,6 +52,7 @@
 #include "kernels.cuh"
 #include "tc_common.cuh"
 
+#if F2GPU_EXPERIMENTAL  // evaluated, not used: built only with F2GPU_EXPERIMENTAL=1
 namespace f2 {
 
 namespace {
@@ -451,3 +452,5 @@ size_t update_tc_bt_rows(int ncols) {
 }
 
 }  // namespace f2
+
+#endif  // F2GPU_EXPERIMENTAL

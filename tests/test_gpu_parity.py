@@ -8,6 +8,17 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+def experimental() -> bool:
+    """libf2gpu built with F2GPU_BUILD_EXPERIMENTAL=1 (the evaluated-and-rejected variants)."""
+    from paper_1209_5198_b200 import _lib
+
+    return b"experimental" in _lib.load().f2gpu_version()
+
+
+needs_experimental = pytest.mark.skipif("not experimental()",
+                                        reason="variant built only with F2GPU_BUILD_EXPERIMENTAL=1")
+
+
 def bm(f2, arr, n, m):
     return f2.BitMatrix(n, m, arr)
 
@@ -125,6 +136,10 @@ def _tc(f2, ctx, lib, a, b, n, k, m, acc, c0=None):
 @pytest.mark.parametrize("n,k,m", TC_SHAPES)
 def test_gemm_tc(f2, ctx, po, n, k, m):
     lib = f2._lib.load()
+    if m % 256 and not experimental():  # the int8 leaf: only in experimental builds
+        with pytest.raises(ValueError):
+            _tc(f2, ctx, lib, po.zeros(n, k), po.zeros(k, m), n, k, m, 0)
+        return
     a = po.random_dense(n, k, 0.5, n + 3 * k)
     b = po.random_dense(k, m, 0.5, k + 5 * m)
     assert same(_tc(f2, ctx, lib, a, b, n, k, m, 0), po.m4rm_mult(a, n, k, b, m), n)
@@ -166,6 +181,7 @@ UPD_TC_CASES = [  # n, m, lo, hi, q0, nwc, kwords
     (5000, 4096, 4999, 5000, 10, 54, 1)]
 
 
+@needs_experimental
 @pytest.mark.parametrize("n,m,lo,hi,q0,nwc,kw", UPD_TC_CASES)
 def test_update_tc(f2, ctx, po, n, m, lo, hi, q0, nwc, kw):
     lib = f2._lib.load()
@@ -489,6 +505,7 @@ def test_decompose_recursive_host(f2, ctx, po, n, m, kind, mc):
     assert same(wout, w, n)
 
 
+@needs_experimental
 def test_gemm_tc_pair_kernel(f2, po):
     """The cta_group::2 leaf (opt-in via F2GPU_TC_PAIR=1) in a fresh process."""
     import os
@@ -508,6 +525,7 @@ def test_gemm_tc_pair_kernel(f2, po):
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
+@needs_experimental
 def test_gemm_tc_persistent_kernel(f2, po):
     """The persistent fp4 leaf k_gemm_tc5 (opt-in via F2GPU_TC_PERSIST=1), in a fresh
     process: single products across tile counts below / above one wave, and the
@@ -532,6 +550,7 @@ def test_gemm_tc_persistent_kernel(f2, po):
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
+@needs_experimental
 def test_gemm_tc_double_buffered_kernel(f2, po):
     """The double-buffered short-k fp4 leaf k_gemm_tc6 (opt-in via F2GPU_TC6_MAXK) in a
     fresh process, on every product and on the batched Strassen-Winograd leaves."""
