@@ -54,9 +54,9 @@ namespace {
 constexpr int kP7M = 256;             // output columns per pair tile (MMA M)
 constexpr int kP7MH = kP7M / 2;       // M rows per CTA (its TMEM lanes)
 constexpr int kP7Grp = 8;             // k-blocks per TMA request (box height)
-constexpr int kP7Threads = 26 * 32;
+constexpr int kP7Threads = 27 * 32;
 constexpr int kP7EpiW0 = 16, kP7EpiWarps = 8;
-constexpr int kP7Mma = 24, kP7Load = 25;
+constexpr int kP7Mma = 24, kP7Mma2 = 25, kP7Load = 26;
 
 // NN: output rows per pair tile (MMA N); NACC: TMEM accumulators (2 = the next
 // tile's MMAs overlap this tile's epilogue); STG x KPS: the operand ring, STG
@@ -163,7 +163,14 @@ __device__ __forceinline__ bool p7_tile(uint32_t t, const Tc7Prob* probs, uint32
 }
 
 // MODE (diagnostics): 0 product; 1 no MMA (commits only); 7 cycle accounting
-template <int NN, int NACC, int STG, int KPS, int RG, int MODE, bool POLL = false>
+// DUAL: two MMA-issuing warps take alternate stages.  A tcgen05.mma issue blocks
+// until the tensor pipe takes it (a one-deep queue, tools/micro/mma_rate.cu), so
+// one issuing thread idles the pipe while it commits a stage and waits for the
+// next one (~270 of every ~1300 cycles at 8 k-blocks per stage); with two, one
+// thread's waits overlap the other's MMAs.  The MMAs of a tile interleave in any
+// order (sums commute) except its first (accumulate = 0), which the stage-0
+// thread issues before it publishes the tile as started.
+template <int NN, int NACC, int STG, int KPS, int RG, int MODE, bool POLL = false, bool DUAL = true>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP7Threads, 1)
     k_gemm_tc7(const Tc7Prob* __restrict__ probs, uint32_t GX, uint32_t GY, uint32_t NT) {
     using G = P7<NN, NACC, STG, KPS, RG>;
@@ -184,6 +191,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP7Threads, 1)
     const uint32_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
     if (tid == 0) {
+        tmem_slot[1] = 0;  // tiles whose first MMA is issued (DUAL)
         for (int s = 0; s < kStages; ++s) {
             mbar_init_n(&full[s], 32);
             mbar_init_n(&empty[s], 1);
@@ -193,7 +201,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP7Threads, 1)
             mbar_init_n(&rempty[g], 16);
         }
         for (int b = 0; b < NACC; ++b) {
-            mbar_init_n(&acc_full[b], 1);
+            mbar_init_n(&acc_full[b], DUAL ? 2 : 1);
             mbar_init_n(&acc_empty[b], 2 * kP7EpiWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -242,48 +250,63 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kP7Threads, 1)
             }
         }
         __syncwarp();
-    } else if (warp == kP7Mma) {
-        if (lane == 0 && rank == 0) {
+    } else if (warp == kP7Mma || warp == kP7Mma2) {
+        const int me = warp - kP7Mma;
+        if (lane == 0 && rank == 0 && (DUAL || me == 0)) {
             const uint32_t tsf = tmem + G::SfCol;
-            const bool prof = MODE == 7 && cid == 0;
-            uint32_t nst = 0;
+            const bool prof = MODE == 7 && cid == 0 && me == 0;
+            volatile uint32_t* tstart = reinterpret_cast<volatile uint32_t*>(tmem_slot + 1);  // tiles started
+            uint32_t nst = 0, gs = 0;
             int s = 0;
             uint32_t ph = 0, it = 0;
             for (uint32_t t = cid; t < NT; t += ncl, ++it) {
                 P7Tile T;
                 if (!p7_tile<NN>(t, probs, GX, GY, T)) { --it; continue; }
                 const uint32_t buf = it % NACC;
-                long long tt = prof ? clock64() : 0;
-                if (it >= NACC) {  // both CTAs' epilogues have drained this accumulator
-                    mbar_wait1(&acc_empty[buf], ((it / NACC) - 1) & 1);
-                    asm volatile("tcgen05.fence::after_thread_sync;");
-                }
-                if (prof) p7_acc(3, tt);
                 const uint32_t d = tmem + buf * G::AccCol;
                 const size_t KB = (T.Q->P.k + 63) / 64;
-                for (size_t kb = 0; kb < KB; kb += KPS) {
-                    if ((MODE == 8 || MODE == 10) && cid == 0) p7_ev(0, nst);
-                    if (POLL) mbar_poll(&full[s], ph);
-                    else mbar_wait1(&full[s], ph);
-                    asm volatile("tcgen05.fence::after_thread_sync;");
-                    if ((MODE == 8 || MODE == 10) && cid == 0) p7_ev(1, nst);
-                    if (prof) p7_acc(0, tt);
-                    const uint32_t bs = sm_u32(btile + size_t(s) * G::BStage);
+                for (size_t kb = 0; kb < KB; kb += KPS, ++gs) {
+                    const bool mine = !DUAL || int(gs & 1) == me;
+                    if (mine) {
+                        long long tt = prof ? clock64() : 0;
+                        if (kb == 0) {
+                            if (it >= NACC) {  // both CTAs' epilogues have drained this accumulator
+                                // DUAL: the other thread may still be behind on this barrier;
+                                // a parity wait is only unambiguous once the previous tile
+                                // has started (its owner passed the phase before ours)
+                                if (DUAL) while (*tstart < it) {}
+                                mbar_wait1(&acc_empty[buf], ((it / NACC) - 1) & 1);
+                                asm volatile("tcgen05.fence::after_thread_sync;");
+                            }
+                        } else if (DUAL) {
+                            while (*tstart <= it) {}  // the tile's first MMA is issued
+                        }
+                        if (prof) p7_acc(3, tt);
+                        if ((MODE == 8 || MODE == 10) && cid == 0) p7_ev(0, nst);
+                        if (POLL) mbar_poll(&full[s], ph);
+                        else mbar_wait1(&full[s], ph);
+                        asm volatile("tcgen05.fence::after_thread_sync;");
+                        if ((MODE == 8 || MODE == 10) && cid == 0) p7_ev(1, nst);
+                        if (prof) p7_acc(0, tt);
+                        const uint32_t bs = sm_u32(btile + size_t(s) * G::BStage);
 #pragma unroll
-                    for (int j = 0; j < KPS; ++j) {
-                        if (kb + j >= KB) break;
-                        if (MODE != 1)
-                            mma_f4_pair_ts(d, tmem + G::ACol + uint32_t(8 * (KPS * s + j)),
-                                           umma_desc(bs + (j >> 1) * G::Slot + 32 * (j & 1)), kb + j > 0 ? 1u : 0u,
-                                           G::Idesc, tsf);
+                        for (int j = 0; j < KPS; ++j) {
+                            if (kb + j >= KB) break;
+                            if (MODE != 1)
+                                mma_f4_pair_ts(d, tmem + G::ACol + uint32_t(8 * (KPS * s + j)),
+                                               umma_desc(bs + (j >> 1) * G::Slot + 32 * (j & 1)),
+                                               kb + j > 0 ? 1u : 0u, G::Idesc, tsf);
+                            if (DUAL && kb == 0 && j == 0) *tstart = it + 1;
+                        }
+                        if (prof) p7_acc(1, tt);
+                        if ((MODE == 8 || MODE == 10) && cid == 0) p7_ev(2, nst);
+                        tc_commit_pair(&empty[s], 0x3);
+                        ++nst;
+                        if (prof) { p7_acc(2, tt); atomicAdd(&g_p7_prof[15], 1ull); }
                     }
-                    if (prof) p7_acc(1, tt);
-                    if ((MODE == 8 || MODE == 10) && cid == 0) p7_ev(2, nst);
-                    tc_commit_pair(&empty[s], 0x3);
-                    ++nst;
-                    if (prof) { p7_acc(2, tt); atomicAdd(&g_p7_prof[15], 1ull); }
                     if (++s == kStages) { s = 0; ph ^= 1; }
                 }
+                // every issuing thread commits every tile (no MMA pending: immediate)
                 tc_commit_pair(&acc_full[buf], 0x3);
             }
         }
@@ -453,6 +476,7 @@ Tc7Cfg make7() {
     Tc7Cfg c;
     // MODE 9: the MMA thread polls `full` with test_wait instead of try_wait
     if (MODE == 9) c.fn = k_gemm_tc7<NN, NACC, STG, KPS, RG, 0, true>;
+    else if (MODE == 11) c.fn = k_gemm_tc7<NN, NACC, STG, KPS, RG, 0, false, false>;
     else c.fn = k_gemm_tc7<NN, NACC, STG, KPS, RG, MODE>;
     c.nn = NN;
     c.smem = P7<NN, NACC, STG, KPS, RG>::Smem;
@@ -477,6 +501,7 @@ const Tc7Cfg& tc7_cfg() {
 #define F2_TC7_PICK(NN, NACC, STG, KPS, RG)                               \
     switch (mode) {                                                       \
         case 10: return make7<NN, NACC, STG, KPS, RG, 10>();              \
+        case 11: return make7<NN, NACC, STG, KPS, RG, 11>();              \
         case 1: return make7<NN, NACC, STG, KPS, RG, 1>();                \
         case 7: return make7<NN, NACC, STG, KPS, RG, 7>();                \
         case 3: return make7<NN, NACC, STG, KPS, RG, 3>();                \
