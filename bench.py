@@ -592,14 +592,14 @@ def measure_update_roofline(f2, lib, _lib, ctx, stream, torch, n: int) -> dict:
             "unit_workload": f"C({n}x{n}) ^= A({n}x64)*B(64x{n})",
             "algorithmic_bytes": alg, "us_per_launch": round(t * 1e6, 1),
             "bitops_per_s": round(n * 64 * n / t, 1),
-            "share_of_step": "22% of the decomposition (profiles/r1_launches_rec_summary.txt)",
+            "share_of_step": "25% of the decomposition's kernel time (profiles/r2_launches_rec_summary.txt)",
             "peak_source": src}
 
 
 def measure_tensor_roofline(f2, lib, _lib, ctx, stream, torch, n: int = 16384) -> dict:
-    """The fp4 tensor-core product leaf (k_gemm_tc3) on C = A*B, n^3 (BASELINE
-    configs[1] shape): fp4 MACs executed = one per (i, j, k), 2 FLOP each.  The
-    timed call includes the B^T staging transpose (~2% of it)."""
+    """The fp4 tensor-core product leaf (k_gemm_tc7, CTA pairs) on C = A*B, n^3
+    (BASELINE configs[1] shape): fp4 MACs executed = one per (i, j, k), 2 FLOP
+    each.  The timed call includes the B^T staging transpose (~2% of it)."""
     Am, Bm, Cm = (f2.DeviceMatrix(n, n, ctx) for _ in range(3))
     Am.random_dense(0.5, 2)
     Bm.random_dense(0.5, 3)
@@ -621,7 +621,7 @@ def measure_tensor_roofline(f2, lib, _lib, ctx, stream, torch, n: int = 16384) -
     peak, src = tensor_peak()
     ach = 2.0 * n ** 3 / t / 1e12
     traffic = None
-    tp = ROOT / "profiles" / "tc3_traffic.json"
+    tp = ROOT / "profiles" / "tc7_traffic.json"
     if tp.exists():
         try:
             traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
@@ -630,10 +630,10 @@ def measure_tensor_roofline(f2, lib, _lib, ctx, stream, torch, n: int = 16384) -
     Am.free(); Bm.free(); Cm.free()
     return {"bound": "tensor", "achieved": round(ach, 1), "peak": round(peak, 1), "unit": "TFLOP/s",
             "frac": round(ach / peak, 4), "traffic": traffic,
-            "kernel": "k_gemm_tc3 (fp4 kind::mxf4 GF(2) product leaf)",
+            "kernel": "k_gemm_tc7 (fp4 kind::mxf4 GF(2) product leaf, cta_group::2, M-side operand in TMEM)",
             "unit_workload": f"C({n}x{n}) = A({n}x{n})*B({n}x{n}), 2*n^3 fp4 FLOP",
             "us_per_launch": round(t * 1e6, 1), "bitops_per_s": round(n ** 3 / t, 1),
-            "share_of_step": "42% of the decomposition (profiles/r1_launches_rec_summary.txt)",
+            "share_of_step": "34% of the decomposition's kernel time (profiles/r2_launches_rec_summary.txt)",
             "peak_source": src}
 
 
