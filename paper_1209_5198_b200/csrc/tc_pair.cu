@@ -514,6 +514,8 @@ const Tc7Cfg& tc7_cfg() {
         if (v == 3) { F2_TC7_PICK(192, 2, 3, 4, 6) }
         if (v == 4) { F2_TC7_PICK(160, 2, 5, 4, 6) }
         if (v == 5) { F2_TC7_PICK(224, 2, 3, 2, 6) }
+        if (v == 6) { F2_TC7_PICK(128, 2, 3, 8, 6) }
+        if (v == 7) { F2_TC7_PICK(160, 2, 2, 8, 6) }
         F2_TC7_PICK(256, 1, 3, 8, 6)
 #undef F2_TC7_PICK
     }();
