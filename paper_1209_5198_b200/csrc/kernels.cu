@@ -322,6 +322,29 @@ __device__ __forceinline__ void lds_tab(uint32_t off, uint32_t& a, uint32_t& b) 
                  : "=r"(a), "=r"(b)
                  : "r"(off), "n"(kTabAddr + T * 16384));
 }
+template <int T>
+__device__ __forceinline__ void lds_tab2(uint32_t off, uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4 + %5];"
+                 : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+                 : "r"(off), "n"(kTabAddr + T * 16384));
+}
+// two adjacent columns (colofs = 16-byte offset of the pair) from one 128-bit load per
+// group: half the index arithmetic and half the shared-load instructions of two lookup9
+template <int T>
+__device__ __forceinline__ void lk2(uint32_t lo, uint32_t hi, uint32_t colofs, uint32_t (&acc)[4]) {
+    uint32_t a, b, c, d;
+    lds_tab2<T>(tab_off<T>(lo, hi, colofs), a, b, c, d);
+    acc[0] ^= a; acc[1] ^= b; acc[2] ^= c; acc[3] ^= d;
+}
+__device__ __forceinline__ void lookup9x2(uint32_t colofs, uint64_t w, uint64_t& d0, uint64_t& d1) {
+    const uint32_t lo = uint32_t(w), hi = uint32_t(w >> 32);
+    uint32_t acc[4] = {0u, 0u, 0u, 0u};
+    lk2<0>(lo, hi, colofs, acc); lk2<1>(lo, hi, colofs, acc); lk2<2>(lo, hi, colofs, acc);
+    lk2<3>(lo, hi, colofs, acc); lk2<4>(lo, hi, colofs, acc); lk2<5>(lo, hi, colofs, acc);
+    lk2<6>(lo, hi, colofs, acc); lk2<7>(lo, hi, colofs, acc); lk2<8>(lo, hi, colofs, acc);
+    d0 = (uint64_t(acc[1]) << 32) | acc[0];
+    d1 = (uint64_t(acc[3]) << 32) | acc[2];
+}
 // all 9 groups (full 64-bit k-block), branch-free
 __device__ __forceinline__ uint64_t lookup9(uint32_t colofs, uint64_t w) {
     const uint32_t lo = uint32_t(w), hi = uint32_t(w >> 32);
@@ -516,6 +539,9 @@ __device__ __forceinline__ void fence_async_smem() {
 // pipe carries only table lookups and the delta stores.  The 128 driving words
 // of each tile come through a separate 8-deep bulk-load ring.  Rows outside
 // [row_lo, row_hi) get a zero delta (the XOR leaves them unchanged).
+#ifndef F2_UPDATE_COL2
+#define F2_UPDATE_COL2 1  // consumer lanes own 2 rows x 2 columns (128-bit lookups); 0: 4 rows x 1 column
+#endif
 constexpr int kV3Warps = 16;                      // consumer warps
 constexpr int kV3Threads = (kV3Warps + 1) * 32;   // + producer warp
 constexpr int kV3Rows = 128;                      // tile rows (lane owns 4)
@@ -780,9 +806,18 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
     }
 
     // ===== consumer warps =====
+#if F2_UPDATE_COL2
+    // lane = (row pair r4 = lane >> 3, column pair c8 = lane & 7): rows 8 w + 2 r4 (+1),
+    // columns 2 c8 (+1) -- one 128-bit table load serves two columns; a quarter-warp
+    // reads one whole 128-byte entry (conflict-free)
+    const int r4 = lane >> 3, c8 = lane & 7;
+    const uint32_t colofs = uint32_t(c8) * 16u;
+    const int rl = 8 * warp + 2 * r4;
+#else
     const int h = lane >> 4, col = lane & 15;
     const uint32_t colofs = uint32_t(col) * 8u;
     const int rl = 8 * warp + 4 * h;  // this lane's 4 rows within the tile
+#endif
     size_t gcur = ~size_t(0);
     TileCursor cc;
     cc.init(T, s0, len0, s1);
@@ -800,6 +835,33 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
             gcur = g;
         }
         mbar_wait(&a_full[as], aph);
+#if F2_UPDATE_COL2
+        const ulonglong2 av = *(reinterpret_cast<const ulonglong2*>(aring + size_t(as) * kV3ABytes) + rl / 2);
+        uint64_t x[2] = {av.x, av.y};
+        const size_t row = base + cc.tt * kV3Rows + rl;
+        if (row < row_lo || row + 2 > row_hi) {
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+                if (row + q < row_lo || row + q >= row_hi) x[q] = 0;
+        }
+        uint64_t d[2][2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) lookup9x2(colofs, x[q], d[q][0], d[q][1]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_empty[as]);
+        if (t >= size_t(kV3DStages)) mbar_wait(&d_free[s], dph ^ 1);
+        // store j writes column 2 c8 + (j ^ hb): the 8 lanes of a quarter-warp then hit 8
+        // distinct column residues mod 8, i.e. 8 distinct 16-byte bank groups at the
+        // 1040-byte column pitch (j alone would pair columns c and c + 8: 2-way conflicts)
+        const int hb = (c8 >> 2) & 1;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int c = j ^ hb;
+            ulonglong2* dp = reinterpret_cast<ulonglong2*>(dring + size_t(s) * kV3DBytes +
+                                                           (2 * c8 + c) * kV3ColPitch) + rl / 2;
+            dp[0] = c ? make_ulonglong2(d[0][1], d[1][1]) : make_ulonglong2(d[0][0], d[1][0]);
+        }
+#else
         const ulonglong2* ap = reinterpret_cast<const ulonglong2*>(aring + size_t(as) * kV3ABytes) + rl / 2;
         uint64_t x[4];
 #pragma unroll
@@ -826,6 +888,7 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
         ulonglong2* dp = reinterpret_cast<ulonglong2*>(dring + size_t(s) * kV3DBytes + col * kV3ColPitch) + rl / 2;
         dp[0] = make_ulonglong2(d[0], d[1]);
         dp[1] = make_ulonglong2(d[2], d[3]);
+#endif
 #if !F2_FENCE_IN_PRODUCER
         fence_async_smem();  // generic-proxy smem writes -> async-proxy bulk reductions
 #endif
