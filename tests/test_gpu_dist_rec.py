@@ -94,3 +94,50 @@ def test_recursive_dist_through_nccl_one_rank(f2, po, monkeypatch):
         assert np.array_equal(W.download().words[:, :n], w[:, :n])
         W.free()
     ctx.close()
+
+
+def test_recursive_sharded_cfg5_digest(f2, ctx, po):
+    """BASELINE configs[4] (262144 x 131072, p = 0.05, 4 GiB) over 8 logical shards."""
+    from paper_1209_5198_b200 import _lib
+
+    p5 = GOLD / "digests_cfg5.json"
+    if not p5.exists():
+        pytest.skip("cfg5 digest not generated")
+    g = json.loads(p5.read_text())["cfg5"]
+    n, m = g["n"], g["m"]
+    A = f2.DeviceMatrix(n, m, ctx)
+    A.random_dense(g["p"], g["seed"])
+    perm = np.zeros(n, np.uint32)
+    rj = np.zeros(m // 64, np.uint32)
+    rk = C.c_size_t()
+    _lib.check(_lib.load().f2gpu_decompose_recursive_sharded(ctx.handle, A.handle, 8, 0, perm.ctypes.data,
+                                                              rj.ctypes.data, C.byref(rk)))
+    assert int(rk.value) == g["rank"]
+    assert po.digest_u32(rj) == g["rj_digest"] and po.digest_u32(perm) == g["perm_digest"]
+    assert po.digest(A.download().words, n, m) == g["w_digest"]
+    A.free()
+
+
+def test_recursive_dist_nccl_cfg4_digest(f2, po, monkeypatch):
+    """The NCCL driver (1-rank communicator) on the bench configuration."""
+    import torch  # noqa: F401
+
+    from paper_1209_5198_b200 import _lib
+
+    monkeypatch.setenv("F2GPU_FORCE_NCCL", "1")
+    g = json.loads((GOLD / "digests.json").read_text())["cfg4"]
+    n = g["n"]
+    ctx = f2.Context(0)
+    ctx.init_comm(0, 1, f2.Context.nccl_unique_id())
+    A = f2.DeviceMatrix(n, n, ctx)
+    A.random_dense(0.5, g["seed"])
+    perm = np.zeros(n, np.uint32)
+    rj = np.zeros(n // 64, np.uint32)
+    rk = C.c_size_t()
+    _lib.check(_lib.load().f2gpu_decompose_recursive_dist(ctx.handle, A.handle, n, 0, perm.ctypes.data,
+                                                          rj.ctypes.data, C.byref(rk)))
+    assert int(rk.value) == g["rank"]
+    assert po.digest_u32(rj) == g["rj_digest"] and po.digest_u32(perm) == g["perm_digest"]
+    assert po.digest(A.download().words, n, n) == g["w_digest"]
+    A.free()
+    ctx.close()
