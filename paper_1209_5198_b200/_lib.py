@@ -10,9 +10,10 @@ Python analogues of the reference's exceptions:
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libf2gpu.so"
+LIB_PATH = Path(os.environ["F2GPU_LIB"]) if os.environ.get("F2GPU_LIB") else Path(__file__).resolve().parent / "libf2gpu.so"  # F2GPU_LIB: A/B builds
 
 OK, EINVAL, ERANGE, ECUDA, ENCCL, ENOMEM = range(6)
 OWN_STREAM = (1 << 64) - 1  # F2GPU_OWN_STREAM (include/f2gpu.h)

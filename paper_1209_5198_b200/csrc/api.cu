@@ -27,9 +27,20 @@
 namespace {
 
 thread_local std::string g_err;
+// F2GPU_SPIN_DIAG=1: host-mapped record of a timed-out cross-kernel wait (kernels.cu
+// SpinGuard), appended to the next CUDA error message; g_diag_flags = the counter base
+unsigned long long* g_diag = nullptr;
+const void* g_diag_flags = nullptr;
 
 int set_err(int code, const std::string& msg) {
     g_err = msg;
+    if (code == F2GPU_ECUDA && g_diag && (g_diag[0] & 1)) {
+        const long long off = static_cast<long long>(g_diag[2]) - reinterpret_cast<long long>(g_diag_flags);
+        char b[256];
+        snprintf(b, sizeof b, " [spin timeout: site %llu block %llu counter +%lld B (panel %lld idx %lld) value %llu target %llu]",
+                 g_diag[0] >> 8, g_diag[1], off, off / 32, (off % 32) / 4, g_diag[3] >> 32, g_diag[3] & 0xffffffffull);
+        g_err += b;
+    }
     return code;
 }
 
@@ -672,6 +683,7 @@ int ensure_scratch(f2gpu_ctx* c, size_t n, size_t mu) {
             cudaFree(c->scr_flags);
             c->scr_flags = nullptr;
             CUDA_TRY(cudaMalloc(&c->scr_flags, mu * 4 * kFlagsPerPanel));
+            g_diag_flags = c->scr_flags;
             c->scr_flags_cap = mu;
         }
     }
@@ -1653,6 +1665,15 @@ int f2gpu_ctx_create(int device, f2gpu_ctx** out) {
     if (const char* tcc = getenv("F2GPU_TC_CUT")) {
         c->tc_cutover = size_t(atoll(tcc));
         c->use_tc_cut_default = false;
+    }
+    if (const char* sd = getenv("F2GPU_SPIN_DIAG"); sd && sd[0] == '1' && !g_diag) {
+        void* h = nullptr;
+        CUDA_TRY(cudaHostAlloc(&h, 64, cudaHostAllocMapped));
+        memset(h, 0, 64);
+        void* d = nullptr;
+        CUDA_TRY(cudaHostGetDevicePointer(&d, h, 0));
+        CUDA_TRY(f2::spin_diag_set(static_cast<unsigned long long*>(d)));
+        g_diag = static_cast<unsigned long long*>(h);
     }
     CUDA_TRY(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&c->side2, cudaStreamNonBlocking));

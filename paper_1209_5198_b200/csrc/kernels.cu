@@ -38,16 +38,37 @@ __device__ __forceinline__ uint64_t gtimer() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+// F2GPU_SPIN_DIAG=1 (diagnostics): a timed-out wait records where it was stuck in
+// host-mapped memory (readable after the trap killed the context; api.cu appends it
+// to the error message):
+//   [0] = 1 | site << 8, [1] = block, [2] = the counter's address, [3] = its last
+//   value << 32 | the target
+__device__ unsigned long long* g_spin_diag = nullptr;
 struct SpinGuard {
     uint64_t t0 = 0;
     uint32_t polls = 0;
-    __device__ __forceinline__ void tick() {
+    __device__ __forceinline__ void tick(uint32_t site = 0, const void* addr = nullptr, uint32_t v = 0,
+                                         uint32_t target = 0) {
         if ((++polls & 1023u) != 0) return;
         const uint64_t now = gtimer();
         if (t0 == 0) t0 = now;
-        else if (now - t0 > kSpinLimitNs) __trap();
+        else if (now - t0 > kSpinLimitNs) {
+            if (unsigned long long* d = g_spin_diag) {
+                d[1] = blockIdx.x;
+                d[2] = reinterpret_cast<unsigned long long>(addr);
+                d[3] = (uint64_t(v) << 32) | target;
+                __threadfence_system();
+                d[0] = 1ull | (uint64_t(site) << 8);
+                __threadfence_system();
+            }
+            __trap();
+        }
     }
 };
+
+cudaError_t spin_diag_set(unsigned long long* mapped) {
+    return cudaMemcpyToSymbol(g_spin_diag, &mapped, sizeof(mapped));
+}
 
 __device__ __forceinline__ void trace_ev(uint32_t ev, int j) {
     unsigned long long* b = g_trace;
@@ -1371,7 +1392,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
                 asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(wait_flag) : "memory");
                 if (v >= wait_count) break;
                 __nanosleep(64);
-                g.tick();
+                g.tick(1, wait_flag, v, wait_count);
             }
         }
         __syncthreads();
@@ -1730,7 +1751,7 @@ struct GjStep {
     uint32_t sw[kGjWords];
 };
 
-__device__ __forceinline__ void wait_count_ge(const uint32_t* flag, uint32_t count) {
+__device__ __forceinline__ void wait_count_ge(const uint32_t* flag, uint32_t count, uint32_t site = 2) {
     if (!flag) return;
     uint32_t v;
     SpinGuard g;
@@ -1738,13 +1759,13 @@ __device__ __forceinline__ void wait_count_ge(const uint32_t* flag, uint32_t cou
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
         if (v >= count) break;
         __nanosleep(32);
-        g.tick();
+        g.tick(site, flag, v, count);
     }
 }
 
 // the whole warp spins (no lane-divergent loop: a warp that diverged around a
 // long spin can stay split afterwards and run every later shuffle twice)
-__device__ __forceinline__ void wait_count_ge_warp(const uint32_t* flag, uint32_t count) {
+__device__ __forceinline__ void wait_count_ge_warp(const uint32_t* flag, uint32_t count, uint32_t site = 3) {
     if (!flag) return;
     SpinGuard g;
     while (true) {
@@ -1752,7 +1773,7 @@ __device__ __forceinline__ void wait_count_ge_warp(const uint32_t* flag, uint32_
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
         if (__all_sync(0xffffffffu, v >= count)) break;
         __nanosleep(32);
-        g.tick();
+        g.tick(site, flag, v, count);
     }
 }
 
@@ -1765,7 +1786,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
     // every warp waits for the previous panel's head chunk (or the fused post's
     // head) before reading its state: the kernel may be queued on another stream
     // and resident while the previous panel kernel still runs
-    wait_count_ge_warp(link.head, link.head_count);
+    wait_count_ge_warp(link.head, link.head_count, 10);
     const size_t R = j == 0 ? 0 : size_t(st_all[j - 1].R) + st_all[j - 1].r;
     PanelState* st = st_all + j;
     const size_t rows = R < n ? n - R : 0;
@@ -1832,7 +1853,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
         asm volatile("bar.sync 3, 96;" ::: "memory");  // the log is zeroed
     } else {
         // warps 2..7 load the window; warp 2 then replays the swaps on it
-        if (warp == 2) wait_count_ge_warp(link.win, link.win_count);
+        if (warp == 2) wait_count_ge_warp(link.win, link.win_count, 11);
         asm volatile("bar.sync 2, 192;" ::: "memory");
         for (uint32_t x = tid - 64; x < winrows; x += kPanelThreads - 64) {
             S.win[x] = A[x];
@@ -1986,7 +2007,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
         if (lane == 0) st->npairs = np;
         // column j+1 is final for the earlier panels once the previous update has
         // released it: needed by the swaps below AND by the head chunk's reads
-        if (link.next) wait_count_ge_warp(link.next_ready, link.next_count);
+        if (link.next) wait_count_ge_warp(link.next_ready, link.next_count, 13);
         if (link.next && np) {
             // this panel's row swaps on column j+1 (the fused POST skips it)
             __threadfence_block();
@@ -2192,7 +2213,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
             ++n_slow;
 #endif
             if (lane == 0) st_volatile(&S.want, ib + 1);
-            wait_count_ge_warp(link.all, link.all_count);  // rows beyond the window
+            wait_count_ge_warp(link.all, link.all_count, 14);  // rows beyond the window
             while (!__all_sync(0xffffffffu, ld_volatile(&S.done) == ib + 1)) {}
             __syncwarp();
             __threadfence_block();
@@ -2556,7 +2577,7 @@ __global__ void __launch_bounds__(256) k_post_col(uint64_t* __restrict__ w, size
                 asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(wait_panel) : "memory");
                 if (__all_sync(0xffffffffu, v != 0)) break;
                 __nanosleep(128);
-                g.tick();
+                g.tick(4, wait_panel, v, 1);
             }
         }
         __syncthreads();

@@ -71,6 +71,7 @@ enum TraceEvent : uint32_t {
     kTrUpdBegin = 7, kTrUpdRelease = 8, kTrUpdEnd = 9,
 };
 cudaError_t trace_set(unsigned long long* buf, uint32_t cap);  // buf = nullptr: off
+cudaError_t spin_diag_set(unsigned long long* mapped);            // device view of host-mapped memory
 cudaError_t trace_count(uint32_t* n);
 
 struct GemmArgs {

@@ -47,7 +47,10 @@ names = {0: "P.w1end", 1: "P.begin", 2: "P.chain_end", 3: "P.end", 4: "post.begi
          7: "U.begin", 8: "U.release", 9: "U.end", 10: "U0.tab0", 11: "U0.tile0", 12: "U0.end", 13: "P.done", 14: "U0.state", 15: "U0.barriers"}
 mu = w // 64
 T = {k: np.full(mu, np.nan) for k in names}
+post_blk = [((ti - t0) / 1000.0, ji) for ti, ci, ji in zip(t, code, j) if ci == 0]  # lean post block starts
 for ti, ci, ji in zip(t, code, j):
+    if ci == 0:
+        continue
     if ci in T and ji < mu and np.isnan(T[ci][ji]):
         T[ci][ji] = (ti - t0) / 1000.0  # us
 
@@ -83,3 +86,25 @@ rows = [
 ]
 for name, v in rows:
     print(f"{name:34s} {med(v)}")
+if len(sys.argv) > 3:  # dump panels [a, a+k): event times relative to P(j) begin (us)
+    a, k = int(sys.argv[3]), int(sys.argv[4]) if len(sys.argv) > 4 else 6
+    cols = [(1, "P.beg"), (2, "P.chn"), (3, "P.end"), (13, "P.done"), (4, "po.beg"), (5, "po.head"), (6, "po.end"),
+            (7, "U.beg"), (8, "U.rel"), (12, "U0.end")]
+    print("panel " + " ".join(f"{nm:>8s}" for _, nm in cols) + "   (U(j-1).end0  U(j-1).beg)")
+    for jj in range(a, min(mu, a + k)):
+        b0 = T[1][jj]
+        vals = " ".join(f"{T[c][jj] - b0:8.2f}" for c, _ in cols)
+        prev = f"{T[12][jj - 1] - b0:8.2f} {T[7][jj - 1] - b0:8.2f}" if jj > 0 else ""
+        print(f"{jj:5d} {vals}   ({prev})")
+    if post_blk:
+        jj = a + 1
+        lo, hi = T[4][jj] - 0.5, T[6][jj] + 0.5
+        sel = sorted(x for x in post_blk if lo <= x[0] <= hi)
+        if sel:
+            b0 = T[1][jj]
+            ts = np.array([x[0] - b0 for x in sel])
+            sms = np.array([x[1] for x in sel])
+            print(f"post({jj}) block starts: {len(sel)} in [{ts.min():.2f}, {ts.max():.2f}] us after P({jj}) begin; "
+                  f"{len(set(sms.tolist()))} distinct SMs; U({jj-1}) CTA0 end at {T[12][jj-1]-b0:.2f}")
+            for q in (0.1, 0.25, 0.5, 0.75, 0.9):
+                print(f"   {q:4.2f} quantile start {np.quantile(ts, q):7.2f}")
