@@ -55,6 +55,13 @@ typedef struct f2gpu_mat f2gpu_mat; /* device-resident packed matrix (owning) */
 const char *f2gpu_last_error(void);
 const char *f2gpu_version(void);
 
+/* Every switch of the library (environment variables, read once; all of them select
+ * among bit-identical paths, tune a size, or turn on a diagnostic) as a text table:
+ * one line per switch, "NAME value[*] (default D) meaning", * = set in the
+ * environment.  Writes at most cap-1 bytes + NUL into buf (buf may be NULL);
+ * *len (if non-NULL) = the full length. */
+int f2gpu_options_describe(char *buf, size_t cap, size_t *len);
+
 /* ---- context -------------------------------------------------------------- */
 int f2gpu_ctx_create(int device, f2gpu_ctx **out);
 int f2gpu_ctx_destroy(f2gpu_ctx *ctx);

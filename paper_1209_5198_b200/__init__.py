@@ -281,6 +281,17 @@ class Context:
 _default: Context | None = None
 
 
+def options() -> str:
+    """Every switch of the library (csrc/options.h) with the value in effect: one line per
+    environment variable, "NAME value[*] (default D) meaning" (* = set in the environment)."""
+    lib = _lib.load()
+    n = C.c_size_t()
+    _lib.check(lib.f2gpu_options_describe(None, 0, C.byref(n)), "options_describe")
+    buf = C.create_string_buffer(n.value + 1)
+    _lib.check(lib.f2gpu_options_describe(buf, n.value + 1, None), "options_describe")
+    return buf.value.decode()
+
+
 def default_context() -> Context:
     global _default
     if _default is None:

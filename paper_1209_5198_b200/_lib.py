@@ -25,7 +25,7 @@ class F2GpuError(RuntimeError):
 
 # every exported symbol declared in include/f2gpu.h
 SYMBOLS = [
-    "f2gpu_last_error", "f2gpu_version",
+    "f2gpu_last_error", "f2gpu_version", "f2gpu_options_describe",
     "f2gpu_ctx_create", "f2gpu_ctx_destroy", "f2gpu_ctx_set_stream", "f2gpu_ctx_sync",
     "f2gpu_ctx_launches", "f2gpu_ctx_set_strassen_cutover", "f2gpu_ctx_set_tc",
     "f2gpu_mat_alloc", "f2gpu_mat_free", "f2gpu_mat_shape", "f2gpu_mat_device_ptr",
@@ -52,6 +52,7 @@ u32p = C.POINTER(C.c_uint32)
 _SIG = {
     "f2gpu_last_error": ([], C.c_char_p),
     "f2gpu_version": ([], C.c_char_p),
+    "f2gpu_options_describe": ([C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)], C.c_int),
     "f2gpu_ctx_create": ([C.c_int, C.POINTER(vp)], C.c_int),
     "f2gpu_ctx_destroy": ([vp], C.c_int),
     "f2gpu_ctx_set_stream": ([vp, vp], C.c_int),
@@ -136,6 +137,8 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         _build.build()
     lib = C.CDLL(str(LIB_PATH))
     for name, (args, res) in _SIG.items():
+        if os.environ.get("F2GPU_LIB") and not hasattr(lib, name):
+            continue  # an older build selected for an A/B run
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res

@@ -17,7 +17,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libf2gpu.so"
 SOURCES = [CSRC / "kernels.cu", CSRC / "tc_leaf.cu", CSRC / "tc_pair.cu", CSRC / "tc_update.cu", CSRC / "api.cu"]
-HEADERS = [CSRC / "kernels.cuh", CSRC / "tc_common.cuh", ROOT / "include" / "f2gpu.h"]
+HEADERS = [CSRC / "kernels.cuh", CSRC / "tc_common.cuh", CSRC / "options.h", ROOT / "include" / "f2gpu.h"]
 
 # F2GPU_BUILD_EXPERIMENTAL=1 also compiles the evaluated-and-rejected variants
 # (int8 leaves, single-CTA pair / persistent / double-buffered fp4 leaves, the

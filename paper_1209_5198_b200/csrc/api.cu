@@ -21,8 +21,35 @@
 
 #include "../../include/f2gpu.h"
 #include "kernels.cuh"
+#include "options.h"
 
 #define F2GPU_VERSION "0.2.0"
+
+namespace f2 {
+// options.h: the environment read once.  A value is parsed after any leading
+// non-digits ("i8" -> 8); an unparsable one keeps the default.
+const Options& options() {
+    static const Options o = [] {
+        Options r;
+        auto rd = [](const char* env, long long& v, bool& set) {
+            const char* e = getenv(env);
+            if (!e) return;
+            const char* q = e;
+            while (*q && !(*q >= '0' && *q <= '9') && *q != '-') ++q;
+            char* end = nullptr;
+            const long long x = strtoll(q, &end, 10);
+            if (end == q) return;
+            v = x;
+            set = true;
+        };
+#define F2_OPT_READ(field, env, def, doc) rd(env, r.field, r.field##_set);
+        F2_OPTIONS(F2_OPT_READ)
+#undef F2_OPT_READ
+        return r;
+    }();
+    return o;
+}
+}  // namespace f2
 
 namespace {
 
@@ -1095,22 +1122,21 @@ int decompose_recursive(f2gpu_ctx* c, View w, size_t min_cols, uint32_t* perm, u
     // -> 87.6 ms (8192: 93.4, 32768: 88.9), see DESIGN.md
     RecRun r{c, &s, n, mu, std::max<size_t>(1, (min_cols ? min_cols : 256 * 64) / 64),
              lookahead_ok(c, s, n), 16384, 16};
-    if (const char* e = getenv("F2GPU_REC_CUT")) r.cut = size_t(atol(e));
-    if (const char* e = getenv("F2GPU_REC_BASE")) r.base = std::max<size_t>(1, size_t(atol(e)));
-    if (const char* e = getenv("F2GPU_REC_TBASE")) r.tbase = std::max<size_t>(1, size_t(atol(e)));
-    if (const char* e = getenv("F2GPU_REC_TRSM")) r.trsm_kernel = e[0] != '0';
+    const f2::Options& o = f2::options();
+    r.cut = size_t(o.rec_cut);
+    if (o.rec_base_set) r.base = std::max<size_t>(1, size_t(o.rec_base));
+    r.tbase = std::max<size_t>(1, size_t(o.rec_tbase));
+    r.trsm_kernel = o.rec_trsm != 0;
     // tall leaves: 128 panels once a leaf has >= 20000 rows below its first panel
     // (65536^2 sweeps over 12000..56000 rows x 32..128 panels; first 70.5 -> 67.5 ms
     // with 64 panels, re-swept after the panel-chain work: 128 panels 64.3 ms,
     // 64: 64.6, 32: 66.3)
-    r.tall_rows = 20000;
-    if (const char* e = getenv("F2GPU_REC_TALL")) r.tall_rows = size_t(atol(e));
-    r.tall_base = 128;
+    r.tall_rows = size_t(o.rec_tall);
+    r.tall_base = std::max<size_t>(1, size_t(o.rec_tall_base));
     if (!r.c->use_tc_cut_default) r.tc_cut = r.c->tc_cutover;  // set explicitly (F2GPU_TC_CUT / ctx_set_tc)
-    if (const char* e = getenv("F2GPU_REC_TC_CUT")) r.tc_cut = size_t(atol(e));
-    if (const char* e = getenv("F2GPU_REC_FINAL")) r.final_base = size_t(atol(e));
-    if (const char* e = getenv("F2GPU_TRSM_M4RM_K")) r.trsm_m4rm_k = size_t(atol(e));
-    if (const char* e = getenv("F2GPU_REC_TALL_BASE")) r.tall_base = std::max<size_t>(1, size_t(atol(e)));
+    if (o.rec_tc_cut_set || r.c->use_tc_cut_default) r.tc_cut = size_t(o.rec_tc_cut);
+    r.final_base = size_t(o.rec_final);
+    r.trsm_m4rm_k = size_t(o.trsm_m4rm_k);
     r.on_final = std::move(on_final);
     if (pend && frontier < mu) {
         r.frontier = r.frontier0 = frontier;
@@ -1123,7 +1149,7 @@ int decompose_recursive(f2gpu_ctx* c, View w, size_t min_cols, uint32_t* perm, u
     c->tl.mark(c->stream, "start");
     F2_TRY(check_launch(c, f2::launch_iota(s.perm, n, c->stream), "k_iota"));
     std::map<std::string, RecRun::Phase> phases;
-    if (const char* e = getenv("F2GPU_REC_TIMES"); e && e[0] == '1') r.phases = &phases;
+    if (f2::options().rec_times) r.phases = &phases;
     F2_TRY(rec_decompose(r, 0, mu));
     if (r.phases) {
         CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -1586,11 +1612,10 @@ struct DistGpu {
 // leaf geometry shared with the single-GPU recursion (decompose_recursive)
 void rec_leaf_params(size_t min_cols, size_t* base, size_t* tall_rows, size_t* tall_base) {
     *base = std::max<size_t>(1, (min_cols ? min_cols : 256 * 64) / 64);
-    *tall_rows = 20000;
-    *tall_base = 128;
-    if (const char* e = getenv("F2GPU_REC_BASE")) *base = std::max<size_t>(1, size_t(atol(e)));
-    if (const char* e = getenv("F2GPU_REC_TALL")) *tall_rows = size_t(atol(e));
-    if (const char* e = getenv("F2GPU_REC_TALL_BASE")) *tall_base = std::max<size_t>(1, size_t(atol(e)));
+    const f2::Options& o = f2::options();
+    *tall_rows = size_t(o.rec_tall);
+    *tall_base = std::max<size_t>(1, size_t(o.rec_tall_base));
+    if (o.rec_base_set) *base = std::max<size_t>(1, size_t(o.rec_base));
 }
 
 int run_dist_recursive(f2gpu_ctx* c, std::vector<Shard>& sh, int base, int G, size_t n, size_t mu, size_t min_cols,
@@ -1621,6 +1646,25 @@ const char* f2gpu_version(void) {
 #endif
 }
 
+int f2gpu_options_describe(char* buf, size_t cap, size_t* len) {
+    std::string t;
+    const f2::Options& o = f2::options();
+    char line[512];
+#define F2_OPT_DESC(field, env, def, doc)                                                                  \
+    snprintf(line, sizeof line, "%-24s %8lld%s  (default %lld)  %s\n", env, o.field, o.field##_set ? "*" : " ", \
+             (long long)(def), doc);                                                                       \
+    t += line;
+    F2_OPTIONS(F2_OPT_DESC)
+#undef F2_OPT_DESC
+    if (len) *len = t.size();
+    if (buf && cap) {
+        const size_t k = std::min(cap - 1, t.size());
+        memcpy(buf, t.data(), k);
+        buf[k] = 0;
+    }
+    return F2GPU_OK;
+}
+
 int f2gpu_ctx_create(int device, f2gpu_ctx** out) {
     if (!out) return set_err(F2GPU_EINVAL, "ctx_create: null out");
     *out = nullptr;
@@ -1647,26 +1691,29 @@ int f2gpu_ctx_create(int device, f2gpu_ctx** out) {
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
         }
     }
-    if (const char* pf = getenv("F2GPU_PROFILE")) c->tl.on = pf[0] == '1';
-    if (const char* gr = getenv("F2GPU_GRAPHS")) c->use_graphs = gr[0] != '0';
-    if (const char* la = getenv("F2GPU_LOOKAHEAD")) c->lookahead = la[0] != '0';
-    if (const char* lc = getenv("F2GPU_LOOKAHEAD_COL")) c->lookahead_col = lc[0] != '0';
-    if (const char* pc = getenv("F2GPU_POSTCOL")) c->fuse_post = pc[0] != '0';
-    if (const char* pe = getenv("F2GPU_PANEL_EARLY")) c->panel_early = pe[0] != '0';
-    if (const char* pn = getenv("F2GPU_POLL_NS")) c->poll_ns = uint32_t(atoi(pn));
-    if (const char* uf = getenv("F2GPU_U_FIRSTCOL")) c->u_first_col = uf[0] != '0';
-    if (const char* e = getenv("F2GPU_U_FC_CTAS")) c->u_fc_ctas = atoi(e);
-    if (const char* e = getenv("F2GPU_U_FC_W")) c->u_fc_weight = std::max(1, std::min(4, atoi(e)));
-    if (const char* ph = getenv("F2GPU_PANEL_HEAD")) c->panel_head = ph[0] != '0';
-    if (const char* ps = getenv("F2GPU_POST_SPIN")) c->post_spin = ps[0] != '0';
-    if (const char* pd = getenv("F2GPU_PDL")) c->pdl = pd[0] != '0';
-    if (const char* ph2 = getenv("F2GPU_PANEL_HAND")) c->panel_hand = ph2[0] != '0';
-    if (const char* tc = getenv("F2GPU_TC")) c->use_tc = tc[0] != '0';
-    if (const char* tcc = getenv("F2GPU_TC_CUT")) {
-        c->tc_cutover = size_t(atoll(tcc));
-        c->use_tc_cut_default = false;
+    {  // the schedule switches (options.h)
+        const f2::Options& o = f2::options();
+        c->tl.on = o.profile != 0;
+        c->use_graphs = o.graphs != 0;
+        c->lookahead = o.lookahead != 0;
+        c->lookahead_col = o.lookahead_col != 0;
+        c->fuse_post = o.postcol != 0;
+        c->panel_early = o.panel_early != 0;
+        c->poll_ns = uint32_t(std::max<long long>(0, o.poll_ns));
+        c->u_first_col = o.u_firstcol != 0;
+        c->u_fc_ctas = int(o.u_fc_ctas);
+        c->u_fc_weight = int(std::max<long long>(1, std::min<long long>(4, o.u_fc_w)));
+        c->panel_head = o.panel_head != 0;
+        c->post_spin = o.post_spin != 0;
+        c->pdl = o.pdl != 0;
+        c->panel_hand = o.panel_hand != 0;
+        c->use_tc = o.tc != 0;
+        if (o.tc_cut_set) {
+            c->tc_cutover = size_t(o.tc_cut);
+            c->use_tc_cut_default = false;
+        }
     }
-    if (const char* sd = getenv("F2GPU_SPIN_DIAG"); sd && sd[0] == '1' && !g_diag) {
+    if (f2::options().spin_diag && !g_diag) {
         void* h = nullptr;
         CUDA_TRY(cudaHostAlloc(&h, 64, cudaHostAllocMapped));
         memset(h, 0, 64);
@@ -1972,8 +2019,7 @@ int f2gpu_gemm_tc(f2gpu_ctx* c, const f2gpu_mat* a, const f2gpu_mat* b, f2gpu_ma
         return set_err(F2GPU_EINVAL, "gemm_tc: shape mismatch");
 #if F2GPU_EXPERIMENTAL
     static const int kind = [] {
-        const char* e = getenv("F2GPU_TC_KIND");  // evaluation switch: "i8" selects the int8 leaf
-        return (e && e[0] == 'i') ? 8 : 4;
+        return f2::options().tc_kind == 8 ? 8 : 4;  // evaluation switch: the int8 leaf
     }();
 #else
     constexpr int kind = 4;
@@ -2337,18 +2383,16 @@ int f2gpu_decompose_recursive_host(f2gpu_ctx* c, const uint64_t* a, size_t n, si
     // first chunk = the recursion's first leaf (tall leaves are narrower)
     size_t cw = std::max<size_t>(1, (min_cols ? min_cols : 256 * 64) / 64);
     {
-        size_t tall = 20000, tall_base = 128;
-        if (const char* e = getenv("F2GPU_REC_TALL")) tall = size_t(atol(e));
-        if (const char* e = getenv("F2GPU_REC_TALL_BASE")) tall_base = std::max<size_t>(1, size_t(atol(e)));
-        if (const char* e = getenv("F2GPU_REC_BASE")) cw = std::max<size_t>(1, size_t(atol(e)));
+        const f2::Options& o = f2::options();
+        const size_t tall = size_t(o.rec_tall), tall_base = std::max<size_t>(1, size_t(o.rec_tall_base));
+        if (o.rec_base_set) cw = std::max<size_t>(1, size_t(o.rec_base));
         if (tall && n >= tall) cw = std::min(cw, tall_base);
         // first leaf = upload chunk width (F2GPU_REC_FIRST; 65536^2 e2e: 128: 67.83 ms,
         // 64: 67.36, 32: 67.40-67.45, 16: 67.62 at the same 63.2 ms device time)
-        size_t first = 64;
-        if (const char* e = getenv("F2GPU_REC_FIRST")) first = std::max<size_t>(1, size_t(atol(e)));
+        const size_t first = std::max<size_t>(1, size_t(o.rec_first));
         cw = std::min(cw, first);
     }
-    if (n == 0 || mu <= cw || !a || getenv("F2GPU_NO_UPLOAD_OVERLAP")) {
+    if (n == 0 || mu <= cw || !a || f2::options().no_upload_overlap) {
         F2_TRY(f2gpu_mat_upload(c, W, a, stride));
         F2_TRY(f2gpu_decompose_recursive(c, W, min_cols, perm, rj, rank));
     } else {
@@ -2436,8 +2480,7 @@ int f2gpu_ctx_init_comm(f2gpu_ctx* c, int rank, int world, const void* id) {
     c->world = world;
     // world == 1 needs no communicator; F2GPU_FORCE_NCCL=1 builds a 1-rank one so
     // the NCCL exchange path can be exercised on a single GPU.
-    const char* force = getenv("F2GPU_FORCE_NCCL");
-    if (world == 1 && !(force && force[0] == '1')) return F2GPU_OK;
+    if (world == 1 && !f2::options().force_nccl) return F2GPU_OK;
     NcclApi& api = nccl();
     if (!api.ok) return set_err(F2GPU_ENCCL, api.why);
     CUDA_TRY(cudaSetDevice(c->device));

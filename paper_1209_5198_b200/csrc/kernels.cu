@@ -10,6 +10,7 @@
 //   k_xor           block XOR for Strassen-Winograd        (bit_matrix.hpp:241-250)
 //   k_transpose     64x64 bit-tile transpose               (bit_matrix.hpp:59-70,220-238)
 #include "kernels.cuh"
+#include "options.h"
 
 #include <algorithm>
 
@@ -2930,8 +2931,8 @@ cudaError_t init_kernel_attrs() {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_panel_gj, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(kPanelGjSmemMax));
-    if (const char* ps = getenv("F2GPU_PANEL_SMEM")) kPanelGjSmemBytes = ps[0] != '0' ? kPanelGjSmemMax : sizeof(PanelGjSmem);
-    if (const char* pk = getenv("F2GPU_PANEL")) g_panel_gj = pk[0] != '0';
+    kPanelGjSmemBytes = options().panel_smem ? kPanelGjSmemMax : sizeof(PanelGjSmem);
+    g_panel_gj = options().panel != 0;
     return e;
 }
 

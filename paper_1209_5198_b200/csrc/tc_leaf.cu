@@ -21,6 +21,7 @@
 #include <cstdlib>
 
 #include "kernels.cuh"
+#include "options.h"
 #include "tc_common.cuh"
 
 namespace f2 {
@@ -1228,8 +1229,7 @@ cudaError_t launch_gemm_tc2(const uint64_t* A, size_t sa, const uint64_t* BT, si
                                                  int(kT2Smem));
             if (e != cudaSuccess) return e;
         }
-        const char* env = getenv("F2GPU_TC_MODE");
-        mode = env ? atoi(env) : 0;
+        mode = int(options().tc_mode);
         attr = true;
     }
     if (!gemm_tc2_ok(n, k, m) || (sbt % 2) || (sa % 2) ||
@@ -1472,13 +1472,11 @@ Tc5Fn tc5_fn() {
         tried = true;
         // opt-in: at 65536^2 it measured no faster (64.66-64.71 ms for k <= 1024..4096
         // vs 64.71 without), and its main loop is ~9% slower at large k
-        const char* pe = getenv("F2GPU_TC_PERSIST");
-        if (!pe || pe[0] != '1') return nullptr;
+        if (options().tc_persist != 1) return nullptr;
         for (auto f : {k_gemm_tc5<0>, k_gemm_tc5<1>, k_gemm_tc5<2>, k_gemm_tc5<3>})
             if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kT3Smem)) != cudaSuccess)
                 return nullptr;
-        const char* env = getenv("F2GPU_TC_MODE");
-        const int mode = env ? atoi(env) : 0;
+        const int mode = int(options().tc_mode);
         fn = mode == 1 ? k_gemm_tc5<1> : mode == 2 ? k_gemm_tc5<2> : mode == 3 ? k_gemm_tc5<3> : k_gemm_tc5<0>;
     }
     return fn;
@@ -1491,8 +1489,7 @@ using Tc6Fn = void (*)(TcGemmArgs, const TcGemmArgs*, uint32_t, uint32_t, uint32
 // showed no gain (64.08 vs 64.13 ms at k <= 1024).
 size_t tc6_max_k() {
     static const size_t v = [] {
-        const char* e = getenv("F2GPU_TC6_MAXK");
-        return e ? size_t(atoll(e)) : size_t(0);
+        return size_t(std::max<long long>(0, options().tc6_maxk));
     }();
     return v;
 }
@@ -1505,15 +1502,13 @@ Tc6Fn tc6_fn() {
         for (auto f : {k_gemm_tc6<0>, k_gemm_tc6<2>})
             if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kT6Smem)) != cudaSuccess)
                 return nullptr;
-        const char* env = getenv("F2GPU_TC_MODE");
-        fn = (env && atoi(env) == 2) ? k_gemm_tc6<2> : k_gemm_tc6<0>;
+        fn = options().tc_mode == 2 ? k_gemm_tc6<2> : k_gemm_tc6<0>;
     }
     return fn;
 }
 size_t tc5_max_k() {  // F2GPU_TC5_MAXK (default 2048)
     static const size_t v = [] {
-        const char* e = getenv("F2GPU_TC5_MAXK");
-        return e ? size_t(atoll(e)) : size_t(2048);
+        return size_t(std::max<long long>(0, options().tc5_maxk));
     }();
     return v;
 }
@@ -1537,8 +1532,7 @@ Tc3Fn tc3_fn() {
         for (auto f : {k_gemm_tc3<0>, k_gemm_tc3<1>, k_gemm_tc3<2>, k_gemm_tc3<3>})
             if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kT3Smem)) != cudaSuccess)
                 return nullptr;
-        const char* env = getenv("F2GPU_TC_MODE");
-        const int mode = env ? atoi(env) : 0;
+        const int mode = int(options().tc_mode);
         fn = mode == 1 ? k_gemm_tc3<1> : mode == 2 ? k_gemm_tc3<2> : mode == 3 ? k_gemm_tc3<3> : k_gemm_tc3<0>;
     }
     return fn;
@@ -1551,8 +1545,7 @@ Tc3Fn tc3_fn() {
 // simpler single-CTA kernel stays the default.
 bool tc4_use(size_t m) {
     static const int on = [] {
-        const char* e = getenv("F2GPU_TC_PAIR");
-        if (!e || e[0] != '1') return 0;
+        if (options().tc_pair != 1) return 0;
         return cudaFuncSetAttribute(k_gemm_tc4, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kT4Smem)) ==
                        cudaSuccess
                    ? 1

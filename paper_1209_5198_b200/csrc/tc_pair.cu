@@ -45,6 +45,7 @@
 #include <vector>
 
 #include "kernels.cuh"
+#include "options.h"
 #include "tc_common.cuh"
 
 namespace f2 {
@@ -493,10 +494,8 @@ Tc7Cfg make7() {
 // F2GPU_TC7_MODE: diagnostics (see k_gemm_tc7)
 const Tc7Cfg& tc7_cfg() {
     static const Tc7Cfg cfg = [] {
-        const char* e = getenv("F2GPU_TC7");
-        const int v = e ? atoi(e) : 1;
-        const char* me = getenv("F2GPU_TC7_MODE");
-        const int mode = me ? atoi(me) : 0;
+        const int v = int(options().tc7);
+        const int mode = int(options().tc7_mode);
         if (v == 0) return Tc7Cfg{};
 #define F2_TC7_PICK(NN, NACC, STG, KPS, RG)                               \
     switch (mode) {                                                       \

@@ -48,6 +48,7 @@
 // update_tc_release_count() increments in total).
 #include <cstdint>
 #include <cstdlib>
+#include "options.h"
 
 #include "kernels.cuh"
 #include "tc_common.cuh"
@@ -439,7 +440,7 @@ cudaError_t launch_update_tc(const TcUpdateArgs& a, int grid, cudaStream_t s) {
             cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(UtSmem)));
             if (e != cudaSuccess) return e;
         }
-        if (const char* env = getenv("F2GPU_UT_MODE")) mode = atoi(env) & 31;
+        mode = int(options().ut_mode) & 31;
         attr = true;
     }
     if (!update_tc_ok(a)) return cudaErrorInvalidValue;

@@ -115,3 +115,27 @@ def test_cpp_shim_compiles_against_reference(name):
            "-o", str(out), f"-L{_lib.LIB_PATH.parent}", "-lf2gpu",
            f"-Wl,-rpath,{_lib.LIB_PATH.parent}"]
     subprocess.run(cmd, check=True)
+
+
+def test_every_switch_is_in_the_options_table():
+    """csrc/options.h is the one place the library reads its environment: every F2GPU_*
+    name in the sources is a row of the table, no source calls getenv() directly (except
+    the table's reader), and f2gpu_options_describe() lists every row with its default."""
+    import paper_1209_5198_b200 as f2
+
+    csrc = ROOT / "paper_1209_5198_b200" / "csrc"
+    table = (csrc / "options.h").read_text()
+    rows = set(re.findall(r'X\(\w+, "(F2GPU_\w+)"', table))
+    assert len(rows) >= 35
+    for src in csrc.glob("*.cu"):
+        text = src.read_text()
+        calls = re.findall(r"\bgetenv\(", text)
+        assert len(calls) == (1 if src.name == "api.cu" else 0), (src.name, len(calls))
+        for name in set(re.findall(r'"(F2GPU_[A-Z0-9_]+)"', text)):
+            assert name in rows, (src.name, name)
+    desc = f2.options()
+    listed = re.findall(r"^(F2GPU_\w+)\s+(-?\d+)", desc, flags=re.M)
+    assert {n for n, _ in listed} == rows
+    for n, _ in listed:  # the defaults as documented in the table
+        default = re.search(r'"%s", (-?\d+)' % n, table).group(1)
+        assert re.search(r"^%s\s+-?\d+\*?\s+\(default %s\)" % (n, default), desc, flags=re.M), n
