@@ -193,8 +193,8 @@ int f2gpu_decompose_block(f2gpu_ctx *ctx, f2gpu_mat *w, uint32_t *perm, uint32_t
  * factor the left half, update the right half with a block TRSM + one
  * Strassen-Winograd GEMM (A' = D ^ L21 L11^-1 C), recurse.  Exact arithmetic and
  * 64-aligned splits make the result bit-identical to decompose_block.
- * min_cols = 0 -> leaves of at most 256 panels (16384 columns), 128 panels once
- * a leaf has >= 20000 rows below its first panel. */
+ * min_cols = 0 -> leaves of at most 256 panels (16384 columns), 64 panels once
+ * a leaf has >= 30000 rows below its first panel (csrc/options.h). */
 int f2gpu_decompose_recursive(f2gpu_ctx *ctx, f2gpu_mat *w, size_t min_cols, uint32_t *perm,
                               uint32_t *rj, size_t *rank);
 /* Same algorithm, column blocks distributed round-robin over `shards` logical

@@ -514,7 +514,7 @@ def decompose_recursive(a, min_cols: int = 0, ctx: Context | None = None) -> LUF
     Strassen-Winograd GEMM (A' = D + L21 L11^-1 C), then recursion.  Exact
     arithmetic with 64-aligned splits: the factors equal decompose_block's
     bit-for-bit.  min_cols = 0 picks the device default (leaves of at most 256 panels =
-    16384 columns; 128 panels once a leaf has >= 20000 rows below it)."""
+    16384 columns; 64 panels once a leaf has >= 30000 rows below it; csrc/options.h)."""
     ctx = ctx or (a.ctx if isinstance(a, DeviceMatrix) else default_context())
     host = a.download() if isinstance(a, DeviceMatrix) else a
     n, m = host.rows(), host.cols()

@@ -996,7 +996,7 @@ int timed(RecRun& r, const char* what, F&& f);
 int rec_trsm(RecRun& r, size_t a, size_t b, size_t Ra, size_t col0, size_t col1) {
     const size_t Rb = Ra + 64 * (b - a);
     if (b - a <= r.tbase) {
-        if (b - a <= 16 && r.trsm_kernel)
+        if (b - a <= size_t(f2::trsm_max_panels()) && r.trsm_kernel)
             return timed(r, "trsm.base", [&] {
                 return check_launch(r.c, f2::launch_trsm_block(r.s->w.p, r.s->w.stride, int(a), int(b - a), Ra,
                                                                col0, int(col1 - col0), r.c->stream),
@@ -1125,7 +1125,7 @@ int decompose_recursive(f2gpu_ctx* c, View w, size_t min_cols, uint32_t* perm, u
     const f2::Options& o = f2::options();
     r.cut = size_t(o.rec_cut);
     if (o.rec_base_set) r.base = std::max<size_t>(1, size_t(o.rec_base));
-    r.tbase = std::max<size_t>(1, size_t(o.rec_tbase));
+    r.tbase = std::max<size_t>(1, size_t(o.rec_tbase));  // > trsm_max_panels(): rank-64 updates below
     r.trsm_kernel = o.rec_trsm != 0;
     // tall leaves: 128 panels once a leaf has >= 20000 rows below its first panel
     // (65536^2 sweeps over 12000..56000 rows x 32..128 panels; first 70.5 -> 67.5 ms
@@ -1623,6 +1623,13 @@ int run_dist_recursive(f2gpu_ctx* c, std::vector<Shard>& sh, int base, int G, si
     for (auto& s : sh) F2_TRY(check_launch(c, f2::launch_iota(s.perm, n, c->stream), "k_iota"));
     DistGpu d;
     d.c = c; d.sh = &sh; d.base = base; d.G = G; d.n = n; d.mu = mu; d.ex = &ex;
+    {  // the single-GPU recursion's TRSM base and product cutovers (options.h)
+        const f2::Options& o = f2::options();
+        d.tbase = std::min<size_t>(size_t(f2::trsm_max_panels()), std::max<size_t>(1, size_t(o.rec_tbase)));
+        d.trsm_m4rm_k = size_t(o.trsm_m4rm_k);
+        d.cut = size_t(o.rec_cut);
+        d.tc_cut = size_t(o.rec_tc_cut);
+    }
     if (!c->use_tc_cut_default) d.tc_cut = c->tc_cutover;
     size_t lb = 0, tr = 0, tb = 0;
     rec_leaf_params(min_cols, &lb, &tr, &tb);

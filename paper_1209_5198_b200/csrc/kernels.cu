@@ -2679,45 +2679,46 @@ cudaError_t launch_post_col(uint64_t* w, size_t stride, int ncols, int panel_col
 // multiplier words for the panel at once.  Replaces P launches of the rank-64
 // update.
 // ---------------------------------------------------------------------------
-constexpr int kTrsmThreads = 128;  // one CTA per word-column
-constexpr int kTrsmMaxP = 16;
-constexpr int kTrsmRowsPerThread = 64 * kTrsmMaxP / kTrsmThreads;
-// L: panel a's column at row Ra (panel a + t at L + t * ls); C: the first of the
-// ncols word-columns at row Ra (column q at C + q * sc).  L and C may live in
-// different matrices (the distributed recursion keeps L in a gathered copy).
-__global__ void __launch_bounds__(kTrsmThreads) k_trsm_block(const uint64_t* __restrict__ L, size_t ls,
-                                                             uint64_t* __restrict__ C, size_t sc, int P) {
-    __shared__ uint64_t cs[64 * kTrsmMaxP];
+// NT threads per CTA (one CTA per word-column), up to MAXP panels, the multiplier
+// words prefetched PF panels ahead (their L2 round trip is the step's latency floor).
+template <int NT, int MAXP, int PF>
+__global__ void __launch_bounds__(NT) k_trsm_block(const uint64_t* __restrict__ L, size_t ls,
+                                                   uint64_t* __restrict__ C, size_t sc, int P) {
+    constexpr int RPT = 64 * MAXP / NT;  // row slots per thread
+    __shared__ uint64_t cs[64 * MAXP];
     __shared__ uint64_t tb[256];
     const int tid = threadIdx.x;
     uint64_t* col = C + size_t(blockIdx.x) * sc;
     const int rows = 64 * P;
-    // multiplier words of panel t for this thread's rows; panel t+1's are loaded
-    // while panel t is applied (one L2 round trip per panel otherwise)
-    auto load_y = [&](int t, uint64_t (&y)[kTrsmRowsPerThread]) {
+    // multiplier words of panel t for this thread's rows (rows of panels > t)
+    auto load_y = [&](int t, uint64_t (&y)[RPT]) {
         const uint64_t* Y = L + size_t(t) * ls;
         const int r0 = 64 * (t + 1) + tid;
 #pragma unroll
-        for (int i = 0; i < kTrsmRowsPerThread; ++i) {
-            const int r = r0 + kTrsmThreads * i;
-            y[i] = r < rows ? Y[r] : 0;
+        for (int i = 0; i < RPT; ++i) {
+            const int r = r0 + NT * i;
+            y[i] = (t < P && r < rows) ? Y[r] : 0;
         }
     };
-    uint64_t ynext[kTrsmRowsPerThread];
-    load_y(0, ynext);
-    for (int i = tid; i < rows; i += kTrsmThreads) cs[i] = col[i];
+    uint64_t yq[PF][RPT];
+#pragma unroll
+    for (int f = 0; f < PF; ++f) load_y(f, yq[f]);
+    for (int i = tid; i < rows; i += NT) cs[i] = col[i];
     __syncthreads();
     for (int t = 0; t < P; ++t) {
         const int r0 = 64 * (t + 1) + tid;
-        uint64_t y[kTrsmRowsPerThread];
+        uint64_t y[RPT];
 #pragma unroll
-        for (int i = 0; i < kTrsmRowsPerThread; ++i) y[i] = ynext[i];
-        if (t + 1 < P) load_y(t + 1, ynext);
-        // 4-bit table of panel t's final pivot words (2 entries per thread)
+        for (int i = 0; i < RPT; ++i) y[i] = yq[0][i];
+#pragma unroll
+        for (int f = 0; f + 1 < PF; ++f)
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) yq[f][i] = yq[f + 1][i];
+        if (t + PF < P) load_y(t + PF, yq[PF - 1]);
+        // 4-bit table of panel t's final pivot words
         const uint64_t* B = cs + 64 * t;
-#pragma unroll
-        for (int e2 = 0; e2 < 2; ++e2) {
-            const int e = tid + kTrsmThreads * e2, g = e >> 4, v = e & 15;
+        for (int e = tid; e < 256; e += NT) {
+            const int g = e >> 4, v = e & 15;
             uint64_t x = 0;
 #pragma unroll
             for (int i = 0; i < 4; ++i)
@@ -2726,8 +2727,8 @@ __global__ void __launch_bounds__(kTrsmThreads) k_trsm_block(const uint64_t* __r
         }
         __syncthreads();
 #pragma unroll
-        for (int i = 0; i < kTrsmRowsPerThread; ++i) {
-            const int r = r0 + kTrsmThreads * i;
+        for (int i = 0; i < RPT; ++i) {
+            const int r = r0 + NT * i;
             if (r < rows) {
                 uint64_t x = 0;
 #pragma unroll
@@ -2737,7 +2738,7 @@ __global__ void __launch_bounds__(kTrsmThreads) k_trsm_block(const uint64_t* __r
         }
         __syncthreads();
     }
-    for (int i = 64 + tid; i < rows; i += kTrsmThreads) col[i] = cs[i];  // panel 0's rows are unchanged
+    for (int i = 64 + tid; i < rows; i += NT) col[i] = cs[i];  // panel 0's rows are unchanged
 }
 
 cudaError_t launch_trsm_block(uint64_t* W, size_t stride, int a, int P, size_t Ra, size_t col0, int ncols,
@@ -2745,10 +2746,25 @@ cudaError_t launch_trsm_block(uint64_t* W, size_t stride, int a, int P, size_t R
     return launch_trsm_block_l(W + size_t(a) * stride + Ra, stride, W + col0 * stride + Ra, stride, P, ncols, s);
 }
 
+int trsm_max_panels() { return 64; }
+
 cudaError_t launch_trsm_block_l(const uint64_t* L, size_t ls, uint64_t* C, size_t sc, int P, int ncols,
                                 cudaStream_t s) {
-    if (P < 1 || P > kTrsmMaxP || ncols < 1) return cudaErrorInvalidValue;
-    k_trsm_block<<<ncols, kTrsmThreads, 0, s>>>(L, ls, C, sc, P);
+    if (P < 1 || P > trsm_max_panels() || ncols < 1) return cudaErrorInvalidValue;
+    // F2GPU_TRSM_KERNEL=1: the multiplier words two panels ahead / 512 threads at P > 32
+    // (65536^2, TRSM base 32: no faster -- at the top split the base is bound by the
+    // shared-memory lookups, 16 per row and panel, not by the L2 round trips)
+    const bool alt = options().trsm_kernel == 1;
+    if (P <= 16) {
+        if (alt) k_trsm_block<128, 16, 2><<<ncols, 128, 0, s>>>(L, ls, C, sc, P);
+        else k_trsm_block<128, 16, 1><<<ncols, 128, 0, s>>>(L, ls, C, sc, P);
+    } else if (P <= 32) {
+        if (alt) k_trsm_block<256, 32, 2><<<ncols, 256, 0, s>>>(L, ls, C, sc, P);
+        else k_trsm_block<256, 32, 1><<<ncols, 256, 0, s>>>(L, ls, C, sc, P);
+    } else {
+        if (alt) k_trsm_block<512, 64, 1><<<ncols, 512, 0, s>>>(L, ls, C, sc, P);
+        else k_trsm_block<256, 64, 1><<<ncols, 256, 0, s>>>(L, ls, C, sc, P);
+    }
     return cudaGetLastError();
 }
 

@@ -230,6 +230,7 @@ cudaError_t launch_update_tc(const TcUpdateArgs& a, int grid, cudaStream_t s);
 
 // block TRSM base (decompose_recursive, full rank): P <= 16 panels a.., pivot
 // rows Ra .. Ra+64P, in place on word-columns [col0, col0+ncols)
+int trsm_max_panels();  // largest P one k_trsm_block launch solves
 cudaError_t launch_trsm_block(uint64_t* W, size_t stride, int a, int P, size_t Ra, size_t col0, int ncols,
                               cudaStream_t s);
 // the same with L and C in separate matrices: L = panel a's column at row Ra

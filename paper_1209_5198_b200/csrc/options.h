@@ -31,14 +31,15 @@
     /* ---- decompose_recursive ---- */                                                                      \
     X(rec_cut, "F2GPU_REC_CUT", 16384, "Strassen cutover of the recursion's M4RM products")                   \
     X(rec_base, "F2GPU_REC_BASE", 256, "leaf width in panels (when set: overrides min_cols)")                \
-    X(rec_tbase, "F2GPU_REC_TBASE", 16, "TRSM base in panels (one k_trsm_block launch)")                     \
+    X(rec_tbase, "F2GPU_REC_TBASE", 32, "TRSM base in panels (one k_trsm_block launch; <= 64)")              \
     X(rec_trsm, "F2GPU_REC_TRSM", 1, "TRSM base by k_trsm_block (0: rank-64 updates)")                        \
-    X(rec_tall, "F2GPU_REC_TALL", 20000, "leaves with at least this many rows below them are narrower")      \
-    X(rec_tall_base, "F2GPU_REC_TALL_BASE", 128, "their width in panels")                                     \
+    X(rec_tall, "F2GPU_REC_TALL", 30000, "leaves with at least this many rows below them are narrower")      \
+    X(rec_tall_base, "F2GPU_REC_TALL_BASE", 64, "their width in panels")                                      \
     X(rec_tc_cut, "F2GPU_REC_TC_CUT", 8192, "Strassen-Winograd leaf of the recursion's tensor-core products") \
     X(rec_final, "F2GPU_REC_FINAL", 32, "host entry: right-spine leaf width (panels) for early downloads")    \
     X(rec_first, "F2GPU_REC_FIRST", 64, "host entry: first leaf / upload chunk width (panels)")              \
     X(trsm_m4rm_k, "F2GPU_TRSM_M4RM_K", 1024, "TRSM products with k <= this run on M4RM")                     \
+    X(trsm_kernel, "F2GPU_TRSM_KERNEL", 0, "1: k_trsm_block prefetching two panels ahead (512 threads at P > 32)") \
     X(rec_times, "F2GPU_REC_TIMES", 0, "per-phase CUDA-event times of the recursion on stderr")               \
     X(no_upload_overlap, "F2GPU_NO_UPLOAD_OVERLAP", 0, "host entry: upload everything before factoring")     \
     /* ---- kernel selection ---- */                                                                          \
