@@ -592,7 +592,7 @@ def measure_update_roofline(f2, lib, _lib, ctx, stream, torch, n: int) -> dict:
             "unit_workload": f"C({n}x{n}) ^= A({n}x64)*B(64x{n})",
             "algorithmic_bytes": alg, "us_per_launch": round(t * 1e6, 1),
             "bitops_per_s": round(n * 64 * n / t, 1),
-            "share_of_step": "25% of the decomposition's kernel time (profiles/r2_launches_rec_summary.txt)",
+            "share_of_step": "21% of the decomposition's kernel time (profiles/r2b_launches_summary.txt)",
             "peak_source": src}
 
 
@@ -633,7 +633,7 @@ def measure_tensor_roofline(f2, lib, _lib, ctx, stream, torch, n: int = 16384) -
             "kernel": "k_gemm_tc7 (fp4 kind::mxf4 GF(2) product leaf, cta_group::2, M-side operand in TMEM)",
             "unit_workload": f"C({n}x{n}) = A({n}x{n})*B({n}x{n}), 2*n^3 fp4 FLOP",
             "us_per_launch": round(t * 1e6, 1), "bitops_per_s": round(n ** 3 / t, 1),
-            "share_of_step": "34% of the decomposition's kernel time (profiles/r2_launches_rec_summary.txt)",
+            "share_of_step": "37% of the decomposition's kernel time (profiles/r2b_launches_summary.txt)",
             "peak_source": src}
 
 
