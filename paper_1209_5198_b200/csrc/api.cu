@@ -28,19 +28,24 @@
 namespace f2 {
 // options.h: the environment read once.  A value is parsed after any leading
 // non-digits ("i8" -> 8); an unparsable one keeps the default.
+// One environment variable: true (and *v set) when present and parsable.
+bool env_value(const char* env, long long* v) {
+    const char* e = getenv(env);
+    if (!e) return false;
+    const char* q = e;
+    while (*q && !(*q >= '0' && *q <= '9') && *q != '-') ++q;
+    char* end = nullptr;
+    const long long x = strtoll(q, &end, 10);
+    if (end == q) return false;
+    *v = x;
+    return true;
+}
+
 const Options& options() {
     static const Options o = [] {
         Options r;
         auto rd = [](const char* env, long long& v, bool& set) {
-            const char* e = getenv(env);
-            if (!e) return;
-            const char* q = e;
-            while (*q && !(*q >= '0' && *q <= '9') && *q != '-') ++q;
-            char* end = nullptr;
-            const long long x = strtoll(q, &end, 10);
-            if (end == q) return;
-            v = x;
-            set = true;
+            if (env_value(env, &v)) set = true;
         };
 #define F2_OPT_READ(field, env, def, doc) rd(env, r.field, r.field##_set);
         F2_OPTIONS(F2_OPT_READ)
@@ -817,7 +822,8 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
                                                        j + 1 < c1 ? int(j + 1) : -1, s.perm, n, s.st + j, f,
                                                        c->stream, c->trace_buf != nullptr,
                                                        j + 1 < c1 && c->panel_head ? f2::kPanelHeadRows : 0,
-                                                       j > c0 && spin ? f + 4 : nullptr),
+                                                       j > c0 && spin ? f + 4 : nullptr,
+                                                       j > c0 && spin && f2::options().post_pdl),
                                 "k_post_col"));
             if (j + 1 >= c1) break;
             if (!c->panel_early) CUDA_TRY(cudaEventRecord(c->ev_post, c->stream));
@@ -2487,7 +2493,10 @@ int f2gpu_ctx_init_comm(f2gpu_ctx* c, int rank, int world, const void* id) {
     c->world = world;
     // world == 1 needs no communicator; F2GPU_FORCE_NCCL=1 builds a 1-rank one so
     // the NCCL exchange path can be exercised on a single GPU.
-    if (world == 1 && !f2::options().force_nccl) return F2GPU_OK;
+    // read at each call (tests switch it per test within one process)
+    long long force = 0;
+    f2::env_value("F2GPU_FORCE_NCCL", &force);
+    if (world == 1 && !force) return F2GPU_OK;
     NcclApi& api = nccl();
     if (!api.ok) return set_err(F2GPU_ENCCL, api.why);
     CUDA_TRY(cudaSetDevice(c->device));

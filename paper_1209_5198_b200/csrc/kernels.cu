@@ -2567,9 +2567,9 @@ __global__ void __launch_bounds__(256) k_post_col(uint64_t* __restrict__ w, size
                                                   int skip, const uint32_t* wait_panel) {
     __shared__ uint64_t zs[64], bs[64];
     __shared__ uint64_t zt[256], bt[256];
-    // the update that follows (UpdateArgs::pdl) may start placing its CTAs now; it
-    // waits for this grid's completion before touching data
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // launched as a programmatic dependent of the previous update (pdl): placed as its
+    // CTAs retire, then waits for its completion before touching any column
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (wait_panel) {  // queued ahead: the panel kernel's writes are complete
         if (threadIdx.x < 32) {
             SpinGuard g;
@@ -2583,6 +2583,11 @@ __global__ void __launch_bounds__(256) k_post_col(uint64_t* __restrict__ w, size
         }
         __syncthreads();
     }
+    // the update that follows (UpdateArgs::pdl) may start placing its CTAs now (it
+    // waits for this grid's completion before touching data).  Not before the panel
+    // kernel is done: 146 update CTAs placed early could take the SM it still needs
+    // (its post would wait for it forever -- seen with the post launched early too)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (int(blockIdx.x) < swap_blocks) {
         swaps_body(w, stride, ncols, panel_col, perm, st,
                    int((size_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5), next_col);
@@ -2660,8 +2665,21 @@ __global__ void __launch_bounds__(256) k_post_col(uint64_t* __restrict__ w, size
 
 cudaError_t launch_post_col(uint64_t* w, size_t stride, int ncols, int panel_col, int next_col, uint32_t* perm,
                             size_t n, const PanelState* st, uint32_t* flags, cudaStream_t s, bool trace,
-                            int skip, const uint32_t* wait_panel) {
+                            int skip, const uint32_t* wait_panel, bool pdl) {
     const int swap_blocks = (ncols + 1 + 7) / 8;
+    if (pdl) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(swap_blocks + post_col_yblocks(n));
+        cfg.blockDim = dim3(256);
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, k_post_col, w, stride, ncols, panel_col, next_col, perm, n, st, swap_blocks,
+                                  flags, trace, skip, wait_panel);
+    }
     k_post_col<<<swap_blocks + post_col_yblocks(n), 256, 0, s>>>(w, stride, ncols, panel_col, next_col, perm, n,
                                                                   st, swap_blocks, flags, trace, skip, wait_panel);
     return cudaGetLastError();

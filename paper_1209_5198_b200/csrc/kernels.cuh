@@ -160,7 +160,8 @@ bool panel_link_ok();  // false when F2GPU_PANEL=0 selects the older panel kerne
 int post_col_yblocks(size_t n);
 cudaError_t launch_post_col(uint64_t* w, size_t stride, int ncols, int panel_col, int next_col, uint32_t* perm,
                             size_t n, const PanelState* st, uint32_t* flags, cudaStream_t s,
-                            bool trace = false, int skip = 0, const uint32_t* wait_panel = nullptr);
+                            bool trace = false, int skip = 0, const uint32_t* wait_panel = nullptr,
+                            bool pdl = false);
 // lookahead: panel j's update of word-column j+1 only; increments *done per CTA
 int update_col_grid(size_t n, int num_sms);
 cudaError_t launch_update_col(uint64_t* next, const uint64_t* ycol, size_t n, const PanelState* st, uint32_t* done,

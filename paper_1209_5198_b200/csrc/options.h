@@ -23,11 +23,12 @@
     X(panel_head, "F2GPU_PANEL_HEAD", 0, "the panel kernel computes the first 256 rows below its pivots")      \
     X(post_spin, "F2GPU_POST_SPIN", 1, "k_post_col waits for its panel kernel on a counter (0: by event)")     \
     X(pdl, "F2GPU_PDL", 1, "the update is a programmatic dependent launch of k_post_col")                    \
+    X(post_pdl, "F2GPU_POST_PDL", 1, "k_post_col is a programmatic dependent launch of the previous update")   \
     X(panel_hand, "F2GPU_PANEL_HAND", 0, "P(j+1) starts on P(j)'s done counter with a hand-off block")         \
     X(tc, "F2GPU_TC", 1, "products on the fp4 tensor-core leaf (0: M4RM only)")                              \
     X(tc_cut, "F2GPU_TC_CUT", 16384, "Strassen-Winograd leaf of the tensor-core products (strassen_mult)")    \
     X(spin_diag, "F2GPU_SPIN_DIAG", 0, "record a timed-out cross-kernel wait in host-mapped memory")          \
-    X(force_nccl, "F2GPU_FORCE_NCCL", 0, "build a 1-rank NCCL communicator at world size 1")                  \
+    X(force_nccl, "F2GPU_FORCE_NCCL", 0, "build a 1-rank NCCL communicator at world size 1 (read per call)")  \
     /* ---- decompose_recursive ---- */                                                                      \
     X(rec_cut, "F2GPU_REC_CUT", 16384, "Strassen cutover of the recursion's M4RM products")                   \
     X(rec_base, "F2GPU_REC_BASE", 256, "leaf width in panels (when set: overrides min_cols)")                \
@@ -66,5 +67,7 @@ struct Options {
 };
 
 const Options& options();  // the environment, read once
+// one variable, read now (for the few switches read per call: F2GPU_FORCE_NCCL)
+bool env_value(const char* env, long long* v);
 
 }  // namespace f2
