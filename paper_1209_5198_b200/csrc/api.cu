@@ -258,6 +258,18 @@ struct f2gpu_ctx {
     unsigned long long* trace_buf = nullptr;  // device trace (diagnostics)
     size_t trace_cap = 0;
     uint32_t* scr_flags = nullptr;        // per-panel counters (kFlagsPerPanel each)
+    // device copies of batched-launch descriptors (Strassen XOR jobs, M4RM / fp4 problem
+    // lists), cached by content: a repeated call (same operands and shapes) launches
+    // without an in-stream H2D copy (desc_copy)
+    struct DescEntry {
+        std::string key;
+        void* d = nullptr;
+        cudaStream_t origin = nullptr;
+        cudaEvent_t ready = nullptr;
+        uint64_t used = 0;
+    };
+    std::vector<DescEntry> desc_cache;
+    uint64_t desc_tick = 0;
     size_t scr_flags_cap = 0;
     uint64_t* scr_hand = nullptr;         // per-panel hand-off blocks (f2::kHandWords each)
     void* scr_st = nullptr;   // persistent PanelState[mu]
@@ -331,6 +343,48 @@ struct DevBuf {  // RAII stream-ordered allocation
     template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
+// A batched launch's descriptor array on the device.  Outside a stream capture it comes
+// from the context's content-keyed cache (a hit on another stream waits for the copy);
+// inside one it is a stream-ordered allocation that `tmp` frees after the launch.
+int desc_copy(f2gpu_ctx* c, const void* host, size_t bytes, DevBuf& tmp, const void** out) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CUDA_TRY(cudaStreamIsCapturing(c->stream, &cap));
+    if (cap != cudaStreamCaptureStatusNone) {
+        F2_TRY(tmp.alloc(bytes));
+        CUDA_TRY(cudaMemcpyAsync(tmp.p, host, bytes, cudaMemcpyHostToDevice, c->stream));
+        *out = tmp.p;
+        return F2GPU_OK;
+    }
+    const std::string key(static_cast<const char*>(host), bytes);
+    for (auto& e : c->desc_cache) {
+        if (e.key == key) {
+            if (e.origin != c->stream) CUDA_TRY(cudaStreamWaitEvent(c->stream, e.ready, 0));
+            e.used = ++c->desc_tick;
+            *out = e.d;
+            return F2GPU_OK;
+        }
+    }
+    if (c->desc_cache.size() >= 1024) {  // evict the least recently used
+        size_t v = 0;
+        for (size_t i = 1; i < c->desc_cache.size(); ++i)
+            if (c->desc_cache[i].used < c->desc_cache[v].used) v = i;
+        CUDA_TRY(cudaFree(c->desc_cache[v].d));  // synchronising: no launch still reads it
+        cudaEventDestroy(c->desc_cache[v].ready);
+        c->desc_cache.erase(c->desc_cache.begin() + long(v));
+    }
+    f2gpu_ctx::DescEntry e;
+    e.key = key;
+    e.origin = c->stream;
+    e.used = ++c->desc_tick;
+    CUDA_TRY(cudaMalloc(&e.d, bytes));
+    CUDA_TRY(cudaMemcpyAsync(e.d, host, bytes, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(cudaEventCreateWithFlags(&e.ready, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(e.ready, c->stream));
+    *out = e.d;
+    c->desc_cache.push_back(std::move(e));
+    return F2GPU_OK;
+}
+
 // C ^= A*B on views (stream-K M4RM kernel)
 int gemm_acc(f2gpu_ctx* c, View C, View A, View B) {
     if (A.rows == 0 || A.cols == 0 || B.cols == 0) return F2GPU_OK;
@@ -389,13 +443,12 @@ f2::XorJob xjob(View dst, bool acc, std::initializer_list<View> srcs) {
 
 int launch_xor_jobs(f2gpu_ctx* c, const std::vector<f2::XorJob>& jobs) {
     if (jobs.empty()) return F2GPU_OK;
-    DevBuf d(c);
-    F2_TRY(d.alloc(jobs.size() * sizeof(f2::XorJob)));
-    CUDA_TRY(cudaMemcpyAsync(d.p, jobs.data(), jobs.size() * sizeof(f2::XorJob),
-                             cudaMemcpyHostToDevice, c->stream));
+    DevBuf tmp(c);
+    const void* d = nullptr;
+    F2_TRY(desc_copy(c, jobs.data(), jobs.size() * sizeof(f2::XorJob), tmp, &d));
     size_t mr = 0, mw = 0;
     for (auto& j : jobs) { mr = std::max(mr, j.rows); mw = std::max(mw, j.wcols); }
-    return check_launch(c, f2::launch_xor_batched(d.as<f2::XorJob>(), int(jobs.size()), mr, mw,
+    return check_launch(c, f2::launch_xor_batched(static_cast<const f2::XorJob*>(d), int(jobs.size()), mr, mw,
                                                   c->stream),
                         "k_xor_batched");
 }
@@ -478,14 +531,11 @@ int strassen_acc(f2gpu_ctx* c, View C, View A, View B, size_t cutover) {
         probs.push_back(g);
         offs.push_back(offs.back() + f2::gemm_units_host(g));
     }
-    DevBuf dp(c), doff(c);
-    F2_TRY(dp.alloc(probs.size() * sizeof(f2::GemmArgs)));
-    F2_TRY(doff.alloc(offs.size() * sizeof(size_t)));
-    CUDA_TRY(cudaMemcpyAsync(dp.p, probs.data(), probs.size() * sizeof(f2::GemmArgs),
-                             cudaMemcpyHostToDevice, c->stream));
-    CUDA_TRY(cudaMemcpyAsync(doff.p, offs.data(), offs.size() * sizeof(size_t),
-                             cudaMemcpyHostToDevice, c->stream));
-    F2_TRY(check_launch(c, f2::launch_gemm_batched(dp.as<f2::GemmArgs>(), doff.as<size_t>(),
+    DevBuf tp(c), toff(c);
+    const void *dp = nullptr, *doff = nullptr;
+    F2_TRY(desc_copy(c, probs.data(), probs.size() * sizeof(f2::GemmArgs), tp, &dp));
+    F2_TRY(desc_copy(c, offs.data(), offs.size() * sizeof(size_t), toff, &doff));
+    F2_TRY(check_launch(c, f2::launch_gemm_batched(static_cast<const f2::GemmArgs*>(dp), static_cast<const size_t*>(doff),
                                                    int(probs.size()), offs.back(), c->num_sms,
                                                    c->stream),
                         "k_gemm_batched"));
@@ -575,12 +625,13 @@ int strassen_tc(f2gpu_ctx* c, View C, View A, View BT, int L) {
     for (const Node& nd : level)
         probs.push_back({nd.A.p, nd.A.stride, nd.A.rows, nd.BT.p, nd.BT.stride, nd.C.p, nd.C.stride, nd.A.cols,
                          nd.BT.rows, 0});
-    DevBuf dp(c);
-    F2_TRY(dp.alloc(probs.size() * sizeof(f2::TcGemmArgs)));
-    CUDA_TRY(cudaMemcpyAsync(dp.p, probs.data(), probs.size() * sizeof(f2::TcGemmArgs), cudaMemcpyHostToDevice,
-                             c->stream));
-    F2_TRY(check_launch(c, f2::launch_gemm_tc3_batched(probs.data(), dp.as<f2::TcGemmArgs>(), int(probs.size()),
-                                                       c->stream),
+    // the pair leaf (default) takes the host list (its own descriptor cache); the
+    // single-CTA leaves read a device copy
+    DevBuf tp(c);
+    const void* dp = nullptr;
+    if (!f2::gemm_tc7_enabled()) F2_TRY(desc_copy(c, probs.data(), probs.size() * sizeof(f2::TcGemmArgs), tp, &dp));
+    F2_TRY(check_launch(c, f2::launch_gemm_tc3_batched(probs.data(), static_cast<const f2::TcGemmArgs*>(dp),
+                                                       int(probs.size()), c->stream),
                         "k_gemm_tc3_batched"));
     for (int l = L - 1; l >= 0; --l) F2_TRY(launch_xor_jobs(c, post[l]));
     return F2GPU_OK;
@@ -1770,6 +1821,10 @@ int f2gpu_ctx_destroy(f2gpu_ctx* c) {
     cudaFree(c->scr_st);
     cudaFree(c->scr_perm);
     cudaFree(c->scr_flags);
+    for (auto& e : c->desc_cache) {
+        cudaFree(e.d);
+        cudaEventDestroy(e.ready);
+    }
     cudaFree(c->scr_hand);
     if (c->trace_buf) { f2::trace_set(nullptr, 0); cudaFree(c->trace_buf); }
     for (cudaEvent_t e : c->chunk_ev) cudaEventDestroy(e);
