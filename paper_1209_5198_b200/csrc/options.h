@@ -23,7 +23,7 @@
     X(panel_head, "F2GPU_PANEL_HEAD", 0, "the panel kernel computes the first 256 rows below its pivots")      \
     X(post_spin, "F2GPU_POST_SPIN", 1, "k_post_col waits for its panel kernel on a counter (0: by event)")     \
     X(pdl, "F2GPU_PDL", 1, "the update is a programmatic dependent launch of k_post_col")                    \
-    X(post_pdl, "F2GPU_POST_PDL", 1, "k_post_col is a programmatic dependent launch of the previous update")   \
+    X(post_pdl, "F2GPU_POST_PDL", 0, "k_post_col as a programmatic dependent of the previous update (can starve P)") \
     X(panel_hand, "F2GPU_PANEL_HAND", 0, "P(j+1) starts on P(j)'s done counter with a hand-off block")         \
     X(tc, "F2GPU_TC", 1, "products on the fp4 tensor-core leaf (0: M4RM only)")                              \
     X(tc_cut, "F2GPU_TC_CUT", 16384, "Strassen-Winograd leaf of the tensor-core products (strassen_mult)")    \

@@ -169,6 +169,35 @@ def test_cfg4_decompose_recursive_host_65536(f2, ctx, po):
     check_against(po, g, None, f2.BitMatrix(n, n, wout), perm, rj, int(rk.value), n, n, freivalds=False)
 
 
+def test_cfg4_decompose_recursive_host_65536_repeated(f2, po):
+    """The host entry as bench.py's e2e leg runs it: repeated calls on one fresh context
+    (eager leaves, then captured, then replayed leaf graphs, with the copy stream's
+    uploads and downloads around them), every call digest-checked."""
+    from paper_1209_5198_b200 import _lib
+
+    g = digests()["cfg4"]
+    n = g["n"]
+    lib = _lib.load()
+    ctx = f2.Context(0)
+    try:
+        A = f2.DeviceMatrix(n, n, ctx)
+        A.random_dense(0.5, g["seed"])
+        a = np.ascontiguousarray(A.download().words)
+        del A
+        wout = np.zeros_like(a)
+        perm = np.zeros(n, np.uint32)
+        rj = np.zeros(n // 64, np.uint32)
+        rk = C.c_size_t()
+        for _ in range(4):
+            wout[:] = 0
+            _lib.check(lib.f2gpu_decompose_recursive_host(ctx.handle, a.ctypes.data, n, n, a.shape[1], 0,
+                                                          wout.ctypes.data, perm.ctypes.data, rj.ctypes.data,
+                                                          C.byref(rk)))
+            check_against(po, g, None, f2.BitMatrix(n, n, wout), perm, rj, int(rk.value), n, n, freivalds=False)
+    finally:
+        ctx.close()
+
+
 def _run_recursive(f2, ctx, A, n, m):
     from paper_1209_5198_b200 import _lib
     lib = _lib.load()
