@@ -16,13 +16,17 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libf2gpu.so"
-SOURCES = [CSRC / "kernels.cu", CSRC / "tc_leaf.cu", CSRC / "tc_pair.cu", CSRC / "tc_update.cu", CSRC / "api.cu"]
+SOURCES = [CSRC / "kernels.cu", CSRC / "tc_leaf.cu", CSRC / "tc_pair.cu", CSRC / "api.cu"]
 HEADERS = [CSRC / "kernels.cuh", CSRC / "tc_common.cuh", CSRC / "options.h", ROOT / "include" / "f2gpu.h"]
 
 # F2GPU_BUILD_EXPERIMENTAL=1 also compiles the evaluated-and-rejected variants
 # (int8 leaves, single-CTA pair / persistent / double-buffered fp4 leaves, the
 # tensor-core update); the default library carries only the kernels in use.
 EXPERIMENTAL = os.environ.get("F2GPU_BUILD_EXPERIMENTAL", "0") == "1"
+# csrc/experimental/: whole files of evaluated-and-rejected kernels (the tensor-core
+# trailing update), compiled only into experimental builds
+if EXPERIMENTAL:
+    SOURCES.insert(3, CSRC / "experimental" / "tc_update.cu")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

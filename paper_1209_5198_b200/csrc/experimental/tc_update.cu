@@ -48,10 +48,10 @@
 // update_tc_release_count() increments in total).
 #include <cstdint>
 #include <cstdlib>
-#include "options.h"
+#include "../options.h"
 
-#include "kernels.cuh"
-#include "tc_common.cuh"
+#include "../kernels.cuh"
+#include "../tc_common.cuh"
 
 #if F2GPU_EXPERIMENTAL  // evaluated, not used: built only with F2GPU_EXPERIMENTAL=1
 namespace f2 {

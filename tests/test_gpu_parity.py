@@ -174,7 +174,7 @@ def test_gemm_tc_rejects_shapes(f2, ctx):
         f2._lib.check(lib.f2gpu_gemm_tc(ctx.handle, A.handle, B.handle, C.handle, 0))
 
 
-# tensor-core trailing update (tc_update.cu): C[lo, hi) x [q0, q0+nwc) ^= A * BT^T
+# tensor-core trailing update (csrc/experimental/tc_update.cu): C[lo, hi) x [q0, q0+nwc) ^= A * BT^T
 UPD_TC_CASES = [  # n, m, lo, hi, q0, nwc, kwords
     (300, 640, 5, 290, 1, 7, 2), (1000, 192, 0, 1000, 0, 3, 1), (4096, 1280, 1000, 4096, 3, 17, 2),
     (129, 256, 128, 129, 0, 4, 2), (20000, 3200, 777, 19999, 2, 47, 2), (640, 128, 0, 640, 0, 1, 2),
