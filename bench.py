@@ -588,7 +588,7 @@ def measure_update_roofline(f2, lib, _lib, ctx, stream, torch, n: int) -> dict:
     Cm.free(); Bm.free()
     return {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
             "frac": round(ach / peak, 4), "traffic": traffic,
-            "kernel": "k_update (fused M4RM table build + XOR sweep)",
+            "kernel": "k_update_v4 (fused M4RM table build + XOR sweep: 8-bit tables over 8-column groups, delta applied by bulk XOR reductions)",
             "unit_workload": f"C({n}x{n}) ^= A({n}x64)*B(64x{n})",
             "algorithmic_bytes": alg, "us_per_launch": round(t * 1e6, 1),
             "bitops_per_s": round(n * 64 * n / t, 1),

@@ -922,6 +922,394 @@ __global__ void __launch_bounds__(kV3Threads, 1) k_update_v3(UpdateArgs p) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// K2 v4: the same delta + bulk-XOR design over 8-column groups with 8-bit tables
+// ---------------------------------------------------------------------------
+// v3 is bound by the shared-memory data pipe: 9 table lookups of 8 B per output
+// word (16 columns x 1280 entries = 160 KiB).  With 8 columns per group the same
+// space holds eight 8-bit tables (8 x 256 entries x 64 B = 128 KiB): 8 lookups
+// per output word, and 32 KiB more for the delta ring.  A 64-byte entry is half a
+// bank row, so tables 2p and 2p+1 share region p, one in each half:
+//   byte offset of entry g of table t, column c = (t>>1)*32 KiB + g*128 + (t&1)*64 + 8c.
+// A quarter-warp (8 lanes x 16 B) holds two row slots of 4 lanes; at step s the even
+// slot reads table s and the odd slot table s^1, i.e. the two halves of one
+// region: every 128-bit lookup is conflict-free, and each slot still visits all
+// eight tables.  The odd slot's driving word has its adjacent bytes swapped
+// (PRMT) so both slots take byte s.  The table sits at a 32 KiB-aligned shared
+// address, so base, half and column fold into one LOP3 with the index.
+// Measured at the north-star unit (C 65536^2 ^= A(65536x64) B(64x65536), tools/upd_time.py):
+//   v3 243.9 us; v4 16 warps 243 -> 222 us (producer loop restructured); 20 warps 213.5;
+//   24 warps 193-194 us = 5.55 TB/s (0.85 of the measured HBM copy peak); 28 / 30 warps
+//   (64 registers) 205 / 211.  Two delta stages beat three or four (206 vs 213 at 20 warps),
+//   one is slower (196.8).  Write-back depth > 0 (F2_V4_PIPE) and one producer-side proxy
+//   fence per tile (F2_V4_FENCE_PRODUCER) were slower (246 / 228.6 us at 16 warps).
+//   Diagnostic modes at 16 warps: no lookups 205 us (the write-back alone), no write-back
+//   185 us (the lookups alone), no delta stores 226 us.
+#ifndef F2_V4_PIPE
+#define F2_V4_PIPE 0  // tiles whose write-back reductions may still read shared memory (< stages)
+#endif
+#ifndef F2_V4_FENCE_PRODUCER
+#define F2_V4_FENCE_PRODUCER 0  // one proxy fence per tile in the producer instead of one per consumer warp
+#endif
+#ifndef F2_V4_DSTAGES
+#define F2_V4_DSTAGES 2
+#endif
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+#ifndef F2_V4_MODE
+#define F2_V4_MODE 0  // diagnostics: 1 no lookups, 2 no write-back, 3 no delta stores
+#endif
+constexpr int kV4Cols = 8;
+#ifndef F2_V4_WARPS
+#define F2_V4_WARPS 24
+#endif
+constexpr int kV4Warps = F2_V4_WARPS;              // consumer warps
+constexpr int kV4Threads = (kV4Warps + 1) * 32;
+constexpr int kV4Rows = 16 * kV4Warps;             // tile rows: 8 slots x 2 rows per warp
+constexpr int kV4DStages = F2_V4_DSTAGES;
+static_assert(F2_V4_PIPE < F2_V4_DSTAGES && F2_V4_DSTAGES <= 4, "pipelined write-back depth");
+constexpr int kV4AStages = 6;
+constexpr int kV4ColPitch = kV4Rows * 8 + 16;      // 2064 B: conflict-free 128-bit delta stores
+constexpr int kV4DBytes = kV4Cols * kV4ColPitch;   // 16512 B per delta tile
+constexpr int kV4ABytes = kV4Rows * 8;             // 2 KiB of driving words
+constexpr uint32_t kV4TabAddr = 0x8000;            // 32 KiB-aligned (bits disjoint from the index)
+constexpr uint32_t kV4TabBytes = 4u * 32768u;      // 128 KiB
+constexpr uint32_t kV4LowBytes = uint32_t(kV4AStages) * kV4ABytes + 256;  // A ring + barriers, below
+constexpr size_t kV4Smem = size_t(kV4TabAddr) + kV4TabBytes + size_t(kV4DStages) * kV4DBytes;
+static_assert(kV4LowBytes + 1024 <= kV4TabAddr, "A ring must fit below the table window");
+static_assert(kV4Smem <= 232448, "exceeds the 227 KiB per-CTA limit");
+
+__device__ __forceinline__ void v4_consumers_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(kV4Warps * 32) : "memory");
+}
+
+// one lookup of step S: byte S of the (byte-pair-swapped for odd slots) word,
+// table region S/2, half and column pair in `co` (with the table base bit)
+template <int S>
+__device__ __forceinline__ void lk8(uint32_t lo, uint32_t hi, uint32_t co, uint32_t (&acc)[4]) {
+    const uint32_t u = S < 4 ? lo : hi;
+    uint32_t x;
+    if ((S & 3) == 0) x = u << 7;
+    else if ((S & 3) == 1) x = u >> 1;
+    else if ((S & 3) == 2) x = u >> 9;
+    else x = u >> 17;
+    const uint32_t off = (x & 0x7F80u) | co;
+    uint32_t a, b, c, d;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4 + %5];"
+                 : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+                 : "r"(off), "n"((S >> 1) * 32768));
+    acc[0] ^= a; acc[1] ^= b; acc[2] ^= c; acc[3] ^= d;
+}
+__device__ __forceinline__ void lookup8x2(uint32_t sel, uint32_t co_e, uint32_t co_o, uint64_t w,
+                                          uint64_t& d0, uint64_t& d1) {
+    const uint32_t lo = __byte_perm(uint32_t(w), 0u, sel), hi = __byte_perm(uint32_t(w >> 32), 0u, sel);
+    uint32_t acc[4] = {0u, 0u, 0u, 0u};
+    lk8<0>(lo, hi, co_e, acc); lk8<1>(lo, hi, co_o, acc); lk8<2>(lo, hi, co_e, acc); lk8<3>(lo, hi, co_o, acc);
+    lk8<4>(lo, hi, co_e, acc); lk8<5>(lo, hi, co_o, acc); lk8<6>(lo, hi, co_e, acc); lk8<7>(lo, hi, co_o, acc);
+    d0 = (uint64_t(acc[1]) << 32) | acc[0];
+    d1 = (uint64_t(acc[3]) << 32) | acc[2];
+}
+
+// the eight 8-bit tables of one 8-column group (512 consumer threads, one
+// 32-entry item each: column, half, region, chunk), B staged through the table
+// space first (coalesced), doubling in registers (m4rm.hpp:74-88)
+__device__ __forceinline__ void build_tables8(unsigned char* tabb, const uint64_t* __restrict__ B, size_t sb,
+                                              size_t b_row0, size_t bcol0, int ncols_valid, int k_bits) {
+    static_assert(kV4Warps * 32 >= 512, "one item per consumer thread");
+    uint64_t* stage = reinterpret_cast<uint64_t*>(tabb);
+    const int it = threadIdx.x;
+    if (it < 512) {
+        const int col = it >> 6, r = it & 63;
+        stage[col * kStagePitch + r] =
+            (col < ncols_valid && r < k_bits) ? __ldg(B + (bcol0 + col) * sb + b_row0 + r) : 0ull;
+    }
+    v4_consumers_sync();
+    const int col = it & 7, half = (it >> 3) & 1, reg = (it >> 4) & 3, chunk = it >> 6;
+    const int t = 2 * reg + half;
+    uint64_t rows[8];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) rows[b] = it < 512 ? stage[col * kStagePitch + 8 * t + b] : 0ull;
+    v4_consumers_sync();
+    if (it >= 512) return;
+    uint64_t cur = 0;
+#pragma unroll
+    for (int hb = 0; hb < 3; ++hb)
+        if ((chunk >> hb) & 1) cur ^= rows[5 + hb];
+    uint64_t* dst = reinterpret_cast<uint64_t*>(tabb + size_t(reg) * 32768 + size_t(chunk * 32) * 128 +
+                                                half * 64 + col * 8);
+    uint64_t v[32];
+    v[0] = cur;
+#pragma unroll
+    for (int b = 0; b < 5; ++b)
+#pragma unroll
+        for (int g = 1 << b; g < (2 << b); ++g) v[g] = v[g - (1 << b)] ^ rows[b];
+#pragma unroll
+    for (int g = 0; g < 32; ++g) dst[g * 16] = v[g];
+}
+
+__global__ void __launch_bounds__(kV4Threads, 1) k_update_v4(UpdateArgs p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (p.tag >= 0 && blockIdx.x == 0 && threadIdx.x == 0) trace_ev(kTrUpdBegin, p.tag);
+    const uint32_t smem_base = smem_u32(smem_raw);
+    if (smem_base > kV4TabAddr - kV4LowBytes) __trap();  // layout assumption violated
+    unsigned char* tabb = smem_raw + (kV4TabAddr - smem_base);
+    unsigned char* aring = tabb - kV4LowBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(aring + size_t(kV4AStages) * kV4ABytes);
+    unsigned char* dring = tabb + kV4TabBytes;
+    uint64_t* a_full = bars;
+    uint64_t* a_empty = a_full + kV4AStages;
+    uint64_t* d_done = a_empty + kV4AStages;
+    uint64_t* d_free = d_done + kV4DStages;
+
+    size_t row_lo = p.row_lo, b_row0 = p.b_row0;
+    int k = p.k_bits;
+    if (p.st) {
+        const uint32_t R = p.st->R, r = p.st->r;
+        row_lo = size_t(R) + r;
+        k = int(r);
+        b_row0 = R;
+    }
+    const size_t row_hi = p.row_hi;
+    if (k <= 0 || row_lo >= row_hi || p.ncols <= 0) {
+        if (p.release && threadIdx.x == 0) release_signal(p.release, p.tag);
+        return;
+    }
+    const size_t G_all = gridDim.x;
+    size_t fc_n = 0;
+    if (p.release && p.first_col)
+        fc_n = p.fc_ctas > 0 ? min(G_all, size_t(p.fc_ctas)) : G_all;
+    const bool fc_mine = fc_n != 0 && blockIdx.x >= G_all - fc_n;
+    if (fc_n != 0 && !fc_mine) {
+        if (threadIdx.x == 0) release_signal(p.release, p.tag);
+        p.release = nullptr;
+        ++p.c_wcol0;
+        ++p.b_wcol0;
+        if (--p.ncols <= 0) return;
+    }
+    if (fc_mine) {
+        // the first column alone (as in k_update_v3): 4-bit table, rows split over
+        // the first-column CTAs, plain loads/stores, then the release
+        uint64_t* t4 = reinterpret_cast<uint64_t*>(tabb);
+        const uint64_t* Bc = p.B + p.b_wcol0 * p.sb + b_row0;
+        if (threadIdx.x < 256) {
+            const int g = threadIdx.x >> 4, v = threadIdx.x & 15;
+            uint64_t x = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (((v >> q) & 1) && 4 * g + q < k) x ^= __ldg(Bc + 4 * g + q);
+            t4[threadIdx.x] = x;
+        }
+        __syncthreads();
+        uint64_t* Cc = p.C + p.c_wcol0 * p.sc;
+        const size_t nrows = row_hi - row_lo, per = (nrows + fc_n - 1) / fc_n;
+        const size_t r0 = row_lo + size_t(blockIdx.x - (G_all - fc_n)) * per, r1 = min(row_hi, r0 + per);
+        for (size_t i0 = r0 + threadIdx.x; i0 < r1; i0 += 4 * size_t(blockDim.x)) {
+            uint64_t a[4], x[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const size_t i = i0 + size_t(u) * blockDim.x;
+                a[u] = i < r1 ? p.a[i] : 0;
+                x[u] = i < r1 ? Cc[i] : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const size_t i = i0 + size_t(u) * blockDim.x;
+#pragma unroll
+                for (int g = 0; g < 16; ++g) x[u] ^= t4[16 * g + int((a[u] >> (4 * g)) & 15)];
+                if (i < r1) Cc[i] = x[u];
+            }
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) release_signal(p.release, p.tag);
+        __syncthreads();
+        p.release = nullptr;
+        ++p.c_wcol0;
+        ++p.b_wcol0;
+        if (--p.ncols <= 0) return;
+    }
+    const size_t base = row_lo & ~size_t(127);
+    const size_t T = (row_hi - base + kV4Rows - 1) / kV4Rows;
+    const size_t ncg = (size_t(p.ncols) + kV4Cols - 1) / kV4Cols;
+    const size_t row_end = (row_hi + 1) & ~size_t(1);  // bulk sizes in 16-byte units
+    const size_t G = gridDim.x, b = blockIdx.x;
+    size_t s0, len0, s1, len1;
+    if (p.release) {
+        s0 = T * b / G;
+        len0 = T * (b + 1) / G - s0;
+        const size_t TB = T * (ncg - 1);
+        s1 = T + TB * b / G;
+        len1 = T + TB * (b + 1) / G - s1;
+    } else if (fc_n != 0 && fc_n < G && p.fc_weight < 4) {
+        const size_t TU = T * ncg, d = size_t(4 - p.fc_weight), gf = G - fc_n;
+        const size_t Wt = 4 * G - d * fc_n;
+        auto W = [&](size_t x) { return 4 * x - d * (x > gf ? x - gf : 0); };
+        s0 = TU * W(b) / Wt;
+        len0 = TU * W(b + 1) / Wt - s0;
+        s1 = s0 + len0;
+        len1 = 0;
+    } else {
+        const size_t TU = T * ncg;
+        s0 = TU * b / G;
+        len0 = TU * (b + 1) / G - s0;
+        s1 = s0 + len0;
+        len1 = 0;
+    }
+    const size_t cnt = len0 + len1;
+    if (cnt == 0) {
+        if (p.release && threadIdx.x == 0) release_signal(p.release, p.tag);
+        return;
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kV4AStages; ++s) {
+            mbar_init(&a_full[s], 1);
+            mbar_init(&a_empty[s], kV4Warps);
+        }
+        for (int s = 0; s < kV4DStages; ++s) {
+            mbar_init(&d_done[s], kV4Warps);
+            mbar_init(&d_free[s], 1);
+        }
+        fence_async_smem();
+    }
+    __syncthreads();
+
+    if (warp == kV4Warps) {
+        // ===== producer warp =====
+        TileCursor ac;
+        ac.init(T, s0, len0, s1);
+        uint32_t a_stage = 0;
+        auto issue_a = [&]() {
+            if (lane == 0) {
+                const size_t r0 = base + ac.tt * kV4Rows;
+                const uint32_t bytes = uint32_t(min(size_t(kV4Rows), row_end - r0) * 8);
+                mbar_expect_tx(&a_full[a_stage], bytes);
+                bulk_g2s(aring + size_t(a_stage) * kV4ABytes, p.a + r0, bytes, &a_full[a_stage]);
+            }
+            ac.next();
+            if (++a_stage == kV4AStages) a_stage = 0;
+        };
+        if (p.release && len0 == 0 && lane == 0) release_signal(p.release, p.tag);
+        const size_t pre = cnt < size_t(kV4AStages) ? cnt : size_t(kV4AStages);
+        for (size_t i = 0; i < pre; ++i) issue_a();
+        TileCursor dc;
+        dc.init(T, s0, len0, s1);
+        int s = 0, ae = 0;
+        uint32_t dph = 0, aph = 0;
+        int pq[4], pq0 = 0, npend = 0;
+        for (size_t t = 0; t < cnt; ++t) {
+            const size_t r0 = base + dc.tt * kV4Rows;
+            const uint32_t bytes = uint32_t(min(size_t(kV4Rows), row_end - r0) * 8);
+            const int nvalid = min(kV4Cols, int(size_t(p.ncols) - dc.g * kV4Cols));
+            mbar_wait(&d_done[s], dph);
+#if F2_V4_FENCE_PRODUCER
+            fence_async_smem();
+#endif
+            const bool issued = lane < nvalid && F2_V4_MODE != 2;
+            if (issued) {
+                bulk_red_xor(p.C + (p.c_wcol0 + dc.g * kV4Cols + lane) * p.sc + r0,
+                             dring + size_t(s) * kV4DBytes + lane * kV4ColPitch, bytes);
+                bulk_commit();
+            }
+            const bool rel_point = p.release && t + 1 == len0;
+            // pipelined write-back: the reductions of the last F2_V4_PIPE tiles may
+            // still be reading shared memory; a stage is freed once its reads are done
+            pq[(pq0 + npend) & 3] = s;
+            ++npend;
+            if (rel_point) {
+                bulk_wait0();  // group-0 writes complete in memory
+                __syncwarp();
+                if (lane == 0) {
+                    release_signal(p.release, p.tag);
+                    for (int q = 0; q < npend; ++q) mbar_arrive(&d_free[pq[(pq0 + q) & 3]]);
+                }
+                pq0 = (pq0 + npend) & 3;
+                npend = 0;
+            } else if (npend > F2_V4_PIPE) {
+                bulk_wait_read<F2_V4_PIPE>();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&d_free[pq[pq0]]);
+                pq0 = (pq0 + 1) & 3;
+                --npend;
+            }
+            if (t + kV4AStages < cnt) {
+                mbar_wait(&a_empty[ae], aph);
+                issue_a();
+            }
+            if (++ae == kV4AStages) { ae = 0; aph ^= 1; }
+            if (++s == kV4DStages) { s = 0; dph ^= 1; }
+            dc.next();
+        }
+        bulk_wait0();
+        return;
+    }
+
+    // ===== consumer warps =====
+    // lane = (row slot sl = lane >> 2, column pair cp = lane & 3): rows 16 w + 2 sl (+1),
+    // columns 2 cp (+1); odd slots read the other half of each table region
+    const int sl = lane >> 2, cp = lane & 3, hsl = sl & 1;
+    const uint32_t sel = hsl ? 0x2301u : 0x3210u;
+    const uint32_t co_e = kV4TabAddr | uint32_t(hsl * 64 + cp * 16);
+    const uint32_t co_o = kV4TabAddr | uint32_t((hsl ^ 1) * 64 + cp * 16);
+    const int rl = 16 * warp + 2 * sl;
+    size_t gcur = ~size_t(0);
+    TileCursor cc;
+    cc.init(T, s0, len0, s1);
+    int as = 0, s = 0;
+    uint32_t aph = 0, dph = 0;
+    for (size_t t = 0; t < cnt; ++t) {
+        const size_t g = cc.g;
+        if (g != gcur) {
+            v4_consumers_sync();
+            const int nvalid = min(kV4Cols, int(size_t(p.ncols) - g * kV4Cols));
+            build_tables8(tabb, p.B, p.sb, b_row0, p.b_wcol0 + g * kV4Cols, nvalid, k);
+            v4_consumers_sync();
+            gcur = g;
+        }
+        mbar_wait(&a_full[as], aph);
+        const ulonglong2 av = *(reinterpret_cast<const ulonglong2*>(aring + size_t(as) * kV4ABytes) + rl / 2);
+        uint64_t x[2] = {av.x, av.y};
+        const size_t row = base + cc.tt * kV4Rows + rl;
+        if (row < row_lo || row + 2 > row_hi) {
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+                if (row + q < row_lo || row + q >= row_hi) x[q] = 0;
+        }
+        uint64_t d[2][2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+#if F2_V4_MODE == 1
+            d[q][0] = x[q]; d[q][1] = x[q] ^ co_o;
+#else
+            lookup8x2(sel, co_e, co_o, x[q], d[q][0], d[q][1]);
+#endif
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_empty[as]);
+        if (t >= size_t(kV4DStages)) mbar_wait(&d_free[s], dph ^ 1);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+#if F2_V4_MODE == 3
+            if (d[0][c] != 0x123456789ull) continue;
+#endif
+            ulonglong2* dp = reinterpret_cast<ulonglong2*>(dring + size_t(s) * kV4DBytes +
+                                                           (2 * cp + c) * kV4ColPitch) + rl / 2;
+            dp[0] = make_ulonglong2(d[0][c], d[1][c]);
+        }
+#if !F2_V4_FENCE_PRODUCER
+        fence_async_smem();
+#endif
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&d_done[s]);
+        if (++as == kV4AStages) { as = 0; aph ^= 1; }
+        if (++s == kV4DStages) { s = 0; dph ^= 1; }
+        cc.next();
+    }
+}
+
 bool update_fast_ok(const UpdateArgs& a);
 bool update_v3_ok(const UpdateArgs& a) {
     return (a.sc % kV3Rows) == 0 && (reinterpret_cast<uintptr_t>(a.C) % 16) == 0 &&
@@ -934,20 +1322,22 @@ cudaError_t launch_update(const UpdateArgs& a, int num_sms, cudaStream_t s) {
     if (a.ncols <= 0) return cudaSuccess;
     if (a.release && !update_v3_ok(a)) return cudaErrorInvalidValue;
     if (update_v3_ok(a)) {
+        const bool v4 = options().update == 4;
         if (a.pdl) {
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(num_sms);
-            cfg.blockDim = dim3(kV3Threads);
-            cfg.dynamicSmemBytes = kV3Smem;
+            cfg.blockDim = dim3(v4 ? kV4Threads : kV3Threads);
+            cfg.dynamicSmemBytes = v4 ? kV4Smem : kV3Smem;
             cfg.stream = s;
             cudaLaunchAttribute at[1];
             at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
             at[0].val.programmaticStreamSerializationAllowed = 1;
             cfg.attrs = at;
             cfg.numAttrs = 1;
-            return cudaLaunchKernelEx(&cfg, k_update_v3, a);
+            return v4 ? cudaLaunchKernelEx(&cfg, k_update_v4, a) : cudaLaunchKernelEx(&cfg, k_update_v3, a);
         }
-        k_update_v3<<<num_sms, kV3Threads, kV3Smem, s>>>(a);
+        if (v4) k_update_v4<<<num_sms, kV4Threads, kV4Smem, s>>>(a);
+        else k_update_v3<<<num_sms, kV3Threads, kV3Smem, s>>>(a);
         return cudaGetLastError();
     }
     k_update<<<num_sms, kUpdThreads, kTabBytes, s>>>(a);
@@ -2950,6 +3340,9 @@ cudaError_t init_kernel_attrs() {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_update_v3, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(kV3Smem));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_update_v4, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(kV4Smem));
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(kTabBytes));

@@ -44,6 +44,7 @@
     X(rec_times, "F2GPU_REC_TIMES", 0, "per-phase CUDA-event times of the recursion on stderr")               \
     X(no_upload_overlap, "F2GPU_NO_UPLOAD_OVERLAP", 0, "host entry: upload everything before factoring")     \
     /* ---- kernel selection ---- */                                                                          \
+    X(update, "F2GPU_UPDATE", 4, "Schur update kernel: 4 = k_update_v4 (8-column groups, 8-bit tables, 24 consumer warps), 3 = k_update_v3 (16-column groups, 7-bit tables)") \
     X(panel, "F2GPU_PANEL", 1, "panel kernel k_panel_gj (0: the older transposed-M k_panel)")                 \
     X(panel_smem, "F2GPU_PANEL_SMEM", 1, "the panel kernel reserves a whole SM's shared memory")              \
     X(tc7, "F2GPU_TC7", 1, "fp4 pair leaf k_gemm_tc7 geometry 1..7 (0: single-CTA k_gemm_tc3)")               \
