@@ -272,6 +272,14 @@ int f2gpu_decompose_recursive_sharded(f2gpu_ctx *ctx, f2gpu_mat *w, int shards, 
  *   solve(c0, cm, R0, lo, hi): X = L11^-1 C on own columns in [lo, hi)
  *   product(c0, cm, R0, R1, lo, hi): rows [R1, n) of own columns ^= L21 X
  *   rank_update(c0, cm, lo, hi): panels [c0, cm) as rank-r_j updates (not full rank)
+ *   leaf(c0, c1, row_lo):     OPTIONAL (may be NULL).  When set it replaces the
+ *                             per-panel panel/apply calls of a leaf: columns
+ *                             [c0, c1), rows [row_lo, n), are replicated once, every
+ *                             rank factors the leaf on its copy (deterministic, so
+ *                             states and perm agree without a further exchange),
+ *                             keeps its own columns and applies the leaf's row swaps
+ *                             to its other columns.  The GPU drivers use it unless
+ *                             F2GPU_DIST_LEAF=0.
  * A non-zero callback return aborts the schedule with that code. */
 typedef struct f2gpu_dist_ops {
     void *user;
@@ -282,6 +290,7 @@ typedef struct f2gpu_dist_ops {
     int (*solve)(void *user, size_t c0, size_t cm, size_t R0, size_t col_lo, size_t col_hi);
     int (*product)(void *user, size_t c0, size_t cm, size_t R0, size_t R1, size_t col_lo, size_t col_hi);
     int (*rank_update)(void *user, size_t c0, size_t cm, size_t col_lo, size_t col_hi);
+    int (*leaf)(void *user, size_t c0, size_t c1, size_t row_lo);
 } f2gpu_dist_ops;
 int f2gpu_dist_schedule(size_t n_rows, size_t mu, int world, size_t leaf_panels, size_t tall_rows,
                         size_t tall_leaf_panels, const f2gpu_dist_ops *ops);

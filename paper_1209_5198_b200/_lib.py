@@ -111,12 +111,13 @@ GATHER_FN = C.CFUNCTYPE(C.c_int, vp, sz, sz, sz)
 SOLVE_FN = C.CFUNCTYPE(C.c_int, vp, sz, sz, sz, sz, sz)
 PRODUCT_FN = C.CFUNCTYPE(C.c_int, vp, sz, sz, sz, sz, sz, sz)
 RANKUPD_FN = C.CFUNCTYPE(C.c_int, vp, sz, sz, sz, sz)
+LEAF_FN = C.CFUNCTYPE(C.c_int, vp, sz, sz, sz)
 
 
 class DistOps(C.Structure):
     _fields_ = [("user", vp), ("panel", PANEL_FN), ("apply", APPLY_FN), ("state", STATE_FN),
                 ("gather", GATHER_FN), ("solve", SOLVE_FN), ("product", PRODUCT_FN),
-                ("rank_update", RANKUPD_FN)]
+                ("rank_update", RANKUPD_FN), ("leaf", LEAF_FN)]
 
 
 _SIG["f2gpu_dist_schedule"] = ([sz, sz, C.c_int, sz, sz, sz, C.POINTER(DistOps)], C.c_int)

@@ -272,6 +272,8 @@ struct f2gpu_ctx {
     uint64_t desc_tick = 0;
     size_t scr_flags_cap = 0;
     uint64_t* scr_hand = nullptr;         // per-panel hand-off blocks (f2::kHandWords each)
+    uint64_t* leafbuf = nullptr;          // distributed leaves: the gathered leaf columns (persistent: graph keys)
+    size_t leafbuf_words = 0;
     void* scr_st = nullptr;   // persistent PanelState[mu]
     size_t scr_st_cap = 0;
     uint32_t* scr_perm = nullptr;
@@ -784,18 +786,21 @@ int ensure_scratch(f2gpu_ctx* c, size_t n, size_t mu) {
 // swap_cols: word-columns [0, swap_cols) receive the row swaps (default: all);
 // the recursive driver's upload overlap keeps not-yet-materialised columns out
 int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_t c1, bool la,
-                   size_t swap_cols = size_t(-1)) {
+                   size_t swap_cols = size_t(-1), size_t coff = 0) {
+    // coff: s.w's word-column 0 is global word-column coff (a distributed leaf runs on
+    // a gathered copy of its own columns); states, flags and c0/c1/j stay global
     if (swap_cols > mu) swap_cols = mu;
+    auto colp = [&](size_t j) { return s.w.p + (j - coff) * s.w.stride; };
     const bool fused = la && c->fuse_post && f2::panel_link_ok();
     // fused schedule: two panel kernels can be resident (the running one and the
     // next one waiting for its head), each on its own SM
     const int grid = !la ? c->num_sms : (fused && c->num_sms > 2 ? c->num_sms - 2 : c->num_sms - 1);
     auto upd = [&](size_t j, uint32_t* release, size_t skip = 0, bool pdl = false) {
         f2::UpdateArgs u{};
-        u.C = s.w.p; u.sc = s.w.stride; u.c_wcol0 = j + 1 + skip; u.ncols = int(c1 - j - 1 - skip);
+        u.C = s.w.p; u.sc = s.w.stride; u.c_wcol0 = j + 1 + skip - coff; u.ncols = int(c1 - j - 1 - skip);
         if (u.ncols <= 0) return F2GPU_OK;
-        u.row_lo = 0; u.row_hi = n; u.a = s.w.p + j * s.w.stride; u.k_bits = 0;
-        u.B = s.w.p; u.sb = s.w.stride; u.b_row0 = 0; u.b_wcol0 = j + 1 + skip;
+        u.row_lo = 0; u.row_hi = n; u.a = colp(j); u.k_bits = 0;
+        u.B = s.w.p; u.sb = s.w.stride; u.b_row0 = 0; u.b_wcol0 = j + 1 + skip - coff;
         u.st = s.st + j;
         u.release = release;
         u.first_col = release != nullptr && c->u_first_col;
@@ -808,10 +813,10 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
     const bool colfirst = c->lookahead_col;
     if (!la) {
         for (size_t j = c0; j < c1; ++j) {
-            F2_TRY(check_launch(c, f2::launch_panel(s.w.p + j * s.w.stride, n, s.st, int(j),
+            F2_TRY(check_launch(c, f2::launch_panel(colp(j), n, s.st, int(j),
                                                     c->stream),
                                 "k_panel"));
-            F2_TRY(check_launch(c, f2::launch_post(s.w.p, s.w.stride, int(swap_cols), int(j), s.perm, n,
+            F2_TRY(check_launch(c, f2::launch_post(s.w.p, s.w.stride, int(swap_cols), int(j - coff), s.perm, n,
                                                    s.st + j, c->stream),
                                 "k_post"));
             if (j + 1 < c1) F2_TRY(upd(j, nullptr));
@@ -845,7 +850,7 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
                 if (j + 1 < c1) { l.next_ready = f + 3; l.next_count = uint32_t(grid); }
             }
             if (j + 1 < c1) {
-                l.next = s.w.p + (j + 1) * s.w.stride;
+                l.next = colp(j + 1);
                 if (c->panel_head) l.head_out = c->scr_flags + j * kFlagsPerPanel;  // this panel's head counter
             }
             l.poll_ns = c->poll_ns;
@@ -854,7 +859,7 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
             if (hand && j + 1 < c1) l.hand_out = c->scr_hand + j * f2::kHandWords;
             return l;
         };
-        F2_TRY(check_launch(c, f2::launch_panel_link(s.w.p + c0 * s.w.stride, n, s.st, int(c0), link_for(c0),
+        F2_TRY(check_launch(c, f2::launch_panel_link(colp(c0), n, s.st, int(c0), link_for(c0),
                                                      c->stream),
                             "k_panel"));
         // the side stream forks once after P(c0); every later panel kernel is queued
@@ -869,8 +874,8 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
         for (size_t j = c0; j < c1; ++j) {
             if (j > c0 && !spin) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_panel, 0));
             uint32_t* f = c->scr_flags + j * kFlagsPerPanel;
-            F2_TRY(check_launch(c, f2::launch_post_col(s.w.p, s.w.stride, int(swap_cols), int(j),
-                                                       j + 1 < c1 ? int(j + 1) : -1, s.perm, n, s.st + j, f,
+            F2_TRY(check_launch(c, f2::launch_post_col(s.w.p, s.w.stride, int(swap_cols), int(j - coff),
+                                                       j + 1 < c1 ? int(j + 1 - coff) : -1, s.perm, n, s.st + j, f,
                                                        c->stream, c->trace_buf != nullptr,
                                                        j + 1 < c1 && c->panel_head ? f2::kPanelHeadRows : 0,
                                                        j > c0 && spin ? f + 4 : nullptr,
@@ -883,7 +888,7 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
             // it is resident while P(j) runs and starts on P(j)'s head counter
             cudaStream_t ps = c->panel_early ? sides[(j - c0) & 1] : c->side;
             if (!c->panel_early) CUDA_TRY(cudaStreamWaitEvent(ps, c->ev_post, 0));
-            F2_TRY(check_launch(c, f2::launch_panel_link(s.w.p + (j + 1) * s.w.stride, n, s.st, int(j + 1),
+            F2_TRY(check_launch(c, f2::launch_panel_link(colp(j + 1), n, s.st, int(j + 1),
                                                          link_for(j + 1), ps),
                                 "k_panel"));
             CUDA_TRY(cudaEventRecord(c->ev_panel, ps));
@@ -896,11 +901,11 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
         }
         return F2GPU_OK;
     }
-    F2_TRY(check_launch(c, f2::launch_panel(s.w.p + c0 * s.w.stride, n, s.st, int(c0), c->stream),
+    F2_TRY(check_launch(c, f2::launch_panel(colp(c0), n, s.st, int(c0), c->stream),
                         "k_panel"));
     for (size_t j = c0; j < c1; ++j) {
         if (j > c0) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_panel, 0));
-        F2_TRY(check_launch(c, f2::launch_post(s.w.p, s.w.stride, int(swap_cols), int(j), s.perm, n,
+        F2_TRY(check_launch(c, f2::launch_post(s.w.p, s.w.stride, int(swap_cols), int(j - coff), s.perm, n,
                                                s.st + j, c->stream),
                             "k_post"));
         if (j + 1 >= c1) break;
@@ -910,7 +915,7 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
             // the next panel's column alone first (small CTAs, counter), then the
             // persistent update from column j+2 with no early release
             const int g1 = f2::update_col_grid(n, c->num_sms);
-            F2_TRY(check_launch(c, f2::launch_update_col(s.w.p + (j + 1) * s.w.stride, s.w.p + j * s.w.stride, n,
+            F2_TRY(check_launch(c, f2::launch_update_col(colp(j + 1), colp(j), n,
                                                          s.st + j, c->scr_flags + j * kFlagsPerPanel, g1,
                                                          c->stream),
                                 "k_update_col"));
@@ -920,7 +925,7 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
             F2_TRY(upd(j, c->scr_flags + j * kFlagsPerPanel));
         }
         CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_post, 0));
-        F2_TRY(check_launch(c, f2::launch_panel(s.w.p + (j + 1) * s.w.stride, n, s.st, int(j + 1),
+        F2_TRY(check_launch(c, f2::launch_panel(colp(j + 1), n, s.st, int(j + 1),
                                                 c->side, c->scr_flags + j * kFlagsPerPanel, wait_count),
                             "k_panel"));
         CUDA_TRY(cudaEventRecord(c->ev_panel, c->side));
@@ -1072,16 +1077,12 @@ int rec_trsm(RecRun& r, size_t a, size_t b, size_t Ra, size_t col0, size_t col1)
     return rec_trsm(r, m, b, Rm, col0, col1);
 }
 
-// a leaf: the block algorithm (with lookahead) on panels [c0, c1), replayed from
-// a CUDA graph from the second call with the same matrix, shape and range
-int rec_leaf(RecRun& r, size_t c0, size_t c1) {
-    f2gpu_ctx* c = r.c;
-    Shard& s = *r.s;
-    F2_TRY(ensure_cols(r, c1));
-    const size_t sw = std::min(r.frontier, r.mu);
-    if (!c->use_graphs || !c->graphs_stream_ok || c->tl.on) return enqueue_panels(c, s, r.n, r.mu, c0, c1, r.la, sw);
-    const std::array<uintptr_t, 8> key{uintptr_t(s.w.p), s.w.stride, r.n, r.mu, c0, c1,
-                                       uintptr_t(s.st) ^ (r.la ? 1u : 0u), sw};
+// Run `enqueue` (a leaf's launch sequence) through the per-context leaf-graph cache:
+// eager on the first call with this key, captured + instantiated + launched on the
+// second, replayed from the third.
+template <typename F>
+int leaf_graph_run(f2gpu_ctx* c, const std::array<uintptr_t, 8>& key, F&& enqueue) {
+    if (!c->use_graphs || !c->graphs_stream_ok || c->tl.on) return enqueue();
     LeafGraph& g = c->leaf_graphs.m[key];
     if (g.exec) {
         CUDA_TRY(cudaGraphLaunch(g.exec, c->stream));
@@ -1090,12 +1091,12 @@ int rec_leaf(RecRun& r, size_t c0, size_t c1) {
     }
     if (g.seen < 1) {
         g.seen += 1;
-        return enqueue_panels(c, s, r.n, r.mu, c0, c1, r.la, sw);
+        return enqueue();
     }
     cudaGraph_t graph = nullptr;
     const uint64_t l0 = c->launches;
     CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    int rc = enqueue_panels(c, s, r.n, r.mu, c0, c1, r.la, sw);
+    int rc = enqueue();
     cudaError_t ec = cudaStreamEndCapture(c->stream, &graph);
     if (rc != F2GPU_OK) { if (graph) cudaGraphDestroy(graph); return rc; }
     if (ec != cudaSuccess) return set_err(F2GPU_ECUDA, std::string("leaf graph capture: ") + cudaGetErrorString(ec));
@@ -1108,6 +1109,18 @@ int rec_leaf(RecRun& r, size_t c0, size_t c1) {
     g.nodes = c->launches - l0;
     CUDA_TRY(cudaGraphLaunch(g.exec, c->stream));
     return F2GPU_OK;
+}
+
+// a leaf: the block algorithm (with lookahead) on panels [c0, c1), replayed from
+// a CUDA graph from the second call with the same matrix, shape and range
+int rec_leaf(RecRun& r, size_t c0, size_t c1) {
+    f2gpu_ctx* c = r.c;
+    Shard& s = *r.s;
+    F2_TRY(ensure_cols(r, c1));
+    const size_t sw = std::min(r.frontier, r.mu);
+    const std::array<uintptr_t, 8> key{uintptr_t(s.w.p), s.w.stride, r.n, r.mu, c0, c1,
+                                       uintptr_t(s.st) ^ (r.la ? 1u : 0u), sw};
+    return leaf_graph_run(c, key, [&] { return enqueue_panels(c, s, r.n, r.mu, c0, c1, r.la, sw); });
 }
 
 template <typename F>
@@ -1496,6 +1509,7 @@ int dist_schedule(size_t n, size_t mu, int world, size_t base, size_t tall_rows,
     std::function<int(size_t, size_t, size_t)> rec = [&](size_t c0, size_t c1, size_t rlb) -> int {
         const size_t rows0 = n - std::min(n, 64 * c0);
         const size_t leaf = (tall_rows && rows0 >= tall_rows) ? std::min(base, tall_base) : base;
+        if (c1 - c0 <= leaf && o->leaf) return o->leaf(o->user, c0, c1, rlb);
         if (c1 - c0 <= leaf) {
             for (size_t j = c0; j < c1; ++j) {
                 const int owner = int(j % size_t(world));
@@ -1536,8 +1550,66 @@ struct DistGpu {
     std::deque<DevBuf> lg_keep;
     size_t lg_cols = 0;
     size_t tbase = 16, trsm_m4rm_k = 1024, cut = 16384, tc_cut = 8192;
+    // whole-leaf mode: the leaf last factored on the gathered copy [lf_c0, lf_c1) (rows
+    // >= lf_row valid); a split whose left half is exactly that leaf reuses it as Lg
+    size_t lf_c0 = 0, lf_c1 = 0, lf_row = 0;
+    bool lf_valid = false;
+    bool whole_leaf = true;
 
     static DistGpu& of(void* u) { return *static_cast<DistGpu*>(u); }
+    // Whole-leaf mode (default): a leaf is the latency-bound panel chain, which G GPUs
+    // cannot speed up; replicating each panel (one NCCL launch on the chain per panel)
+    // only slows it.  So the leaf's columns, rows [row_lo, n), are replicated ONCE
+    // (the split's own gather primitive), every process factors the leaf on its copy
+    // with the single-GPU schedule (fused lookahead, CUDA-graph replay) -- the kernels
+    // are deterministic, so every copy, state and perm comes out identical with no
+    // further exchange -- and then takes its own columns back and applies the leaf's
+    // row swaps to its other columns in one launch.  Per-leaf traffic: (n - row_lo) x
+    // leaf columns words; over a whole decomposition about half the matrix.
+    static int leaf(void* u, size_t c0, size_t c1, size_t row_lo) {
+        DistGpu& d = of(u);
+        f2gpu_ctx* c = d.c;
+        const size_t cols = c1 - c0, gs = dev_stride(d.n);
+        if (c->leafbuf_words < gs * cols) {
+            CUDA_TRY(cudaStreamSynchronize(c->stream));
+            c->leaf_graphs.clear();  // graphs hold the old pointer
+            cudaFree(c->leafbuf);
+            c->leafbuf = nullptr;
+            c->leafbuf_words = 0;
+            CUDA_TRY(cudaMalloc(&c->leafbuf, gs * cols * 8));
+            c->leafbuf_words = gs * cols;
+        }
+        const View lv{c->leafbuf, d.n, cols * 64, gs, gs};
+        d.lf_valid = false;
+        F2_TRY(d.ex->gather(c, *d.sh, d.base, d.G, c0, c1, row_lo, d.n, lv));
+        Shard& s0 = (*d.sh)[0];
+        Shard lf;
+        lf.w = lv; lf.lw = cols; lf.st = s0.st; lf.perm = s0.perm;
+        const bool la = lookahead_ok(c, lf, d.n);
+        const std::array<uintptr_t, 8> key{uintptr_t(lv.p), gs, d.n, d.mu, c0, c1,
+                                           uintptr_t(lf.st) ^ (la ? 1u : 0u), cols | (size_t(1) << 40)};
+        F2_TRY(leaf_graph_run(c, key, [&] { return enqueue_panels(c, lf, d.n, d.mu, c0, c1, la, cols, c0); }));
+        for (size_t i = 0; i < d.sh->size(); ++i) {
+            Shard& s = (*d.sh)[i];
+            const int gg = d.base + int(i);
+            if (i > 0)  // logical shards on one device: the states are factored once
+                CUDA_TRY(cudaMemcpyAsync(s.st + c0, s0.st + c0, cols * kStateBytes, cudaMemcpyDeviceToDevice,
+                                         c->stream));
+            const size_t l0 = lidx(gg, d.G, c0), l1 = lidx(gg, d.G, c1);
+            if (l1 > l0 && row_lo < d.n) {
+                const size_t q0 = size_t(gg) + l0 * size_t(d.G) - c0;
+                CUDA_TRY(cudaMemcpy2DAsync(s.w.p + l0 * s.w.stride + row_lo, s.w.stride * 8,
+                                           lv.p + q0 * gs + row_lo, size_t(d.G) * gs * 8, (d.n - row_lo) * 8,
+                                           l1 - l0, cudaMemcpyDeviceToDevice, c->stream));
+            }
+            F2_TRY(check_launch(c, f2::launch_swaps_range(s.w.p, s.w.stride, int(s.lw), int(l0), int(l1),
+                                                          i == 0 ? nullptr : s.perm, s.st, int(c0), int(c1),
+                                                          c->stream),
+                                "k_swaps_range"));
+        }
+        d.lf_c0 = c0; d.lf_c1 = c1; d.lf_row = row_lo; d.lf_valid = true;
+        return F2GPU_OK;
+    }
     int local(int owner) const { return owner - base; }  // may be outside [0, sh.size())
 
     static int panel(void* u, size_t j, int owner, size_t row_lo) {
@@ -1587,6 +1659,11 @@ struct DistGpu {
     static int gather(void* u, size_t c0, size_t cm, size_t row_lo) {
         DistGpu& d = of(u);
         const size_t cols = cm - c0, gs = dev_stride(d.n);
+        if (d.lf_valid && d.lf_c0 == c0 && d.lf_c1 == cm && d.lf_row <= row_lo) {
+            // the left half is the leaf every process has just factored on its copy
+            d.Lg = View{d.c->leafbuf, d.n, cols * 64, gs, gs};
+            return F2GPU_OK;
+        }
         if (cols > d.lg_cols) {
             d.lg_keep.clear();
             d.lg_keep.emplace_back(d.c);
@@ -1662,6 +1739,7 @@ struct DistGpu {
         o.solve = &DistGpu::solve;
         o.product = &DistGpu::product;
         o.rank_update = &DistGpu::rank_update;
+        if (whole_leaf) o.leaf = &DistGpu::leaf;
         return o;
     }
 };
@@ -1677,9 +1755,18 @@ void rec_leaf_params(size_t min_cols, size_t* base, size_t* tall_rows, size_t* t
 
 int run_dist_recursive(f2gpu_ctx* c, std::vector<Shard>& sh, int base, int G, size_t n, size_t mu, size_t min_cols,
                        Exchange& ex) {
-    for (auto& s : sh) F2_TRY(check_launch(c, f2::launch_iota(s.perm, n, c->stream), "k_iota"));
     DistGpu d;
     d.c = c; d.sh = &sh; d.base = base; d.G = G; d.n = n; d.mu = mu; d.ex = &ex;
+    d.whole_leaf = f2::options().dist_leaf != 0;
+    if (d.whole_leaf) {
+        // the leaves replay captured graphs: their state array, perm and counters are
+        // the context's persistent ones (stable addresses across calls)
+        F2_TRY(ensure_scratch(c, n, mu));
+        sh[0].st = static_cast<f2::PanelState*>(c->scr_st);
+        sh[0].perm = c->scr_perm;
+        CUDA_TRY(cudaMemsetAsync(c->scr_flags, 0, mu * 4 * kFlagsPerPanel, c->stream));
+    }
+    for (auto& s : sh) F2_TRY(check_launch(c, f2::launch_iota(s.perm, n, c->stream), "k_iota"));
     {  // the single-GPU recursion's TRSM base and product cutovers (options.h)
         const f2::Options& o = f2::options();
         d.tbase = std::min<size_t>(size_t(f2::trsm_max_panels()), std::max<size_t>(1, size_t(o.rec_tbase)));
@@ -1821,6 +1908,7 @@ int f2gpu_ctx_destroy(f2gpu_ctx* c) {
     cudaFree(c->scr_st);
     cudaFree(c->scr_perm);
     cudaFree(c->scr_flags);
+    cudaFree(c->leafbuf);
     for (auto& e : c->desc_cache) {
         cudaFree(e.d);
         cudaEventDestroy(e.ready);

@@ -2911,6 +2911,70 @@ cudaError_t launch_swaps(uint64_t* w, size_t stride, int ncols, int skip_col, ui
     return cudaGetLastError();
 }
 
+// Distributed recursion: the row swaps of a whole leaf (panels [j0, j1), in order)
+// on the word-columns outside [skip_lo, skip_hi) and on perm, one launch.  One warp
+// per column; panel j+1's header and pair list are loaded while panel j's rows move,
+// so a panel costs one dependent round trip (the rows), not two.
+__global__ void __launch_bounds__(256) k_swaps_range(uint64_t* __restrict__ w, size_t stride, int ncols,
+                                                     int skip_lo, int skip_hi, uint32_t* __restrict__ perm,
+                                                     const PanelState* __restrict__ st, int j0, int j1) {
+    const int gw = int((size_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (gw > ncols || (gw >= skip_lo && gw < skip_hi) || j0 >= j1) return;
+    if (gw == ncols && !perm) return;
+    uint32_t np = st[j0].npairs, R = st[j0].R;
+    uint32_t sidx[4], didx[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        sidx[e] = st[j0].src[lane + 32 * e];
+        didx[e] = st[j0].dst[lane + 32 * e];
+    }
+    for (int j = j0; j < j1; ++j) {
+        const uint32_t cnp = np, cR = R;
+        uint32_t cs[4], cd[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) { cs[e] = sidx[e]; cd[e] = didx[e]; }
+        if (j + 1 < j1) {
+            np = st[j + 1].npairs;
+            R = st[j + 1].R;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                sidx[e] = st[j + 1].src[lane + 32 * e];
+                didx[e] = st[j + 1].dst[lane + 32 * e];
+            }
+        }
+        if (cnp == 0) continue;
+        if (gw == ncols) {
+            uint32_t v[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (lane + 32 * e < int(cnp)) v[e] = perm[cR + cs[e]];
+            __syncwarp();
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (lane + 32 * e < int(cnp)) perm[cR + cd[e]] = v[e];
+        } else {
+            uint64_t* cp = w + size_t(gw) * stride + cR;
+            uint64_t v[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (lane + 32 * e < int(cnp)) v[e] = cp[cs[e]];
+            __syncwarp();
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (lane + 32 * e < int(cnp)) cp[cd[e]] = v[e];
+        }
+        __syncwarp();  // panel j's writes are visible to the warp before panel j+1's reads
+    }
+}
+
+cudaError_t launch_swaps_range(uint64_t* w, size_t stride, int ncols, int skip_lo, int skip_hi, uint32_t* perm,
+                               const PanelState* st, int j0, int j1, cudaStream_t s) {
+    const int warps = ncols + 1;
+    k_swaps_range<<<(warps + 7) / 8, 256, 0, s>>>(w, stride, ncols, skip_lo, skip_hi, perm, st, j0, j1);
+    return cudaGetLastError();
+}
+
 // Swaps on every other word-column (+perm) and Y = D*Z on the panel column in
 // ONE launch: the two touch disjoint data (skip_col is the panel column).
 constexpr int kPostYBlocks = 64;

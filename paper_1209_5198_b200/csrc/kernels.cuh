@@ -103,6 +103,10 @@ cudaError_t launch_panel_y(uint64_t* col, size_t n, const PanelState* st, int nu
                            cudaStream_t s);
 cudaError_t launch_swaps(uint64_t* w, size_t stride, int ncols, int skip_col, uint32_t* perm,
                          const PanelState* st, cudaStream_t s);
+// the row swaps of panels [j0, j1) in order, on word-columns outside [skip_lo, skip_hi)
+// and on perm (may be null); st = the state array (distributed leaves)
+cudaError_t launch_swaps_range(uint64_t* w, size_t stride, int ncols, int skip_lo, int skip_hi, uint32_t* perm,
+                               const PanelState* st, int j0, int j1, cudaStream_t s);
 // swaps on all columns but panel_col (+perm) and Y on panel_col, one launch
 cudaError_t launch_post(uint64_t* w, size_t stride, int ncols, int panel_col, uint32_t* perm,
                         size_t n, const PanelState* st, cudaStream_t s);

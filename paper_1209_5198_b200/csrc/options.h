@@ -41,6 +41,7 @@
     X(rec_first, "F2GPU_REC_FIRST", 64, "host entry: first leaf / upload chunk width (panels)")              \
     X(trsm_m4rm_k, "F2GPU_TRSM_M4RM_K", 1024, "TRSM products with k <= this run on M4RM")                     \
     X(trsm_kernel, "F2GPU_TRSM_KERNEL", 0, "1: k_trsm_block prefetching two panels ahead (512 threads at P > 32)") \
+    X(dist_leaf, "F2GPU_DIST_LEAF", 1, "distributed recursion: leaves factored whole on a replicated copy (0: per-panel broadcasts)") \
     X(rec_times, "F2GPU_REC_TIMES", 0, "per-phase CUDA-event times of the recursion on stderr")               \
     X(no_upload_overlap, "F2GPU_NO_UPLOAD_OVERLAP", 0, "host entry: upload everything before factoring")     \
     /* ---- kernel selection ---- */                                                                          \

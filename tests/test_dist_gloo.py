@@ -192,7 +192,7 @@ def test_sharded_multiply_protocol(po, n, k, m):
 # (f2gpu_dist_schedule, the host code the GPU drivers run) executed on two
 # gloo ranks with numpy/oracle callbacks for the device work.
 # ---------------------------------------------------------------------------
-def rec_worker(rank, world, port, n, m, kind, leaf, out_q):
+def rec_worker(rank, world, port, n, m, kind, leaf, whole_leaf, out_q):
     import ctypes as C
     import traceback
 
@@ -338,9 +338,58 @@ def rec_worker(rank, world, port, n, m, kind, leaf, out_q):
             for l, _q in own_cols(lo, hi):
                 update(l, Lg[j], int(Rj[j]), int(rj[j]))
 
+    @guard
+    def leaf_op(_, c0, c1, row_lo):
+        """Whole-leaf mode: replicate the leaf's columns once, factor the leaf on every
+        rank's copy (no further exchange), keep the own columns, swap the others."""
+        L = {}
+        for q in range(c0, c1):
+            t = torch.zeros(n - row_lo, dtype=torch.int64)
+            if q % world == rank:
+                t[:] = torch.from_numpy(W[local_of(q), row_lo:n].view(np.int64).copy())
+            dist.broadcast(t, src=q % world)
+            full = np.zeros(S, np.uint64)
+            full[row_lo:n] = t.numpy().view(np.uint64)
+            L[q] = full
+        for j in range(c0, c1):
+            R = int(Rj[j])
+            pnl = L[j][R:n].copy()
+            r, A, P, Z, sb = po.build_z(pnl) if n - R > 0 else (0, pnl, None, np.zeros(64, np.uint64), [])
+            pairs = composite_pairs(sb, r)
+            D = A[r:]
+            Y = np.zeros_like(D)
+            for t in range(64):
+                sel = ((D >> np.uint64(t)) & np.uint64(1)).astype(bool)
+                Y[sel] ^= Z[t]
+            A[r:] = Y
+            L[j][R:n] = A
+            for q in range(c0, c1):
+                if q != j:
+                    permute(L[q], R, pairs)
+            permute(perm, R, pairs)
+            rj[j] = r
+            Rj[j + 1] = R + r
+            pairs_of[j] = pairs
+            if r and R + r < n:
+                aw = np.ascontiguousarray(L[j][R + r:n])
+                for q in range(j + 1, c1):
+                    colv = np.ascontiguousarray(L[q][None, :])
+                    ol.f2o_m4rm_update(colv, S, R + r, aw, n - R - r, r, colv, S, R, 1, 8)
+                    L[q] = colv[0]
+        for l, q in enumerate(mine):
+            if c0 <= q < c1:
+                W[l, row_lo:n] = L[q][row_lo:n]
+            else:
+                for j in range(c0, c1):
+                    permute(W[l], int(Rj[j]), pairs_of[j])
+        Lg.clear()
+        Lg.update(L)  # a split whose left half is this leaf reuses the copy (DistGpu::gather)
+
     ops = _lib.DistOps(None, _lib.PANEL_FN(panel), _lib.APPLY_FN(apply), _lib.STATE_FN(state),
                        _lib.GATHER_FN(gather), _lib.SOLVE_FN(solve), _lib.PRODUCT_FN(product),
                        _lib.RANKUPD_FN(rank_update))
+    if whole_leaf:
+        ops.leaf = _lib.LEAF_FN(leaf_op)
     rc = lib.f2gpu_dist_schedule(n, mu, world, leaf, 0, leaf, C.byref(ops))
     out_q.put((rank, rc, mine, W, perm, rj.astype(np.uint32)))
     dist.barrier()
@@ -354,17 +403,20 @@ def make_input(po, n, m, kind):
     return po.random_dense(n, m, 0.5 if kind == "dense" else 0.05, 33)
 
 
+@pytest.mark.parametrize("whole_leaf", [False, True], ids=["per_panel", "whole_leaf"])
 @pytest.mark.parametrize("n,m,kind,leaf", [(700, 640, "dense", 2), (400, 1000, "dense", 1), (900, 512, "xy", 2),
                                            (300, 577, "sparse", 3)])
-def test_recursive_schedule_matches_oracle(po, n, m, kind, leaf):
+def test_recursive_schedule_matches_oracle(po, n, m, kind, leaf, whole_leaf):
     """The distributed recursion (leaves, splits with gather + solve + product, and
     the rank-deficient fallback) driven by libf2gpu's f2gpu_dist_schedule on two
-    gloo ranks gives the single-process oracle's W, perm and r_j bit-for-bit."""
+    gloo ranks gives the single-process oracle's W, perm and r_j bit-for-bit, with
+    per-panel replication and with whole leaves factored on a replicated copy (the
+    GPU drivers' default, f2gpu_dist_ops.leaf)."""
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=rec_worker, args=(r, world, port, n, m, kind, leaf, q)) for r in range(world)]
+    procs = [ctx.Process(target=rec_worker, args=(r, world, port, n, m, kind, leaf, whole_leaf, q)) for r in range(world)]
     for pr in procs:
         pr.start()
     res = [q.get(timeout=300) for _ in range(world)]
