@@ -10,8 +10,11 @@ both give the identical overlay, perm and r_j).  Metric: Gbitop/s = n^3 / t.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 (torchrun): column blocks round-robin over the ranks, one NCCL broadcast
-per panel (strong scaling: the job is one 65536^2 decomposition).
+N > 1 (torchrun): word-columns round-robin over the ranks; decompose_recursive
+replicates each leaf's columns once and every rank factors the leaf on its copy
+(no per-panel exchange), the splits' TRSM + products are sharded by output
+word-columns after one gather of the left columns (--variant block: one NCCL
+broadcast per panel).  Strong scaling: the job is one 65536^2 decomposition.
 
 The JSON line carries: value (device-resident, CUDA events, max over ranks),
 parity (the LAST timed step's W, perm and r_j -- a CUDA-graph replay --
@@ -367,7 +370,7 @@ def cfg_json(cfg, gpus, variant="block"):
     mib = n * ((m + 63) // 64) * 8 / 2 ** 20
     return {"workload": f"decompose {n}x{m} dense F2, Bernoulli({cfg['p']}), seed {cfg['seed']} ({which})",
             "n": n, "m": m, "density": cfg["p"], "seed": cfg["seed"],
-            "word_bits": 64, "tables": "9 groups (7x8+8 bits), 16 word-cols/CTA",
+            "word_bits": 64, "tables": "k_update_v4: 8 x 8-bit tables per 8 word-column group (128 KiB shared memory per CTA)",
             "parallelism": f"column-round-robin x{gpus}" if gpus > 1 else "single GPU",
             "variant": VARIANTS[variant] + (f"; word-columns round-robin over {gpus} GPUs (f2gpu_decompose_{variant}_dist)"
                                             if gpus > 1 else ""),
@@ -592,7 +595,7 @@ def measure_update_roofline(f2, lib, _lib, ctx, stream, torch, n: int) -> dict:
             "unit_workload": f"C({n}x{n}) ^= A({n}x64)*B(64x{n})",
             "algorithmic_bytes": alg, "us_per_launch": round(t * 1e6, 1),
             "bitops_per_s": round(n * 64 * n / t, 1),
-            "share_of_step": "21% of the decomposition's kernel time (profiles/r2b_launches_summary.txt)",
+            "share_of_step": "20% of the decomposition's kernel time (profiles/r2c_launches_summary.txt)",
             "peak_source": src}
 
 
@@ -633,7 +636,7 @@ def measure_tensor_roofline(f2, lib, _lib, ctx, stream, torch, n: int = 16384) -
             "kernel": "k_gemm_tc7 (fp4 kind::mxf4 GF(2) product leaf, cta_group::2, M-side operand in TMEM)",
             "unit_workload": f"C({n}x{n}) = A({n}x{n})*B({n}x{n}), 2*n^3 fp4 FLOP",
             "us_per_launch": round(t * 1e6, 1), "bitops_per_s": round(n ** 3 / t, 1),
-            "share_of_step": "37% of the decomposition's kernel time (profiles/r2b_launches_summary.txt)",
+            "share_of_step": "37% of the decomposition's kernel time (profiles/r2c_launches_summary.txt)",
             "peak_source": src}
 
 

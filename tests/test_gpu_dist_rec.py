@@ -1,7 +1,7 @@
 """decompose_recursive over word-column shards on one GPU.
 
 f2gpu_decompose_recursive_sharded runs the distributed recursion's schedule
-(f2gpu_dist_schedule: per-leaf panel replication, one left-column gather per
+(f2gpu_dist_schedule: each leaf factored whole on a replicated copy, one left-column gather per
 split, TRSM + A' product on each shard's own right-half columns) over G
 logical shards with device-to-device exchanges; f2gpu_decompose_recursive_dist
 runs it through NCCL (a 1-rank communicator here).  Every result must equal the
@@ -141,3 +141,61 @@ def test_recursive_dist_nccl_cfg4_digest(f2, po, monkeypatch):
     assert po.digest(A.download().words, n, n) == g["w_digest"]
     A.free()
     ctx.close()
+
+
+def test_recursive_sharded_leaf_graphs_replay(f2, ctx, po):
+    """Whole-leaf mode replays each leaf from a captured CUDA graph from the third
+    call with the same shape (the leaf runs on the context's persistent copy, so
+    the graph does not depend on the caller's buffers or on G): eager, capture,
+    replays -- with different inputs (full rank, rank-deficient, sparse) and
+    different shard counts through the same graphs, every call against the oracle."""
+    n, m, mc = 3000, 2560, 640   # 40 panels, leaves of 10
+    inputs = [po.random_dense(n, m, 0.5, 91), po.random_dense(n, m, 0.5, 92),
+              po.m4rm_mult(po.random_dense(n, 900, 0.5, 93), n, 900, po.random_dense(900, m, 0.5, 94), m),
+              po.random_dense(n, m, 0.03, 95), po.random_dense(n, m, 0.5, 96)]
+    for a, G in zip(inputs, [2, 2, 3, 8, 1]):
+        w0, p0, r0, k0 = po.decompose_block(a, n, m)
+        w, perm, rj, rank = _sharded(f2, ctx, a, n, m, G, mc)
+        assert rank == k0 and np.array_equal(rj, r0) and np.array_equal(perm, p0), G
+        assert np.array_equal(w.words[:, :n], w0[:, :n]), G
+
+
+_CHILD_PER_PANEL = r"""
+import sys
+sys.path.insert(0, sys.argv[1])
+import ctypes as C
+import numpy as np
+import paper_1209_5198_b200 as f2
+from paper_1209_5198_b200 import _lib
+from oracle import pyoracle as po
+
+ctx = f2.Context(0)
+lib = _lib.load()
+for n, m, p, mc, G in [(1000, 1000, 0.5, 128, 2), (2048, 4096, 0.5, 256, 3), (3000, 1280, 0.1, 64, 8)]:
+    a = po.random_dense(n, m, p, n + m + G)
+    w0, p0, r0, k0 = po.decompose_block(a, n, m)
+    W = f2.DeviceMatrix.from_host(f2.BitMatrix(n, m, a), ctx)
+    perm = np.zeros(n, np.uint32)
+    rj = np.zeros((m + 63) // 64, np.uint32)
+    rk = C.c_size_t()
+    _lib.check(lib.f2gpu_decompose_recursive_sharded(ctx.handle, W.handle, G, mc, perm.ctypes.data,
+                                                     rj.ctypes.data, C.byref(rk)))
+    assert rk.value == k0 and np.array_equal(rj, r0) and np.array_equal(perm, p0), (n, m, G)
+    assert np.array_equal(W.download().words[:, :n], w0[:, :n]), (n, m, G)
+    W.free()
+print("OK")
+"""
+
+
+def test_recursive_sharded_per_panel_mode():
+    """F2GPU_DIST_LEAF=0: the per-panel replication schedule (panel / apply callbacks)
+    stays bit-exact.  Options are read once per process, hence the child."""
+    import os
+    import subprocess
+    import sys
+
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, F2GPU_DIST_LEAF="0")
+    r = subprocess.run([sys.executable, "-c", _CHILD_PER_PANEL, str(root)], env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0 and r.stdout.strip().endswith("OK"), r.stdout[-2000:] + r.stderr[-4000:]
