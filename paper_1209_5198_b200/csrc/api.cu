@@ -272,6 +272,7 @@ struct f2gpu_ctx {
     uint64_t desc_tick = 0;
     size_t scr_flags_cap = 0;
     uint64_t* scr_hand = nullptr;         // per-panel hand-off blocks (f2::kHandWords each)
+    uint32_t* zero_flag = nullptr;        // rank-deficient splits: "trailing block is not all zero"
     uint64_t* leafbuf = nullptr;          // distributed leaves: the gathered leaf columns (persistent: graph keys)
     size_t leafbuf_words = 0;
     void* scr_st = nullptr;   // persistent PanelState[mu]
@@ -1150,26 +1151,55 @@ int rec_decompose(RecRun& r, size_t c0, size_t c1) {
     if (c1 - c0 <= leaf) return timed(r, "leaf", [&] { return rec_leaf(r, c0, c1); });
     const size_t cm = c0 + (c1 - c0) / 2;
     F2_TRY(rec_decompose(r, c0, cm));
-    size_t R0, r0, Rl, rl;
-    F2_TRY(rec_state(r, c0, &R0, &r0));
-    F2_TRY(rec_state(r, cm - 1, &Rl, &rl));
-    const size_t R1 = Rl + rl;
-    const bool full = R1 - R0 == 64 * (cm - c0) && R0 % 64 == 0;
+    // (R_j, r_j) of the left half in one read-back (one stream sync per split)
+    std::vector<uint32_t> Rr(2 * (cm - c0));
+    CUDA_TRY(cudaStreamSynchronize(r.c->stream));
+    CUDA_TRY(cudaMemcpy2D(Rr.data(), 8, r.s->st + c0, kStateBytes, 8, cm - c0, cudaMemcpyDeviceToHost));
+    const size_t R0 = Rr[0], R1 = size_t(Rr[2 * (cm - c0 - 1)]) + Rr[2 * (cm - c0 - 1) + 1];
+    // cf: the left half's full-rank prefix [c0, cf) (r_j = 64, pivot rows 64-aligned):
+    // its panels reach the right half as X = L11^-1 C and A' = D ^ L21 X; the panels
+    // after it (rank-deficient inputs only) as rank-r_j updates, zero-rank ones skipped
+    size_t cf = c0;
+    if (R0 % 64 == 0)
+        while (cf < cm && Rr[2 * (cf - c0) + 1] == 64) ++cf;
+    const bool full = cf == cm;
+    const size_t Rf = R0 + 64 * (cf - c0);
     F2_TRY(ensure_cols(r, c1));
-    if (full) {
-        F2_TRY(timed(r, "trsm", [&] { return rec_trsm(r, c0, cm, R0, cm, c1); }));
+    if (cf > c0) {
+        F2_TRY(timed(r, "trsm", [&] { return rec_trsm(r, c0, cf, R0, cm, c1); }));
         // rows [0, R1) are final once the TRSM is done (the product writes rows >= R1
         // only), so their download overlaps the product too
-        if (c1 == r.mu && r.on_final) F2_TRY(r.on_final(R1));
-        if (R1 < r.n)
+        if (full && c1 == r.mu && r.on_final) F2_TRY(r.on_final(R1));
+        if (Rf < r.n)
             F2_TRY(timed(r, "product", [&] {
-                return best_product(r.c, wview(*r.s, R1, r.n - R1, cm, c1 - cm),
-                                    wview(*r.s, R1, r.n - R1, c0, cm - c0),
-                                    wview(*r.s, R0, R1 - R0, cm, c1 - cm), r.cut, r.tc_cut);
+                return best_product(r.c, wview(*r.s, Rf, r.n - Rf, cm, c1 - cm),
+                                    wview(*r.s, Rf, r.n - Rf, c0, cf - c0),
+                                    wview(*r.s, R0, Rf - R0, cm, c1 - cm), r.cut, r.tc_cut);
             }));
-    } else {
-        F2_TRY(rank_updates(r, c0, cm, cm, c1, r.n));
+    }
+    if (!full) {
+        for (size_t j = cf; j < cm; ++j)
+            if (Rr[2 * (j - c0) + 1] != 0) F2_TRY(rank_updates(r, j, j + 1, cm, c1, r.n));
         if (c1 == r.mu && r.on_final) F2_TRY(r.on_final(R1));
+        // a rank-deficient left half: when what is left of the right half is all zero
+        // (or no rows are left), its panels have rank 0 and no swaps -- skip the chain
+        bool zero = R1 >= r.n;
+        if (!zero) {
+            f2gpu_ctx* c = r.c;
+            if (!c->zero_flag) CUDA_TRY(cudaMalloc(&c->zero_flag, 4));
+            CUDA_TRY(cudaMemsetAsync(c->zero_flag, 0, 4, c->stream));
+            F2_TRY(check_launch(c, f2::launch_any_nonzero(r.s->w.p + cm * r.s->w.stride, r.s->w.stride, R1, r.n,
+                                                          c1 - cm, c->zero_flag, c->num_sms, c->stream),
+                                "k_any_nonzero"));
+            uint32_t nz = 1;
+            CUDA_TRY(cudaMemcpyAsync(&nz, c->zero_flag, 4, cudaMemcpyDeviceToHost, c->stream));
+            CUDA_TRY(cudaStreamSynchronize(c->stream));
+            zero = nz == 0;
+        }
+        if (zero)
+            return check_launch(r.c, f2::launch_fill_zero_states(r.s->st, int(cm), int(c1), uint32_t(std::min(R1, r.n)),
+                                                                 r.c->stream),
+                                "k_fill_zero_states");
     }
     return rec_decompose(r, cm, c1);
 }
@@ -1909,6 +1939,7 @@ int f2gpu_ctx_destroy(f2gpu_ctx* c) {
     cudaFree(c->scr_perm);
     cudaFree(c->scr_flags);
     cudaFree(c->leafbuf);
+    cudaFree(c->zero_flag);
     for (auto& e : c->desc_cache) {
         cudaFree(e.d);
         cudaEventDestroy(e.ready);

@@ -2911,6 +2911,43 @@ cudaError_t launch_swaps(uint64_t* w, size_t stride, int ncols, int skip_col, ui
     return cudaGetLastError();
 }
 
+// Rank-deficient inputs (decompose_recursive): is the block rows [row0, n) x nwc
+// word-columns all zero?  *flag |= 1 otherwise.  One pass over the block (HBM-bound),
+// run only after a split whose left half was not at full rank.
+__global__ void __launch_bounds__(256) k_any_nonzero(const uint64_t* __restrict__ w, size_t stride, size_t row0,
+                                                     size_t n, size_t nwc, uint32_t* __restrict__ flag) {
+    const size_t rows = n - row0, total = rows * nwc;
+    uint64_t acc = 0;
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += size_t(gridDim.x) * blockDim.x) {
+        const size_t q = i / rows, r = i - q * rows;
+        acc |= w[q * stride + row0 + r];
+    }
+    if (__syncthreads_or(acc != 0) && threadIdx.x == 0) atomicOr(flag, 1u);
+}
+
+cudaError_t launch_any_nonzero(const uint64_t* w, size_t stride, size_t row0, size_t n, size_t nwc, uint32_t* flag,
+                               int num_sms, cudaStream_t s) {
+    if (row0 >= n || nwc == 0) return cudaSuccess;
+    const size_t total = (n - row0) * nwc;
+    const int grid = int(std::min<size_t>(size_t(num_sms) * 8, (total + 255) / 256));
+    k_any_nonzero<<<grid, 256, 0, s>>>(w, stride, row0, n, nwc, flag);
+    return cudaGetLastError();
+}
+
+// ... and when it is: panels [j0, j1) have rank 0 and no swaps -- exactly what the
+// panel kernel writes for an all-zero column (R, r = 0, npairs = 0, Z = 0)
+__global__ void __launch_bounds__(64) k_fill_zero_states(PanelState* __restrict__ st, int j0, uint32_t R) {
+    PanelState* p = st + j0 + blockIdx.x;
+    if (threadIdx.x == 0) { p->R = R; p->r = 0; p->npairs = 0; p->flags = 0; }
+    p->Z[threadIdx.x] = 0;
+}
+
+cudaError_t launch_fill_zero_states(PanelState* st, int j0, int j1, uint32_t R, cudaStream_t s) {
+    if (j1 <= j0) return cudaSuccess;
+    k_fill_zero_states<<<j1 - j0, 64, 0, s>>>(st, j0, R);
+    return cudaGetLastError();
+}
+
 // Distributed recursion: the row swaps of a whole leaf (panels [j0, j1), in order)
 // on the word-columns outside [skip_lo, skip_hi) and on perm, one launch.  One warp
 // per column; panel j+1's header and pair list are loaded while panel j's rows move,

@@ -107,6 +107,11 @@ cudaError_t launch_swaps(uint64_t* w, size_t stride, int ncols, int skip_col, ui
 // and on perm (may be null); st = the state array (distributed leaves)
 cudaError_t launch_swaps_range(uint64_t* w, size_t stride, int ncols, int skip_lo, int skip_hi, uint32_t* perm,
                                const PanelState* st, int j0, int j1, cudaStream_t s);
+// rank-deficient inputs: *flag |= 1 unless rows [row0, n) of nwc word-columns at w are all zero
+cudaError_t launch_any_nonzero(const uint64_t* w, size_t stride, size_t row0, size_t n, size_t nwc, uint32_t* flag,
+                               int num_sms, cudaStream_t s);
+// states of panels [j0, j1) as the panel kernel leaves them on all-zero columns (R, r = 0, no swaps)
+cudaError_t launch_fill_zero_states(PanelState* st, int j0, int j1, uint32_t R, cudaStream_t s);
 // swaps on all columns but panel_col (+perm) and Y on panel_col, one launch
 cudaError_t launch_post(uint64_t* w, size_t stride, int ncols, int panel_col, uint32_t* perm,
                         size_t n, const PanelState* st, cudaStream_t s);

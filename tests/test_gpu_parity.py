@@ -458,6 +458,49 @@ def test_decompose_recursive_rank_deficient(f2, ctx, po):
     assert same(got.overlay.words, w, 3000)
 
 
+def _wcols(po, n, parts, seed):
+    """Word-column concatenation of blocks: ("rand", cols) | ("zero", cols) | ("xy", cols, rank)."""
+    out = []
+    for i, part in enumerate(parts):
+        kind, cols = part[0], part[1]
+        assert cols % 64 == 0
+        if kind == "rand":
+            blk = po.random_dense(n, cols, 0.5, seed + 10 * i)
+        elif kind == "zero":
+            blk = np.zeros_like(po.random_dense(n, cols, 0.5, 1))
+        else:
+            blk = po.m4rm_mult(po.random_dense(n, part[2], 0.5, seed + 10 * i), n, part[2],
+                               po.random_dense(part[2], cols, 0.5, seed + 10 * i + 1), cols)
+        out.append(blk[:cols // 64])
+    return np.ascontiguousarray(np.concatenate(out, axis=0))
+
+
+@pytest.mark.parametrize("n,parts,min_cols", [
+    # left half = 5 full-rank panels, 2 zero panels, 1 full panel; the rest is dense
+    (2048, [("rand", 320), ("zero", 128), ("rand", 1600)], 512),
+    # a full-rank prefix, then rank 100 spread over two panels, then nothing (all-zero remainder)
+    (2048, [("rand", 640), ("xy", 3456, 100)], 1024),
+    # no rows left after the left half (n < m): every later panel has rank 0
+    (512, [("rand", 2048)], 512),
+    # rank runs out inside a left half whose pivot rows are not 64-aligned
+    (1500, [("xy", 1024, 70), ("rand", 1024)], 256),
+    # all zero
+    (700, [("zero", 1024)], 256),
+])
+def test_decompose_recursive_deficient_splits(f2, ctx, po, n, parts, min_cols):
+    """Rank-deficient left halves: the full-rank prefix goes through TRSM + product,
+    the panels after it through rank-r_j updates (zero-rank ones skipped), and an
+    all-zero remainder skips its panel chain (k_any_nonzero / k_fill_zero_states)."""
+    m = sum(p[1] for p in parts)
+    a = _wcols(po, n, parts, 31)
+    w, perm, rj, rank = po.decompose_block(a, n, m)
+    for _ in range(3):  # eager, capture, replay of the leaves
+        got = f2.decompose_recursive(bm(f2, a, n, m), min_cols=min_cols, ctx=ctx)
+        assert got.rank == rank
+        assert np.array_equal(got.P.perm, perm) and np.array_equal(got.block_ranks, rj)
+        assert same(got.overlay.words, w, n)
+
+
 # ---------------------------------------------------------------------------
 # product leaf selection: the fp4 tensor-core Strassen plan (B transposed once,
 # batched leaves) against M4RM and the oracle, 0-2 Strassen levels
