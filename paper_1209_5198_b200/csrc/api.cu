@@ -72,6 +72,12 @@ int set_err(int code, const std::string& msg) {
         snprintf(b, sizeof b, " [spin timeout: site %llu block %llu counter +%lld B (panel %lld idx %lld) value %llu target %llu]",
                  g_diag[0] >> 8, g_diag[1], off, off / 32, (off % 32) / 4, g_diag[3] >> 32, g_diag[3] & 0xffffffffull);
         g_err += b;
+        if (g_diag[6]) {  // k_panel_chain's progress: panel << 8 | stage per team
+            snprintf(b, sizeof b, " [chain %llu..%llu: team 0 panel %llu stage %llu, team 1 panel %llu stage %llu]",
+                     g_diag[6] >> 32, g_diag[6] & 0xffffffffull, g_diag[4] >> 8, g_diag[4] & 255, g_diag[5] >> 8,
+                     g_diag[5] & 255);
+            g_err += b;
+        }
     }
     return code;
 }
@@ -213,6 +219,12 @@ struct LeafGraph {
     int seen = 0;
     cudaGraphExec_t exec = nullptr;
     uint64_t nodes = 0;
+    // the leaf's k_panel_chain launch stays OUTSIDE the graph (launched on the side
+    // stream just before the graph): the kernels in the graph spin on its counters, and
+    // a graph gives no guarantee that an independent root node is submitted before
+    // ~770 dependent nodes of the other branch have been (seen: it was not, at 256 panels)
+    bool has_chain = false;
+    f2::ChainArgs chain{};
 };
 struct LeafGraphs {
     std::map<std::array<uintptr_t, 8>, LeafGraph> m;
@@ -247,6 +259,10 @@ struct f2gpu_ctx {
     // Off: measured no faster at 65536^2 (64.12 vs 64.17 ms); kept opt-in
     // (tests/test_gpu_parity.py::test_panel_hand_off)
     bool panel_hand = false;
+    // the panel chain of a leaf in one persistent CTA (k_panel_chain): panel j+1 starts
+    // on an in-CTA hand-off instead of k_post_col(j)'s first rows
+    bool panel_chain = false;
+    int chain_sms = 2;
     cudaEvent_t ev_panel2 = nullptr;
     cudaStream_t side = nullptr;          // lookahead: panel kernels run here
     cudaStream_t side2 = nullptr;         // fused schedule: alternate panels (the next one is resident early)
@@ -786,16 +802,35 @@ int ensure_scratch(f2gpu_ctx* c, size_t n, size_t mu) {
 // swaps of every panel are applied to all mu word-columns.
 // swap_cols: word-columns [0, swap_cols) receive the row swaps (default: all);
 // the recursive driver's upload overlap keeps not-yet-materialised columns out
+// chain_defer: when the stream is being captured, the k_panel_chain launch (and its
+// fork / join) is left to the caller, who gets its arguments here (has = true) and must
+// launch it on c->side before the graph (chain_fork / chain_join); a capturing caller
+// without chain_defer gets the per-panel launches instead
+struct ChainDefer {
+    bool has = false;
+    f2::ChainArgs args{};
+};
+int chain_fork(f2gpu_ctx* c, const f2::ChainArgs& a);
+int chain_join(f2gpu_ctx* c);
+
 int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_t c1, bool la,
-                   size_t swap_cols = size_t(-1), size_t coff = 0) {
+                   size_t swap_cols = size_t(-1), size_t coff = 0, ChainDefer* chain_defer = nullptr) {
     // coff: s.w's word-column 0 is global word-column coff (a distributed leaf runs on
     // a gathered copy of its own columns); states, flags and c0/c1/j stay global
     if (swap_cols > mu) swap_cols = mu;
     auto colp = [&](size_t j) { return s.w.p + (j - coff) * s.w.stride; };
     const bool fused = la && c->fuse_post && f2::panel_link_ok();
+    // chain: the leaf's panel kernels are one persistent CTA (needs counter-driven posts)
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CUDA_TRY(cudaStreamIsCapturing(c->stream, &cap));
+    const bool capturing = cap != cudaStreamCaptureStatusNone;
+    const bool chain = fused && c->panel_chain && c->post_spin && c->panel_early && !c->panel_head &&
+                       !c->panel_hand && c->num_sms > 2 && (!capturing || chain_defer != nullptr);
     // fused schedule: two panel kernels can be resident (the running one and the
     // next one waiting for its head), each on its own SM
-    const int grid = !la ? c->num_sms : (fused && c->num_sms > 2 ? c->num_sms - 2 : c->num_sms - 1);
+    const int grid = !la ? c->num_sms
+                         : (chain ? c->num_sms - std::max(1, std::min(c->chain_sms, c->num_sms - 1))
+                                  : (fused && c->num_sms > 2 ? c->num_sms - 2 : c->num_sms - 1));
     auto upd = [&](size_t j, uint32_t* release, size_t skip = 0, bool pdl = false) {
         f2::UpdateArgs u{};
         u.C = s.w.p; u.sc = s.w.stride; u.c_wcol0 = j + 1 + skip - coff; u.ncols = int(c1 - j - 1 - skip);
@@ -860,6 +895,44 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
             if (hand && j + 1 < c1) l.hand_out = c->scr_hand + j * f2::kHandWords;
             return l;
         };
+        if (chain) {
+            // P(c0) in stream order, then one k_panel_chain launch on the side stream for
+            // panels (c0, c1), forked BEFORE P(c0) so that the chain CTA is resident while
+            // P(c0) runs; the posts on the main stream wait on the done counters, the
+            // updates are unchanged
+            const bool has_chain = c0 + 1 < c1;
+            f2::ChainArgs a{};
+            a.w = s.w.p; a.stride = s.w.stride; a.n = n; a.st = s.st; a.flags = c->scr_flags;
+            a.flags_per_panel = int(kFlagsPerPanel);
+            a.leaf0 = int(c0); a.c0 = int(c0 + 1); a.c1 = int(c1); a.coff = int(coff);
+            a.yblocks = uint32_t(f2::post_col_yblocks(n));
+            a.upd_grid = uint32_t(grid);
+            a.poll_ns = uint32_t(c->poll_ns);
+            a.trace = c->trace_buf != nullptr;
+            if (has_chain) {
+                if (capturing) {
+                    chain_defer->has = true;
+                    chain_defer->args = a;
+                } else {
+                    F2_TRY(chain_fork(c, a));
+                }
+            }
+            F2_TRY(check_launch(c, f2::launch_panel_link(colp(c0), n, s.st, int(c0), link_for(c0), c->stream),
+                                "k_panel"));
+            for (size_t j = c0; j < c1; ++j) {
+                uint32_t* f = c->scr_flags + j * kFlagsPerPanel;
+                F2_TRY(check_launch(c, f2::launch_post_col(s.w.p, s.w.stride, int(swap_cols), int(j - coff),
+                                                           j + 1 < c1 ? int(j + 1 - coff) : -1, s.perm, n, s.st + j,
+                                                           f, c->stream, c->trace_buf != nullptr, 0,
+                                                           j > c0 ? f + 4 : nullptr,
+                                                           j > c0 && f2::options().post_pdl),
+                                    "k_post_col"));
+                if (j + 1 >= c1) break;
+                F2_TRY(upd(j, f + 3, 1, c->pdl));
+            }
+            if (has_chain && !capturing) F2_TRY(chain_join(c));
+            return F2GPU_OK;
+        }
         F2_TRY(check_launch(c, f2::launch_panel_link(colp(c0), n, s.st, int(c0), link_for(c0),
                                                      c->stream),
                             "k_panel"));
@@ -931,6 +1004,19 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
                             "k_panel"));
         CUDA_TRY(cudaEventRecord(c->ev_panel, c->side));
     }
+    return F2GPU_OK;
+}
+
+// the k_panel_chain launch of a leaf on the side stream, ordered after the main stream's
+// earlier work, and the join after the leaf's main-stream launches (or graph)
+int chain_fork(f2gpu_ctx* c, const f2::ChainArgs& a) {
+    CUDA_TRY(cudaEventRecord(c->ev_post, c->stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_post, 0));
+    return check_launch(c, f2::launch_panel_chain(a, c->side), "k_panel_chain");
+}
+int chain_join(f2gpu_ctx* c) {
+    CUDA_TRY(cudaEventRecord(c->ev_panel, c->side));
+    CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_panel, 0));
     return F2GPU_OK;
 }
 
@@ -1083,21 +1169,28 @@ int rec_trsm(RecRun& r, size_t a, size_t b, size_t Ra, size_t col0, size_t col1)
 // second, replayed from the third.
 template <typename F>
 int leaf_graph_run(f2gpu_ctx* c, const std::array<uintptr_t, 8>& key, F&& enqueue) {
-    if (!c->use_graphs || !c->graphs_stream_ok || c->tl.on) return enqueue();
+    if (!c->use_graphs || !c->graphs_stream_ok || c->tl.on) return enqueue(nullptr);
     LeafGraph& g = c->leaf_graphs.m[key];
-    if (g.exec) {
+    auto launch = [&]() {
+        if (g.has_chain) F2_TRY(chain_fork(c, g.chain));
         CUDA_TRY(cudaGraphLaunch(g.exec, c->stream));
+        if (g.has_chain) F2_TRY(chain_join(c));
+        return int(F2GPU_OK);
+    };
+    if (g.exec) {
+        F2_TRY(launch());
         c->launches += g.nodes;
         return F2GPU_OK;
     }
     if (g.seen < 1) {
         g.seen += 1;
-        return enqueue();
+        return enqueue(nullptr);
     }
     cudaGraph_t graph = nullptr;
     const uint64_t l0 = c->launches;
+    ChainDefer cd;
     CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    int rc = enqueue();
+    int rc = enqueue(&cd);
     cudaError_t ec = cudaStreamEndCapture(c->stream, &graph);
     if (rc != F2GPU_OK) { if (graph) cudaGraphDestroy(graph); return rc; }
     if (ec != cudaSuccess) return set_err(F2GPU_ECUDA, std::string("leaf graph capture: ") + cudaGetErrorString(ec));
@@ -1108,8 +1201,9 @@ int leaf_graph_run(f2gpu_ctx* c, const std::array<uintptr_t, 8>& key, F&& enqueu
         return set_err(F2GPU_ECUDA, std::string("leaf graph instantiate: ") + cudaGetErrorString(ei));
     }
     g.nodes = c->launches - l0;
-    CUDA_TRY(cudaGraphLaunch(g.exec, c->stream));
-    return F2GPU_OK;
+    g.has_chain = cd.has;
+    g.chain = cd.args;
+    return launch();
 }
 
 // a leaf: the block algorithm (with lookahead) on panels [c0, c1), replayed from
@@ -1121,7 +1215,9 @@ int rec_leaf(RecRun& r, size_t c0, size_t c1) {
     const size_t sw = std::min(r.frontier, r.mu);
     const std::array<uintptr_t, 8> key{uintptr_t(s.w.p), s.w.stride, r.n, r.mu, c0, c1,
                                        uintptr_t(s.st) ^ (r.la ? 1u : 0u), sw};
-    return leaf_graph_run(c, key, [&] { return enqueue_panels(c, s, r.n, r.mu, c0, c1, r.la, sw); });
+    return leaf_graph_run(c, key, [&](ChainDefer* cd) {
+        return enqueue_panels(c, s, r.n, r.mu, c0, c1, r.la, sw, 0, cd);
+    });
 }
 
 template <typename F>
@@ -1618,7 +1714,9 @@ struct DistGpu {
         const bool la = lookahead_ok(c, lf, d.n);
         const std::array<uintptr_t, 8> key{uintptr_t(lv.p), gs, d.n, d.mu, c0, c1,
                                            uintptr_t(lf.st) ^ (la ? 1u : 0u), cols | (size_t(1) << 40)};
-        F2_TRY(leaf_graph_run(c, key, [&] { return enqueue_panels(c, lf, d.n, d.mu, c0, c1, la, cols, c0); }));
+        F2_TRY(leaf_graph_run(c, key, [&](ChainDefer* cd) {
+            return enqueue_panels(c, lf, d.n, d.mu, c0, c1, la, cols, c0, cd);
+        }));
         for (size_t i = 0; i < d.sh->size(); ++i) {
             Shard& s = (*d.sh)[i];
             const int gg = d.base + int(i);
@@ -1888,6 +1986,8 @@ int f2gpu_ctx_create(int device, f2gpu_ctx** out) {
         c->post_spin = o.post_spin != 0;
         c->pdl = o.pdl != 0;
         c->panel_hand = o.panel_hand != 0;
+        c->panel_chain = o.panel_chain != 0;
+        c->chain_sms = int(o.chain_sms);
         c->use_tc = o.tc != 0;
         if (o.tc_cut_set) {
             c->tc_cutover = size_t(o.tc_cut);

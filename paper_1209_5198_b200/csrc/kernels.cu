@@ -2104,6 +2104,18 @@ struct PanelGjSmem {
     uint64_t bt[256];
     uint32_t want;  // warp 0's slow path needs entries < want - 1 applied to win/orig
     uint32_t done;  // = want once they are (published by warp 2 on request)
+    uint32_t r_fin; // chain kernel: this panel's r, for the helper warps
+    // chain kernel: the window stays as loaded and slot[p] = where position p's row sits
+    // in it (swapped like orig), so the replay moves indices only; win_ready = j + 1
+    // once the window of panel j is in shared memory
+    uint32_t win_ready;
+    uint32_t slot[kPanelWin];
+};
+// Chain kernel (k_panel_chain): the next panel's first kGjPos rows, already updated by
+// this panel (x ^= (D*Z)*B), and its first row R + r -- the in-CTA hand-off
+struct ChainHand {
+    uint64_t rows0[kGjPos];
+    uint32_t R;
 };
 static_assert(kGjWords == 3, "log entries carry three position words");
 
@@ -2168,17 +2180,58 @@ __device__ __forceinline__ void wait_count_ge_warp(const uint32_t* flag, uint32_
     }
 }
 
-__global__ void __launch_bounds__(kPanelThreads, 1)
-    k_panel_gj(uint64_t* __restrict__ col, size_t n, PanelState* __restrict__ st_all, int j,
-               const PanelLink link) {
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    PanelGjSmem& S = *reinterpret_cast<PanelGjSmem*>(smem_raw);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// Named barriers of the panel body: ids 2..7 (+ boff in the chain kernel, whose two
+// teams of kPanelThreads threads each run one body at a time).
+#define GJ_BAR_SYNC(id, cnt) asm volatile("bar.sync %0, %1;" ::"r"((id) + boff), "n"(cnt) : "memory")
+#define GJ_BAR_ARRIVE(id, cnt) asm volatile("bar.arrive %0, %1;" ::"r"((id) + boff), "n"(cnt) : "memory")
+// the barriers both variants use: literal ids in k_panel_gj (its code stays as it was)
+#define GJ_SYNC(id, cnt)                                                     \
+    do {                                                                     \
+        if constexpr (CHAIN) GJ_BAR_SYNC(id, cnt);                           \
+        else asm volatile("bar.sync " #id ", " #cnt ";" ::: "memory");       \
+    } while (0)
+#define GJ_ARRIVE(id, cnt)                                                   \
+    do {                                                                     \
+        if constexpr (CHAIN) GJ_BAR_ARRIVE(id, cnt);                         \
+        else asm volatile("bar.arrive " #id ", " #cnt ";" ::: "memory");     \
+    } while (0)
+constexpr int kChainHelpers = kPanelThreads - 96;  // warps 3..7
+static_assert(kChainHelpers == 64 + int(kGjPos), "one helper thread per gathered row");
+
+// One panel.  CHAIN = false: the whole k_panel_gj kernel (tid = threadIdx.x).  CHAIN =
+// true: one iteration of a team of k_panel_chain -- the panel starts on the hand-off
+// of the team that ran panel j-1 (hin, named barrier hb_in) instead of on counters of
+// k_post_col, and its warps 3..7 prepare the same hand-off for panel j+1 (hout, hb_out).
+template <bool CHAIN>
+__device__ __forceinline__ void panel_gj_body(uint64_t* __restrict__ col, size_t n, PanelState* __restrict__ st_all,
+                                              int j, const PanelLink& link, PanelGjSmem& S, const int tid,
+                                              const int boff, const ChainHand* hin, ChainHand* hout,
+                                              const int hb_in, const int hb_out) {
+    const int lane = tid & 31, warp = tid >> 5;
+    // F2GPU_SPIN_DIAG=1: the chain kernel's progress, words 4 (team 0) and 5 (team 1) of
+    // the host-mapped record: panel << 8 | stage
+    auto mark = [&](int stage) {
+        if constexpr (CHAIN) {
+            if (unsigned long long* d = g_spin_diag)
+                *reinterpret_cast<volatile unsigned long long*>(d + 4 + (boff ? 1 : 0)) =
+                    (uint64_t(j) << 8) | uint64_t(stage);
+        }
+    };
+    if (tid == 0) mark(1);
     // every warp waits for the previous panel's head chunk (or the fused post's
     // head) before reading its state: the kernel may be queued on another stream
     // and resident while the previous panel kernel still runs
-    wait_count_ge_warp(link.head, link.head_count, 10);
-    const size_t R = j == 0 ? 0 : size_t(st_all[j - 1].R) + st_all[j - 1].r;
+    if constexpr (CHAIN) {
+        // ... or, in the chain kernel, for the other team's hand-off (also the
+        // iteration barrier of this team: every warp is done with the panel before)
+        if (hin) asm volatile("bar.sync %0, %1;" ::"r"(hb_in), "n"(kPanelThreads + kChainHelpers) : "memory");
+        else wait_count_ge_warp(link.head, link.head_count, 10);  // the chain's first panel
+    } else {
+        wait_count_ge_warp(link.head, link.head_count, 10);
+    }
+    if (tid == 0) mark(2);
+    const size_t R = (CHAIN && hin) ? size_t(hin->R)
+                                    : (j == 0 ? 0 : size_t(st_all[j - 1].R) + st_all[j - 1].r);
     PanelState* st = st_all + j;
     const size_t rows = R < n ? n - R : 0;
     if (rows == 0) {
@@ -2186,14 +2239,23 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
         if (tid < 64) st->Z[tid] = 0;
         if (link.head_out || link.done_out) {  // counters other kernels wait on
             __threadfence();
-            __syncthreads();
+            if constexpr (CHAIN) GJ_BAR_SYNC(2, kPanelThreads);
+            else __syncthreads();
             if (tid == 0 && link.head_out) atomicAdd(link.head_out, 1u);
             if (tid == 0 && link.done_out) atomicAdd(link.done_out, 1u);
+        }
+        if constexpr (CHAIN) {
+            if (hout) {  // no rows left for the next panel either
+                if (tid == 96) hout->R = uint32_t(R < n ? R : n);
+                __threadfence_block();
+                if (tid >= 96)
+                    asm volatile("bar.arrive %0, %1;" ::"r"(hb_out), "n"(kPanelThreads + kChainHelpers) : "memory");
+            }
         }
         return;
     }
     uint64_t* A = col + R;
-    if (link.hand_in && warp < 3) {
+    if (!CHAIN && link.hand_in && warp < 3) {
         // the previous panel's update of this panel's first kGjPos rows, from its
         // hand-off block: Y = D*Z, rows ^= Y*B (4-bit tables), warps 0-2
         const int t3 = tid;
@@ -2232,27 +2294,113 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
 #ifdef GJ_PROFILE
     const long long t_start = clock64();
 #endif
+    // Chain kernel, warps 3..7 after the window load: the hand-off for panel j+1.  Once
+    // the chain has ended (r, Z, win/orig final: barrier 4) one thread per row gathers
+    // column j+1's pivot rows and its next kGjPos rows through orig (= after this
+    // panel's swaps, which warp 2 applies to the column only after barrier 6), and the
+    // rows get this panel's update (Y = D*Z, x ^= Y*B by 4-bit tables) in shared
+    // memory: the next panel's selection starts ~2 us after this one's ends, without
+    // the round trip through the done counter and k_post_col's first rows.
+    auto chain_helper = [&]() {
+        const int h = tid - 96;  // 0..159
+        GJ_BAR_SYNC(4, kPanelThreads);
+        if (!hout) return;
+        // device trace (diagnostics): code 0, panel | stage << 8 (leaves of <= 256 panels)
+        auto stamp = [&](int stage) {
+            if (link.trace && h == 0) trace_ev(0, (j & 255) | (stage << 8));
+        };
+        stamp(1);
+        if (h == 0) mark(4);
+        const uint32_t r = S.r_fin;
+        // column j+1 is final for the earlier panels once update j-1 released it
+        if (warp == 3) wait_count_ge_warp(link.next_ready, link.next_count, 15);
+        GJ_BAR_SYNC(5, kChainHelpers);
+        stamp(2);
+        const uint64_t* nx0 = link.next + R;
+        uint64_t x = 0;
+        if (h < 64) {
+            S.bs[h] = uint32_t(h) < r ? __ldcg(nx0 + S.orig[h]) : 0ull;
+        } else {
+            const size_t pos = size_t(r) + (h - 64);
+            if (pos < rows) x = __ldcg(nx0 + S.orig[pos]);
+            S.rows0[h - 64] = x;  // keeps the load ahead of the arrival below
+        }
+        __threadfence_block();
+        GJ_BAR_ARRIVE(6, kChainHelpers + 32);  // warp 2 may now swap column j+1
+        GJ_BAR_SYNC(5, kChainHelpers);
+        stamp(3);
+        for (int e = h; e < 256; e += kChainHelpers) {
+            const int g = e >> 4, v = e & 15;
+            uint64_t za = 0, zb = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if ((v >> q) & 1) { za ^= S.z[4 * g + q]; zb ^= S.bs[4 * g + q]; }
+            S.zt[e] = za;
+            S.bt[e] = zb;
+        }
+        GJ_BAR_SYNC(5, kChainHelpers);
+        if (h >= 64) {
+            const size_t pos = size_t(r) + (h - 64);
+            if (pos < rows) {
+                const uint64_t d = S.win[S.slot[pos]];
+                uint64_t y = 0;
+#pragma unroll
+                for (int g = 0; g < 16; ++g) y ^= S.zt[16 * g + int((d >> (4 * g)) & 15)];
+#pragma unroll
+                for (int g = 0; g < 16; ++g) x ^= S.bt[16 * g + int((y >> (4 * g)) & 15)];
+            }
+            hout->rows0[h - 64] = x;
+        } else if (h == 0) {
+            hout->R = uint32_t(R + r);
+        }
+        __threadfence_block();
+        stamp(4);
+        if (h == 0) mark(5);
+        asm volatile("bar.arrive %0, %1;" ::"r"(hb_out), "n"(kPanelThreads + kChainHelpers) : "memory");
+    };
     if (warp == 0) {
         // warp 0 starts on its own rows (loaded below) without waiting for the
         // window; it zeroes the log, then releases the two consumer warps
         for (int t = lane; t < 66; t += 32) S.log[t] = make_uint4(0, 0, 0, 0);
         if (lane == 0) { S.done = 0; S.want = 0; S.fin = 0; }
-        asm volatile("bar.arrive 3, 96;" ::: "memory");
+        GJ_ARRIVE(3, 96);
         if (link.trace && lane == 0) trace_ev(kTrPanelBegin, j);
         __syncwarp();
     } else if (warp == 1) {
-        asm volatile("bar.sync 3, 96;" ::: "memory");  // the log is zeroed
+        GJ_SYNC(3, 96);  // the log is zeroed
+    } else if constexpr (CHAIN) {
+        // The chain's panels start before their window is in memory (it comes with
+        // k_post_col(j-1), ~3 us into the selection), and a replay that starts late
+        // trails the selection to its end.  So the replay (warp 2) moves indices only and
+        // starts with the selection: orig[p] = the original row at position p, slot[p] =
+        // where its value sits in the window, which warps 3..7 load whenever it arrives
+        // and nobody permutes.
+        for (uint32_t x = tid - 64; x < winrows; x += kPanelThreads - 64) S.orig[x] = S.slot[x] = x;
+        GJ_BAR_SYNC(2, 192);
+        if (warp > 2) {
+            if (warp == 3) wait_count_ge_warp(link.win, link.win_count, 11);
+            GJ_BAR_SYNC(5, kChainHelpers);
+            // one kernel over many panels: not through L1
+            for (uint32_t x = tid - 96; x < winrows; x += kChainHelpers) S.win[x] = __ldcg(A + x);
+            __threadfence_block();
+            GJ_BAR_SYNC(5, kChainHelpers);
+            if (tid == 96) st_volatile(&S.win_ready, uint32_t(j) + 1);  // warp 0's slow path
+            GJ_BAR_ARRIVE(7, kChainHelpers + 32);                       // warp 2's write-back
+            chain_helper();
+            return;
+        }
+        GJ_BAR_SYNC(3, 96);
     } else {
         // warps 2..7 load the window; warp 2 then replays the swaps on it
         if (warp == 2) wait_count_ge_warp(link.win, link.win_count, 11);
-        asm volatile("bar.sync 2, 192;" ::: "memory");
+        GJ_SYNC(2, 192);
         for (uint32_t x = tid - 64; x < winrows; x += kPanelThreads - 64) {
             S.win[x] = A[x];
             S.orig[x] = x;
         }
-        asm volatile("bar.sync 2, 192;" ::: "memory");
+        GJ_SYNC(2, 192);
         if (warp > 2) return;
-        asm volatile("bar.sync 3, 96;" ::: "memory");
+        GJ_SYNC(3, 96);
     }
 #ifdef GJ_PROFILE
     const long long t_loaded = clock64();
@@ -2314,6 +2462,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
         }
         __threadfence();
         atomicAdd(link.done_out, 1u);
+        mark(6);
         if (link.trace) trace_ev(13, j);
     };
 
@@ -2356,15 +2505,32 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
             tm[2] = (tm[2] << 1) | (tm[1] >> 31);
             tm[1] = (tm[1] << 1) | (tm[0] >> 31);
             tm[0] = tm[0] << 1;
+            if (CHAIN && !(e.w & kLogSlow) && lane == 1 && f != t) {
+                const uint32_t st2 = S.slot[t], sf = S.slot[f];
+                S.slot[t] = sf;
+                S.slot[f] = st2;
+            }
             if (!(e.w & kLogSlow) && lane == 0) {
                 if (f != t) {
-                    const uint64_t vt = S.win[t], vf = S.win[f];
-                    const uint32_t ot = S.orig[t], of = S.orig[f];
-                    S.win[t] = vf; S.orig[t] = of;
-                    S.win[f] = vt; S.orig[f] = ot;
+                    if constexpr (CHAIN) {  // indices only (lane 1 below: slot)
+                        const uint32_t ot = S.orig[t], of = S.orig[f];
+                        S.orig[t] = of;
+                        S.orig[f] = ot;
+                    } else {
+                        const uint64_t vt = S.win[t], vf = S.win[f];
+                        const uint32_t ot = S.orig[t], of = S.orig[f];
+                        S.win[t] = vf; S.orig[t] = of;
+                        S.win[f] = vt; S.orig[f] = ot;
+                    }
                 }
             }
             __syncwarp();
+        }
+        if constexpr (CHAIN) {  // orig / slot are final: the helper warps may gather through them
+            if (link.trace && lane == 0) trace_ev(0, (j & 255) | (6 << 8));
+            __threadfence_block();
+            GJ_BAR_ARRIVE(4, kPanelThreads);
+            GJ_BAR_SYNC(7, kChainHelpers + 32);  // the window is loaded (the write-back below)
         }
         // ---- composite permutation: window slots with orig != slot, then ext rows ----
         // every position < r may hold a moved row (pivots brought in from beyond
@@ -2377,7 +2543,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
             const uint32_t bal = __ballot_sync(0xffffffffu, moved);
             if (moved) {
                 const uint32_t e = np + __popc(bal & ((1u << lane) - 1));
-                A[x] = S.win[x];
+                A[x] = CHAIN ? S.win[S.slot[x]] : S.win[x];
                 st->dst[e] = S.pd[e] = x;
                 st->src[e] = S.ps[e] = S.orig[x];
             }
@@ -2412,11 +2578,17 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-                if (lane + 32 * q < np) v[q] = nx[sv[q]];
+                if (lane + 32 * q < np) v[q] = CHAIN ? __ldcg(nx + sv[q]) : nx[sv[q]];
             __syncwarp();
+            // the helper warps gather the unswapped column: wait for their loads
+            if constexpr (CHAIN) GJ_BAR_SYNC(6, kChainHelpers + 32);
 #pragma unroll
             for (int q = 0; q < 4; ++q)
                 if (lane + 32 * q < np) nx[d[q]] = v[q];
+        } else {
+            if constexpr (CHAIN) {
+                if (hout) GJ_BAR_SYNC(6, kChainHelpers + 32);
+            }
         }
         if (link.trace && lane == 0) trace_ev(kTrPanelEnd, j);
 #ifdef GJ_PROFILE
@@ -2529,6 +2701,11 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
             const uint32_t kz = (S.log[lane + 32].w >> 8) & 63u;
             st->Z[kz] = S.z[kz] = (1ull << (lane + 32)) ^ x1;
         }
+        if constexpr (CHAIN) {
+            if (link.trace && lane == 0) trace_ev(0, (j & 255) | (5 << 8));
+            __threadfence_block();
+            GJ_BAR_ARRIVE(4, kPanelThreads);
+        }
 #ifdef GJ_PROFILE
         if (lane == 0) reinterpret_cast<long long*>(st->src)[57] = clock64() - t_start;
 #endif
@@ -2540,7 +2717,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
     // ---- warp 0: the selection chain ----
     uint32_t c0[kGjWords], c1[kGjWords], live[kGjWords];
     {
-        const uint64_t* src0 = link.hand_in ? S.rows0 : A;
+        const uint64_t* src0 = CHAIN ? (hin ? hin->rows0 : A) : (link.hand_in ? S.rows0 : A);
         uint64_t x0 = uint32_t(lane) < npos ? src0[lane] : 0;
         uint64_t x1 = uint32_t(lane) + 32 < npos ? src0[lane + 32] : 0;
         uint64_t z0 = uint32_t(lane) + 64 < npos ? src0[lane + 64] : 0;
@@ -2605,7 +2782,8 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
 #endif
             if (lane == 0) st_volatile(&S.want, ib + 1);
             wait_count_ge_warp(link.all, link.all_count, 14);  // rows beyond the window
-            while (!__all_sync(0xffffffffu, ld_volatile(&S.done) == ib + 1)) {}
+            while (!__all_sync(0xffffffffu, ld_volatile(&S.done) == ib + 1 &&
+                                                (!CHAIN || ld_volatile(&S.win_ready) == uint32_t(j) + 1))) {}
             __syncwarp();
             __threadfence_block();
             // ck holds only dead positions (no live one has bit k): the RREF rows
@@ -2623,7 +2801,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
                 for (int t = 0; t < 8; ++t) {
                     const size_t ii = base + 32 * t + lane;
                     uint64_t vv = 0;
-                    if (ii < winrows) vv = S.win[ii];
+                    if (ii < winrows) vv = CHAIN ? S.win[S.slot[ii]] : S.win[ii];
                     else if (ii < rows) vv = A[ii];
                     orr |= vv;
                     hits[t] = __ballot_sync(0xffffffffu, ii < rows && (__popcll(c & vv) & 1));
@@ -2640,7 +2818,7 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
                 if (warp_or64(orr) == 0 && !__any_sync(0xffffffffu, anyl != 0)) stop = true;
                 return;
             }
-            const uint64_t x = found < winrows ? S.win[found] : A[found];
+            const uint64_t x = found < winrows ? (CHAIN ? S.win[S.slot[found]] : S.win[found]) : A[found];
             // reduction set: dead positions u with x[k_u] = 1
             const bool u0 = uint32_t(lane) < ib && ((x >> ((S.log[lane].w >> 8) & 63u)) & 1);
             const bool u1 = uint32_t(lane) + 32 < ib && ((x >> ((S.log[lane + 32].w >> 8) & 63u)) & 1);
@@ -2657,16 +2835,22 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
             if (!hi) upd(c0, lane);
             upd(c1, lane + 32);
             if (lane == 0) {
-                const uint64_t vb = S.win[ib];
+                const uint32_t sb = CHAIN ? S.slot[ib] : ib;  // where position ib's value sits
+                const uint64_t vb = S.win[sb];
                 const uint32_t ob = S.orig[ib];
                 if (found < winrows) {
-                    S.win[ib] = x;
+                    if constexpr (CHAIN) {
+                        S.slot[ib] = S.slot[found];
+                        S.slot[found] = sb;
+                    } else {
+                        S.win[ib] = x;
+                        S.win[found] = vb;
+                    }
                     S.orig[ib] = S.orig[found];
-                    S.win[found] = vb;
                     S.orig[found] = ob;
                 } else {
                     A[found] = vb;
-                    S.win[ib] = x;
+                    S.win[sb] = x;
                     uint32_t e = 0;
                     while (e < n_ext && S.ext_pos[e] != found) ++e;
                     if (e == n_ext) { S.ext_pos[e] = found; S.ext_orig[e] = found; }
@@ -2699,12 +2883,18 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
 
     __threadfence_block();
     if (lane == 0) st_log(&S.log[ib], n_ext, 0, 0, kLogValid | kLogEnd | ib);
+    if (lane == 0) mark(3);
     if (link.trace && lane == 0) trace_ev(kTrPanelChainEnd, j);
 #ifdef GJ_PROFILE
     const long long t_chain = clock64();
 #endif
     if (!((sel >> lane) & 1)) st->Z[lane] = S.z[lane] = 0;
     if (!((sel >> (lane + 32)) & 1)) st->Z[lane + 32] = S.z[lane + 32] = 0;
+    if constexpr (CHAIN) {
+        if (lane == 0) S.r_fin = ib;
+        __threadfence_block();
+        GJ_BAR_ARRIVE(4, kPanelThreads);
+    }
     if (lane == 0) {
         st->R = uint32_t(R);
         st->r = ib;
@@ -2721,6 +2911,68 @@ __global__ void __launch_bounds__(kPanelThreads, 1)
 #endif
     if (link.head_out) head_chunk(ib);
     finish();
+}
+#undef GJ_SYNC
+#undef GJ_ARRIVE
+#undef GJ_BAR_SYNC
+#undef GJ_BAR_ARRIVE
+
+__global__ void __launch_bounds__(kPanelThreads, 1)
+    k_panel_gj(uint64_t* __restrict__ col, size_t n, PanelState* __restrict__ st_all, int j,
+               const PanelLink link) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    PanelGjSmem& S = *reinterpret_cast<PanelGjSmem*>(smem_raw);
+    panel_gj_body<false>(col, n, st_all, j, link, S, threadIdx.x, 0, nullptr, nullptr, 0, 0);
+}
+
+// ---------------------------------------------------------------------------
+// K4'': the panel chain of a whole leaf in ONE persistent CTA
+// ---------------------------------------------------------------------------
+// Panels [c0, c1) of a leaf, one launch (c0 = the leaf's second panel: the first one is
+// a k_panel_gj launch in stream order, during which this CTA becomes resident -- a
+// chain queued beside the first k_post_col could find every SM holding one of its
+// spinning blocks).  Two teams of kPanelThreads threads take the
+// panels alternately (team = (j - c0) & 1), each running the k_panel_gj body on its
+// own shared-memory block, so panel j's tail (pair list, next-column swaps, state,
+// done counter) overlaps panel j+1's selection exactly as two resident k_panel_gj
+// kernels did -- but the hand-off between them stays inside the CTA: the helper warps
+// of panel j gather and update the next column's first rows in shared memory and
+// release the other team through a named barrier (panel_gj_body, CHAIN = true).
+// Every other wait (k_post_col's window / all-rows counters, the update's
+// first-column release) and every output (PanelState, pair list, swaps on column j+1,
+// done counter for k_post_col(j)) is the same as with per-panel launches, so the
+// fused post and the updates on the main stream are unchanged.
+struct ChainSmem {
+    PanelGjSmem S[2];
+    ChainHand H[2];
+};
+
+__global__ void __launch_bounds__(2 * kPanelThreads, 1) k_panel_chain(const ChainArgs a) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    ChainSmem& M = *reinterpret_cast<ChainSmem*>(smem_raw);
+    const int team = threadIdx.x / kPanelThreads, tid = threadIdx.x % kPanelThreads;
+    if (threadIdx.x < 2) M.S[threadIdx.x].win_ready = 0;  // epochs j + 1 > 0
+    if (threadIdx.x == 0 && g_spin_diag)
+        *reinterpret_cast<volatile unsigned long long*>(g_spin_diag + 6) = (uint64_t(a.c0) << 32) | uint32_t(a.c1);
+    __syncthreads();
+    // named barriers: team-local ids 2..7 (+ 6 * team), hand-off barriers 14 + team
+    for (int j = a.c0 + team; j < a.c1; j += 2) {
+        PanelLink l{};
+        if (j > a.leaf0) {
+            const uint32_t* f = a.flags + size_t(j - 1) * a.flags_per_panel;
+            if (j == a.c0) { l.head = f; l.head_count = 1; }  // k_post_col(j-1)'s first rows
+            l.win = f + 1; l.win_count = 8;
+            l.all = f + 2; l.all_count = a.yblocks;
+            if (j + 1 < a.c1) { l.next_ready = f + 3; l.next_count = a.upd_grid; }
+        }
+        if (j + 1 < a.c1) l.next = a.w + size_t(j + 1 - a.coff) * a.stride;
+        l.poll_ns = a.poll_ns;
+        l.trace = a.trace;
+        l.done_out = a.flags + size_t(j) * a.flags_per_panel + 4;
+        panel_gj_body<true>(a.w + size_t(j - a.coff) * a.stride, a.n, a.st, j, l, M.S[team], tid, 6 * team,
+                            j > a.c0 ? &M.H[team] : nullptr, j + 1 < a.c1 ? &M.H[team ^ 1] : nullptr,
+                            14 + team, 14 + (team ^ 1));
+    }
 }
 
 static bool g_panel_gj = true;  // F2GPU_PANEL=0: the transposed-M k_panel
@@ -2752,6 +3004,13 @@ cudaError_t launch_panel_link(uint64_t* col, size_t n, PanelState* st_all, int j
 }
 
 bool panel_link_ok() { return g_panel_gj; }
+
+cudaError_t launch_panel_chain(const ChainArgs& a, cudaStream_t s) {
+    if (!g_panel_gj) return cudaErrorNotSupported;
+    if (a.c1 <= a.c0) return cudaSuccess;
+    k_panel_chain<<<1, 2 * kPanelThreads, kPanelGjSmemMax, s>>>(a);
+    return cudaGetLastError();
+}
 
 // ---------------------------------------------------------------------------
 // Y = D*Z over D (rows R+r .. n of the panel column), written in place
@@ -3459,6 +3718,18 @@ cudaError_t init_kernel_attrs() {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_panel_gj, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(kPanelGjSmemMax));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_panel_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(kPanelGjSmemMax));
+    static_assert(sizeof(ChainSmem) <= kPanelGjSmemMax, "chain smem");
+    // CUDA loads kernels lazily, and a first launch that has to load can wait for the
+    // device to go idle.  k_panel_chain spins on counters of kernels launched after it,
+    // so every kernel of the fused schedule is loaded here, before any launch (the ones
+    // above by their attribute calls, the fused post by this query).
+    if (e == cudaSuccess) {
+        cudaFuncAttributes fa;
+        e = cudaFuncGetAttributes(&fa, k_post_col);
+    }
     kPanelGjSmemBytes = options().panel_smem ? kPanelGjSmemMax : sizeof(PanelGjSmem);
     g_panel_gj = options().panel != 0;
     return e;

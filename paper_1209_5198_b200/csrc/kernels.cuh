@@ -161,6 +161,24 @@ constexpr int kPanelHeadRows = 256;
 cudaError_t launch_panel_link(uint64_t* col, size_t n, PanelState* st_all, int j, const PanelLink& link,
                               cudaStream_t s);
 bool panel_link_ok();  // false when F2GPU_PANEL=0 selects the older panel kernel
+// The panel chain of a whole leaf [c0, c1) in one persistent CTA (k_panel_chain): the
+// same inputs, waits and outputs as launch_panel_link per panel under the fused
+// schedule with counter-driven posts (done counter = flags[j * flags_per_panel + 4]),
+// but panel j+1 starts on an in-CTA hand-off from panel j.
+struct ChainArgs {
+    uint64_t* w;        // the matrix the leaf runs on; its word-column 0 is global column coff
+    size_t stride, n;
+    PanelState* st;     // global panel index
+    uint32_t* flags;    // kFlagsPerPanel counters per panel (global panel index)
+    int flags_per_panel;
+    int leaf0;          // the leaf's first panel (panels > leaf0 wait on the previous post / update)
+    int c0, c1, coff;   // the chain's panels [c0, c1), c0 >= leaf0
+    uint32_t yblocks;   // post_col_yblocks(n)
+    uint32_t upd_grid;  // CTAs of the update (first-column release count)
+    uint32_t poll_ns;
+    bool trace;
+};
+cudaError_t launch_panel_chain(const ChainArgs& a, cudaStream_t s);
 // POST + the next column's update in one launch: swaps on every word-column
 // except panel_col and next_col, Y = D*Z on the panel column, and (next_col >=
 // 0) next[i] ^= Y_i * B for i >= R + r.  flags[0] += 1 by row block 0 after

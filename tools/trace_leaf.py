@@ -47,7 +47,12 @@ names = {0: "P.w1end", 1: "P.begin", 2: "P.chain_end", 3: "P.end", 4: "post.begi
          7: "U.begin", 8: "U.release", 9: "U.end", 10: "U0.tab0", 11: "U0.tile0", 12: "U0.end", 13: "P.done", 14: "U0.state", 15: "U0.barriers"}
 mu = w // 64
 T = {k: np.full(mu, np.nan) for k in names}
-post_blk = [((ti - t0) / 1000.0, ji) for ti, ci, ji in zip(t, code, j) if ci == 0]  # lean post block starts
+post_blk = []
+# chain kernel (F2GPU_PANEL_CHAIN=1): helper stamps, code 0, panel | stage << 8
+H = {st: np.full(mu, np.nan) for st in (1, 2, 3, 4, 5, 6, 7)}
+for ti, ci, ji in zip(t, code, j):
+    if ci == 0 and (ji >> 8) in H and (ji & 255) < mu and mu <= 256:
+        H[ji >> 8][ji & 255] = (ti - t0) / 1000.0
 for ti, ci, ji in zip(t, code, j):
     if ci == 0:
         continue
@@ -83,6 +88,16 @@ rows = [
     ("  U0 end -> next post begin", nx(T[4]) - T[12]),
     ("next P chain end -> U release", nx(T[2]) - T[8]),
     ("cycle (P begin -> next P begin)", nx(T[1]) - T[1]),
+]
+rows += [
+    ("chain: chain end -> warp 1 end", H[5] - T[2]),
+    ("chain: chain end -> warp 2 replay end", H[6] - T[2]),
+    ("chain: chain end -> helpers start", H[1] - T[2]),
+    ("chain: helpers start -> col ready", H[2] - H[1]),
+    ("chain:   U(j-1) release -> col ready", H[2] - np.append([np.nan], T[8][:-1])),
+    ("chain: col ready -> gathered", H[3] - H[2]),
+    ("chain: gathered -> hand-off", H[4] - H[3]),
+    ("chain: hand-off -> next P begin", nx(T[1]) - H[4]),
 ]
 for name, v in rows:
     print(f"{name:34s} {med(v)}")
