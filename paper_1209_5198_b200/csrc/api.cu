@@ -757,7 +757,8 @@ int read_results(f2gpu_ctx* c, const Shard& s, size_t n, size_t mu, uint32_t* pe
 }
 
 // per panel j: [0] head, [1] window, [2] all row blocks of k_post_col(j);
-// [3] the release of update j's first column (group); [4] panel kernel j done
+// [3] the release of update j's first column (group); [4] panel kernel j done;
+// [5] (a leaf's first panel) k_panel_chain is resident
 // (plain lookahead: [0] only)
 constexpr size_t kFlagsPerPanel = 8;
 
@@ -917,8 +918,9 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
                     F2_TRY(chain_fork(c, a));
                 }
             }
-            F2_TRY(check_launch(c, f2::launch_panel_link(colp(c0), n, s.st, int(c0), link_for(c0), c->stream),
-                                "k_panel"));
+            f2::PanelLink l0 = link_for(c0);
+            if (has_chain) l0.chain_up = c->scr_flags + c0 * kFlagsPerPanel + 5;
+            F2_TRY(check_launch(c, f2::launch_panel_link(colp(c0), n, s.st, int(c0), l0, c->stream), "k_panel"));
             for (size_t j = c0; j < c1; ++j) {
                 uint32_t* f = c->scr_flags + j * kFlagsPerPanel;
                 F2_TRY(check_launch(c, f2::launch_post_col(s.w.p, s.w.stride, int(swap_cols), int(j - coff),

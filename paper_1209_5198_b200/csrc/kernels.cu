@@ -2399,7 +2399,10 @@ __device__ __forceinline__ void panel_gj_body(uint64_t* __restrict__ col, size_t
             S.orig[x] = x;
         }
         GJ_SYNC(2, 192);
-        if (warp > 2) return;
+        if (warp > 2) {
+            if (warp == 7) wait_count_ge_warp(link.chain_up, 1, 16);
+            return;
+        }
         GJ_SYNC(3, 96);
     }
 #ifdef GJ_PROFILE
@@ -2954,6 +2957,8 @@ __global__ void __launch_bounds__(2 * kPanelThreads, 1) k_panel_chain(const Chai
     if (threadIdx.x < 2) M.S[threadIdx.x].win_ready = 0;  // epochs j + 1 > 0
     if (threadIdx.x == 0 && g_spin_diag)
         *reinterpret_cast<volatile unsigned long long*>(g_spin_diag + 6) = (uint64_t(a.c0) << 32) | uint32_t(a.c1);
+    // resident: the leaf's first panel kernel (PanelLink::chain_up) may exit
+    if (threadIdx.x == 0) atomicAdd(a.flags + size_t(a.leaf0) * a.flags_per_panel + 5, 1u);
     __syncthreads();
     // named barriers: team-local ids 2..7 (+ 6 * team), hand-off barriers 14 + team
     for (int j = a.c0 + team; j < a.c1; j += 2) {

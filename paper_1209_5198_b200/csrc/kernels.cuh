@@ -155,6 +155,10 @@ struct PanelLink {
     uint64_t* hand_out = nullptr;
     const uint64_t* hand_in = nullptr;
     const PanelState* prev = nullptr;  // the previous panel's state (Z, r) for hand_in
+    // the leaf's first panel kernel under the chain schedule: it does not exit before
+    // *chain_up != 0, i.e. before k_panel_chain is resident.  The posts that follow in
+    // stream order spin with blocks on every SM, and the chain CTA needs a whole one.
+    const uint32_t* chain_up = nullptr;
 };
 constexpr int kHandWords = 256;
 constexpr int kPanelHeadRows = 256;

@@ -25,7 +25,7 @@
     X(pdl, "F2GPU_PDL", 1, "the update is a programmatic dependent launch of k_post_col")                    \
     X(post_pdl, "F2GPU_POST_PDL", 0, "k_post_col as a programmatic dependent of the previous update (can starve P)") \
     X(panel_hand, "F2GPU_PANEL_HAND", 0, "P(j+1) starts on P(j)'s done counter with a hand-off block")         \
-    X(panel_chain, "F2GPU_PANEL_CHAIN", 0, "one persistent k_panel_chain CTA per leaf: panel j+1 starts on an in-CTA hand-off") \
+    X(panel_chain, "F2GPU_PANEL_CHAIN", 1, "one persistent k_panel_chain CTA per leaf: panel j+1 starts on an in-CTA hand-off") \
     X(chain_sms, "F2GPU_CHAIN_SMS", 2, "SMs the updates leave free under F2GPU_PANEL_CHAIN (the chain CTA needs one)") \
     X(tc, "F2GPU_TC", 1, "products on the fp4 tensor-core leaf (0: M4RM only)")                              \
     X(tc_cut, "F2GPU_TC_CUT", 16384, "Strassen-Winograd leaf of the tensor-core products (strassen_mult)")    \
