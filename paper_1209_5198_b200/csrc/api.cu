@@ -202,12 +202,15 @@ struct GraphCache {
     int seen = 0;                 // eager runs with this key
     cudaGraphExec_t exec = nullptr;
     uint64_t nodes = 0;
+    bool has_chain = false;       // k_panel_chain is launched outside the graph (see LeafGraph)
+    f2::ChainArgs chain{};
     void reset() {
         if (exec) cudaGraphExecDestroy(exec);
         exec = nullptr;
         seen = 0;
         nodes = 0;
         w = nullptr;
+        has_chain = false;
     }
     bool match(uint64_t* w_, size_t s_, size_t n_, size_t mu_, void* st_) const {
         return w == w_ && stride == s_ && n == n_ && mu == mu_ && st == st_;
@@ -1027,10 +1030,13 @@ int chain_join(f2gpu_ctx* c) {
 //   side: P(j+1) waits POST(j) (event) and then spins on flag j on the spare SM,
 //         so the panel factorisation of j+1 overlaps the bulk of update j.
 //   main waits P(j+1) (event) before POST(j+1).
-int enqueue_lookahead(f2gpu_ctx* c, Shard& s, size_t n, size_t mu) {
-    CUDA_TRY(cudaMemsetAsync(c->scr_flags, 0, mu * 4 * kFlagsPerPanel, c->stream));
+// cd != nullptr (captured by decompose_single): the caller zeroes the counters itself,
+// before it forks the chain kernel -- a memset inside the graph could wipe the chain's
+// "resident" counter
+int enqueue_lookahead(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, ChainDefer* cd = nullptr) {
+    if (!cd) CUDA_TRY(cudaMemsetAsync(c->scr_flags, 0, mu * 4 * kFlagsPerPanel, c->stream));
     F2_TRY(check_launch(c, f2::launch_iota(s.perm, n, c->stream), "k_iota"));
-    return enqueue_panels(c, s, n, mu, 0, mu, true);
+    return enqueue_panels(c, s, n, mu, 0, mu, true, size_t(-1), 0, cd);
 }
 
 bool lookahead_ok(f2gpu_ctx* c, const Shard& s, size_t n) {
@@ -1040,8 +1046,8 @@ bool lookahead_ok(f2gpu_ctx* c, const Shard& s, size_t n) {
     return f2::update_fast_ok(u);
 }
 
-int enqueue_single(f2gpu_ctx* c, Shard& s, size_t n, size_t mu) {
-    if (lookahead_ok(c, s, n)) return enqueue_lookahead(c, s, n, mu);
+int enqueue_single(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, ChainDefer* cd = nullptr) {
+    if (lookahead_ok(c, s, n)) return enqueue_lookahead(c, s, n, mu, cd);
     F2_TRY(check_launch(c, f2::launch_iota(s.perm, n, c->stream), "k_iota"));
     for (size_t j = 0; j < mu; ++j) F2_TRY(step_single(c, s, n, mu, j));
     return F2GPU_OK;
@@ -1383,15 +1389,24 @@ int decompose_single(f2gpu_ctx* c, View w, uint32_t* perm, uint32_t* rj, size_t*
     s.w = w; s.lw = mu; s.st = static_cast<f2::PanelState*>(c->scr_st); s.perm = c->scr_perm;
     GraphCache& g = c->graph;
     const bool graphs = c->use_graphs && c->graphs_stream_ok && !c->tl.on;
-    if (graphs && g.match(w.p, w.stride, n, mu, s.st) && g.exec) {
+    auto launch = [&]() {
+        // the counters are zeroed here, not in the graph (enqueue_lookahead)
+        CUDA_TRY(cudaMemsetAsync(c->scr_flags, 0, mu * 4 * kFlagsPerPanel, c->stream));
+        if (g.has_chain) F2_TRY(chain_fork(c, g.chain));
         CUDA_TRY(cudaGraphLaunch(g.exec, c->stream));
+        if (g.has_chain) F2_TRY(chain_join(c));
+        return int(F2GPU_OK);
+    };
+    if (graphs && g.match(w.p, w.stride, n, mu, s.st) && g.exec) {
+        F2_TRY(launch());
         c->launches += g.nodes;
     } else if (graphs && g.match(w.p, w.stride, n, mu, s.st) && g.seen >= 1) {
         // second run with this key: capture the launch sequence once, then replay
         cudaGraph_t graph = nullptr;
         const uint64_t l0 = c->launches;
+        ChainDefer cd;
         CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-        int rc = enqueue_single(c, s, n, mu);
+        int rc = enqueue_single(c, s, n, mu, &cd);
         cudaError_t ec = cudaStreamEndCapture(c->stream, &graph);
         if (rc != F2GPU_OK) { if (graph) cudaGraphDestroy(graph); return rc; }
         if (ec != cudaSuccess) return set_err(F2GPU_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ec));
@@ -1399,7 +1414,9 @@ int decompose_single(f2gpu_ctx* c, View w, uint32_t* perm, uint32_t* rj, size_t*
         cudaGraphDestroy(graph);
         if (ei != cudaSuccess) { g.exec = nullptr; return set_err(F2GPU_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei)); }
         g.nodes = c->launches - l0;
-        CUDA_TRY(cudaGraphLaunch(g.exec, c->stream));
+        g.has_chain = cd.has;
+        g.chain = cd.args;
+        F2_TRY(launch());
     } else {
         if (graphs) {
             if (!g.match(w.p, w.stride, n, mu, s.st)) {

@@ -660,6 +660,49 @@ def test_panel_hand_off():
         "print('ok')\n", F2GPU_PANEL_HAND="1")
 
 
+_CHAIN_CASES = (
+    "import numpy as np, paper_1209_5198_b200 as f2; from oracle import pyoracle as po\n"
+    "ctx=f2.Context(0)\n"
+    # dense, ragged, wide (no rows left), sparse (pivots beyond the register block and the
+    # 2048-row window: the slow path through slot/orig), rank-deficient, all-zero
+    "cases=[(300,257,0.5,1),(1000,257,0.5,2),(513,257,0.5,3),(2000,700,0.5,4),(700,2000,0.5,5),"
+    "(3000,3000,0.02,6),(6000,1024,0.003,8),(4096,4096,0.5,7),(5000,640,0.0,9)]\n"
+    "for (n,m,d,seed) in cases:\n"
+    "  a=po.random_dense(n,m,d,seed); w,perm,rj,rank=po.decompose_block(a,n,m)\n"
+    "  for fn in (f2.decompose_block, f2.decompose_recursive):\n"
+    "    for rep in range(3):\n"  # eager, capture (chain kernel outside the graph), replay
+    "      got=fn(f2.BitMatrix(n,m,a), ctx=ctx)\n"
+    "      assert got.rank==rank and np.array_equal(got.P.perm, perm), (n, m, fn, rep)\n"
+    "      assert np.array_equal(got.block_ranks, rj), (n, m, fn, rep)\n"
+    "      assert np.array_equal(got.overlay.words[:, :n], w[:, :n]), (n, m, fn, rep)\n"
+    "x=po.random_dense(3000,900,0.5,4); y=po.random_dense(900,4000,0.5,5); a=po.m4rm_mult(x,3000,900,y,4000)\n"
+    "w,perm,rj,rank=po.decompose_block(a,3000,4000)\n"
+    "for fn in (f2.decompose_block, f2.decompose_recursive):\n"
+    "  got=fn(f2.BitMatrix(3000,4000,a), ctx=ctx)\n"
+    "  assert got.rank==rank==900 and np.array_equal(got.P.perm, perm) and np.array_equal(got.block_ranks, rj)\n"
+    "  assert np.array_equal(got.overlay.words[:, :3000], w[:, :3000])\n"
+    "print('ok')\n")
+
+
+def test_panel_chain_fresh_process():
+    """k_panel_chain (default): the very first decomposition of a process -- the chain
+    CTA spins on counters of kernels launched after it, so every kernel of the fused
+    schedule must already be loaded (CUDA loads lazily) -- then dense, ragged, wide,
+    sparse (slow path), rank-deficient and zero inputs, eager / captured / replayed."""
+    _fresh_process(_CHAIN_CASES, F2GPU_PANEL_CHAIN="1")
+
+
+def test_panel_per_kernel_schedule():
+    """F2GPU_PANEL_CHAIN=0: one k_panel_gj launch per panel on alternating side streams
+    (the round-1/2 schedule, still used when a caller captures the library's launches)."""
+    _fresh_process(_CHAIN_CASES, F2GPU_PANEL_CHAIN="0")
+
+
+def test_panel_chain_one_sm_left():
+    """F2GPU_CHAIN_SMS=1: the updates take every SM but the chain's."""
+    _fresh_process(_CHAIN_CASES, F2GPU_PANEL_CHAIN="1", F2GPU_CHAIN_SMS="1")
+
+
 @pytest.mark.parametrize("G", [2, 3, 8])
 def test_strassen_mult_dist_shards(f2, ctx, po, G):
     """The column-sharded multiply at world 1 (broadcast = no-op), G shards emulated
