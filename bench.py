@@ -358,8 +358,10 @@ def run_reference(args, cfg) -> None:
 
 
 VARIANTS = {
-    "block": "decompose_block (lookahead 1, CUDA-graph replay)",
-    "recursive": "decompose_recursive (block leaves of <= 256 panels with lookahead, replayed from CUDA graphs; "
+    "block": "decompose_block (lookahead 1: the panel chain in one persistent k_panel_chain CTA beside the "
+             "graph-replayed posts and updates)",
+    "recursive": "decompose_recursive (block leaves of <= 256 panels with lookahead: each leaf's panel chain is one "
+                 "persistent k_panel_chain CTA, its posts and updates replayed from CUDA graphs; "
                  "TRSM + A' = D ^ L21 X products on the fp4 tensor-core leaf, Strassen-Winograd over 8192 leaves)",
 }
 
@@ -595,7 +597,7 @@ def measure_update_roofline(f2, lib, _lib, ctx, stream, torch, n: int) -> dict:
             "unit_workload": f"C({n}x{n}) ^= A({n}x64)*B(64x{n})",
             "algorithmic_bytes": alg, "us_per_launch": round(t * 1e6, 1),
             "bitops_per_s": round(n * 64 * n / t, 1),
-            "share_of_step": "20% of the decomposition's kernel time (profiles/r2c_launches_summary.txt)",
+            "share_of_step": "19% of the decomposition's kernel time (profiles/r2d_launches_summary.txt)",
             "peak_source": src}
 
 
@@ -636,7 +638,7 @@ def measure_tensor_roofline(f2, lib, _lib, ctx, stream, torch, n: int = 16384) -
             "kernel": "k_gemm_tc7 (fp4 kind::mxf4 GF(2) product leaf, cta_group::2, M-side operand in TMEM)",
             "unit_workload": f"C({n}x{n}) = A({n}x{n})*B({n}x{n}), 2*n^3 fp4 FLOP",
             "us_per_launch": round(t * 1e6, 1), "bitops_per_s": round(n ** 3 / t, 1),
-            "share_of_step": "37% of the decomposition's kernel time (profiles/r2c_launches_summary.txt)",
+            "share_of_step": "38% of the decomposition's kernel time (profiles/r2d_launches_summary.txt)",
             "peak_source": src}
 
 

@@ -26,11 +26,14 @@
  * host threads (the reference contract is single-threaded per call).
  * Distinct contexts may be used concurrently.
  *
- * Device use: the decompositions' lookahead schedule runs kernels on three
- * streams that wait on each other through device counters, so they must be
+ * Device use: the decompositions' lookahead schedule runs kernels on two
+ * streams (the posts and updates of a leaf, and its one persistent panel-chain
+ * CTA) that wait on each other through device counters, so they must be
  * co-resident: run them with the GPU to themselves (no concurrent kernels from
  * other streams or MPS clients).  Every such wait is bounded (20 s); a wait that
- * expires traps and the call returns F2GPU_ECUDA instead of hanging.
+ * expires traps and the call returns F2GPU_ECUDA instead of hanging.  The chain
+ * launch is never captured: inside a caller's own stream capture the library
+ * uses one panel kernel per panel instead.
  */
 #ifndef F2GPU_H
 #define F2GPU_H
