@@ -97,6 +97,15 @@ int f2gpu_ctx_set_tc(f2gpu_ctx *ctx, int on, size_t tc_min_leaf_bits);
 int f2gpu_trace_enable(f2gpu_ctx *ctx, size_t cap);
 int f2gpu_trace_read(f2gpu_ctx *ctx, uint64_t *out, size_t cap, size_t *n);
 
+/* Profiling hook (diagnostics, no reference counterpart): k_panel_chain ALONE on
+ * the word-columns [1, ncols) of a device matrix, every counter it would wait on
+ * pre-satisfied, so the chain free-runs (no posts, no updates: each panel is
+ * factored on the column as it stands, and the matrix is NOT a decomposition
+ * afterwards).  In the pipeline the chain spins on kernels launched after it and
+ * cannot run under ncu, which serialises kernels; this entry can.  It also gives
+ * the chain's intrinsic per-panel cycle (selection + in-CTA hand-off). */
+int f2gpu_debug_panel_chain(f2gpu_ctx *ctx, f2gpu_mat *a, size_t ncols);
+
 /* One panel kernel (Procedure buildZ) on a host column of
  * n words: col_out receives the column with the panel's row swaps applied,
  * z_out the 64 words of the pseudo-inverse Z and r_out the block rank;

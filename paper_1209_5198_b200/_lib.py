@@ -33,7 +33,7 @@ SYMBOLS = [
     "f2gpu_mat_copy", "f2gpu_mat_select_wcols", "f2gpu_mat_xor", "f2gpu_mat_transpose",
     "f2gpu_m4rm_mult", "f2gpu_m4rm_mult_acc", "f2gpu_mult_acc", "f2gpu_mult_acc_host", "f2gpu_strassen_mult",
     "f2gpu_gemm_tc",
-    "f2gpu_update_tc", "f2gpu_panel_build_z", "f2gpu_trace_enable", "f2gpu_trace_read",
+    "f2gpu_update_tc", "f2gpu_panel_build_z", "f2gpu_trace_enable", "f2gpu_trace_read", "f2gpu_debug_panel_chain",
     "f2gpu_decompose_block", "f2gpu_decompose_recursive", "f2gpu_decompose_block_sharded",
     "f2gpu_rank",
     "f2gpu_m4rm_mult_host", "f2gpu_strassen_mult_host", "f2gpu_decompose_block_host",
@@ -90,6 +90,7 @@ _SIG = {
     "f2gpu_rank_host": ([vp, vp, sz, sz, sz, C.POINTER(sz)], C.c_int),
     "f2gpu_null_space": ([vp, vp, C.POINTER(vp), C.POINTER(sz)], C.c_int),
     "f2gpu_trace_enable": ([vp, sz], C.c_int),
+    "f2gpu_debug_panel_chain": ([vp, vp, sz], C.c_int),
     "f2gpu_trace_read": ([vp, vp, sz, C.POINTER(sz)], C.c_int),
     "f2gpu_panel_build_z": ([vp, vp, sz, vp, vp, C.POINTER(C.c_uint32), vp, C.POINTER(C.c_uint32)], C.c_int),
     "f2gpu_solve": ([vp, vp, vp, vp, C.POINTER(C.c_int)], C.c_int),

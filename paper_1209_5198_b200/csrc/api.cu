@@ -2111,6 +2111,26 @@ int f2gpu_ctx_set_tc(f2gpu_ctx* c, int on, size_t leaf) {
 }
 
 // ---- device trace (diagnostics) ----
+int f2gpu_debug_panel_chain(f2gpu_ctx* c, f2gpu_mat* a, size_t ncols) {
+    if (!c || !a) return set_err(F2GPU_EINVAL, "debug_panel_chain: null argument");
+    const size_t n = a->rows, mu = (a->cols + 63) / 64;
+    if (ncols < 2 || ncols > mu) return set_err(F2GPU_ERANGE, "debug_panel_chain: ncols out of range");
+    if (!f2::panel_link_ok()) return set_err(F2GPU_EINVAL, "debug_panel_chain: needs the k_panel_gj body");
+    F2_TRY(ensure_scratch(c, n, mu));
+    // every counter satisfied (waits are >= count or != 0), panel 0 "factored" with rank 0
+    CUDA_TRY(cudaMemsetAsync(c->scr_flags, 0x3f, mu * 4 * kFlagsPerPanel, c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->scr_st, 0, kStateBytes, c->stream));
+    f2::ChainArgs ca{};
+    ca.w = a->d; ca.stride = a->stride; ca.n = n; ca.st = static_cast<f2::PanelState*>(c->scr_st);
+    ca.flags = c->scr_flags; ca.flags_per_panel = int(kFlagsPerPanel);
+    ca.leaf0 = 0; ca.c0 = 1; ca.c1 = int(ncols); ca.coff = 0;
+    ca.yblocks = uint32_t(f2::post_col_yblocks(n));
+    ca.upd_grid = uint32_t(c->num_sms);
+    ca.poll_ns = uint32_t(c->poll_ns);
+    ca.trace = false;
+    return check_launch(c, f2::launch_panel_chain(ca, c->stream), "k_panel_chain");
+}
+
 int f2gpu_trace_enable(f2gpu_ctx* c, size_t cap) {
     if (!c) return set_err(F2GPU_EINVAL, "trace_enable: null ctx");
     CUDA_TRY(cudaStreamSynchronize(c->stream));
