@@ -255,6 +255,7 @@ struct f2gpu_ctx {
     int u_fc_ctas = 24;         // F2GPU_U_FC_CTAS: CTAs doing that first column (0: all; 65536^2:
                                 // 16: 63.18, 20: 63.21, 24: 63.00, 28: 63.30, 32: 63.28 ms)
     int u_fc_weight = 3;        // F2GPU_U_FC_W: their bulk share in quarters
+    bool u_fc_ctas_set = false, u_fc_w_set = false;  // given in the environment (else 40, 2/4 in chain leaves)
     bool panel_head = false;    // F2GPU_PANEL_HEAD=1: the panel kernel does the first rows itself (measured slower)
     bool post_spin = true;      // F2GPU_POST_SPIN=0: k_post_col(j) waits for P(j) by event, not by counter
     bool pdl = true;            // F2GPU_PDL=0: the update after k_post_col is a plain stream-ordered launch
@@ -844,8 +845,13 @@ int enqueue_panels(f2gpu_ctx* c, Shard& s, size_t n, size_t mu, size_t c0, size_
         u.st = s.st + j;
         u.release = release;
         u.first_col = release != nullptr && c->u_first_col;
-        u.fc_ctas = c->u_fc_ctas;
-        u.fc_weight = c->u_fc_weight;
+        // chain schedule, leaves of the recursion (<= 256 panels): the update's END is on the
+        // critical path (the next post waits for it) and its first-column CTAs finish last,
+        // while the release has ~2 us of slack: more of them with a smaller bulk share
+        // (40 CTAs, 2/4: 48.25 -> 47.93 ms at 65536^2; wider block-variant runs keep 24, 3/4)
+        const bool narrow = chain && c1 - c0 <= 256;
+        u.fc_ctas = narrow && !c->u_fc_ctas_set ? 40 : c->u_fc_ctas;
+        u.fc_weight = narrow && !c->u_fc_w_set ? 2 : c->u_fc_weight;
         u.tag = c->trace_buf ? int(j) : -1;
         u.pdl = pdl;
         return check_launch(c, f2::launch_update(u, grid, c->stream), "k_update");
@@ -2000,6 +2006,8 @@ int f2gpu_ctx_create(int device, f2gpu_ctx** out) {
         c->poll_ns = uint32_t(std::max<long long>(0, o.poll_ns));
         c->u_first_col = o.u_firstcol != 0;
         c->u_fc_ctas = int(o.u_fc_ctas);
+        c->u_fc_ctas_set = o.u_fc_ctas_set;
+        c->u_fc_w_set = o.u_fc_w_set;
         c->u_fc_weight = int(std::max<long long>(1, std::min<long long>(4, o.u_fc_w)));
         c->panel_head = o.panel_head != 0;
         c->post_spin = o.post_spin != 0;

@@ -18,8 +18,8 @@
     X(panel_early, "F2GPU_PANEL_EARLY", 1, "queue P(j+1) ahead on alternating side streams (0: after post j)")  \
     X(poll_ns, "F2GPU_POLL_NS", 0, "sleep (ns) between polls of the panel kernel's consumer warps")            \
     X(u_firstcol, "F2GPU_U_FIRSTCOL", 1, "the update releases the next panel's column first (0: group 0)")     \
-    X(u_fc_ctas, "F2GPU_U_FC_CTAS", 24, "update CTAs doing that first column (0: all)")                       \
-    X(u_fc_w, "F2GPU_U_FC_W", 3, "their share of the bulk tiles, in quarters (1..4)")                        \
+    X(u_fc_ctas, "F2GPU_U_FC_CTAS", 24, "update CTAs doing that first column (0: all; unset: 40 in chain-schedule leaves)")                       \
+    X(u_fc_w, "F2GPU_U_FC_W", 3, "their share of the bulk tiles, in quarters (1..4; unset: 2 in chain-schedule leaves)")                        \
     X(panel_head, "F2GPU_PANEL_HEAD", 0, "the panel kernel computes the first 256 rows below its pivots")      \
     X(post_spin, "F2GPU_POST_SPIN", 1, "k_post_col waits for its panel kernel on a counter (0: by event)")     \
     X(pdl, "F2GPU_PDL", 1, "the update is a programmatic dependent launch of k_post_col")                    \
