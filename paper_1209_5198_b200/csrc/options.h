@@ -23,7 +23,7 @@
     X(panel_head, "F2GPU_PANEL_HEAD", 0, "the panel kernel computes the first 256 rows below its pivots")      \
     X(post_spin, "F2GPU_POST_SPIN", 1, "k_post_col waits for its panel kernel on a counter (0: by event)")     \
     X(pdl, "F2GPU_PDL", 1, "the update is a programmatic dependent launch of k_post_col")                    \
-    X(post_pdl, "F2GPU_POST_PDL", 0, "k_post_col as a programmatic dependent of the previous update (can starve P)") \
+    X(post_pdl, "F2GPU_POST_PDL", 0, "k_post_col as a programmatic dependent of the previous update (unset: on in the chain schedule, off with per-panel launches, where it can starve P)") \
     X(panel_hand, "F2GPU_PANEL_HAND", 0, "P(j+1) starts on P(j)'s done counter with a hand-off block")         \
     X(panel_chain, "F2GPU_PANEL_CHAIN", 1, "one persistent k_panel_chain CTA per leaf: panel j+1 starts on an in-CTA hand-off") \
     X(chain_sms, "F2GPU_CHAIN_SMS", 2, "SMs the updates leave free under F2GPU_PANEL_CHAIN (the chain CTA needs one)") \
